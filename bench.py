@@ -1,0 +1,377 @@
+#!/usr/bin/env python
+"""GP-SPCA power-iteration benchmark (BASELINE.json metric: iterations/s and
+A-stream HBM GB/s).
+
+Workload (N=1, BASELINE configs[1] = SURVEY C2): single-unit l0 GP-SPCA on a
+low-rank + noise matrix A, p = 4096 samples x n = 2^20 variables, fp32
+storage (16 GiB, > 126 MB L2, so no flush is needed between steps),
+gamma = (0.1 * max_i ||a_i||)^2, start at the max-norm column.  The data are
+drawn on the device with the distribution of the reference generator
+(`synthetic_sparse_factors`, datasets.py:278-309: 16 classes x 256 samples,
+5 factors on disjoint supports of n/100 features, class_scale 4, noise 1).
+
+One step = one power iteration = fused sweep (K1) + cross-CTA reduction (K2)
++ power step (K3).  `value` times K steps on device-resident A with CUDA
+events; `e2e` times full `solve_single_unit` calls from pinned host memory
+(A upload, norms pass, init, device loop to convergence, loadings download).
+`--impl reference` times the CPU reference algorithm (the NumPy oracle port
+in oracle/, BLAS on all host cores) on a bounded column sample of the same
+workload and extrapolates per-iteration time linearly in n.
+
+N > 1 (torchrun): strong scaling of the same A, column-sharded, one NCCL
+all-reduce of the p+4 exchange vector per iteration.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+P, N_COLS = 4096, 1 << 20
+METRIC = "GP-SPCA iters/s & A-stream HBM GB/s vs 8 TB/s peak at 1/2/4/8 B200"
+WORKLOAD = ("C2: single-unit l0 GP-SPCA, synthetic low-rank+noise A p=4096 n=2^20 fp32 (16 GiB), "
+            "gamma=(0.1*max||a_i||)^2, max-norm-column start")
+FALLBACK_HBM = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=N_COLS, help="columns (default 2^20)")
+    ap.add_argument("--p", type=int, default=P)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- helpers
+
+def hbm_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """dram bytes per sweep launch from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_sweep_summary.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        if d.get("p") == P and d.get("n") == N_COLS:
+            return d.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and
+                          r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def make_c2(torch, p, n_local, col0, n_global, device, seed=0):
+    """Low-rank + noise A (p x n_local, column-major == torch (n_local, p)),
+    distributed like synthetic_sparse_factors(16, 256, n, 5, n//100, 4, 1, 1)."""
+    n_classes, n_factors = 16, 5
+    support = n_global // 100
+    rng = np.random.default_rng(seed)
+    means = rng.standard_normal((n_classes, n_factors)) * 4.0
+    labels = np.repeat(np.arange(n_classes), p // n_classes)
+    latent = means[labels] + rng.standard_normal((p, n_factors))
+    gen = torch.Generator(device=device)
+    gen.manual_seed(1000 + col0)
+    At = torch.randn((n_local, p), generator=gen, device=device, dtype=torch.float32)
+    lat = torch.as_tensor(latent, dtype=torch.float32, device=device)
+    for f in range(n_factors):
+        lo, hi = max(f * support, col0), min((f + 1) * support, col0 + n_local)
+        if lo >= hi:
+            continue
+        e = np.random.default_rng([seed, f]).standard_normal(support)
+        e = e / np.linalg.norm(e)
+        w = torch.as_tensor(e[lo - f * support: hi - f * support], dtype=torch.float32, device=device)
+        At[lo - col0: hi - col0] += w[:, None] * lat[:, f][None, :]
+    return At
+
+
+# ------------------------------------------------------------ reference arm
+
+def cpu_reference_iteration_time(p, n_sample, iters, seed=0):
+    """Seconds per power iteration of the CPU reference algorithm (oracle port,
+    2 reads of A per iteration as in single_unit.py:167-180) on p x n_sample."""
+    import oracle
+
+    rng = np.random.default_rng(seed)
+    A = np.asfortranarray(rng.standard_normal((p, n_sample)).astype(np.float32).astype(np.float64))
+    norms = oracle.column_norms(A)
+    gamma = (0.1 * float(norms.max())) ** 2
+    x = A[:, int(np.argmax(norms))] / norms.max()
+    c = A.T @ x
+    t0 = time.perf_counter()
+    for _ in range(iters):
+        g = oracle.su_gradient(A, c, gamma, "l0")
+        x = g / np.linalg.norm(g)
+        c = A.T @ x
+        oracle.su_objective(c, gamma, "l0")
+    return (time.perf_counter() - t0) / iters
+
+
+def cpu_baseline_entry(p, n_full, n_sample=1 << 16, iters=8):
+    t = cpu_reference_iteration_time(p, n_sample, iters)
+    per_iter_full = t * (n_full / n_sample)
+    return {"value": 1.0 / per_iter_full, "unit": "iters/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{iters} power iterations of the NumPy fp64 oracle (oracle/gpower.py, BLAS threads = "
+                      f"{os.cpu_count()}) on p={p} x n={n_sample} Gaussian columns, "
+                      f"{t * 1e3:.1f} ms/iter, extrapolated linearly to n={n_full}"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n_sample = 1 << 15
+    times = []
+    for s in range(args.warmup + args.steps):
+        t = cpu_reference_iteration_time(args.p, n_sample, 1, seed=s)
+        if s >= args.warmup:
+            times.append(t * (args.n / n_sample))
+    per = statistics.mean(times)
+    value = 1.0 / per
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "p": args.p, "n": args.n},
+            "cpu_baseline": {"value": value, "unit": "iters/s", "cores": os.cpu_count(), "kind": "port",
+                             "sample": f"each step: 1 power iteration of the NumPy fp64 oracle on p={args.p} x "
+                                       f"n={n_sample} columns (BLAS on all {os.cpu_count()} host threads), "
+                                       f"extrapolated linearly to n={args.n}"},
+            "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+
+def run_ours(args):
+    import torch
+
+    import paper_1312_6182_b200 as gps
+    from paper_1312_6182_b200 import _native
+    from paper_1312_6182_b200.distributed import Comm, column_partition, global_max_norm_start
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    p, n = args.p, args.n
+    offset, n_local = column_partition(n, world)[rank]
+
+    # --- data (device), engine storage, gamma from the device norms pass
+    At = make_c2(torch, p, n_local, offset, n, dev)
+    torch.cuda.synchronize()
+    ctx = _native.context(local)
+    A = gps.DataMatrix.from_device(At.data_ptr(), p, n_local, ld=p, dtype=np.float32, device=local)
+    comm = Comm() if world > 1 else None
+    top = float(A.norms.max())
+    if comm:
+        top = comm.max_scalar(top, dev)
+    gamma = (0.1 * top) ** 2
+    if comm:
+        x0, _ = global_max_norm_start(A.norms, offset, A.column, comm, p, dev)
+    else:
+        i = int(np.argmax(A.norms))
+        x0 = A.column(i) / A.norms[i]
+
+    # --- device-resident timed loop (tol = 0: every step is a real iteration)
+    stream = torch.cuda.current_stream(dev)
+    ctx.set_stream(stream.cuda_stream)
+    total = args.warmup + args.steps
+    loop = gps.single_unit.PowerLoop(A, "l0", gamma, 0.0, total + 1)
+    exch = None
+    if world > 1:
+        cnt = _native.C.c_int64()
+        _native.check(_native.lib().gps_su_exchange(loop.handle, None, _native.C.byref(cnt)))
+        exch = torch.zeros(cnt.value, dtype=torch.float64, device=dev)
+        _native.check(_native.lib().gps_su_set_exchange(loop.handle, _native.C.c_void_p(exch.data_ptr())))
+    loop.start(x0)
+    L = _native.lib()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+
+    def iteration(i=None):
+        if i is not None:
+            ev[i][0].record(stream)
+        _native.check(L.gps_su_enqueue(loop.handle, 1))
+        if i is not None:
+            ev[i][1].record(stream)
+        _native.check(L.gps_su_enqueue(loop.handle, 2))
+        if exch is not None:
+            comm.all_reduce_sum(exch)
+        _native.check(L.gps_su_enqueue(loop.handle, 4))
+
+    for _ in range(args.warmup):
+        iteration()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.launch_count
+    t_start, t_stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        t_start.record(stream)
+        for i in range(args.steps):
+            iteration(i)
+        t_stop.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    launches = ctx.launch_count - launches0
+    done, it, _ = (lambda d, i_, c: (d.value, i_.value, c.value))(*_poll(loop))
+    assert not done and it == total, f"loop stopped early (iter {it}, expected {total})"
+    elapsed = t_start.elapsed_time(t_stop) / 1e3
+    sweep_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
+    if world > 1:
+        t = torch.tensor([elapsed, sweep_ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        elapsed, sweep_ms = float(t[0]), float(t[1])
+    del loop
+
+    iters_per_s = args.steps / elapsed
+    a_bytes_local = p * n_local * 4
+    peak, peak_src = hbm_peak()
+    achieved = a_bytes_local / (sweep_ms / 1e3) / 1e9  # GB/s of the sweep kernel on this rank
+    stream_gbs = p * n * 4 * iters_per_s / 1e9          # whole-job A-stream GB/s (all ranks)
+
+    # --- end to end through the public API from pinned host memory (N=1 only)
+    e2e = None
+    if world == 1 and args.e2e_steps > 0:
+        host = torch.empty((n_local, p), dtype=torch.float32, pin_memory=True)
+        host.copy_(At)
+        A_host = host.numpy().T  # (p, n) Fortran-ordered view of pinned memory
+        del A, At
+        torch.cuda.empty_cache()
+        cfg = gps.SolverConfig(penalty="l0", gamma=gamma)
+        e_iters, e_time = 0, 0.0
+        for s in range(args.e2e_steps + 1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            Ad = gps.DataMatrix(A_host)
+            loadings, report = gps.solve_single_unit(Ad, cfg)
+            nnz = loadings.nnz_per_component()[0]
+            dt = time.perf_counter() - t0
+            del Ad
+            if s > 0:  # first call warms the context / allocator
+                e_iters += report.iterations
+                e_time += dt
+        e2e = {"value": e_iters / e_time, "unit": "iters/s", "h2d_bytes_per_step": p * n * 4 + p * 8,
+               "d2h_bytes_per_step": n * 8 + (report.iterations + 1) * 8 + n * 8,
+               "solve_s": e_time / args.e2e_steps, "iterations_per_solve": report.iterations, "nnz": nnz,
+               "note": "per step: DataMatrix(A pinned host) upload + norms pass + solve_single_unit to "
+                       "convergence (tol 1e-6) + loadings download"}
+    else:
+        del At
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_entry(p, n)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": iters_per_s, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "p": p, "n": n, "storage": "f32 (A), f64 accumulate",
+                       "penalty": "l0", "gamma": gamma, "parallelism": f"column-shard x{world}",
+                       "l2": "no flush: A (16 GiB) >> L2 (126 MB)"},
+            "a_stream_gbs": stream_gbs,
+            "a_stream_frac_of_8tbs": stream_gbs / world / 8000.0,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic(), "peak_source": peak_src,
+                         "kernel": "su_sweep_kernel<float,4,256,kFused>",
+                         "algorithmic_bytes_per_launch": a_bytes_local, "avg_launch_ms": sweep_ms},
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def _poll(loop):
+    from paper_1312_6182_b200 import _native
+
+    d, i, c = _native.C.c_int(), _native.C.c_int(), _native.C.c_int()
+    _native.check(_native.lib().gps_su_poll(loop.handle, _native.C.byref(d), _native.C.byref(i), _native.C.byref(c)))
+    return d, i, c
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,143 @@
+/*
+ * gpspca_b200.h -- C ABI of the B200-native GP-SPCA engine (libgpspca_b200.so).
+ *
+ * The reference (`gpspca` 0.1.0, /root/reference/pkg/src/gpspca) is a pure
+ * Python/NumPy package with no FFI; its GPU "extension seam" is the kernel
+ * set named in SPEC.md:424 (par_matvec_t, par_gram_apply,
+ * par_threshold_accumulate, dense SVD) plus the solver loops that call it.
+ * Each entry point below cites the reference interface it replaces
+ * (path:line relative to /root/reference/pkg/src/gpspca/).  Plain C types
+ * only: host buffers are caller-owned, device memory is owned by the
+ * library objects, calls are stream-ordered on the context's stream and
+ * BLOCKING at return unless the name says `enqueue`.
+ *
+ * Layout: A is p x n, column-major, column i contiguous (core.py:36,52-54),
+ * stored on the device with a padded leading dimension ld = roundup(p, 32)
+ * and zero padding rows.  Iterates x (length p) and all reductions are fp64.
+ *
+ * Error model (mapped by the Python host to the reference's exceptions):
+ *   GPS_E_ARG      -> ValueError           (shape / argument / finiteness)
+ *   GPS_E_RANK     -> RankDeficiencyError  (block.py:33-49)
+ *   GPS_E_OOM      -> MemoryError          (parallel.py:145-156 analogue)
+ *   GPS_E_CUDA     -> RuntimeError
+ *   GPS_E_UNSUPPORTED -> NotImplementedError (shape outside the built kernels)
+ * gps_last_error() returns a thread-local message for the last failure.
+ */
+#ifndef GPSPCA_B200_H
+#define GPSPCA_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum gps_status {
+  GPS_OK = 0,
+  GPS_E_ARG = 1,
+  GPS_E_RANK = 2,
+  GPS_E_OOM = 3,
+  GPS_E_CUDA = 4,
+  GPS_E_UNSUPPORTED = 5
+};
+enum gps_dtype { GPS_F32 = 0, GPS_F64 = 1 };
+enum gps_penalty { GPS_L1 = 0, GPS_L0 = 1 }; /* core.py:13 PENALTIES */
+
+typedef struct gps_ctx gps_ctx;       /* one device + one stream            */
+typedef struct gps_matrix gps_matrix; /* device-resident DataMatrix         */
+typedef struct gps_su gps_su;         /* single-unit solver state           */
+
+/* ---- library / context ------------------------------------------------ */
+int gps_version(void);
+const char* gps_last_error(void);
+int gps_device_count(int* count);
+int gps_ctx_create(int device, gps_ctx** out);
+int gps_ctx_destroy(gps_ctx* ctx);
+/* Use a caller stream (e.g. torch.cuda.current_stream().cuda_stream). */
+int gps_ctx_set_stream(gps_ctx* ctx, void* cuda_stream);
+int gps_ctx_sync(gps_ctx* ctx);
+/* Number of kernels this context launched so far (instrumentation). */
+int64_t gps_ctx_launch_count(gps_ctx* ctx);
+
+/* ---- data matrix: core.py:25-68 DataMatrix / as_data_matrix ------------ */
+/* Copies a host column-major p x n matrix (leading dimension ld_src >= p)
+ * into device memory.  dtype selects the device storage (GPS_F32 keeps an
+ * fp32 input in fp32; reductions are always fp64). */
+int gps_matrix_create(gps_ctx* ctx, const void* host, int64_t p, int64_t n, int64_t ld_src, int dtype,
+                      gps_matrix** out);
+/* Same, from a DEVICE column-major buffer (copied into padded storage). */
+int gps_matrix_create_device(gps_ctx* ctx, const void* dev_src, int64_t p, int64_t n, int64_t ld_src, int dtype,
+                             gps_matrix** out);
+/* Same, from a host ROW-major p x n buffer (C order), transposed on device. */
+int gps_matrix_create_rowmajor(gps_ctx* ctx, const void* host, int64_t p, int64_t n, int dtype,
+                               gps_matrix** out);
+int gps_matrix_destroy(gps_matrix* A);
+int gps_matrix_info(const gps_matrix* A, int64_t* p, int64_t* n, int64_t* ld, int* dtype);
+/* Device copy back to a host column-major buffer with leading dimension p. */
+int gps_matrix_download(gps_matrix* A, void* host);
+/* Column i as fp64 (length p) -- core.py:52-54 DataMatrix.column. */
+int gps_matrix_column(gps_matrix* A, int64_t i, double* out);
+/* Device pointer of the padded storage (for callers that own a stream). */
+void* gps_matrix_device_ptr(gps_matrix* A);
+
+/* core.py:243-246 column_norms + core.py:42 isfinite check, one pass (K0).
+ * Results are cached on the matrix; norms_out may be NULL. */
+int gps_column_norms(gps_matrix* A, double* norms_out, int* nonfinite_out);
+
+/* single_unit.py:287-296 deflate: new fp64 matrix (I - xx')A (x unit). */
+int gps_matrix_deflate(gps_matrix* A, const double* x, gps_matrix** out);
+
+/* Columns idx[0..k) as a new matrix (support-restricted power iteration,
+ * single_unit.py:219-230 `A.values[:, support]`). */
+int gps_matrix_gather(gps_matrix* A, const int64_t* idx, int64_t k, gps_matrix** out);
+
+/* ---- kernel seam: parallel.py:85-142 ----------------------------------- */
+int gps_matvec_t(gps_matrix* A, const double* x, double* c_out);               /* parallel.py:85  */
+int gps_gram_apply(gps_matrix* A, const double* coef, double* out);            /* parallel.py:108 */
+int gps_threshold_accumulate(gps_matrix* A, const double* c, double gamma,     /* parallel.py:131 */
+                             int penalty, double* out);
+/* One fused sweep at x: f = objective (single_unit.py:44-48), g_half =
+ * sum_i w(a_i'x) a_i (the ascent direction / 2, single_unit.py:67-81),
+ * optional c = A'x and w = threshold(c) (single_unit.py:100-121 before
+ * normalisation).  Any output may be NULL. */
+int gps_su_sweep(gps_matrix* A, const double* x, double gamma, int penalty, double* f_out,
+                 double* g_half_out, double* c_out, double* w_out, int64_t* nnz_out);
+
+/* ---- single-unit power iteration: single_unit.py:160-181 --------------- */
+/* tol = 0 disables the relative-change test (benchmarking fixed-length loops). */
+int gps_su_create(gps_matrix* A, int penalty, double gamma, double tol, int max_iter, gps_su** out);
+int gps_su_destroy(gps_su* s);
+/* Reset the loop at x0 (length p, unit norm). */
+int gps_su_start(gps_su* s, const double* x0);
+/* Implicit deflation (single_unit.py:287-296 without rewriting A): the
+ * step projects the gradient off the k orthonormal columns of X (p x k,
+ * column-major), applied in column order. k = 0 disables. */
+int gps_su_set_deflation(gps_su* s, const double* X, int k);
+/* Native single-device loop: device-resident iterate, history and stopping
+ * rule; the host polls the control block every poll_every iterations. */
+int gps_su_run(gps_su* s, int poll_every);
+/* Building blocks for a multi-rank loop (column shards): sweep + local
+ * reduce into the exchange vector [g (ld) | f | nnz | sum w^2 | 0]; the
+ * caller all-reduces it (sum) across ranks; then the step. */
+int gps_su_enqueue_sweep(gps_su* s);
+int gps_su_exchange(gps_su* s, void** dev_ptr, int64_t* count);
+/* Use a caller-owned device buffer (ld + 4 doubles) as the exchange vector,
+ * e.g. a torch tensor handed to an NCCL all-reduce. */
+int gps_su_set_exchange(gps_su* s, void* dev_ptr);
+int gps_su_enqueue_step(gps_su* s);
+/* Fine-grained enqueue for instrumentation: bit 1 sweep kernel, bit 2 the
+ * cross-CTA reduction, bit 4 the step (gps_su_enqueue_sweep == mask 3). */
+int gps_su_enqueue(gps_su* s, int mask);
+/* Copies the control block to the host (synchronises the stream). */
+int gps_su_poll(gps_su* s, int* done, int* iter, int* converged);
+/* Results of the finished loop: x (p), history (n_hist <= max_iter+1),
+ * the weights w of the final sweep (n; z = w / ||w||), sum w^2. */
+int gps_su_result(gps_su* s, double* x_out, double* hist_out, int* n_hist, int* converged, double* w_out,
+                  double* w_sumsq_out);
+/* Kernel launches per power iteration of gps_su_run (instrumentation). */
+int gps_su_launches_per_iter(gps_su* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GPSPCA_B200_H */

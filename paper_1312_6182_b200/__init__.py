@@ -1,0 +1,55 @@
+"""B200-native GP-SPCA engine: a drop-in for the power-iteration path of the
+reference `gpspca` package (sparse PCA by the generalized power method,
+arXiv:1312.6182).
+
+Same public names, signatures and exceptions as the reference API
+(`/root/reference/pkg/src/gpspca/__init__.py:8-69`) for the hot path:
+single-unit l1/l0 and block l1/l0 solvers, their one-shot objectives /
+ascent directions / recovery, and the column kernel seam.  Arithmetic runs in
+hand-written sm_100a CUDA (libgpspca_b200.so, include/gpspca_b200.h); there is
+no CPU fallback.
+"""
+
+from .core import (
+    DataMatrix,
+    RunReport,
+    SolverConfig,
+    SparseLoadings,
+    StiefelPoint,
+    as_data_matrix,
+    column_norms,
+    positive_part,
+)
+from .parallel import (
+    DEFAULT_PLAN,
+    KernelPlan,
+    fused_sweep,
+    par_gram_apply,
+    par_matvec_t,
+    par_threshold_accumulate,
+    threshold_weights,
+)
+from .single_unit import (
+    SingleUnitState,
+    ascent_direction_sl0,
+    ascent_direction_sl1,
+    deflate,
+    objective_sl0,
+    objective_sl1,
+    power_step,
+    recover_pattern_sl0,
+    recover_pattern_sl1,
+    solve_multi_sequential,
+    solve_single_unit,
+)
+from .block import (
+    BlockState,
+    RankDeficiencyError,
+    ascent_direction_block,
+    objective_bl0,
+    objective_bl1,
+    polar_projection,
+    solve_block,
+)
+
+__version__ = "0.1.0+b200"

@@ -1,0 +1,165 @@
+"""ctypes binding of libgpspca_b200.so (include/gpspca_b200.h).
+
+There is no fallback: if the library is missing or no sm_100 device is
+visible, every numeric entry point raises.  Importing this module does not
+touch the GPU; the first call that needs a context does.
+"""
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libgpspca_b200.so")
+
+GPS_OK, GPS_E_ARG, GPS_E_RANK, GPS_E_OOM, GPS_E_CUDA, GPS_E_UNSUPPORTED = range(6)
+F32, F64 = 0, 1
+PENALTY_CODE = {"l1": 0, "l0": 1}
+
+_dp = C.POINTER(C.c_double)
+_vp = C.c_void_p
+_i64 = C.c_int64
+_i64p = C.POINTER(C.c_int64)
+_ip = C.POINTER(C.c_int)
+
+# name -> (restype, argtypes); the exported surface of include/gpspca_b200.h
+SIGNATURES = {
+    "gps_version": (C.c_int, []),
+    "gps_last_error": (C.c_char_p, []),
+    "gps_device_count": (C.c_int, [_ip]),
+    "gps_ctx_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
+    "gps_ctx_destroy": (C.c_int, [_vp]),
+    "gps_ctx_set_stream": (C.c_int, [_vp, _vp]),
+    "gps_ctx_sync": (C.c_int, [_vp]),
+    "gps_ctx_launch_count": (_i64, [_vp]),
+    "gps_matrix_create": (C.c_int, [_vp, _vp, _i64, _i64, _i64, C.c_int, C.POINTER(_vp)]),
+    "gps_matrix_create_device": (C.c_int, [_vp, _vp, _i64, _i64, _i64, C.c_int, C.POINTER(_vp)]),
+    "gps_matrix_create_rowmajor": (C.c_int, [_vp, _vp, _i64, _i64, C.c_int, C.POINTER(_vp)]),
+    "gps_matrix_destroy": (C.c_int, [_vp]),
+    "gps_matrix_info": (C.c_int, [_vp, _i64p, _i64p, _i64p, _ip]),
+    "gps_matrix_download": (C.c_int, [_vp, _vp]),
+    "gps_matrix_column": (C.c_int, [_vp, _i64, _dp]),
+    "gps_matrix_device_ptr": (_vp, [_vp]),
+    "gps_column_norms": (C.c_int, [_vp, _dp, _ip]),
+    "gps_matrix_deflate": (C.c_int, [_vp, _dp, C.POINTER(_vp)]),
+    "gps_matrix_gather": (C.c_int, [_vp, _i64p, _i64, C.POINTER(_vp)]),
+    "gps_matvec_t": (C.c_int, [_vp, _dp, _dp]),
+    "gps_gram_apply": (C.c_int, [_vp, _dp, _dp]),
+    "gps_threshold_accumulate": (C.c_int, [_vp, _dp, C.c_double, C.c_int, _dp]),
+    "gps_su_sweep": (C.c_int, [_vp, _dp, C.c_double, C.c_int, _dp, _dp, _dp, _dp, _i64p]),
+    "gps_su_create": (C.c_int, [_vp, C.c_int, C.c_double, C.c_double, C.c_int, C.POINTER(_vp)]),
+    "gps_su_destroy": (C.c_int, [_vp]),
+    "gps_su_start": (C.c_int, [_vp, _dp]),
+    "gps_su_run": (C.c_int, [_vp, C.c_int]),
+    "gps_su_set_deflation": (C.c_int, [_vp, _dp, C.c_int]),
+    "gps_su_enqueue_sweep": (C.c_int, [_vp]),
+    "gps_su_exchange": (C.c_int, [_vp, C.POINTER(_vp), _i64p]),
+    "gps_su_set_exchange": (C.c_int, [_vp, _vp]),
+    "gps_su_enqueue_step": (C.c_int, [_vp]),
+    "gps_su_enqueue": (C.c_int, [_vp, C.c_int]),
+    "gps_su_poll": (C.c_int, [_vp, _ip, _ip, _ip]),
+    "gps_su_result": (C.c_int, [_vp, _dp, _dp, _ip, _ip, _dp, _dp]),
+    "gps_su_launches_per_iter": (C.c_int, [_vp]),
+}
+
+
+class NativeError(RuntimeError):
+    """A CUDA-side failure inside libgpspca_b200 (GPS_E_CUDA)."""
+
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def lib():
+    """Load the shared library (once).  Raises if it is not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lib_lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(
+                    f"{LIB_PATH} is missing: build it with `python -m paper_1312_6182_b200._build` "
+                    "(there is no CPU fallback)")
+            handle = C.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(handle, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = handle
+    return _lib
+
+
+def last_error():
+    msg = lib().gps_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(rc, what=""):
+    """Map a gps_status to the reference's exception types."""
+    if rc == GPS_OK:
+        return
+    msg = f"{what}: {last_error()}" if what else last_error()
+    if rc == GPS_E_ARG:
+        raise ValueError(msg)
+    if rc == GPS_E_OOM:
+        raise MemoryError(msg)
+    if rc == GPS_E_UNSUPPORTED:
+        raise NotImplementedError(msg)
+    raise NativeError(msg)
+
+
+def dptr(a):
+    """Pointer to a C-contiguous float64 numpy array."""
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_dp)
+
+
+class Context:
+    """One device + one CUDA stream (gps_ctx)."""
+
+    def __init__(self, device):
+        self.device = int(device)
+        h = _vp()
+        check(lib().gps_ctx_create(self.device, C.byref(h)), "gps_ctx_create")
+        self.handle = h
+
+    def sync(self):
+        check(lib().gps_ctx_sync(self.handle))
+
+    def set_stream(self, stream_ptr):
+        check(lib().gps_ctx_set_stream(self.handle, _vp(stream_ptr)))
+
+    @property
+    def launch_count(self):
+        return int(lib().gps_ctx_launch_count(self.handle))
+
+
+_contexts = {}
+_ctx_lock = threading.Lock()
+
+
+def default_device():
+    for var in ("GPSPCA_DEVICE", "LOCAL_RANK"):
+        if var in os.environ:
+            return int(os.environ[var])
+    return 0
+
+
+def context(device=None):
+    device = default_device() if device is None else int(device)
+    with _ctx_lock:
+        ctx = _contexts.get(device)
+        if ctx is None:
+            ctx = Context(device)
+            _contexts[device] = ctx
+        return ctx
+
+
+def device_count():
+    n = C.c_int(0)
+    check(lib().gps_device_count(C.byref(n)))
+    return n.value

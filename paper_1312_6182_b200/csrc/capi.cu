@@ -1,0 +1,923 @@
+// extern "C" implementation of include/gpspca_b200.h.
+//
+// Host runtime of the engine: device/stream context, device-resident data
+// matrices, kernel dispatch on (storage dtype, padded p), and the native
+// single-unit power loop (CUDA-graph captured chunks of iterations whose
+// kernels early-exit once the device-side stopping rule fires).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "../../include/gpspca_b200.h"
+#include "su_kernels.cuh"
+
+using namespace gps;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  cudaGetLastError();  // clear sticky-free errors
+  return fail(e == cudaErrorMemoryAllocation ? GPS_E_OOM : GPS_E_CUDA, "%s: %s (%s)", what,
+              cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+#define GPS_CUDA(call)                                  \
+  do {                                                  \
+    cudaError_t _e = (call);                            \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+  } while (0)
+
+#define GPS_CHECK_LAUNCH(what)                          \
+  do {                                                  \
+    cudaError_t _e = cudaGetLastError();                \
+    if (_e != cudaSuccess) return cuda_fail(_e, what);  \
+  } while (0)
+
+constexpr int kSmemBudget = 227 * 1024;
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace
+
+struct gps_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 148;
+  int64_t launches = 0;
+  std::mutex mu;
+  // scratch for one-shot kernels
+  double* part_g = nullptr;
+  double* part_s = nullptr;
+  size_t part_g_elems = 0;
+  double* dvec = nullptr;  // generic device vector scratch
+  size_t dvec_elems = 0;
+};
+
+struct gps_matrix {
+  gps_ctx* ctx = nullptr;
+  int dtype = GPS_F32;
+  int64_t p = 0, n = 0, ld = 0;
+  void* d = nullptr;
+  bool norms_valid = false;
+  int nonfinite = 0;
+  std::vector<double> norms;
+};
+
+
+
+// ------------------------------------------------------------- dispatch
+
+namespace {
+
+using SweepFn = void (*)(SweepArgs);
+
+struct SweepPlan {
+  SweepFn fn = nullptr;
+  int gs = 0, rv = 0, ng = 0;
+  int cols_per_stage = 0, stages = 0;
+  size_t smem = 0;
+  int64_t total_stages = 0;
+  int grid = 0;
+};
+
+template <typename TA, int MODE>
+bool pick_kernel(int ld, SweepFn& fn, int& gs, int& rv) {
+  constexpr int VN = 16 / sizeof(TA);
+#define GPS_TRY(GS_, RV_)                                 \
+  if (ld <= GS_ * RV_ * VN) {                             \
+    fn = su_sweep_kernel<TA, RV_, GS_, MODE>;             \
+    gs = GS_;                                             \
+    rv = RV_;                                             \
+    return true;                                          \
+  }
+  GPS_TRY(32, 1)
+  GPS_TRY(32, 2)
+  GPS_TRY(32, 4)
+  GPS_TRY(64, 4)
+  GPS_TRY(128, 4)
+  GPS_TRY(256, 4)
+  GPS_TRY(256, 8)
+#undef GPS_TRY
+  return false;
+}
+
+std::mutex g_attr_mu;
+std::set<const void*> g_attr_done;
+
+int ensure_smem_attr(const void* fn, size_t smem) {
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  if (g_attr_done.count(fn)) return GPS_OK;
+  GPS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
+  g_attr_done.insert(fn);
+  return GPS_OK;
+}
+
+int make_plan(const gps_matrix* A, int mode, SweepPlan& plan) {
+  bool ok = false;
+  const int ld = static_cast<int>(A->ld);
+  if (A->dtype == GPS_F32) {
+    if (mode == kFused) ok = pick_kernel<float, kFused>(ld, plan.fn, plan.gs, plan.rv);
+    if (mode == kDotOnly) ok = pick_kernel<float, kDotOnly>(ld, plan.fn, plan.gs, plan.rv);
+    if (mode == kCoef) ok = pick_kernel<float, kCoef>(ld, plan.fn, plan.gs, plan.rv);
+  } else {
+    if (mode == kFused) ok = pick_kernel<double, kFused>(ld, plan.fn, plan.gs, plan.rv);
+    if (mode == kDotOnly) ok = pick_kernel<double, kDotOnly>(ld, plan.fn, plan.gs, plan.rv);
+    if (mode == kCoef) ok = pick_kernel<double, kCoef>(ld, plan.fn, plan.gs, plan.rv);
+  }
+  if (!ok)
+    return fail(GPS_E_UNSUPPORTED, "p=%lld exceeds the fused sweep coverage (%d rows for %s)",
+                (long long)A->p, A->dtype == GPS_F32 ? 8192 : 4096, A->dtype == GPS_F32 ? "fp32" : "fp64");
+  const size_t esz = A->dtype == GPS_F32 ? 4 : 8;
+  plan.ng = kSweepThreads / plan.gs;
+  plan.cols_per_stage = plan.ng * kColsPerGroup;
+  const size_t stage_bytes = size_t(plan.cols_per_stage) * A->ld * esz;
+  const size_t red = sweep_red_bytes(plan.ng, plan.gs);
+  int S = static_cast<int>((size_t(kSmemBudget) - red - 8 * 8) / stage_bytes);
+  S = std::min(S, 8);
+  if (S < 2) return fail(GPS_E_UNSUPPORTED, "stage of %zu bytes does not fit shared memory", stage_bytes);
+  plan.stages = S;
+  plan.smem = size_t(S) * stage_bytes + red + size_t(S) * 8;
+  plan.total_stages = ceil_div(A->n, plan.cols_per_stage);
+  plan.grid = static_cast<int>(std::min<int64_t>(A->ctx->num_sms, plan.total_stages));
+  return ensure_smem_attr(reinterpret_cast<const void*>(plan.fn), plan.smem);
+}
+
+int launch_sweep(gps_matrix* A, const SweepPlan& plan, SweepArgs args) {
+  args.A = A->d;
+  args.n = A->n;
+  args.ld = static_cast<int>(A->ld);
+  args.cols_per_stage = plan.cols_per_stage;
+  args.num_stages = plan.stages;
+  args.total_stages = plan.total_stages;
+  plan.fn<<<plan.grid, kSweepThreads, plan.smem, A->ctx->stream>>>(args);
+  A->ctx->launches++;
+  GPS_CHECK_LAUNCH("su_sweep_kernel launch");
+  return GPS_OK;
+}
+
+int launch_reduce(gps_ctx* ctx, const double* part_g, const double* part_s, int nparts, int ld, double* exch,
+                  const GpsCtl* ctl) {
+  const int blocks = (ld + 255) / 256 + 1;
+  su_reduce_kernel<<<blocks, 256, 0, ctx->stream>>>(part_g, part_s, nparts, ld, exch, ctl);
+  ctx->launches++;
+  GPS_CHECK_LAUNCH("su_reduce_kernel launch");
+  return GPS_OK;
+}
+
+int ctx_scratch(gps_ctx* ctx, int64_t ld, int64_t nvec) {
+  const size_t need_g = size_t(ctx->num_sms) * ld;
+  if (ctx->part_g_elems < need_g) {
+    if (ctx->part_g) cudaFree(ctx->part_g);
+    ctx->part_g = nullptr;
+    GPS_CUDA(cudaMalloc(&ctx->part_g, need_g * sizeof(double)));
+    ctx->part_g_elems = need_g;
+  }
+  if (!ctx->part_s) GPS_CUDA(cudaMalloc(&ctx->part_s, size_t(ctx->num_sms) * 4 * sizeof(double)));
+  if (ctx->dvec_elems < size_t(nvec)) {
+    if (ctx->dvec) cudaFree(ctx->dvec);
+    ctx->dvec = nullptr;
+    GPS_CUDA(cudaMalloc(&ctx->dvec, size_t(nvec) * sizeof(double)));
+    ctx->dvec_elems = nvec;
+  }
+  return GPS_OK;
+}
+
+// Row-major (C order) host chunk -> padded column-major device storage.
+template <typename TA>
+__global__ void transpose_rows_kernel(const TA* __restrict__ src, int64_t rows, int64_t n, TA* __restrict__ dst,
+                                      int64_t ld, int64_t row0) {
+  __shared__ TA tile[32][33];
+  const int64_t c0 = int64_t(blockIdx.x) * 32;
+  const int64_t r0 = int64_t(blockIdx.y) * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t r = r0 + i, c = c0 + threadIdx.x;
+    if (r < rows && c < n) tile[i][threadIdx.x] = src[r * n + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t c = c0 + i, r = r0 + threadIdx.x;
+    if (r < rows && c < n) dst[c * ld + row0 + r] = tile[threadIdx.x][i];
+  }
+}
+
+// out[:, i] = A[:, i] - x * c_i  (fp64 result, single_unit.py:296)
+template <typename TA>
+__global__ void deflate_kernel(const TA* __restrict__ A, int64_t n, int64_t ld, const double* __restrict__ x,
+                               const double* __restrict__ c, double* __restrict__ out) {
+  for (int64_t col = blockIdx.x; col < n; col += gridDim.x) {
+    const double ci = c[col];
+    for (int64_t r = threadIdx.x; r < ld; r += blockDim.x)
+      out[col * ld + r] = static_cast<double>(A[col * ld + r]) - x[r] * ci;
+  }
+}
+
+// out[:, j] = A[:, idx[j]] (padded storage copied as is)
+template <typename TA>
+__global__ void gather_columns_kernel(const TA* __restrict__ A, int64_t ld, const int64_t* __restrict__ idx, int64_t k,
+                                      TA* __restrict__ out) {
+  for (int64_t j = blockIdx.x; j < k; j += gridDim.x) {
+    const TA* src = A + idx[j] * ld;
+    for (int64_t r = threadIdx.x; r < ld; r += blockDim.x) out[j * ld + r] = src[r];
+  }
+}
+
+}  // namespace
+
+struct gps_su {
+  gps_matrix* A = nullptr;
+  int penalty = 0;
+  double gamma = 0, tol = 1e-6;
+  int max_iter = 1000;
+  int grid = 0;
+  double* x = nullptr;     // [2][ld]
+  double* w = nullptr;     // [2][n]
+  double* part_g = nullptr;
+  double* part_s = nullptr;
+  double* exch = nullptr;  // ld + 4
+  double* hist = nullptr;  // max_iter + 1
+  GpsCtl* ctl = nullptr;
+  GpsCtl* ctl_host = nullptr;  // pinned
+  cudaGraphExec_t graph = nullptr;
+  int graph_iters = 0;
+  SweepPlan plan;
+  bool exch_external = false;
+  double* defl = nullptr;  // [defl_cap][ld] previous components (implicit deflation)
+  int defl_k = 0, defl_cap = 0;
+};
+
+// ------------------------------------------------------------------ API
+
+extern "C" {
+
+int gps_version(void) { return 1; }
+
+const char* gps_last_error(void) { return g_last_error.c_str(); }
+
+int gps_device_count(int* count) {
+  if (!count) return fail(GPS_E_ARG, "count is NULL");
+  GPS_CUDA(cudaGetDeviceCount(count));
+  return GPS_OK;
+}
+
+int gps_ctx_create(int device, gps_ctx** out) {
+  if (!out) return fail(GPS_E_ARG, "out is NULL");
+  int count = 0;
+  GPS_CUDA(cudaGetDeviceCount(&count));
+  if (device < 0 || device >= count) return fail(GPS_E_ARG, "device %d not in [0, %d)", device, count);
+  int major = 0;
+  GPS_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device));
+  if (major < 10) return fail(GPS_E_UNSUPPORTED, "device %d is sm_%d0; this build targets sm_100a", device, major);
+  GPS_CUDA(cudaSetDevice(device));
+  auto* ctx = new gps_ctx();
+  ctx->device = device;
+  GPS_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
+  cudaError_t e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return cuda_fail(e, "cudaStreamCreate");
+  }
+  ctx->own_stream = true;
+  *out = ctx;
+  return GPS_OK;
+}
+
+int gps_ctx_destroy(gps_ctx* ctx) {
+  if (!ctx) return GPS_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->part_g) cudaFree(ctx->part_g);
+  if (ctx->part_s) cudaFree(ctx->part_s);
+  if (ctx->dvec) cudaFree(ctx->dvec);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return GPS_OK;
+}
+
+int gps_ctx_set_stream(gps_ctx* ctx, void* stream) {
+  if (!ctx) return fail(GPS_E_ARG, "ctx is NULL");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  ctx->stream = static_cast<cudaStream_t>(stream);
+  ctx->own_stream = false;
+  return GPS_OK;
+}
+
+int gps_ctx_sync(gps_ctx* ctx) {
+  if (!ctx) return fail(GPS_E_ARG, "ctx is NULL");
+  GPS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return GPS_OK;
+}
+
+int64_t gps_ctx_launch_count(gps_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+// ---------------------------------------------------------------- matrix
+
+static int matrix_alloc(gps_ctx* ctx, int64_t p, int64_t n, int dtype, gps_matrix** out) {
+  if (!ctx || !out) return fail(GPS_E_ARG, "NULL argument");
+  if (p < 1 || n < 1) return fail(GPS_E_ARG, "matrix must be at least 1x1, got %lldx%lld", (long long)p, (long long)n);
+  if (dtype != GPS_F32 && dtype != GPS_F64) return fail(GPS_E_ARG, "unknown dtype %d", dtype);
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  auto* A = new gps_matrix();
+  A->ctx = ctx;
+  A->dtype = dtype;
+  A->p = p;
+  A->n = n;
+  A->ld = ceil_div(p, 32) * 32;
+  const size_t esz = dtype == GPS_F32 ? 4 : 8;
+  const size_t bytes = size_t(A->ld) * size_t(n) * esz;
+  cudaError_t e = cudaMalloc(&A->d, bytes);
+  if (e != cudaSuccess) {
+    delete A;
+    return cuda_fail(e, "cudaMalloc(A)");
+  }
+  if (A->ld != p) {
+    e = cudaMemsetAsync(A->d, 0, bytes, ctx->stream);
+    if (e != cudaSuccess) {
+      cudaFree(A->d);
+      delete A;
+      return cuda_fail(e, "cudaMemset(A)");
+    }
+  }
+  *out = A;
+  return GPS_OK;
+}
+
+int gps_matrix_create(gps_ctx* ctx, const void* host, int64_t p, int64_t n, int64_t ld_src, int dtype,
+                      gps_matrix** out) {
+  if (!host) return fail(GPS_E_ARG, "host pointer is NULL");
+  if (ld_src < p) return fail(GPS_E_ARG, "ld_src %lld < p %lld", (long long)ld_src, (long long)p);
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  gps_matrix* A = nullptr;
+  int rc = matrix_alloc(ctx, p, n, dtype, &A);
+  if (rc) return rc;
+  const size_t esz = dtype == GPS_F32 ? 4 : 8;
+  cudaError_t e;
+  if (A->ld == ld_src) {
+    e = cudaMemcpyAsync(A->d, host, size_t(ld_src) * n * esz, cudaMemcpyHostToDevice, ctx->stream);
+  } else {
+    e = cudaMemcpy2DAsync(A->d, A->ld * esz, host, ld_src * esz, p * esz, n, cudaMemcpyHostToDevice,
+                          ctx->stream);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) {
+    cudaFree(A->d);
+    delete A;
+    return cuda_fail(e, "upload A");
+  }
+  *out = A;
+  return GPS_OK;
+}
+
+int gps_matrix_create_device(gps_ctx* ctx, const void* dev_src, int64_t p, int64_t n, int64_t ld_src, int dtype,
+                             gps_matrix** out) {
+  if (!dev_src) return fail(GPS_E_ARG, "device pointer is NULL");
+  if (ld_src < p) return fail(GPS_E_ARG, "ld_src %lld < p %lld", (long long)ld_src, (long long)p);
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  gps_matrix* A = nullptr;
+  int rc = matrix_alloc(ctx, p, n, dtype, &A);
+  if (rc) return rc;
+  const size_t esz = dtype == GPS_F32 ? 4 : 8;
+  cudaError_t e = cudaMemcpy2DAsync(A->d, A->ld * esz, dev_src, ld_src * esz, p * esz, n, cudaMemcpyDeviceToDevice,
+                                    ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) {
+    cudaFree(A->d);
+    delete A;
+    return cuda_fail(e, "copy A (device)");
+  }
+  *out = A;
+  return GPS_OK;
+}
+
+int gps_matrix_create_rowmajor(gps_ctx* ctx, const void* host, int64_t p, int64_t n, int dtype, gps_matrix** out) {
+  if (!host) return fail(GPS_E_ARG, "host pointer is NULL");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  gps_matrix* A = nullptr;
+  int rc = matrix_alloc(ctx, p, n, dtype, &A);
+  if (rc) return rc;
+  const size_t esz = dtype == GPS_F32 ? 4 : 8;
+  // stage ~256 MiB of rows at a time
+  int64_t rows = std::max<int64_t>(1, (int64_t(256) << 20) / (n * esz));
+  rows = std::min<int64_t>(rows, p);
+  void* stage = nullptr;
+  cudaError_t e = cudaMalloc(&stage, size_t(rows) * n * esz);
+  for (int64_t r0 = 0; e == cudaSuccess && r0 < p; r0 += rows) {
+    const int64_t rb = std::min<int64_t>(rows, p - r0);
+    e = cudaMemcpyAsync(stage, static_cast<const char*>(host) + size_t(r0) * n * esz, size_t(rb) * n * esz,
+                        cudaMemcpyHostToDevice, ctx->stream);
+    if (e != cudaSuccess) break;
+    dim3 grid(static_cast<unsigned>(ceil_div(n, 32)), static_cast<unsigned>(ceil_div(rb, 32)));
+    dim3 block(32, 8);
+    if (dtype == GPS_F32)
+      transpose_rows_kernel<float><<<grid, block, 0, ctx->stream>>>(static_cast<const float*>(stage), rb, n,
+                                                                    static_cast<float*>(A->d), A->ld, r0);
+    else
+      transpose_rows_kernel<double><<<grid, block, 0, ctx->stream>>>(static_cast<const double*>(stage), rb, n,
+                                                                     static_cast<double*>(A->d), A->ld, r0);
+    ctx->launches++;
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (stage) cudaFree(stage);
+  if (e != cudaSuccess) {
+    cudaFree(A->d);
+    delete A;
+    return cuda_fail(e, "upload A (row-major)");
+  }
+  *out = A;
+  return GPS_OK;
+}
+
+int gps_matrix_destroy(gps_matrix* A) {
+  if (!A) return GPS_OK;
+  cudaSetDevice(A->ctx->device);
+  cudaStreamSynchronize(A->ctx->stream);
+  cudaFree(A->d);
+  delete A;
+  return GPS_OK;
+}
+
+int gps_matrix_info(const gps_matrix* A, int64_t* p, int64_t* n, int64_t* ld, int* dtype) {
+  if (!A) return fail(GPS_E_ARG, "matrix is NULL");
+  if (p) *p = A->p;
+  if (n) *n = A->n;
+  if (ld) *ld = A->ld;
+  if (dtype) *dtype = A->dtype;
+  return GPS_OK;
+}
+
+void* gps_matrix_device_ptr(gps_matrix* A) { return A ? A->d : nullptr; }
+
+int gps_matrix_download(gps_matrix* A, void* host) {
+  if (!A || !host) return fail(GPS_E_ARG, "NULL argument");
+  std::lock_guard<std::mutex> lk(A->ctx->mu);
+  GPS_CUDA(cudaSetDevice(A->ctx->device));
+  const size_t esz = A->dtype == GPS_F32 ? 4 : 8;
+  GPS_CUDA(cudaMemcpy2DAsync(host, A->p * esz, A->d, A->ld * esz, A->p * esz, A->n, cudaMemcpyDeviceToHost,
+                             A->ctx->stream));
+  GPS_CUDA(cudaStreamSynchronize(A->ctx->stream));
+  return GPS_OK;
+}
+
+int gps_matrix_column(gps_matrix* A, int64_t i, double* out) {
+  if (!A || !out) return fail(GPS_E_ARG, "NULL argument");
+  if (i < 0 || i >= A->n) return fail(GPS_E_ARG, "column %lld out of range", (long long)i);
+  std::lock_guard<std::mutex> lk(A->ctx->mu);
+  GPS_CUDA(cudaSetDevice(A->ctx->device));
+  const size_t esz = A->dtype == GPS_F32 ? 4 : 8;
+  std::vector<unsigned char> buf(A->p * esz);
+  GPS_CUDA(cudaMemcpyAsync(buf.data(), static_cast<const char*>(A->d) + size_t(i) * A->ld * esz, A->p * esz,
+                           cudaMemcpyDeviceToHost, A->ctx->stream));
+  GPS_CUDA(cudaStreamSynchronize(A->ctx->stream));
+  for (int64_t r = 0; r < A->p; ++r)
+    out[r] = A->dtype == GPS_F32 ? double(reinterpret_cast<float*>(buf.data())[r])
+                                 : reinterpret_cast<double*>(buf.data())[r];
+  return GPS_OK;
+}
+
+int gps_column_norms(gps_matrix* A, double* norms_out, int* nonfinite_out) {
+  if (!A) return fail(GPS_E_ARG, "matrix is NULL");
+  gps_ctx* ctx = A->ctx;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  if (!A->norms_valid) {
+    int rc = ctx_scratch(ctx, A->ld, A->n + 1);
+    if (rc) return rc;
+    int* flag = reinterpret_cast<int*>(ctx->dvec + A->n);
+    GPS_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
+    const int blocks = ctx->num_sms * 8;
+    if (A->dtype == GPS_F32)
+      column_norms_kernel<float><<<blocks, 256, 0, ctx->stream>>>(static_cast<const float*>(A->d), A->n,
+                                                                  static_cast<int>(A->ld), ctx->dvec, flag);
+    else
+      column_norms_kernel<double><<<blocks, 256, 0, ctx->stream>>>(static_cast<const double*>(A->d), A->n,
+                                                                   static_cast<int>(A->ld), ctx->dvec, flag);
+    ctx->launches++;
+    GPS_CHECK_LAUNCH("column_norms_kernel launch");
+    A->norms.resize(A->n);
+    GPS_CUDA(cudaMemcpyAsync(A->norms.data(), ctx->dvec, A->n * sizeof(double), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+    GPS_CUDA(cudaMemcpyAsync(&A->nonfinite, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    GPS_CUDA(cudaStreamSynchronize(ctx->stream));
+    A->norms_valid = true;
+  }
+  if (norms_out) std::memcpy(norms_out, A->norms.data(), A->n * sizeof(double));
+  if (nonfinite_out) *nonfinite_out = A->nonfinite;
+  return GPS_OK;
+}
+
+// --------------------------------------------------------- kernel seam
+
+// One sweep with host inputs/outputs on the context scratch buffers.
+static int one_shot(gps_matrix* A, int mode, const double* x, const double* coef, int coef_threshold, double gamma,
+                    int penalty, double* f_out, double* g_out, double* c_out, double* w_out, int64_t* nnz_out) {
+  if (!A) return fail(GPS_E_ARG, "matrix is NULL");
+  if (penalty != GPS_L1 && penalty != GPS_L0) return fail(GPS_E_ARG, "unknown penalty %d", penalty);
+  gps_ctx* ctx = A->ctx;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  SweepPlan plan;
+  int rc = make_plan(A, mode, plan);
+  if (rc) return rc;
+  // dvec layout: [x (ld)] [coef or c (n)] [exch (ld + 4)] [w (n)]
+  rc = ctx_scratch(ctx, A->ld, A->ld + A->n + A->ld + 4 + A->n);
+  if (rc) return rc;
+  double* dx = ctx->dvec;
+  double* dn = ctx->dvec + A->ld;
+  double* exch = dn + A->n;
+  double* dw = exch + A->ld + 4;
+  if (mode != kCoef) {
+    GPS_CUDA(cudaMemsetAsync(dx, 0, A->ld * sizeof(double), ctx->stream));
+    GPS_CUDA(cudaMemcpyAsync(dx, x, A->p * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  } else {
+    GPS_CUDA(cudaMemcpyAsync(dn, coef, A->n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  }
+  SweepArgs args{};
+  args.penalty = penalty;
+  args.gamma = gamma;
+  args.x = dx;
+  args.coef = dn;
+  args.coef_threshold = coef_threshold;
+  args.part_g = ctx->part_g;
+  args.part_s = ctx->part_s;
+  args.c_out = (c_out && mode != kCoef) ? dn : nullptr;
+  args.w_out = (w_out && mode == kFused) ? dw : nullptr;
+  rc = launch_sweep(A, plan, args);
+  if (rc) return rc;
+  rc = launch_reduce(ctx, ctx->part_g, ctx->part_s, plan.grid, static_cast<int>(A->ld), exch, nullptr);
+  if (rc) return rc;
+  std::vector<double> h(A->ld + 4);
+  GPS_CUDA(cudaMemcpyAsync(h.data(), exch, (A->ld + 4) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  if (c_out && mode != kCoef)
+    GPS_CUDA(cudaMemcpyAsync(c_out, dn, A->n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  if (w_out && mode == kFused)
+    GPS_CUDA(cudaMemcpyAsync(w_out, dw, A->n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  GPS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (g_out) std::memcpy(g_out, h.data(), A->p * sizeof(double));
+  if (f_out) *f_out = h[A->ld];
+  if (nnz_out) *nnz_out = static_cast<int64_t>(h[A->ld + 1]);
+  return GPS_OK;
+}
+
+int gps_matvec_t(gps_matrix* A, const double* x, double* c_out) {
+  if (!x || !c_out) return fail(GPS_E_ARG, "NULL argument");
+  return one_shot(A, kDotOnly, x, nullptr, 0, 0.0, GPS_L1, nullptr, nullptr, c_out, nullptr, nullptr);
+}
+
+int gps_gram_apply(gps_matrix* A, const double* coef, double* out) {
+  if (!coef || !out) return fail(GPS_E_ARG, "NULL argument");
+  return one_shot(A, kCoef, nullptr, coef, 0, 0.0, GPS_L1, nullptr, out, nullptr, nullptr, nullptr);
+}
+
+int gps_threshold_accumulate(gps_matrix* A, const double* c, double gamma, int penalty, double* out) {
+  if (!c || !out) return fail(GPS_E_ARG, "NULL argument");
+  return one_shot(A, kCoef, nullptr, c, 1, gamma, penalty, nullptr, out, nullptr, nullptr, nullptr);
+}
+
+int gps_su_sweep(gps_matrix* A, const double* x, double gamma, int penalty, double* f_out, double* g_half_out,
+                 double* c_out, double* w_out, int64_t* nnz_out) {
+  if (!x) return fail(GPS_E_ARG, "x is NULL");
+  return one_shot(A, kFused, x, nullptr, 0, gamma, penalty, f_out, g_half_out, c_out, w_out, nnz_out);
+}
+
+int gps_matrix_deflate(gps_matrix* A, const double* x, gps_matrix** out) {
+  if (!A || !x || !out) return fail(GPS_E_ARG, "NULL argument");
+  std::vector<double> c(A->n);
+  int rc = gps_matvec_t(A, x, c.data());
+  if (rc) return rc;
+  gps_ctx* ctx = A->ctx;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  gps_matrix* B = nullptr;
+  rc = matrix_alloc(ctx, A->p, A->n, GPS_F64, &B);
+  if (rc) return rc;
+  double* dxc = nullptr;
+  cudaError_t e = cudaMalloc(&dxc, (A->ld + A->n) * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemsetAsync(dxc, 0, A->ld * sizeof(double), ctx->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dxc, x, A->p * sizeof(double), cudaMemcpyHostToDevice, ctx->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(dxc + A->ld, c.data(), A->n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream);
+  if (e == cudaSuccess) {
+    const int blocks = static_cast<int>(std::min<int64_t>(A->n, int64_t(ctx->num_sms) * 16));
+    if (A->dtype == GPS_F32)
+      deflate_kernel<float><<<blocks, 256, 0, ctx->stream>>>(static_cast<const float*>(A->d), A->n, A->ld, dxc,
+                                                             dxc + A->ld, static_cast<double*>(B->d));
+    else
+      deflate_kernel<double><<<blocks, 256, 0, ctx->stream>>>(static_cast<const double*>(A->d), A->n, A->ld, dxc,
+                                                              dxc + A->ld, static_cast<double*>(B->d));
+    ctx->launches++;
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (dxc) cudaFree(dxc);
+  if (e != cudaSuccess) {
+    cudaFree(B->d);
+    delete B;
+    return cuda_fail(e, "gps_matrix_deflate");
+  }
+  *out = B;
+  return GPS_OK;
+}
+
+int gps_matrix_gather(gps_matrix* A, const int64_t* idx, int64_t k, gps_matrix** out) {
+  if (!A || !idx || !out || k < 1) return fail(GPS_E_ARG, "bad gather arguments");
+  for (int64_t j = 0; j < k; ++j)
+    if (idx[j] < 0 || idx[j] >= A->n) return fail(GPS_E_ARG, "column %lld out of range", (long long)idx[j]);
+  gps_ctx* ctx = A->ctx;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  gps_matrix* B = nullptr;
+  int rc = matrix_alloc(ctx, A->p, k, A->dtype, &B);
+  if (rc) return rc;
+  int64_t* didx = nullptr;
+  cudaError_t e = cudaMalloc(&didx, k * sizeof(int64_t));
+  if (e == cudaSuccess) e = cudaMemcpyAsync(didx, idx, k * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream);
+  if (e == cudaSuccess) {
+    const int blocks = static_cast<int>(std::min<int64_t>(k, int64_t(ctx->num_sms) * 16));
+    if (A->dtype == GPS_F32)
+      gather_columns_kernel<float><<<blocks, 256, 0, ctx->stream>>>(static_cast<const float*>(A->d), A->ld, didx, k,
+                                                                    static_cast<float*>(B->d));
+    else
+      gather_columns_kernel<double><<<blocks, 256, 0, ctx->stream>>>(static_cast<const double*>(A->d), A->ld, didx,
+                                                                     k, static_cast<double*>(B->d));
+    ctx->launches++;
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (didx) cudaFree(didx);
+  if (e != cudaSuccess) {
+    cudaFree(B->d);
+    delete B;
+    return cuda_fail(e, "gps_matrix_gather");
+  }
+  *out = B;
+  return GPS_OK;
+}
+
+// ----------------------------------------------------- single-unit loop
+
+int gps_su_create(gps_matrix* A, int penalty, double gamma, double tol, int max_iter, gps_su** out) {
+  if (!A || !out) return fail(GPS_E_ARG, "NULL argument");
+  if (penalty != GPS_L1 && penalty != GPS_L0) return fail(GPS_E_ARG, "unknown penalty %d", penalty);
+  if (!(tol >= 0)) return fail(GPS_E_ARG, "tol must be >= 0 (0 disables the tolerance test)");
+  if (max_iter < 1) return fail(GPS_E_ARG, "max_iter must be >= 1");
+  if (!(gamma >= 0)) return fail(GPS_E_ARG, "gamma must be >= 0");
+  gps_ctx* ctx = A->ctx;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  SweepPlan plan;
+  int rc = make_plan(A, kFused, plan);
+  if (rc) return rc;
+  auto* s = new gps_su();
+  s->A = A;
+  s->penalty = penalty;
+  s->gamma = gamma;
+  s->tol = tol;
+  s->max_iter = max_iter;
+  s->grid = plan.grid;
+  s->plan = plan;
+  cudaError_t e = cudaSuccess;
+  auto alloc = [&](double** p, size_t elems) {
+    if (e == cudaSuccess) e = cudaMalloc(p, elems * sizeof(double));
+  };
+  alloc(&s->x, 2 * A->ld);
+  alloc(&s->w, 2 * A->n);
+  alloc(&s->part_g, size_t(plan.grid) * A->ld);
+  alloc(&s->part_s, size_t(plan.grid) * 4);
+  alloc(&s->exch, A->ld + 4);
+  alloc(&s->hist, size_t(max_iter) + 1);
+  if (e == cudaSuccess) e = cudaMalloc(&s->ctl, sizeof(GpsCtl));
+  if (e == cudaSuccess) e = cudaMallocHost(&s->ctl_host, sizeof(GpsCtl));
+  if (e == cudaSuccess) e = cudaMemsetAsync(s->x, 0, 2 * A->ld * sizeof(double), ctx->stream);
+  if (e != cudaSuccess) {
+    gps_su_destroy(s);
+    return cuda_fail(e, "gps_su_create allocation");
+  }
+  *out = s;
+  return GPS_OK;
+}
+
+int gps_su_destroy(gps_su* s) {
+  if (!s) return GPS_OK;
+  cudaSetDevice(s->A->ctx->device);
+  cudaStreamSynchronize(s->A->ctx->stream);
+  if (s->graph) cudaGraphExecDestroy(s->graph);
+  cudaFree(s->x);
+  cudaFree(s->w);
+  cudaFree(s->part_g);
+  cudaFree(s->part_s);
+  if (!s->exch_external) cudaFree(s->exch);
+  cudaFree(s->hist);
+  cudaFree(s->ctl);
+  if (s->defl) cudaFree(s->defl);
+  if (s->ctl_host) cudaFreeHost(s->ctl_host);
+  delete s;
+  return GPS_OK;
+}
+
+int gps_su_start(gps_su* s, const double* x0) {
+  if (!s || !x0) return fail(GPS_E_ARG, "NULL argument");
+  gps_ctx* ctx = s->A->ctx;
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  GPS_CUDA(cudaMemcpyAsync(s->x, x0, s->A->p * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  std::memset(s->ctl_host, 0, sizeof(GpsCtl));
+  GPS_CUDA(cudaMemcpyAsync(s->ctl, s->ctl_host, sizeof(GpsCtl), cudaMemcpyHostToDevice, ctx->stream));
+  GPS_CUDA(cudaStreamSynchronize(ctx->stream));  // x0 / ctl_host are caller / reused buffers
+  return GPS_OK;
+}
+
+static int su_enqueue_sweep_nolock(gps_su* s, int mask = 3) {
+  const SweepPlan& plan = s->plan;
+  int rc = GPS_OK;
+  SweepArgs args{};
+  args.penalty = s->penalty;
+  args.gamma = s->gamma;
+  args.x = s->x;
+  args.x_stride = s->A->ld;
+  args.part_g = s->part_g;
+  args.part_s = s->part_s;
+  args.w_out = s->w;
+  args.w_stride = s->A->n;
+  args.ctl = s->ctl;
+  if (mask & 1) rc = launch_sweep(s->A, plan, args);
+  if (rc) return rc;
+  if (mask & 2)
+    rc = launch_reduce(s->A->ctx, s->part_g, s->part_s, plan.grid, static_cast<int>(s->A->ld), s->exch, s->ctl);
+  return rc;
+}
+
+static int su_enqueue_step_nolock(gps_su* s) {
+  gps_ctx* ctx = s->A->ctx;
+  su_step_kernel<<<1, kStepThreads, 0, ctx->stream>>>(s->exch, static_cast<int>(s->A->ld), s->x, s->A->ld, s->hist,
+                                                      s->ctl, s->tol, s->max_iter, s->defl, s->defl_k);
+  ctx->launches++;
+  GPS_CHECK_LAUNCH("su_step_kernel launch");
+  return GPS_OK;
+}
+
+int gps_su_set_deflation(gps_su* s, const double* X, int k) {
+  if (!s || (k > 0 && !X) || k < 0) return fail(GPS_E_ARG, "bad deflation arguments");
+  gps_ctx* ctx = s->A->ctx;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  if (k > s->defl_cap) {
+    if (s->defl) cudaFree(s->defl);
+    s->defl = nullptr;
+    GPS_CUDA(cudaMalloc(&s->defl, size_t(k) * s->A->ld * sizeof(double)));
+    s->defl_cap = k;
+    if (s->graph) cudaGraphExecDestroy(s->graph);  // captured pointer changed
+    s->graph = nullptr;
+  }
+  if (k > 0) {
+    GPS_CUDA(cudaMemsetAsync(s->defl, 0, size_t(k) * s->A->ld * sizeof(double), ctx->stream));
+    GPS_CUDA(cudaMemcpy2DAsync(s->defl, s->A->ld * sizeof(double), X, s->A->p * sizeof(double),
+                               s->A->p * sizeof(double), k, cudaMemcpyHostToDevice, ctx->stream));
+    GPS_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  if (k != s->defl_k && s->graph) {
+    cudaGraphExecDestroy(s->graph);  // captured scalar changed
+    s->graph = nullptr;
+  }
+  s->defl_k = k;
+  return GPS_OK;
+}
+
+int gps_su_enqueue_sweep(gps_su* s) {
+  if (!s) return fail(GPS_E_ARG, "NULL argument");
+  GPS_CUDA(cudaSetDevice(s->A->ctx->device));
+  return su_enqueue_sweep_nolock(s);
+}
+
+int gps_su_enqueue_step(gps_su* s) {
+  if (!s) return fail(GPS_E_ARG, "NULL argument");
+  GPS_CUDA(cudaSetDevice(s->A->ctx->device));
+  return su_enqueue_step_nolock(s);
+}
+
+int gps_su_enqueue(gps_su* s, int mask) {
+  if (!s) return fail(GPS_E_ARG, "NULL argument");
+  GPS_CUDA(cudaSetDevice(s->A->ctx->device));
+  int rc = GPS_OK;
+  if (mask & 3) rc = su_enqueue_sweep_nolock(s, mask & 3);
+  if (rc == GPS_OK && (mask & 4)) rc = su_enqueue_step_nolock(s);
+  return rc;
+}
+
+int gps_su_set_exchange(gps_su* s, void* dev_ptr) {
+  if (!s || !dev_ptr) return fail(GPS_E_ARG, "NULL argument");
+  if (!s->exch_external) cudaFree(s->exch);
+  s->exch = static_cast<double*>(dev_ptr);
+  s->exch_external = true;
+  if (s->graph) cudaGraphExecDestroy(s->graph);
+  s->graph = nullptr;
+  return GPS_OK;
+}
+
+int gps_su_exchange(gps_su* s, void** dev_ptr, int64_t* count) {
+  if (!s) return fail(GPS_E_ARG, "NULL argument");
+  if (dev_ptr) *dev_ptr = s->exch;
+  if (count) *count = s->A->ld + 4;
+  return GPS_OK;
+}
+
+int gps_su_poll(gps_su* s, int* done, int* iter, int* converged) {
+  if (!s) return fail(GPS_E_ARG, "NULL argument");
+  gps_ctx* ctx = s->A->ctx;
+  GPS_CUDA(cudaMemcpyAsync(s->ctl_host, s->ctl, sizeof(GpsCtl), cudaMemcpyDeviceToHost, ctx->stream));
+  GPS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (done) *done = s->ctl_host->done;
+  if (iter) *iter = s->ctl_host->iter;
+  if (converged) *converged = s->ctl_host->converged;
+  return GPS_OK;
+}
+
+int gps_su_launches_per_iter(gps_su* s) { return s ? 3 : 0; }
+
+int gps_su_run(gps_su* s, int poll_every) {
+  if (!s) return fail(GPS_E_ARG, "NULL argument");
+  if (poll_every < 1) poll_every = 1;
+  gps_ctx* ctx = s->A->ctx;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  if (!s->graph || s->graph_iters != poll_every) {
+    if (s->graph) cudaGraphExecDestroy(s->graph);
+    s->graph = nullptr;
+    cudaGraph_t g = nullptr;
+    GPS_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    int rc = GPS_OK;
+    const int64_t before = ctx->launches;
+    for (int i = 0; i < poll_every && rc == GPS_OK; ++i) {
+      rc = su_enqueue_sweep_nolock(s);
+      if (rc == GPS_OK) rc = su_enqueue_step_nolock(s);
+    }
+    ctx->launches = before;  // captured, not launched
+    cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+    e = cudaGraphInstantiate(&s->graph, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+    s->graph_iters = poll_every;
+  }
+  const int max_chunks = (s->max_iter + 1 + poll_every - 1) / poll_every + 1;
+  for (int c = 0; c < max_chunks; ++c) {
+    GPS_CUDA(cudaGraphLaunch(s->graph, ctx->stream));
+    ctx->launches += int64_t(3) * poll_every;
+    GPS_CUDA(cudaMemcpyAsync(s->ctl_host, s->ctl, sizeof(GpsCtl), cudaMemcpyDeviceToHost, ctx->stream));
+    GPS_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (s->ctl_host->done) return GPS_OK;
+  }
+  return fail(GPS_E_CUDA, "power loop did not reach its stopping rule within max_iter");
+}
+
+int gps_su_result(gps_su* s, double* x_out, double* hist_out, int* n_hist, int* converged, double* w_out,
+                  double* w_sumsq_out) {
+  if (!s) return fail(GPS_E_ARG, "NULL argument");
+  gps_ctx* ctx = s->A->ctx;
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  GpsCtl c;
+  GPS_CUDA(cudaMemcpyAsync(s->ctl_host, s->ctl, sizeof(GpsCtl), cudaMemcpyDeviceToHost, ctx->stream));
+  GPS_CUDA(cudaStreamSynchronize(ctx->stream));
+  c = *s->ctl_host;
+  if (!c.done) return fail(GPS_E_ARG, "loop has not finished");
+  const int k = c.iter;
+  if (x_out)
+    GPS_CUDA(cudaMemcpyAsync(x_out, s->x + (k & 1) * s->A->ld, s->A->p * sizeof(double), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+  if (hist_out)
+    GPS_CUDA(cudaMemcpyAsync(hist_out, s->hist, size_t(k + 1) * sizeof(double), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+  if (w_out)
+    GPS_CUDA(cudaMemcpyAsync(w_out, s->w + (k & 1) * s->A->n, s->A->n * sizeof(double), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+  double s2 = 0.0;
+  GPS_CUDA(cudaMemcpyAsync(&s2, s->exch + s->A->ld + 2, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  GPS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (n_hist) *n_hist = k + 1;
+  if (converged) *converged = c.converged;
+  if (w_sumsq_out) *w_sumsq_out = s2;
+  return GPS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,201 @@
+"""Column-sharded GP-SPCA across GPUs (one process per GPU).
+
+SURVEY §8(e): A is split by columns -- rank r owns the contiguous block
+[offset_r, offset_r + n_r) -- so every column's correlation, threshold,
+objective term and rank-1 update stay local.  The only exchange per power
+iteration is ONE all-reduce (sum) of the exchange vector
+[g (ld) | f | nnz | sum w^2 | 0] produced by each rank's sweep + local
+reduction; every rank then runs the identical step kernel on identical
+data, so no second exchange is needed.  Per solve: a max all-reduce for the
+activation limit, an all-gather of (max norm, global index) for the
+max-norm-column start plus a broadcast of the winning column, and a sum
+all-reduce of ||w||^2 for the recovery normalisation.
+
+Plumbing is torch.distributed (NCCL on GPUs over NVLink; gloo in the CPU
+tests); the arithmetic is libgpspca_b200 on each rank's device.  The loop
+driver is written against a small "shard loop" protocol so the CPU tests
+can drive it with gloo and a test-side loop.
+"""
+
+import time
+
+import numpy as np
+
+from . import _native
+from .core import RunReport, SparseLoadings
+from .single_unit import PowerLoop, _check_unit, _random_unit
+
+
+def column_partition(n, world):
+    """Contiguous, balanced column blocks: [(offset, count)] per rank."""
+    if world < 1 or n < world:
+        raise ValueError(f"cannot split {n} columns over {world} ranks")
+    bounds = [n * r // world for r in range(world + 1)]
+    return [(bounds[r], bounds[r + 1] - bounds[r]) for r in range(world)]
+
+
+class DeviceShardLoop:
+    """PowerLoop on this rank's shard with a torch-owned exchange buffer
+    (so torch.distributed can all-reduce it in place on the same stream)."""
+
+    def __init__(self, A_local, penalty, gamma, tol, max_iter):
+        import torch
+
+        self.A = A_local
+        self.loop = PowerLoop(A_local, penalty, gamma, tol, max_iter)
+        n_exch = _native.C.c_int64()
+        _native.check(_native.lib().gps_su_exchange(self.loop.handle, None, _native.C.byref(n_exch)))
+        dev = torch.device("cuda", A_local.context.device)
+        self.buf = torch.zeros(n_exch.value, dtype=torch.float64, device=dev)
+        _native.check(_native.lib().gps_su_set_exchange(self.loop.handle, _native.C.c_void_p(self.buf.data_ptr())))
+        A_local.context.set_stream(torch.cuda.current_stream(dev).cuda_stream)
+
+    def start(self, x0):
+        self.loop.start(x0)
+
+    def enqueue_sweep(self):
+        _native.check(_native.lib().gps_su_enqueue_sweep(self.loop.handle))
+
+    def exchange(self):
+        return self.buf
+
+    def enqueue_step(self):
+        _native.check(_native.lib().gps_su_enqueue_step(self.loop.handle))
+
+    def poll(self):
+        d, it, cv = _native.C.c_int(), _native.C.c_int(), _native.C.c_int()
+        _native.check(_native.lib().gps_su_poll(self.loop.handle, _native.C.byref(d), _native.C.byref(it),
+                                                _native.C.byref(cv)))
+        return bool(d.value), it.value, bool(cv.value)
+
+    def result(self):
+        return self.loop.result()
+
+
+def run_sharded_loop(loop, x0, all_reduce, poll_every=8, max_iter=1000):
+    """Drive a shard loop to its stopping rule: per iteration sweep ->
+    all_reduce(exchange) -> step; poll the control block every chunk."""
+    loop.start(x0)
+    for _ in range(max_iter // poll_every + 2):
+        for _ in range(poll_every):
+            loop.enqueue_sweep()
+            all_reduce(loop.exchange())
+            loop.enqueue_step()
+        done, _, _ = loop.poll()
+        if done:
+            return loop.result()
+    raise RuntimeError("sharded power loop did not stop within max_iter")
+
+
+class Comm:
+    """The four collectives the sharded solve needs, over torch.distributed."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def all_reduce_sum(self, t):
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+
+    def _host(self, arr, like=None):
+        import torch
+
+        return torch.as_tensor(np.asarray(arr, dtype=np.float64), device=like if like is not None else "cpu")
+
+    def max_scalar(self, v, device="cpu"):
+        import torch
+
+        t = torch.tensor([float(v)], dtype=torch.float64, device=device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())
+
+    def sum_scalar(self, v, device="cpu"):
+        import torch
+
+        t = torch.tensor([float(v)], dtype=torch.float64, device=device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        return float(t.item())
+
+    def all_gather_vec(self, v, device="cpu"):
+        import torch
+
+        t = torch.as_tensor(np.asarray(v, dtype=np.float64)).to(device)
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return [o.cpu().numpy() for o in out]
+
+    def broadcast_vec(self, v, src, size, device="cpu"):
+        import torch
+
+        t = (torch.as_tensor(np.asarray(v, dtype=np.float64)) if v is not None
+             else torch.empty(size, dtype=torch.float64)).to(device)
+        self.dist.broadcast(t, src=src, group=self.group)
+        return t.cpu().numpy()
+
+
+def global_max_norm_start(norms_local, offset, column_fn, comm, p, device="cpu"):
+    """max_norm_column init across shards (single_unit.py:151-153): the
+    largest norm wins, ties go to the lowest GLOBAL index."""
+    i_loc = int(np.argmax(norms_local))
+    cand = comm.all_gather_vec([norms_local[i_loc], offset + i_loc], device)
+    best_val = max(c[0] for c in cand)
+    owner = min(r for r, c in enumerate(cand) if c[0] == best_val and
+                c[1] == min(cc[1] for cc in cand if cc[0] == best_val))
+    col = column_fn(int(cand[owner][1]) - offset) if comm.rank == owner else None
+    col = comm.broadcast_vec(col, owner, p, device)
+    return col / best_val, best_val
+
+
+def solve_single_unit_sharded(A_local, config, offset, n_global, comm=None, loop_factory=None,
+                              device="cpu", poll_every=8):
+    """Sharded drop-in for solve_single_unit (single_unit.py:184-210).
+
+    A_local: this rank's DataMatrix (or a test stand-in exposing .norms,
+    .column(i), .p, .n).  Returns (SparseLoadings over ALL n_global columns,
+    RunReport) on every rank."""
+    comm = comm or Comm()
+    if config.mode != "single_unit" or config.m != 1:
+        raise ValueError("solve_single_unit_sharded handles mode='single_unit', m=1")
+    if config.refine or config.restarts != 1:
+        raise NotImplementedError("restarts/refine are single-device features")
+    gamma = float(config.gamma[0])
+    start = time.perf_counter()
+    top = comm.max_scalar(float(np.max(A_local.norms)), device)
+    limit = top if config.penalty == "l1" else top * top
+    if gamma >= limit:
+        z = np.zeros(n_global)
+        loadings = SparseLoadings(z)
+        return loadings, RunReport([0.0], 0, time.perf_counter() - start, loadings.nnz_per_component(), True,
+                                   [[0.0]])
+    if config.init == "user_supplied":
+        x0 = _check_unit(config.x0, A_local.p)
+    elif config.init == "random_orthonormal":
+        x0 = _random_unit(np.random.default_rng(config.seed), A_local.p)
+    else:
+        x0, _ = global_max_norm_start(A_local.norms, offset, A_local.column, comm, A_local.p, device)
+    factory = loop_factory or DeviceShardLoop
+    loop = factory(A_local, config.penalty, gamma, config.tol, config.max_iter)
+    x, history, converged, w_local = run_sharded_loop(loop, x0, comm.all_reduce_sum, poll_every, config.max_iter)
+    s2 = comm.sum_scalar(float(w_local @ w_local), device)
+    z_local = w_local / np.sqrt(s2) if s2 > 0 else w_local
+    z = _gather_ragged(comm, z_local, offset, n_global, device)
+    loadings = SparseLoadings(z)
+    return loadings, RunReport(history, len(history) - 1, time.perf_counter() - start,
+                               loadings.nnz_per_component(), converged, [history])
+
+
+def _gather_ragged(comm, z_local, offset, n_global, device):
+    """All-gather for unequal shards: pad to the largest shard."""
+    kmax = int(comm.max_scalar(len(z_local), device))
+    buf = np.zeros(kmax + 2)
+    buf[0], buf[1] = offset, len(z_local)
+    buf[2:2 + len(z_local)] = z_local
+    z = np.zeros(n_global)
+    for part in comm.all_gather_vec(buf, device):
+        o, k = int(part[0]), int(part[1])
+        z[o:o + k] = part[2:2 + k]
+    return z

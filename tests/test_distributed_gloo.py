@@ -1,0 +1,173 @@
+"""World-size-2 gloo tests of the column-sharded solve driver (CPU only).
+
+The device shard loop is replaced by a test-side loop that restates the
+device semantics (sweep -> exchange vector [g | f | nnz | sum w^2 | 0] ->
+step) on the rank's NumPy shard; everything else -- partitioning, the
+global max-norm start with lowest-global-index ties, the activation-limit
+max, the per-iteration all-reduce, the ||w||^2 all-reduce and the loadings
+gather -- is the product code in paper_1312_6182_b200/distributed.py.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+
+WORLD = 2
+
+
+class OracleShardLoop:
+    def __init__(self, A_local, penalty, gamma, tol, max_iter):
+        self.A = A_local.values
+        self.penalty, self.gamma, self.tol, self.max_iter = penalty, gamma, tol, max_iter
+        self.buf = torch.zeros(self.A.shape[0] + 4, dtype=torch.float64)
+
+    def start(self, x0):
+        self.x = np.array(x0, dtype=np.float64)
+        self.k, self.done, self.conv, self.f_prev, self.hist = 0, False, False, 0.0, []
+        self.w = np.zeros(self.A.shape[1])
+
+    def enqueue_sweep(self):
+        if self.done:
+            return
+        c = self.A.T @ self.x
+        self.w = oracle.threshold(c, self.gamma, self.penalty)
+        g = self.A @ self.w
+        vec = np.concatenate([g, [oracle.su_objective(c, self.gamma, self.penalty),
+                                  np.count_nonzero(self.w), self.w @ self.w, 0.0]])
+        self.buf.copy_(torch.from_numpy(vec))
+
+    def exchange(self):
+        return self.buf
+
+    def enqueue_step(self):
+        if self.done:
+            return
+        v = self.buf.numpy()
+        p = self.A.shape[0]
+        f = float(v[p])
+        self.hist.append(f)
+        if self.k >= 1 and abs(f - self.f_prev) < self.tol * max(abs(self.f_prev), 1e-30):
+            self.done, self.conv = True, True
+            return
+        if self.k >= self.max_iter:
+            self.done = True
+            return
+        g = v[:p]
+        nrm = np.linalg.norm(g)
+        if nrm == 0.0:
+            self.done, self.conv = True, True
+            return
+        self.x = g / nrm
+        self.f_prev = f
+        self.k += 1
+
+    def poll(self):
+        return self.done, self.k, self.conv
+
+    def result(self):
+        return self.x, list(self.hist), self.conv, self.w
+
+
+class HostShard:
+    """Stand-in for a DataMatrix shard: .values/.norms/.column/.p/.n."""
+
+    def __init__(self, values):
+        self.values = np.asfortranarray(values)
+        self.p, self.n = values.shape
+        self.norms = np.linalg.norm(self.values, axis=0)
+
+    def column(self, i):
+        return self.values[:, i].copy()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, port, case, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    try:
+        from paper_1312_6182_b200 import SolverConfig
+        from paper_1312_6182_b200.distributed import Comm, column_partition, solve_single_unit_sharded
+
+        A = case["A"]
+        off, cnt = column_partition(A.shape[1], WORLD)[rank]
+        shard = HostShard(A[:, off:off + cnt])
+        cfg = SolverConfig(penalty=case["penalty"], gamma=case["gamma"], **case.get("cfg", {}))
+        loadings, report = solve_single_unit_sharded(shard, cfg, off, A.shape[1], comm=Comm(),
+                                                     loop_factory=OracleShardLoop, poll_every=3)
+        out[rank] = (loadings.values[:, 0].copy(), list(report.objective_history), report.converged)
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(case):
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(_free_port(), case, out), nprocs=WORLD, join=True)
+    return dict(out)
+
+
+CASES = {
+    "sl1_gauss": dict(seed=0, shape=(60, 301), penalty="l1", rule=lambda nm: 0.1 * nm),
+    "sl0_gauss": dict(seed=1, shape=(40, 500), penalty="l0", rule=lambda nm: (0.15 * nm) ** 2),
+    "sl1_random_init": dict(seed=2, shape=(30, 201), penalty="l1", rule=lambda nm: 0.2 * nm,
+                            cfg=dict(init="random_orthonormal", seed=5)),
+    "inactive": dict(seed=3, shape=(10, 20), penalty="l1", rule=lambda nm: 2.0 * nm),
+}
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_sharded_solve_matches_oracle(name):
+    spec = CASES[name]
+    A = np.random.default_rng(spec["seed"]).standard_normal(spec["shape"])
+    gamma = float(spec["rule"](np.linalg.norm(A, axis=0).max()))
+    case = {"A": A, "penalty": spec["penalty"], "gamma": gamma, "cfg": spec.get("cfg", {})}
+    res = _run(case)
+    cfg = spec.get("cfg", {})
+    z_ref, hist_ref, conv_ref, _ = oracle.su_solve(A, gamma, spec["penalty"], **cfg)
+    for rank in range(WORLD):
+        z, hist, conv = res[rank]
+        assert conv == conv_ref
+        assert len(hist) == len(hist_ref)
+        np.testing.assert_allclose(hist, hist_ref, rtol=1e-12, atol=1e-14)
+        assert np.array_equal(z != 0, z_ref != 0)
+        np.testing.assert_allclose(z, z_ref, rtol=1e-10, atol=1e-12)
+    np.testing.assert_array_equal(res[0][0], res[1][0])
+
+
+def _tie_worker(rank, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    try:
+        from paper_1312_6182_b200.distributed import Comm, global_max_norm_start
+
+        p = 3
+        # both shards hold an equal max-norm column; rank 0's is the lower global index
+        cols = {0: np.array([[0.0, 3.0], [0.0, 4.0], [1.0, 0.0]]), 1: np.array([[5.0, 1.0], [0.0, 0.0], [0.0, 0.0]])}
+        local = cols[rank]
+        norms = np.linalg.norm(local, axis=0)
+        x0, val = global_max_norm_start(norms, rank * 2, lambda i: local[:, i].copy(), Comm(), p)
+        out[rank] = (x0.copy(), val)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_global_max_norm_tie_breaks_to_lowest_index():
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_tie_worker, args=(_free_port(), out), nprocs=WORLD, join=True)
+    for rank in range(WORLD):
+        x0, val = out[rank]
+        assert val == 5.0
+        np.testing.assert_allclose(x0, [0.6, 0.8, 0.0])  # global column 1 (rank 0), not column 2
