@@ -241,7 +241,8 @@ def run_ours(args):
         x0 = A.column(i) / A.norms[i]
 
     # --- device-resident timed loop (tol = 0: every step is a real iteration)
-    stream = torch.cuda.current_stream(dev)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     total = args.warmup + args.steps
     loop = gps.single_unit.PowerLoop(A, "l0", gamma, 0.0, total + 1)
@@ -293,6 +294,9 @@ def run_ours(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         elapsed, sweep_ms = float(t[0]), float(t[1])
     del loop
+    read_ms = _native.C.c_double()
+    _native.check(L.gps_bench_read_stream(A.handle, 5, _native.C.byref(read_ms)))
+    read_peak = p * n_local * 4 / (read_ms.value / 1e3) / 1e9
 
     iters_per_s = args.steps / elapsed
     a_bytes_local = p * n_local * 4
@@ -303,6 +307,7 @@ def run_ours(args):
     # --- end to end through the public API from pinned host memory (N=1 only)
     e2e = None
     if world == 1 and args.e2e_steps > 0:
+        ctx.set_stream(None)
         host = torch.empty((n_local, p), dtype=torch.float32, pin_memory=True)
         host.copy_(At)
         A_host = host.numpy().T  # (p, n) Fortran-ordered view of pinned memory
@@ -346,7 +351,8 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(), "peak_source": peak_src,
                          "kernel": "su_sweep_kernel<float,4,256,kFused>",
-                         "algorithmic_bytes_per_launch": a_bytes_local, "avg_launch_ms": sweep_ms},
+                         "algorithmic_bytes_per_launch": a_bytes_local, "avg_launch_ms": sweep_ms,
+                         "read_stream_gbs": read_peak, "frac_of_read_stream": achieved / read_peak},
             "gpu_launches": launches,
             "clocks": clocks.summary(),
             "e2e": e2e,

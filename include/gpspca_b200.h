@@ -53,7 +53,9 @@ const char* gps_last_error(void);
 int gps_device_count(int* count);
 int gps_ctx_create(int device, gps_ctx** out);
 int gps_ctx_destroy(gps_ctx* ctx);
-/* Use a caller stream (e.g. torch.cuda.current_stream().cuda_stream). */
+/* Use a caller stream (e.g. a torch.cuda.Stream's cuda_stream; not the legacy
+ * default stream, which cannot be graph-captured).  NULL restores a
+ * library-owned stream. */
 int gps_ctx_set_stream(gps_ctx* ctx, void* cuda_stream);
 int gps_ctx_sync(gps_ctx* ctx);
 /* Number of kernels this context launched so far (instrumentation). */
@@ -90,6 +92,9 @@ int gps_matrix_deflate(gps_matrix* A, const double* x, gps_matrix** out);
 /* Columns idx[0..k) as a new matrix (support-restricted power iteration,
  * single_unit.py:219-230 `A.values[:, support]`). */
 int gps_matrix_gather(gps_matrix* A, const int64_t* idx, int64_t k, gps_matrix** out);
+
+/* Instrumentation: mean ms of the K0 read-only streaming pass over A. */
+int gps_bench_read_stream(gps_matrix* A, int iters, double* ms_out);
 
 /* ---- kernel seam: parallel.py:85-142 ----------------------------------- */
 int gps_matvec_t(gps_matrix* A, const double* x, double* c_out);               /* parallel.py:85  */

@@ -45,6 +45,7 @@ SIGNATURES = {
     "gps_column_norms": (C.c_int, [_vp, _dp, _ip]),
     "gps_matrix_deflate": (C.c_int, [_vp, _dp, C.POINTER(_vp)]),
     "gps_matrix_gather": (C.c_int, [_vp, _i64p, _i64, C.POINTER(_vp)]),
+    "gps_bench_read_stream": (C.c_int, [_vp, C.c_int, _dp]),
     "gps_matvec_t": (C.c_int, [_vp, _dp, _dp]),
     "gps_gram_apply": (C.c_int, [_vp, _dp, _dp]),
     "gps_threshold_accumulate": (C.c_int, [_vp, _dp, C.c_double, C.c_int, _dp]),
@@ -131,7 +132,8 @@ class Context:
         check(lib().gps_ctx_sync(self.handle))
 
     def set_stream(self, stream_ptr):
-        check(lib().gps_ctx_set_stream(self.handle, _vp(stream_ptr)))
+        """Adopt a caller CUDA stream (None: back to a library-owned stream)."""
+        check(lib().gps_ctx_set_stream(self.handle, None if stream_ptr is None else _vp(stream_ptr)))
 
     @property
     def launch_count(self):

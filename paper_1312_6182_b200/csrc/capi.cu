@@ -148,15 +148,16 @@ int make_plan(const gps_matrix* A, int mode, SweepPlan& plan) {
     return fail(GPS_E_UNSUPPORTED, "p=%lld exceeds the fused sweep coverage (%d rows for %s)",
                 (long long)A->p, A->dtype == GPS_F32 ? 8192 : 4096, A->dtype == GPS_F32 ? "fp32" : "fp64");
   const size_t esz = A->dtype == GPS_F32 ? 4 : 8;
-  plan.ng = kSweepThreads / plan.gs;
-  plan.cols_per_stage = plan.ng * kColsPerGroup;
+  plan.ng = kSweepWorkers / plan.gs;
+  plan.cols_per_stage = plan.ng * sweep_cols_per_group(plan.rv);
   const size_t stage_bytes = size_t(plan.cols_per_stage) * A->ld * esz;
-  const size_t red = sweep_red_bytes(plan.ng, plan.gs);
-  int S = static_cast<int>((size_t(kSmemBudget) - red - 8 * 8) / stage_bytes);
-  S = std::min(S, 8);
-  if (S < 2) return fail(GPS_E_UNSUPPORTED, "stage of %zu bytes does not fit shared memory", stage_bytes);
+  const size_t red = sweep_red_bytes(plan.ng, plan.gs, sweep_cols_per_group(plan.rv));
+  int S = static_cast<int>((size_t(kSmemBudget) - red - sweep_bar_bytes(0) - 1024) / (stage_bytes + 16));
+  S = std::min(S, 12);
+  if (S < kSweepLag + 2)
+    return fail(GPS_E_UNSUPPORTED, "stage of %zu bytes does not fit shared memory", stage_bytes);
   plan.stages = S;
-  plan.smem = size_t(S) * stage_bytes + red + size_t(S) * 8;
+  plan.smem = size_t(S) * stage_bytes + red + sweep_bar_bytes(S);
   plan.total_stages = ceil_div(A->n, plan.cols_per_stage);
   plan.grid = static_cast<int>(std::min<int64_t>(A->ctx->num_sms, plan.total_stages));
   return ensure_smem_attr(reinterpret_cast<const void*>(plan.fn), plan.smem);
@@ -316,9 +317,16 @@ int gps_ctx_destroy(gps_ctx* ctx) {
 int gps_ctx_set_stream(gps_ctx* ctx, void* stream) {
   if (!ctx) return fail(GPS_E_ARG, "ctx is NULL");
   std::lock_guard<std::mutex> lk(ctx->mu);
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  GPS_CUDA(cudaStreamSynchronize(ctx->stream));
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
-  ctx->stream = static_cast<cudaStream_t>(stream);
   ctx->own_stream = false;
+  if (stream == nullptr) {  // back to a library-owned non-blocking stream
+    GPS_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    ctx->own_stream = true;
+  } else {
+    ctx->stream = static_cast<cudaStream_t>(stream);
+  }
   return GPS_OK;
 }
 
@@ -523,6 +531,42 @@ int gps_column_norms(gps_matrix* A, double* norms_out, int* nonfinite_out) {
   }
   if (norms_out) std::memcpy(norms_out, A->norms.data(), A->n * sizeof(double));
   if (nonfinite_out) *nonfinite_out = A->nonfinite;
+  return GPS_OK;
+}
+
+// Read-only streaming reference: the K0 norms kernel over A, timed with
+// CUDA events (the "measured read-only stream peak" of SURVEY §6).
+int gps_bench_read_stream(gps_matrix* A, int iters, double* ms_out) {
+  if (!A || iters < 1 || !ms_out) return fail(GPS_E_ARG, "bad arguments");
+  gps_ctx* ctx = A->ctx;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  int rc = ctx_scratch(ctx, A->ld, A->n + 1);
+  if (rc) return rc;
+  int* flag = reinterpret_cast<int*>(ctx->dvec + A->n);
+  cudaEvent_t e0, e1;
+  GPS_CUDA(cudaEventCreate(&e0));
+  GPS_CUDA(cudaEventCreate(&e1));
+  const int blocks = ctx->num_sms * 8;
+  float total = 0.f;
+  for (int i = 0; i <= iters; ++i) {
+    GPS_CUDA(cudaEventRecord(e0, ctx->stream));
+    if (A->dtype == GPS_F32)
+      column_norms_kernel<float><<<blocks, 256, 0, ctx->stream>>>(static_cast<const float*>(A->d), A->n,
+                                                                  static_cast<int>(A->ld), ctx->dvec, flag);
+    else
+      column_norms_kernel<double><<<blocks, 256, 0, ctx->stream>>>(static_cast<const double*>(A->d), A->n,
+                                                                   static_cast<int>(A->ld), ctx->dvec, flag);
+    ctx->launches++;
+    GPS_CUDA(cudaEventRecord(e1, ctx->stream));
+    GPS_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    GPS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    if (i > 0) total += ms;  // first launch is a warm-up
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *ms_out = total / iters;
   return GPS_OK;
 }
 

@@ -62,26 +62,82 @@ struct SweepArgs {
   int64_t total_stages;
 };
 
-constexpr int kSweepThreads = 256;
-constexpr int kColsPerGroup = 2;  // K: columns a group handles per stage
+constexpr int kSweepWorkers = 256;                    // 8 worker warps (dots + updates)
+constexpr int kSweepThreads = kSweepWorkers + 64;     // + reducer warp + producer warp
+constexpr int kSweepD = 4;                            // depth of the partial / weight rings
+constexpr int kSweepLag = 1;                          // update of stage t runs at worker iteration t+1
 
-template <int GS>
-__host__ __device__ constexpr int sweep_groups() { return kSweepThreads / GS; }
+// Columns a group handles per stage: 4 (2 when a thread owns 8 vectors of a
+// column, to keep a stage <= 64 KB).
+__host__ __device__ constexpr int sweep_cols_per_group(int rv) { return rv >= 8 ? 2 : 4; }
 
-// Shared memory layout: S stages | reduction scratch | mbarriers.
-__host__ __device__ inline size_t sweep_red_bytes(int ng, int gs) {
-  const int per_group = (gs / 32) * kColsPerGroup > 4 ? (gs / 32) * kColsPerGroup : 4;
-  return size_t(ng) * per_group * sizeof(double);
+// Shared scratch after the ring (doubles): red[D][NG][K][NW] warp partials,
+// wsm[D][NG][K] thresholded weights, sc[NG*K][3] reducer scalars; then the
+// mbarriers full[S], empty[S], pfull[D], wready[D].
+__host__ __device__ inline size_t sweep_red_bytes(int ng, int gs, int k) {
+  return (size_t(kSweepD) * ng * k * (gs / 32) + size_t(kSweepD) * ng * k + size_t(ng) * k * 3) * sizeof(double);
+}
+__host__ __device__ inline size_t sweep_bar_bytes(int stages) { return size_t(2 * stages + 2 * kSweepD) * 8; }
+
+// Warp reduce-scatter of K column partials (K = 2 or 4): each butterfly
+// round halves the set a lane keeps, so afterwards lane l holds the full
+// warp sum of column sweep_owner_col(l) (owners: lanes 32/K * k).  Lanes
+// that end with the same column hold the same bits (commutative adds).
+template <int K>
+__device__ __forceinline__ double warp_reduce_scatter(const double (&d)[K], int lane) {
+  if constexpr (K == 4) {
+    const bool h16 = (lane & 16) != 0;
+    const double s0 = h16 ? d[0] : d[2], s1 = h16 ? d[1] : d[3];
+    const double k0 = h16 ? d[2] : d[0], k1 = h16 ? d[3] : d[1];
+    const double e0 = k0 + __shfl_xor_sync(0xffffffffu, s0, 16);
+    const double e1 = k1 + __shfl_xor_sync(0xffffffffu, s1, 16);
+    const bool h8 = (lane & 8) != 0;
+    double f = (h8 ? e1 : e0) + __shfl_xor_sync(0xffffffffu, h8 ? e0 : e1, 8);
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1) f += __shfl_xor_sync(0xffffffffu, f, o);
+    return f;
+  } else {
+    const bool hi = (lane & 16) != 0;
+    double f = (hi ? d[1] : d[0]) + __shfl_xor_sync(0xffffffffu, hi ? d[0] : d[1], 16);
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) f += __shfl_xor_sync(0xffffffffu, f, o);
+    return f;
+  }
+}
+// Column held by lane l after warp_reduce_scatter<K>.
+template <int K>
+__device__ __forceinline__ int sweep_owner_col(int lane) {
+  return K == 4 ? (((lane >> 4) & 1) << 1) | ((lane >> 3) & 1) : (lane >> 4) & 1;
 }
 
+// K1: the fused sweep, warp-specialised.  Persistent grid (one CTA per SM);
+// CTA b owns the contiguous stage range [b*NS/G, (b+1)*NS/G).  A stage is
+// T = NG*K whole columns -- one contiguous byte range -- moved by ONE
+// bulk-async copy into an S-deep shared-memory ring.
+//   producer warp : refills a slot once the 8 worker warps released it.
+//   worker warps  : a group of GS threads owns one column per k; thread gt
+//                   owns rows {(gt + v*GS)*VN + e} with x resident in
+//                   registers (fp64).  Iteration t: fp64 partial dots of
+//                   stage t (4 independent chains) -> warp reduce-scatter ->
+//                   warp partials to smem -> arrive pfull[t]; then wait for
+//                   the weights of stage t-2 and apply its (rare) rank-1
+//                   updates to the register-resident fp64 partial of g from
+//                   the still-resident tile -> release the slot.
+//   reducer warp  : per stage, sums the warp partials of each column in a
+//                   fixed order, applies threshold / objective (fp64),
+//                   writes c / w if asked, publishes w -> arrive wready.
+// No CTA-wide barrier inside the stream; every hand-off is an mbarrier, and
+// every summation order is fixed (bitwise reproducible run to run).
 template <typename TA, int RV, int GS, int MODE>
 __global__ void __launch_bounds__(kSweepThreads, 1) su_sweep_kernel(const SweepArgs a) {
-  constexpr int NT = kSweepThreads;
-  constexpr int NG = NT / GS;
+  constexpr int NG = kSweepWorkers / GS;
   constexpr int NW = GS / 32;  // warps per group
-  constexpr int K = kColsPerGroup;
+  constexpr int K = sweep_cols_per_group(RV);
+  constexpr int D = kSweepD;
+  constexpr int L = kSweepLag;
   constexpr int VN = Vec16<TA>::N;
-  constexpr int R = RV * VN;  // rows owned by one thread
+  constexpr int R = RV * VN;  // rows owned by one worker thread
+  constexpr int CH = 4;       // independent accumulation chains per column
   using V = typename Vec16<TA>::T;
 
   extern __shared__ __align__(128) unsigned char smem[];
@@ -90,9 +146,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) su_sweep_kernel(const SweepA
   const int parity = a.ctl != nullptr ? (a.ctl->iter & 1) : 0;
 
   const int tid = threadIdx.x;
-  const int grp = tid / GS;
-  const int gt = tid % GS;
-  const int wig = gt / 32;
+  const int warp = tid >> 5;
   const int lane = tid & 31;
   const int S = a.num_stages;
   const int T = a.cols_per_stage;
@@ -101,14 +155,115 @@ __global__ void __launch_bounds__(kSweepThreads, 1) su_sweep_kernel(const SweepA
   const size_t stage_bytes = size_t(T) * col_bytes;
   unsigned char* ring = smem;
   double* red = reinterpret_cast<double*>(smem + size_t(S) * stage_bytes);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(red) + sweep_red_bytes(NG, GS));
+  double* wsm = red + D * NG * K * NW;
+  double* sc = wsm + D * NG * K;
+  uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(red) + sweep_red_bytes(NG, GS, K));
+  uint64_t* empty = full + S;
+  uint64_t* pfull = empty + S;
+  uint64_t* wready = pfull + D;
 
   const int64_t s_begin = a.total_stages * blockIdx.x / gridDim.x;
   const int64_t s_end = a.total_stages * (blockIdx.x + 1) / gridDim.x;
-  const int64_t ns = s_end - s_begin;
-  const unsigned char* Abytes = static_cast<const unsigned char*>(a.A);
+  const int ns = static_cast<int>(s_end - s_begin);  // stages of this CTA (< 2^31)
+  static_assert((kSweepD & (kSweepD - 1)) == 0, "D must be a power of two");
 
-  // Iterate rows owned by this thread: vectors gt, gt+GS, ... of the column.
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kSweepWorkers / 32);
+    }
+    for (int i = 0; i < D; ++i) {
+      mbar_init(&pfull[i], kSweepWorkers / 32);
+      mbar_init(&wready[i], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == kSweepWorkers / 32 + 1) {
+    // ------------------------------------------------------ producer warp
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      const unsigned char* Abytes = static_cast<const unsigned char*>(a.A);
+      int slot = 0;
+      uint32_t ephase = 0;  // parity of the empty[] completion to wait for
+      for (int s = 0; s < ns; ++s) {
+        if (s >= S) mbar_wait_sleep(&empty[slot], ephase);
+        const int64_t col0 = (s_begin + s) * T;
+        const int64_t ncols = (a.n - col0) < T ? (a.n - col0) : int64_t(T);
+        const uint32_t bytes = static_cast<uint32_t>(ncols * col_bytes);
+        mbar_arrive_expect_tx(&full[slot], bytes);
+        bulk_g2s(ring + slot * stage_bytes, Abytes + col0 * col_bytes, bytes, &full[slot], pol);
+        if (++slot == S) {
+          slot = 0;
+          if (s >= S) ephase ^= 1u;
+          else ephase = 0;
+        }
+      }
+    }
+    return;
+  }
+
+  if (warp == kSweepWorkers / 32) {
+    // ------------------------------------------------------- reducer warp
+    const int i = lane;  // (group, k) handled by this lane
+    const bool mine = i < NG * K;
+    const int grp = mine ? i / K : 0;
+    const int k = mine ? i % K : 0;
+    double f_acc = 0.0, nnz_acc = 0.0, s2_acc = 0.0;
+    for (int s = 0; s < ns; ++s) {
+      const int d = s & (D - 1);
+      mbar_wait_sleep(&pfull[d], static_cast<uint32_t>((s / D) & 1));
+      if (mine) {
+        const int64_t col = (s_begin + s) * T + k * NG + grp;
+        double c, w;
+        if (MODE == kCoef) {
+          c = col < a.n ? a.coef[col] : 0.0;
+          w = a.coef_threshold ? threshold_weight(c, a.gamma, a.penalty) : c;
+        } else {
+          const double* q = red + ((d * NG + grp) * K + k) * NW;
+          double t = 0.0;
+#pragma unroll
+          for (int ww = 0; ww < NW; ++ww) t += q[ww];
+          c = t;
+          w = (MODE == kFused) ? threshold_weight(c, a.gamma, a.penalty) : 0.0;
+        }
+        if (col < a.n) {
+          if (MODE != kCoef) f_acc += objective_term(c, a.gamma, a.penalty);
+          if (w != 0.0) {
+            nnz_acc += 1.0;
+            s2_acc = fma(w, w, s2_acc);
+          }
+          if (a.c_out != nullptr) a.c_out[col] = c;
+          if (a.w_out != nullptr) a.w_out[parity * a.w_stride + col] = w;
+        } else {
+          w = 0.0;
+        }
+        wsm[(d * NG + grp) * K + k] = w;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&wready[d]);
+    }
+    if (mine) {
+      sc[i * 3 + 0] = f_acc;
+      sc[i * 3 + 1] = nnz_acc;
+      sc[i * 3 + 2] = s2_acc;
+    }
+    __syncwarp();
+    if (lane < 3) {
+      double t = 0.0;
+      for (int j = 0; j < NG * K; ++j) t += sc[j * 3 + lane];
+      a.part_s[size_t(blockIdx.x) * 4 + lane] = t;
+    }
+    return;
+  }
+
+  // ---------------------------------------------------------- worker warps
+  const int grp = tid / GS;
+  const int gt = tid % GS;
+  const int wig = gt / 32;
+  const bool full_rows = (ld == GS * RV * VN);
+
   double xr[R];
   double gr[R];
   if (MODE != kCoef) {
@@ -123,122 +278,81 @@ __global__ void __launch_bounds__(kSweepThreads, 1) su_sweep_kernel(const SweepA
 #pragma unroll
   for (int r = 0; r < R; ++r) gr[r] = 0.0;
 
-  if (tid == 0) {
-    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  const uint64_t pol = policy_evict_first();
-  auto issue = [&](int64_t s) {
-    const int64_t col0 = (s_begin + s) * T;
-    const int64_t ncols = (a.n - col0) < T ? (a.n - col0) : int64_t(T);
-    const uint32_t bytes = static_cast<uint32_t>(ncols * col_bytes);
-    const int slot = static_cast<int>(s % S);
-    mbar_arrive_expect_tx(&bars[slot], bytes);
-    bulk_g2s(ring + slot * stage_bytes, Abytes + col0 * col_bytes, bytes, &bars[slot], pol);
-  };
-  if (tid == 0) {
-    const int64_t pre = ns < S ? ns : int64_t(S);
-    for (int64_t s = 0; s < pre; ++s) issue(s);
-  }
-
-  double f_acc = 0.0, nnz_acc = 0.0, s2_acc = 0.0;
-
-  for (int64_t s = 0; s < ns; ++s) {
-    const int slot = static_cast<int>(s % S);
-    const uint32_t phase = static_cast<uint32_t>((s / S) & 1);
-    const int64_t col0 = (s_begin + s) * T;
-    mbar_wait(&bars[slot], phase);
-    const TA* tile = reinterpret_cast<const TA*>(ring + slot * stage_bytes);
-
-    TA av[K][R];
-    double dot[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int j = k * NG + grp;
-      const bool valid = col0 + j < a.n && j < T;
-      dot[k] = 0.0;
-      if (MODE != kCoef) {
-#pragma unroll
-        for (int v = 0; v < RV; ++v) {
-          const int r0 = (gt + v * GS) * VN;
-          V q;
-          if (valid && r0 < ld) {
-            q = *reinterpret_cast<const V*>(tile + size_t(j) * ld + r0);
-          } else {
-            q = V{};
-          }
-          Vec16<TA>::unpack(q, &av[k][v * VN]);
-        }
-        double d = 0.0;
-#pragma unroll
-        for (int r = 0; r < R; ++r) d = fma(static_cast<double>(av[k][r]), xr[r], d);
-        dot[k] = d;
+  int fslot = 0, uslot = 0;  // ring slots of stage t and of stage t-L
+  uint32_t fphase = 0;
+  for (int t = 0; t < ns + L; ++t) {
+    if (t < ns) {
+      const int slot = fslot;
+      mbar_wait(&full[slot], fphase);
+      if (++fslot == S) {
+        fslot = 0;
+        fphase ^= 1u;
       }
-    }
-
-    if (MODE != kCoef) {
-#pragma unroll
-      for (int k = 0; k < K; ++k) dot[k] = warp_sum(dot[k]);
-      if (NW > 1) {
-        if (lane == 0) {
-#pragma unroll
-          for (int k = 0; k < K; ++k) red[(grp * NW + wig) * K + k] = dot[k];
-        }
-        if (NG == 1) {
-          __syncthreads();
-        } else {
-          named_bar_sync(1 + grp, GS);
-        }
+      if (MODE != kCoef) {
+        const int64_t col0 = (s_begin + t) * T;
+        const TA* tile = reinterpret_cast<const TA*>(ring + slot * stage_bytes);
+        const bool fast = full_rows && (col0 + T <= a.n);
+        double dot[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          double t = 0.0;
+          const int j = k * NG + grp;
+          const bool valid = col0 + j < a.n;
+          const TA* colp = tile + size_t(j) * ld;
+          double acc[CH];
 #pragma unroll
-          for (int w = 0; w < NW; ++w) t += red[(grp * NW + w) * K + k];
-          dot[k] = t;
-        }
-      }
-    }
-
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int j = k * NG + grp;
-      const int64_t col = col0 + j;
-      const bool valid = col < a.n && j < T;
-      if (!valid) continue;
-      double c;
-      double w;
-      if (MODE == kCoef) {
-        c = a.coef[col];
-        w = a.coef_threshold ? threshold_weight(c, a.gamma, a.penalty) : c;
-      } else {
-        c = dot[k];
-        f_acc += objective_term(c, a.gamma, a.penalty);
-        w = (MODE == kFused) ? threshold_weight(c, a.gamma, a.penalty) : 0.0;
-      }
-      if (gt == 0) {
-        if (a.c_out != nullptr) a.c_out[col] = c;
-        if (a.w_out != nullptr) a.w_out[parity * a.w_stride + col] = w;
-      }
-      if (MODE != kDotOnly && w != 0.0) {
-        nnz_acc += 1.0;
-        s2_acc = fma(w, w, s2_acc);
-        if (MODE == kCoef) {
+          for (int c = 0; c < CH; ++c) acc[c] = 0.0;
 #pragma unroll
           for (int v = 0; v < RV; ++v) {
             const int r0 = (gt + v * GS) * VN;
-            V q = (r0 < ld) ? *reinterpret_cast<const V*>(tile + size_t(j) * ld + r0) : V{};
-            Vec16<TA>::unpack(q, &av[k][v * VN]);
+            V q;
+            if (fast) {
+              q = *reinterpret_cast<const V*>(colp + r0);
+            } else {
+              q = (valid && r0 < ld) ? *reinterpret_cast<const V*>(colp + r0) : V{};
+            }
+            TA e[VN];
+            Vec16<TA>::unpack(q, e);
+#pragma unroll
+            for (int u = 0; u < VN; ++u)
+              acc[(v * VN + u) % CH] = fma(static_cast<double>(e[u]), xr[v * VN + u], acc[(v * VN + u) % CH]);
+          }
+          dot[k] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+        }
+        const double f = warp_reduce_scatter<K>(dot, lane);
+        if ((lane & (32 / K - 1)) == 0) red[(((t & (D - 1)) * NG + grp) * K + sweep_owner_col<K>(lane)) * NW + wig] = f;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pfull[t & (D - 1)]);
+    }
+    if (t >= L) {
+      const int u = t - L;
+      const int d = u & (D - 1);
+      mbar_wait(&wready[d], static_cast<uint32_t>((u / D) & 1));
+      if (MODE != kDotOnly) {
+        const TA* ptile = reinterpret_cast<const TA*>(ring + uslot * stage_bytes);
+        const double* wp = wsm + (d * NG + grp) * K;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const double w = wp[k];
+          if (w != 0.0) {
+            const TA* colp = ptile + size_t(k * NG + grp) * ld;
+#pragma unroll
+            for (int v = 0; v < RV; ++v) {
+              const int r0 = (gt + v * GS) * VN;
+              V q = (full_rows || r0 < ld) ? *reinterpret_cast<const V*>(colp + r0) : V{};
+              TA e[VN];
+              Vec16<TA>::unpack(q, e);
+#pragma unroll
+              for (int uu = 0; uu < VN; ++uu)
+                gr[v * VN + uu] = fma(w, static_cast<double>(e[uu]), gr[v * VN + uu]);
+            }
           }
         }
-#pragma unroll
-        for (int r = 0; r < R; ++r) gr[r] = fma(w, static_cast<double>(av[k][r]), gr[r]);
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[uslot]);
+      if (++uslot == S) uslot = 0;
     }
-
-    __syncthreads();  // ring slot and reduction scratch are free again
-    if (tid == 0 && s + S < ns) issue(s + S);
   }
 
   // ---- epilogue: fixed-order reduction of the NG group partials ----
@@ -253,7 +367,8 @@ __global__ void __launch_bounds__(kSweepThreads, 1) su_sweep_kernel(const SweepA
           if (r0 + e < ld) pg[r0 + e] = gr[v * VN + e];
       }
     } else {
-      double* scratch = reinterpret_cast<double*>(ring);  // pipeline drained
+      named_bar_sync(1, kSweepWorkers);  // all workers done with the ring
+      double* scratch = reinterpret_cast<double*>(ring);
 #pragma unroll
       for (int v = 0; v < RV; ++v) {
         const int r0 = (gt + v * GS) * VN;
@@ -261,28 +376,14 @@ __global__ void __launch_bounds__(kSweepThreads, 1) su_sweep_kernel(const SweepA
         for (int e = 0; e < VN; ++e)
           if (r0 + e < ld) scratch[size_t(grp) * ld + r0 + e] = gr[v * VN + e];
       }
-      __syncthreads();
-      for (int r = tid; r < ld; r += NT) {
+      named_bar_sync(1, kSweepWorkers);
+      for (int r = tid; r < ld; r += kSweepWorkers) {
         double t = 0.0;
 #pragma unroll
         for (int g = 0; g < NG; ++g) t += scratch[size_t(g) * ld + r];
         pg[r] = t;
       }
     }
-  }
-  // scalar partials (every thread of a group holds identical values)
-  __syncthreads();
-  double* sc = red;  // reuse: NG * 3 doubles <= reduction scratch
-  if (gt == 0) {
-    sc[grp * 3 + 0] = f_acc;
-    sc[grp * 3 + 1] = nnz_acc;
-    sc[grp * 3 + 2] = s2_acc;
-  }
-  __syncthreads();
-  if (tid < 3) {
-    double t = 0.0;
-    for (int g = 0; g < NG; ++g) t += sc[g * 3 + tid];
-    a.part_s[size_t(blockIdx.x) * 4 + tid] = t;
   }
 }
 

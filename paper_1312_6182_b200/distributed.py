@@ -48,7 +48,11 @@ class DeviceShardLoop:
         dev = torch.device("cuda", A_local.context.device)
         self.buf = torch.zeros(n_exch.value, dtype=torch.float64, device=dev)
         _native.check(_native.lib().gps_su_set_exchange(self.loop.handle, _native.C.c_void_p(self.buf.data_ptr())))
-        A_local.context.set_stream(torch.cuda.current_stream(dev).cuda_stream)
+        stream = torch.cuda.current_stream(dev)
+        if stream.cuda_stream == 0:  # the legacy default stream cannot be captured; use a side stream
+            stream = torch.cuda.Stream(dev)
+            torch.cuda.set_stream(stream)
+        A_local.context.set_stream(stream.cuda_stream)
 
     def start(self, x0):
         self.loop.start(x0)

@@ -78,7 +78,7 @@ class TestKernelSeam:
 
     k = load_kernels()
 
-    @pytest.fixture(scope="class", params=[np.float64, np.float32], ids=["fp64", "fp32"])
+    @pytest.fixture(params=[np.float64, np.float32], ids=["fp64", "fp32"])
     def A(self, request):
         return _store(case_matrix(self.k), request.param)
 
