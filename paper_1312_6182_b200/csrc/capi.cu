@@ -152,12 +152,13 @@ int make_plan(const gps_matrix* A, int mode, SweepPlan& plan) {
   plan.cols_per_stage = plan.ng * sweep_cols_per_group(plan.rv);
   const size_t stage_bytes = size_t(plan.cols_per_stage) * A->ld * esz;
   const size_t red = sweep_red_bytes(plan.ng, plan.gs, sweep_cols_per_group(plan.rv));
-  int S = static_cast<int>((size_t(kSmemBudget) - red - sweep_bar_bytes(0) - 1024) / (stage_bytes + 16));
+  const size_t pad = sweep_pad_bytes(static_cast<int>(A->ld), plan.gs * plan.rv * int(16 / esz), esz);
+  int S = static_cast<int>((size_t(kSmemBudget) - red - pad - sweep_bar_bytes(0) - 1024) / (stage_bytes + 16));
   S = std::min(S, 12);
   if (S < kSweepLag + 2)
     return fail(GPS_E_UNSUPPORTED, "stage of %zu bytes does not fit shared memory", stage_bytes);
   plan.stages = S;
-  plan.smem = size_t(S) * stage_bytes + red + sweep_bar_bytes(S);
+  plan.smem = size_t(S) * stage_bytes + pad + red + sweep_bar_bytes(S);
   plan.total_stages = ceil_div(A->n, plan.cols_per_stage);
   plan.grid = static_cast<int>(std::min<int64_t>(A->ctx->num_sms, plan.total_stages));
   return ensure_smem_attr(reinterpret_cast<const void*>(plan.fn), plan.smem);

@@ -77,6 +77,11 @@ __host__ __device__ constexpr int sweep_cols_per_group(int rv) { return rv >= 8 
 __host__ __device__ inline size_t sweep_red_bytes(int ng, int gs, int k) {
   return (size_t(kSweepD) * ng * k * (gs / 32) + size_t(kSweepD) * ng * k + size_t(ng) * k * 3) * sizeof(double);
 }
+// Zeroed tail after the ring covering over-reads past the last column.
+__host__ __device__ inline size_t sweep_pad_bytes(int ld, int coverage, size_t esz) {
+  const size_t p = size_t(coverage - ld) * esz;
+  return (p + 127) / 128 * 128;
+}
 __host__ __device__ inline size_t sweep_bar_bytes(int stages) { return size_t(2 * stages + 2 * kSweepD) * 8; }
 
 // Warp reduce-scatter of K column partials (K = 2 or 4): each butterfly
@@ -154,7 +159,8 @@ __global__ void __launch_bounds__(kSweepThreads, 1) su_sweep_kernel(const SweepA
   const size_t col_bytes = size_t(ld) * sizeof(TA);
   const size_t stage_bytes = size_t(T) * col_bytes;
   unsigned char* ring = smem;
-  double* red = reinterpret_cast<double*>(smem + size_t(S) * stage_bytes);
+  double* red = reinterpret_cast<double*>(smem + size_t(S) * stage_bytes +
+                                          sweep_pad_bytes(ld, GS * RV * VN, sizeof(TA)));
   double* wsm = red + D * NG * K * NW;
   double* sc = wsm + D * NG * K;
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(red) + sweep_red_bytes(NG, GS, K));
@@ -167,6 +173,14 @@ __global__ void __launch_bounds__(kSweepThreads, 1) su_sweep_kernel(const SweepA
   const int ns = static_cast<int>(s_end - s_begin);  // stages of this CTA (< 2^31)
   static_assert((kSweepD & (kSweepD - 1)) == 0, "D must be a power of two");
 
+  {
+    // zero the ring and its tail pad so over-reads (rows >= ld of the last
+    // column, columns >= n of a partial stage) only ever see finite values
+    const size_t nbytes = size_t(S) * stage_bytes + sweep_pad_bytes(ld, GS * RV * VN, sizeof(TA));
+    for (size_t off = size_t(tid) * 16; off < nbytes; off += size_t(kSweepThreads) * 16)
+      *reinterpret_cast<uint4*>(ring + off) = make_uint4(0, 0, 0, 0);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
   if (tid == 0) {
     for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], 1);
@@ -262,7 +276,6 @@ __global__ void __launch_bounds__(kSweepThreads, 1) su_sweep_kernel(const SweepA
   const int grp = tid / GS;
   const int gt = tid % GS;
   const int wig = gt / 32;
-  const bool full_rows = (ld == GS * RV * VN);
 
   double xr[R];
   double gr[R];
@@ -289,27 +302,20 @@ __global__ void __launch_bounds__(kSweepThreads, 1) su_sweep_kernel(const SweepA
         fphase ^= 1u;
       }
       if (MODE != kCoef) {
-        const int64_t col0 = (s_begin + t) * T;
+        // Unconditional loads: columns past n in a partial stage and rows past
+        // ld read finite ring contents (zero-filled at entry) and are either
+        // discarded by the reducer or multiplied by x = 0.
         const TA* tile = reinterpret_cast<const TA*>(ring + slot * stage_bytes);
-        const bool fast = full_rows && (col0 + T <= a.n);
         double dot[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          const int j = k * NG + grp;
-          const bool valid = col0 + j < a.n;
-          const TA* colp = tile + size_t(j) * ld;
+          const TA* colp = tile + size_t(k * NG + grp) * ld;
           double acc[CH];
 #pragma unroll
           for (int c = 0; c < CH; ++c) acc[c] = 0.0;
 #pragma unroll
           for (int v = 0; v < RV; ++v) {
-            const int r0 = (gt + v * GS) * VN;
-            V q;
-            if (fast) {
-              q = *reinterpret_cast<const V*>(colp + r0);
-            } else {
-              q = (valid && r0 < ld) ? *reinterpret_cast<const V*>(colp + r0) : V{};
-            }
+            const V q = *reinterpret_cast<const V*>(colp + (gt + v * GS) * VN);
             TA e[VN];
             Vec16<TA>::unpack(q, e);
 #pragma unroll
@@ -338,8 +344,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) su_sweep_kernel(const SweepA
             const TA* colp = ptile + size_t(k * NG + grp) * ld;
 #pragma unroll
             for (int v = 0; v < RV; ++v) {
-              const int r0 = (gt + v * GS) * VN;
-              V q = (full_rows || r0 < ld) ? *reinterpret_cast<const V*>(colp + r0) : V{};
+              const V q = *reinterpret_cast<const V*>(colp + (gt + v * GS) * VN);
               TA e[VN];
               Vec16<TA>::unpack(q, e);
 #pragma unroll
