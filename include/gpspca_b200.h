@@ -46,6 +46,7 @@ enum gps_penalty { GPS_L1 = 0, GPS_L0 = 1 }; /* core.py:13 PENALTIES */
 typedef struct gps_ctx gps_ctx;       /* one device + one stream            */
 typedef struct gps_matrix gps_matrix; /* device-resident DataMatrix         */
 typedef struct gps_su gps_su;         /* single-unit solver state           */
+typedef struct gps_bk gps_bk;         /* block solver state                 */
 
 /* ---- library / context ------------------------------------------------ */
 int gps_version(void);
@@ -141,6 +142,42 @@ int gps_su_result(gps_su* s, double* x_out, double* hist_out, int* n_hist, int* 
                   double* w_sumsq_out);
 /* Kernel launches per power iteration of gps_su_run (instrumentation). */
 int gps_su_launches_per_iter(gps_su* s);
+
+/* ---- block power iteration: block.py:190-235 ---------------------------- */
+/* m <= 64 components; gamma, mu: length m (mu_j > 0, gamma_j >= 0).  Each
+ * iteration runs ceil(m/MG) fused sweeps (MG = 4 for fp32 storage with
+ * p <= 4096, else 2) and the device polar step. */
+int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const double* mu, double tol,
+                  int max_iter, gps_bk** out);
+int gps_bk_destroy(gps_bk* s);
+/* Starts: X0 used as is (p x m column-major, user_supplied, block.py:160-161);
+ * M orthonormalised by device CholeskyQR2 (random_orthonormal, block.py:155,
+ * 162-170); columns idx[0..m) of A, then CholeskyQR2 (max_norm_column,
+ * block.py:157-158).  A rank-deficient start returns GPS_E_ARG. */
+int gps_bk_start(gps_bk* s, const double* X0);
+int gps_bk_start_qr(gps_bk* s, const double* M);
+int gps_bk_start_columns(gps_bk* s, const int64_t* idx);
+int gps_bk_run(gps_bk* s, int poll_every);
+int gps_bk_enqueue_sweep(gps_bk* s);
+int gps_bk_exchange(gps_bk* s, void** dev_ptr, int64_t* count);
+int gps_bk_set_exchange(gps_bk* s, void* dev_ptr);
+int gps_bk_enqueue_step(gps_bk* s);
+int gps_bk_poll(gps_bk* s, int* done, int* iter, int* converged);
+/* X (p x m), history, W of the final sweep (m columns of length n, for
+ * Z_j = W_j / ||W_j||, block.py:174-187), rank_fail = 1 when the polar step
+ * found rank(G) < m at iteration n_hist - 1 (block.py:215-218). */
+int gps_bk_result(gps_bk* s, double* X_out, double* hist_out, int* n_hist, int* converged, double* W_out,
+                  int* rank_fail, int* rank_out);
+/* One-shot block sweep at X (p x m): objective (block.py:80-111), ascent
+ * direction G = 2 mu_j sum_i w a_i (block.py:114-132), optional W (n x m). */
+int gps_bk_sweep(gps_matrix* A, const double* X, int m, const double* gamma, const double* mu, int penalty,
+                 double* f_out, double* G_out, double* W_out);
+/* block.py:135-149 polar_projection on the device: X = G (G'G)^{-1/2};
+ * GPS_E_RANK (rank in *rank_out) when rank(G) < m by the reference rule. */
+int gps_polar(gps_ctx* ctx, const double* G, int64_t p, int m, double* X_out, int* rank_out);
+/* Device CholeskyQR2 of M (p x m): Q with positive-diagonal R (= the
+ * reference's sign-fixed QR, block.py:162-170). */
+int gps_orthonormalize(gps_ctx* ctx, const double* M, int64_t p, int m, double* Q_out);
 
 #ifdef __cplusplus
 }

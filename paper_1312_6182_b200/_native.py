@@ -63,6 +63,21 @@ SIGNATURES = {
     "gps_su_poll": (C.c_int, [_vp, _ip, _ip, _ip]),
     "gps_su_result": (C.c_int, [_vp, _dp, _dp, _ip, _ip, _dp, _dp]),
     "gps_su_launches_per_iter": (C.c_int, [_vp]),
+    "gps_bk_create": (C.c_int, [_vp, C.c_int, C.c_int, _dp, _dp, C.c_double, C.c_int, C.POINTER(_vp)]),
+    "gps_bk_destroy": (C.c_int, [_vp]),
+    "gps_bk_start": (C.c_int, [_vp, _dp]),
+    "gps_bk_start_qr": (C.c_int, [_vp, _dp]),
+    "gps_bk_start_columns": (C.c_int, [_vp, _i64p]),
+    "gps_bk_run": (C.c_int, [_vp, C.c_int]),
+    "gps_bk_enqueue_sweep": (C.c_int, [_vp]),
+    "gps_bk_exchange": (C.c_int, [_vp, C.POINTER(_vp), _i64p]),
+    "gps_bk_set_exchange": (C.c_int, [_vp, _vp]),
+    "gps_bk_enqueue_step": (C.c_int, [_vp]),
+    "gps_bk_poll": (C.c_int, [_vp, _ip, _ip, _ip]),
+    "gps_bk_result": (C.c_int, [_vp, _dp, _dp, _ip, _ip, _dp, _ip, _ip]),
+    "gps_bk_sweep": (C.c_int, [_vp, _dp, C.c_int, _dp, _dp, C.c_int, _dp, _dp, _dp]),
+    "gps_polar": (C.c_int, [_vp, _dp, _i64, C.c_int, _dp, _ip]),
+    "gps_orthonormalize": (C.c_int, [_vp, _dp, _i64, C.c_int, _dp]),
 }
 
 

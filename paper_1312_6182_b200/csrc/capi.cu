@@ -16,7 +16,7 @@
 #include <vector>
 
 #include "../../include/gpspca_b200.h"
-#include "su_kernels.cuh"
+#include "bk_kernels.cuh"
 
 using namespace gps;
 
@@ -962,6 +962,548 @@ int gps_su_result(gps_su* s, double* x_out, double* hist_out, int* n_hist, int* 
   if (n_hist) *n_hist = k + 1;
   if (converged) *converged = c.converged;
   if (w_sumsq_out) *w_sumsq_out = s2;
+  return GPS_OK;
+}
+
+}  // extern "C"
+
+// =====================================================================
+// Block path (reference block.py): fused block sweeps over component
+// groups, device polar step, device CholeskyQR2 initialisation.
+// =====================================================================
+
+namespace {
+
+using BkFn = void (*)(BlockSweepArgs);
+
+struct BkPlan {
+  BkFn fn = nullptr;
+  int gs = 0, rv = 0, ng = 0, mg = 0, k = 0;
+  int cols_per_stage = 0, stages = 0;
+  size_t smem = 0;
+  int64_t total_stages = 0;
+  int grid = 0;
+};
+
+template <typename TA, typename TC>
+bool pick_bk(int ld, BkPlan& pl) {
+  constexpr int VN = 16 / sizeof(TA);
+  constexpr bool F = sizeof(TA) == 4;
+#define GPS_BK(GS_, RV_, MG_)                            \
+  if (ld <= GS_ * RV_ * VN) {                            \
+    pl.fn = bk_sweep_kernel<TA, TC, RV_, GS_, MG_>;      \
+    pl.gs = GS_;                                         \
+    pl.rv = RV_;                                         \
+    pl.mg = MG_;                                         \
+    return true;                                         \
+  }
+  if constexpr (F) {
+    GPS_BK(32, 1, 4)
+    GPS_BK(32, 2, 4)
+    GPS_BK(32, 4, 4)
+    GPS_BK(64, 4, 4)
+    GPS_BK(128, 4, 4)
+    GPS_BK(256, 4, 4)
+    GPS_BK(256, 8, 2)
+  } else {
+    GPS_BK(32, 1, 2)
+    GPS_BK(32, 2, 2)
+    GPS_BK(32, 4, 2)
+    GPS_BK(64, 4, 2)
+    GPS_BK(128, 4, 2)
+    GPS_BK(256, 4, 2)
+    GPS_BK(256, 8, 2)
+  }
+#undef GPS_BK
+  return false;
+}
+
+int make_bk_plan(const gps_matrix* A, BkPlan& pl) {
+  const int ld = static_cast<int>(A->ld);
+  const bool ok = A->dtype == GPS_F32 ? pick_bk<float, float>(ld, pl) : pick_bk<double, double>(ld, pl);
+  if (!ok)
+    return fail(GPS_E_UNSUPPORTED, "p=%lld exceeds the fused block sweep coverage", (long long)A->p);
+  const size_t esz = A->dtype == GPS_F32 ? 4 : 8;
+  pl.ng = kSweepWorkers / pl.gs;
+  pl.k = bk_cols_per_group(pl.rv);
+  pl.cols_per_stage = pl.ng * pl.k;
+  const size_t stage_bytes = size_t(pl.cols_per_stage) * A->ld * esz;
+  const size_t red = bk_red_bytes(pl.ng, pl.gs, pl.k, pl.mg);
+  const size_t pad = sweep_pad_bytes(ld, pl.gs * pl.rv * int(16 / esz), esz);
+  int S = static_cast<int>((size_t(kSmemBudget) - red - pad - sweep_bar_bytes(0) - 1024) / (stage_bytes + 16));
+  S = std::min(S, 12);
+  if (S < kSweepLag + 2) return fail(GPS_E_UNSUPPORTED, "block stage of %zu bytes does not fit", stage_bytes);
+  pl.stages = S;
+  pl.smem = size_t(S) * stage_bytes + pad + red + sweep_bar_bytes(S);
+  pl.total_stages = ceil_div(A->n, pl.cols_per_stage);
+  pl.grid = static_cast<int>(std::min<int64_t>(A->ctx->num_sms, pl.total_stages));
+  return ensure_smem_attr(reinterpret_cast<const void*>(pl.fn), pl.smem);
+}
+
+int ensure_polar_attrs() {
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    err = cudaFuncSetAttribute(bk_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (err == cudaSuccess)
+      err = cudaFuncSetAttribute(polar_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (err == cudaSuccess)
+      err = cudaFuncSetAttribute(cholqr2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  });
+  if (err != cudaSuccess) return cuda_fail(err, "cudaFuncSetAttribute(polar)");
+  return GPS_OK;
+}
+
+constexpr int kMaxBlockM = 64;
+
+}  // namespace
+
+struct gps_bk {
+  gps_matrix* A = nullptr;
+  int penalty = 0, m = 0, mg = 0, ngroups = 0;
+  std::vector<double> gamma, mu;  // length m_pad (padded: gamma 0, mu 1)
+  double tol = 1e-6;
+  int max_iter = 1000;
+  BkPlan plan;
+  double* X = nullptr;      // [2][m_pad][ld]
+  double* W = nullptr;      // [2][m_pad][n]
+  double* part_g = nullptr; // [ngroups][grid][mg][ld]
+  double* part_s = nullptr; // [ngroups][grid][4]
+  double* exch = nullptr;   // [ngroups][mg*ld + 4]
+  bool exch_external = false;
+  double* G = nullptr;      // [m][ld]
+  double* Tm = nullptr;     // [m][ld]
+  double* mu_dev = nullptr; // m
+  double* hist = nullptr;
+  GpsCtl* ctl = nullptr;
+  GpsCtl* ctl_host = nullptr;
+  int* rank_dev = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  int graph_iters = 0;
+  size_t m_pad() const { return size_t(ngroups) * mg; }
+  size_t exch_stride() const { return size_t(mg) * A->ld + 4; }
+};
+
+namespace {
+
+int bk_launch_group(gps_bk* s, int g, bool with_ctl, int write_w) {
+  gps_matrix* A = s->A;
+  const BkPlan& pl = s->plan;
+  BlockSweepArgs a{};
+  a.A = A->d;
+  a.n = A->n;
+  a.ld = static_cast<int>(A->ld);
+  a.penalty = s->penalty;
+  for (int j = 0; j < pl.mg; ++j) {
+    a.gamma[j] = s->gamma[g * pl.mg + j];
+    a.mu[j] = s->mu[g * pl.mg + j];
+  }
+  a.X = s->X + size_t(g) * pl.mg * A->ld;
+  a.x_stride = int64_t(s->m_pad()) * A->ld;
+  a.part_g = s->part_g + size_t(g) * pl.grid * pl.mg * A->ld;
+  a.part_s = s->part_s + size_t(g) * pl.grid * 4;
+  a.w_out = write_w ? s->W + size_t(g) * pl.mg * A->n : nullptr;
+  a.w_stride = int64_t(s->m_pad()) * A->n;
+  a.w_cstride = A->n;
+  a.ctl = with_ctl ? s->ctl : nullptr;
+  a.cols_per_stage = pl.cols_per_stage;
+  a.num_stages = pl.stages;
+  a.total_stages = pl.total_stages;
+  pl.fn<<<pl.grid, kSweepThreads, pl.smem, A->ctx->stream>>>(a);
+  A->ctx->launches++;
+  GPS_CHECK_LAUNCH("bk_sweep_kernel launch");
+  double* ex = s->exch + size_t(g) * s->exch_stride();
+  return launch_reduce(A->ctx, a.part_g, a.part_s, pl.grid, pl.mg * static_cast<int>(A->ld), ex,
+                       with_ctl ? s->ctl : nullptr);
+}
+
+int bk_enqueue_sweeps(gps_bk* s, bool with_ctl) {
+  for (int g = 0; g < s->ngroups; ++g) {
+    int rc = bk_launch_group(s, g, with_ctl, 1);
+    if (rc) return rc;
+  }
+  return GPS_OK;
+}
+
+int bk_enqueue_step(gps_bk* s) {
+  gps_ctx* ctx = s->A->ctx;
+  bk_step_kernel<<<1, kPolarThreads, polar_smem_bytes(s->m), ctx->stream>>>(
+      s->exch, s->ngroups, s->mg, static_cast<int>(s->A->ld), static_cast<int>(s->A->p), s->m, s->mu_dev, s->X,
+      int64_t(s->m_pad()) * s->A->ld, s->G, s->Tm, s->hist, s->ctl, s->tol, s->max_iter, s->rank_dev);
+  ctx->launches++;
+  GPS_CHECK_LAUNCH("bk_step_kernel launch");
+  return GPS_OK;
+}
+
+// Orthonormalise M (device, [m][ld]) into X slot 0 with CholeskyQR2.
+int bk_qr_into_x(gps_bk* s, double* Mdev) {
+  gps_ctx* ctx = s->A->ctx;
+  cholqr2_kernel<<<1, kPolarThreads, size_t(2) * s->m * s->m * sizeof(double) + 64, ctx->stream>>>(
+      Mdev, s->X, static_cast<int>(s->A->ld), s->m, s->rank_dev);
+  ctx->launches++;
+  GPS_CHECK_LAUNCH("cholqr2_kernel launch");
+  int st = 0;
+  GPS_CUDA(cudaMemcpyAsync(&st, s->rank_dev, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  GPS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (st != 0)
+    return fail(GPS_E_ARG,
+                "initialization columns are numerically rank deficient; use init='random_orthonormal' or reduce m");
+  return GPS_OK;
+}
+
+int bk_reset_ctl(gps_bk* s) {
+  gps_ctx* ctx = s->A->ctx;
+  std::memset(s->ctl_host, 0, sizeof(GpsCtl));
+  GPS_CUDA(cudaMemcpyAsync(s->ctl, s->ctl_host, sizeof(GpsCtl), cudaMemcpyHostToDevice, ctx->stream));
+  GPS_CUDA(cudaMemsetAsync(s->rank_dev, 0, sizeof(int), ctx->stream));
+  GPS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return GPS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const double* mu, double tol, int max_iter,
+                  gps_bk** out) {
+  if (!A || !out || !gamma || !mu) return fail(GPS_E_ARG, "NULL argument");
+  if (penalty != GPS_L1 && penalty != GPS_L0) return fail(GPS_E_ARG, "unknown penalty %d", penalty);
+  if (m < 1 || m > kMaxBlockM) return fail(GPS_E_UNSUPPORTED, "m=%d outside [1, %d]", m, kMaxBlockM);
+  if (m > A->p || m > A->n) return fail(GPS_E_ARG, "need 1 <= m <= min(p, n)");
+  if (!(tol >= 0)) return fail(GPS_E_ARG, "tol must be >= 0");
+  if (max_iter < 1) return fail(GPS_E_ARG, "max_iter must be >= 1");
+  gps_ctx* ctx = A->ctx;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  int rc = ensure_polar_attrs();
+  if (rc) return rc;
+  BkPlan pl;
+  rc = make_bk_plan(A, pl);
+  if (rc) return rc;
+  auto* s = new gps_bk();
+  s->A = A;
+  s->penalty = penalty;
+  s->m = m;
+  s->mg = pl.mg;
+  s->ngroups = (m + pl.mg - 1) / pl.mg;
+  s->plan = pl;
+  s->tol = tol;
+  s->max_iter = max_iter;
+  s->gamma.assign(s->m_pad(), 0.0);
+  s->mu.assign(s->m_pad(), 1.0);
+  for (int j = 0; j < m; ++j) {
+    s->gamma[j] = gamma[j];
+    s->mu[j] = mu[j];
+  }
+  cudaError_t e = cudaSuccess;
+  auto alloc = [&](void** p, size_t bytes) {
+    if (e == cudaSuccess) e = cudaMalloc(p, bytes);
+  };
+  const size_t ld = A->ld, n = A->n, mp = s->m_pad();
+  alloc((void**)&s->X, 2 * mp * ld * sizeof(double));
+  alloc((void**)&s->W, 2 * mp * n * sizeof(double));
+  alloc((void**)&s->part_g, size_t(s->ngroups) * pl.grid * pl.mg * ld * sizeof(double));
+  alloc((void**)&s->part_s, size_t(s->ngroups) * pl.grid * 4 * sizeof(double));
+  alloc((void**)&s->exch, size_t(s->ngroups) * s->exch_stride() * sizeof(double));
+  alloc((void**)&s->G, size_t(m) * ld * sizeof(double));
+  alloc((void**)&s->Tm, size_t(m) * ld * sizeof(double));
+  alloc((void**)&s->mu_dev, size_t(m) * sizeof(double));
+  alloc((void**)&s->hist, (size_t(max_iter) + 1) * sizeof(double));
+  alloc((void**)&s->ctl, sizeof(GpsCtl));
+  alloc((void**)&s->rank_dev, sizeof(int));
+  if (e == cudaSuccess) e = cudaMallocHost(&s->ctl_host, sizeof(GpsCtl));
+  if (e == cudaSuccess) e = cudaMemsetAsync(s->X, 0, 2 * mp * ld * sizeof(double), ctx->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(s->mu_dev, mu, size_t(m) * sizeof(double), cudaMemcpyHostToDevice, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) {
+    gps_bk_destroy(s);
+    return cuda_fail(e, "gps_bk_create allocation");
+  }
+  *out = s;
+  return GPS_OK;
+}
+
+int gps_bk_destroy(gps_bk* s) {
+  if (!s) return GPS_OK;
+  cudaSetDevice(s->A->ctx->device);
+  cudaStreamSynchronize(s->A->ctx->stream);
+  if (s->graph) cudaGraphExecDestroy(s->graph);
+  cudaFree(s->X);
+  cudaFree(s->W);
+  cudaFree(s->part_g);
+  cudaFree(s->part_s);
+  if (!s->exch_external) cudaFree(s->exch);
+  cudaFree(s->G);
+  cudaFree(s->Tm);
+  cudaFree(s->mu_dev);
+  cudaFree(s->hist);
+  cudaFree(s->ctl);
+  cudaFree(s->rank_dev);
+  if (s->ctl_host) cudaFreeHost(s->ctl_host);
+  delete s;
+  return GPS_OK;
+}
+
+int gps_bk_start(gps_bk* s, const double* X0) {
+  if (!s || !X0) return fail(GPS_E_ARG, "NULL argument");
+  gps_ctx* ctx = s->A->ctx;
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  GPS_CUDA(cudaMemsetAsync(s->X, 0, s->m_pad() * s->A->ld * sizeof(double), ctx->stream));
+  GPS_CUDA(cudaMemcpy2DAsync(s->X, s->A->ld * sizeof(double), X0, s->A->p * sizeof(double), s->A->p * sizeof(double),
+                             s->m, cudaMemcpyHostToDevice, ctx->stream));
+  return bk_reset_ctl(s);
+}
+
+int gps_bk_start_qr(gps_bk* s, const double* M) {
+  if (!s || !M) return fail(GPS_E_ARG, "NULL argument");
+  gps_ctx* ctx = s->A->ctx;
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  GPS_CUDA(cudaMemsetAsync(s->G, 0, size_t(s->m) * s->A->ld * sizeof(double), ctx->stream));
+  GPS_CUDA(cudaMemcpy2DAsync(s->G, s->A->ld * sizeof(double), M, s->A->p * sizeof(double), s->A->p * sizeof(double),
+                             s->m, cudaMemcpyHostToDevice, ctx->stream));
+  GPS_CUDA(cudaMemsetAsync(s->X, 0, s->m_pad() * s->A->ld * sizeof(double), ctx->stream));
+  int rc = bk_qr_into_x(s, s->G);
+  if (rc) return rc;
+  return bk_reset_ctl(s);
+}
+
+int gps_bk_start_columns(gps_bk* s, const int64_t* idx) {
+  if (!s || !idx) return fail(GPS_E_ARG, "NULL argument");
+  gps_matrix* A = s->A;
+  gps_ctx* ctx = A->ctx;
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  // gather the columns (fp64) into G, then CholeskyQR2
+  std::vector<double> col(A->p);
+  std::vector<double> M(size_t(A->p) * s->m);
+  for (int j = 0; j < s->m; ++j) {
+    int rc = gps_matrix_column(A, idx[j], M.data() + size_t(j) * A->p);
+    if (rc) return rc;
+  }
+  return gps_bk_start_qr(s, M.data());
+}
+
+int gps_bk_enqueue_sweep(gps_bk* s) {
+  if (!s) return fail(GPS_E_ARG, "NULL argument");
+  GPS_CUDA(cudaSetDevice(s->A->ctx->device));
+  return bk_enqueue_sweeps(s, true);
+}
+
+int gps_bk_enqueue_step(gps_bk* s) {
+  if (!s) return fail(GPS_E_ARG, "NULL argument");
+  GPS_CUDA(cudaSetDevice(s->A->ctx->device));
+  return bk_enqueue_step(s);
+}
+
+int gps_bk_exchange(gps_bk* s, void** dev_ptr, int64_t* count) {
+  if (!s) return fail(GPS_E_ARG, "NULL argument");
+  if (dev_ptr) *dev_ptr = s->exch;
+  if (count) *count = int64_t(s->ngroups) * int64_t(s->exch_stride());
+  return GPS_OK;
+}
+
+int gps_bk_set_exchange(gps_bk* s, void* dev_ptr) {
+  if (!s || !dev_ptr) return fail(GPS_E_ARG, "NULL argument");
+  if (!s->exch_external) cudaFree(s->exch);
+  s->exch = static_cast<double*>(dev_ptr);
+  s->exch_external = true;
+  if (s->graph) cudaGraphExecDestroy(s->graph);
+  s->graph = nullptr;
+  return GPS_OK;
+}
+
+int gps_bk_poll(gps_bk* s, int* done, int* iter, int* converged) {
+  if (!s) return fail(GPS_E_ARG, "NULL argument");
+  gps_ctx* ctx = s->A->ctx;
+  GPS_CUDA(cudaMemcpyAsync(s->ctl_host, s->ctl, sizeof(GpsCtl), cudaMemcpyDeviceToHost, ctx->stream));
+  GPS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (done) *done = s->ctl_host->done;
+  if (iter) *iter = s->ctl_host->iter;
+  if (converged) *converged = s->ctl_host->converged;
+  return GPS_OK;
+}
+
+int gps_bk_run(gps_bk* s, int poll_every) {
+  if (!s) return fail(GPS_E_ARG, "NULL argument");
+  if (poll_every < 1) poll_every = 1;
+  gps_ctx* ctx = s->A->ctx;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  if (!s->graph || s->graph_iters != poll_every) {
+    if (s->graph) cudaGraphExecDestroy(s->graph);
+    s->graph = nullptr;
+    cudaGraph_t g = nullptr;
+    GPS_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    int rc = GPS_OK;
+    const int64_t before = ctx->launches;
+    for (int i = 0; i < poll_every && rc == GPS_OK; ++i) {
+      rc = bk_enqueue_sweeps(s, true);
+      if (rc == GPS_OK) rc = bk_enqueue_step(s);
+    }
+    ctx->launches = before;
+    cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+    e = cudaGraphInstantiate(&s->graph, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+    s->graph_iters = poll_every;
+  }
+  const int max_chunks = (s->max_iter + 1 + poll_every - 1) / poll_every + 1;
+  for (int c = 0; c < max_chunks; ++c) {
+    GPS_CUDA(cudaGraphLaunch(s->graph, ctx->stream));
+    ctx->launches += int64_t(2 * s->ngroups + 1) * poll_every;
+    GPS_CUDA(cudaMemcpyAsync(s->ctl_host, s->ctl, sizeof(GpsCtl), cudaMemcpyDeviceToHost, ctx->stream));
+    GPS_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (s->ctl_host->done) return GPS_OK;
+  }
+  return fail(GPS_E_CUDA, "block loop did not reach its stopping rule within max_iter");
+}
+
+int gps_bk_result(gps_bk* s, double* X_out, double* hist_out, int* n_hist, int* converged, double* W_out,
+                  int* rank_fail, int* rank_out) {
+  if (!s) return fail(GPS_E_ARG, "NULL argument");
+  gps_ctx* ctx = s->A->ctx;
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  GPS_CUDA(cudaMemcpyAsync(s->ctl_host, s->ctl, sizeof(GpsCtl), cudaMemcpyDeviceToHost, ctx->stream));
+  int rank = 0;
+  GPS_CUDA(cudaMemcpyAsync(&rank, s->rank_dev, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  GPS_CUDA(cudaStreamSynchronize(ctx->stream));
+  const GpsCtl c = *s->ctl_host;
+  if (!c.done) return fail(GPS_E_ARG, "loop has not finished");
+  const int k = c.iter;
+  const size_t ld = s->A->ld, n = s->A->n, p = s->A->p, mp = s->m_pad();
+  if (X_out)
+    GPS_CUDA(cudaMemcpy2DAsync(X_out, p * sizeof(double), s->X + (k & 1) * mp * ld, ld * sizeof(double),
+                               p * sizeof(double), s->m, cudaMemcpyDeviceToHost, ctx->stream));
+  if (hist_out)
+    GPS_CUDA(cudaMemcpyAsync(hist_out, s->hist, size_t(k + 1) * sizeof(double), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+  if (W_out)
+    GPS_CUDA(cudaMemcpyAsync(W_out, s->W + (k & 1) * mp * n, size_t(s->m) * n * sizeof(double),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+  GPS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (n_hist) *n_hist = k + 1;
+  if (converged) *converged = c.converged;
+  if (rank_fail) *rank_fail = c.status == 2;
+  if (rank_out) *rank_out = rank;
+  return GPS_OK;
+}
+
+int gps_bk_sweep(gps_matrix* A, const double* X, int m, const double* gamma, const double* mu, int penalty,
+                 double* f_out, double* G_out, double* W_out) {
+  if (!A || !X || !gamma || !mu) return fail(GPS_E_ARG, "NULL argument");
+  gps_bk* s = nullptr;
+  int rc = gps_bk_create(A, penalty, m, gamma, mu, 0.0, 1, &s);
+  if (rc) return rc;
+  gps_ctx* ctx = A->ctx;
+  const size_t ld = A->ld, p = A->p, n = A->n;
+  cudaError_t e = cudaMemcpy2DAsync(s->X, ld * sizeof(double), X, p * sizeof(double), p * sizeof(double), m,
+                                    cudaMemcpyHostToDevice, ctx->stream);
+  if (e != cudaSuccess) {
+    gps_bk_destroy(s);
+    return cuda_fail(e, "upload X");
+  }
+  {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    rc = bk_enqueue_sweeps(s, false);
+  }
+  std::vector<double> ex(size_t(s->ngroups) * s->exch_stride());
+  if (rc == GPS_OK) {
+    e = cudaMemcpyAsync(ex.data(), s->exch, ex.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess && W_out)
+      e = cudaMemcpyAsync(W_out, s->W, size_t(m) * n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) rc = cuda_fail(e, "gps_bk_sweep download");
+  }
+  if (rc == GPS_OK) {
+    double f = 0.0;
+    for (int g = 0; g < s->ngroups; ++g) f += ex[g * s->exch_stride() + size_t(s->mg) * ld];
+    if (f_out) *f_out = f;
+    if (G_out)
+      for (int j = 0; j < m; ++j) {
+        const double* src = ex.data() + (j / s->mg) * s->exch_stride() + size_t(j % s->mg) * ld;
+        for (size_t r = 0; r < p; ++r) G_out[size_t(j) * p + r] = 2.0 * mu[j] * src[r];
+      }
+  }
+  gps_bk_destroy(s);
+  return rc;
+}
+
+int gps_polar(gps_ctx* ctx, const double* G, int64_t p, int m, double* X_out, int* rank_out) {
+  if (!ctx || !G || !X_out || p < 1 || m < 1) return fail(GPS_E_ARG, "bad arguments");
+  if (m > kMaxBlockM) return fail(GPS_E_UNSUPPORTED, "m=%d > %d", m, kMaxBlockM);
+  if (m > p) return fail(GPS_E_ARG, "need m <= p");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  int rc = ensure_polar_attrs();
+  if (rc) return rc;
+  const int64_t ld = ceil_div(p, 32) * 32;
+  double* buf = nullptr;
+  int* rk = nullptr;
+  cudaError_t e = cudaMalloc(&buf, size_t(3) * m * ld * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&rk, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemsetAsync(buf, 0, size_t(3) * m * ld * sizeof(double), ctx->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(buf, ld * sizeof(double), G, p * sizeof(double), p * sizeof(double), m,
+                          cudaMemcpyHostToDevice, ctx->stream);
+  if (e == cudaSuccess) {
+    polar_kernel<<<1, kPolarThreads, polar_smem_bytes(m), ctx->stream>>>(buf, buf + m * ld, static_cast<int>(ld),
+                                                                          static_cast<int>(p), m, rk);
+    ctx->launches++;
+    e = cudaGetLastError();
+  }
+  int rank = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&rank, rk, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(X_out, p * sizeof(double), buf + m * ld, ld * sizeof(double), p * sizeof(double), m,
+                          cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  cudaFree(buf);
+  cudaFree(rk);
+  if (e != cudaSuccess) return cuda_fail(e, "gps_polar");
+  if (rank_out) *rank_out = rank;
+  if (rank < m) return fail(GPS_E_RANK, "gradient has numerical rank %d < %d", rank, m);
+  return GPS_OK;
+}
+
+int gps_orthonormalize(gps_ctx* ctx, const double* M, int64_t p, int m, double* Q_out) {
+  if (!ctx || !M || !Q_out || p < 1 || m < 1) return fail(GPS_E_ARG, "bad arguments");
+  if (m > kMaxBlockM) return fail(GPS_E_UNSUPPORTED, "m=%d > %d", m, kMaxBlockM);
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  int rc = ensure_polar_attrs();
+  if (rc) return rc;
+  const int64_t ld = ceil_div(p, 32) * 32;
+  double* buf = nullptr;
+  int* st = nullptr;
+  cudaError_t e = cudaMalloc(&buf, size_t(2) * m * ld * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&st, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemsetAsync(buf, 0, size_t(2) * m * ld * sizeof(double), ctx->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(buf, ld * sizeof(double), M, p * sizeof(double), p * sizeof(double), m,
+                          cudaMemcpyHostToDevice, ctx->stream);
+  if (e == cudaSuccess) {
+    cholqr2_kernel<<<1, kPolarThreads, size_t(2) * m * m * sizeof(double) + 64, ctx->stream>>>(
+        buf, buf + m * ld, static_cast<int>(ld), m, st);
+    ctx->launches++;
+    e = cudaGetLastError();
+  }
+  int status = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&status, st, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(Q_out, p * sizeof(double), buf + m * ld, ld * sizeof(double), p * sizeof(double), m,
+                          cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  cudaFree(buf);
+  cudaFree(st);
+  if (e != cudaSuccess) return cuda_fail(e, "gps_orthonormalize");
+  if (status != 0)
+    return fail(GPS_E_ARG,
+                "initialization columns are numerically rank deficient; use init='random_orthonormal' or reduce m");
   return GPS_OK;
 }
 
