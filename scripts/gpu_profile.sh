@@ -1,0 +1,10 @@
+# Full bench + reference arm + ncu launch list + ncu --set full of the sweep.
+mkdir -p gpurun_out
+timeout 900 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo "bench rc=$?"
+cat gpurun_out/bench_default.json; tail -3 gpurun_out/bench_default.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc=$?"
+cat gpurun_out/bench_ref.json; tail -3 gpurun_out/bench_ref.err
+CMD="python bench.py --steps 5 --warmup 3 --e2e-steps 0 --no-cpu-baseline"
+$CMD > gpurun_out/plain.log 2>&1 && \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1; echo "ncu1 rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:su_sweep -s 3 -c 1 -o gpurun_out/prof_sweep -f $CMD > gpurun_out/ncu_full.log 2>&1; echo "ncu2 rc=$?"
