@@ -71,6 +71,11 @@ int gps_matrix_create(gps_ctx* ctx, const void* host, int64_t p, int64_t n, int6
 /* Same, from a DEVICE column-major buffer (copied into padded storage). */
 int gps_matrix_create_device(gps_ctx* ctx, const void* dev_src, int64_t p, int64_t n, int64_t ld_src, int dtype,
                              gps_matrix** out);
+/* Adopt caller device memory without a copy: column-major, ld ==
+ * roundup(p, 32) with ZERO padding rows, 128-byte aligned; the caller keeps
+ * it alive and unmodified until gps_matrix_destroy. */
+int gps_matrix_wrap_device(gps_ctx* ctx, void* dev_ptr, int64_t p, int64_t n, int64_t ld, int dtype,
+                           gps_matrix** out);
 /* Same, from a host ROW-major p x n buffer (C order), transposed on device. */
 int gps_matrix_create_rowmajor(gps_ctx* ctx, const void* host, int64_t p, int64_t n, int dtype,
                                gps_matrix** out);

@@ -36,6 +36,7 @@ SIGNATURES = {
     "gps_ctx_launch_count": (_i64, [_vp]),
     "gps_matrix_create": (C.c_int, [_vp, _vp, _i64, _i64, _i64, C.c_int, C.POINTER(_vp)]),
     "gps_matrix_create_device": (C.c_int, [_vp, _vp, _i64, _i64, _i64, C.c_int, C.POINTER(_vp)]),
+    "gps_matrix_wrap_device": (C.c_int, [_vp, _vp, _i64, _i64, _i64, C.c_int, C.POINTER(_vp)]),
     "gps_matrix_create_rowmajor": (C.c_int, [_vp, _vp, _i64, _i64, C.c_int, C.POINTER(_vp)]),
     "gps_matrix_destroy": (C.c_int, [_vp]),
     "gps_matrix_info": (C.c_int, [_vp, _i64p, _i64p, _i64p, _ip]),

@@ -42,7 +42,7 @@ class DataMatrix:
     column-major host copy on first access.
     """
 
-    __slots__ = ("_handle", "_ctx", "p", "n", "dtype", "_values", "_norms", "_nonfinite", "__weakref__")
+    __slots__ = ("_handle", "_ctx", "p", "n", "dtype", "_values", "_norms", "_nonfinite", "_owner", "__weakref__")
 
     def __init__(self, values, dtype=None, device=None):
         if isinstance(values, DataMatrix):
@@ -58,6 +58,7 @@ class DataMatrix:
         ctx = _native.context(device)
         object.__setattr__(self, "_ctx", ctx)
         object.__setattr__(self, "_handle", None)
+        object.__setattr__(self, "_owner", None)
         object.__setattr__(self, "_values", None)
         object.__setattr__(self, "_norms", None)
         object.__setattr__(self, "p", int(p))
@@ -79,16 +80,25 @@ class DataMatrix:
         object.__setattr__(self, "_nonfinite", False)
 
     @classmethod
-    def from_device(cls, ptr, p, n, ld=None, dtype=np.float32, device=None):
-        """Copy a device-resident column-major p x n buffer (e.g. a torch CUDA
-        tensor's data_ptr) into engine storage; finiteness is checked."""
+    def from_device(cls, ptr, p, n, ld=None, dtype=np.float32, device=None, owner=None):
+        """A device-resident column-major p x n buffer (e.g. a torch CUDA
+        tensor's data_ptr).  With `owner` given and ld == roundup(p, 32) the
+        buffer is adopted WITHOUT a copy (owner is kept alive); otherwise it is
+        copied into engine storage.  Finiteness is checked either way."""
         dt = np.dtype(dtype)
         code = _native.F32 if dt == np.float32 else _native.F64
         ctx = _native.context(device)
         h = _native.C.c_void_p()
-        _native.check(_native.lib().gps_matrix_create_device(ctx.handle, _native.C.c_void_p(ptr), int(p), int(n),
-                                                             int(ld or p), code, _native.C.byref(h)))
+        ld = int(ld or p)
+        if owner is not None and ld == -(-int(p) // 32) * 32:
+            _native.check(_native.lib().gps_matrix_wrap_device(ctx.handle, _native.C.c_void_p(ptr), int(p), int(n),
+                                                               ld, code, _native.C.byref(h)))
+        else:
+            owner = None
+            _native.check(_native.lib().gps_matrix_create_device(ctx.handle, _native.C.c_void_p(ptr), int(p),
+                                                                 int(n), ld, code, _native.C.byref(h)))
         self = cls._wrap(ctx, h)
+        object.__setattr__(self, "_owner", owner)
         if self._nonfinite:
             raise ValueError("matrix entries must be finite")
         return self
@@ -101,7 +111,7 @@ class DataMatrix:
         code = _native.C.c_int()
         _native.check(_native.lib().gps_matrix_info(handle, _native.C.byref(p), _native.C.byref(n),
                                                     _native.C.byref(ld), _native.C.byref(code)))
-        for name, value in (("_ctx", ctx), ("_handle", handle), ("_values", None), ("p", p.value),
+        for name, value in (("_ctx", ctx), ("_handle", handle), ("_values", None), ("_owner", None), ("p", p.value),
                             ("n", n.value), ("dtype", np.dtype(np.float32 if code.value == _native.F32
                                                                else np.float64))):
             object.__setattr__(self, name, value)

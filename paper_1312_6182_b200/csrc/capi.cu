@@ -78,6 +78,7 @@ struct gps_matrix {
   int dtype = GPS_F32;
   int64_t p = 0, n = 0, ld = 0;
   void* d = nullptr;
+  bool owns = true;  // false: adopted caller memory (gps_matrix_wrap_device)
   bool norms_valid = false;
   int nonfinite = 0;
   std::vector<double> norms;
@@ -418,6 +419,26 @@ int gps_matrix_create_device(gps_ctx* ctx, const void* dev_src, int64_t p, int64
   return GPS_OK;
 }
 
+int gps_matrix_wrap_device(gps_ctx* ctx, void* dev_ptr, int64_t p, int64_t n, int64_t ld, int dtype,
+                           gps_matrix** out) {
+  if (!ctx || !dev_ptr || !out) return fail(GPS_E_ARG, "NULL argument");
+  if (p < 1 || n < 1 || ld < p) return fail(GPS_E_ARG, "bad shape");
+  if (dtype != GPS_F32 && dtype != GPS_F64) return fail(GPS_E_ARG, "unknown dtype %d", dtype);
+  if (ld % 32 != 0 || ld != ceil_div(p, 32) * 32)
+    return fail(GPS_E_ARG, "wrap needs ld == roundup(p, 32) (got ld=%lld for p=%lld)", (long long)ld, (long long)p);
+  if (reinterpret_cast<uintptr_t>(dev_ptr) % 128 != 0) return fail(GPS_E_ARG, "device pointer not 128-byte aligned");
+  auto* A = new gps_matrix();
+  A->ctx = ctx;
+  A->dtype = dtype;
+  A->p = p;
+  A->n = n;
+  A->ld = ld;
+  A->d = dev_ptr;
+  A->owns = false;
+  *out = A;
+  return GPS_OK;
+}
+
 int gps_matrix_create_rowmajor(gps_ctx* ctx, const void* host, int64_t p, int64_t n, int dtype, gps_matrix** out) {
   if (!host) return fail(GPS_E_ARG, "host pointer is NULL");
   std::lock_guard<std::mutex> lk(ctx->mu);
@@ -461,7 +482,7 @@ int gps_matrix_destroy(gps_matrix* A) {
   if (!A) return GPS_OK;
   cudaSetDevice(A->ctx->device);
   cudaStreamSynchronize(A->ctx->stream);
-  cudaFree(A->d);
+  if (A->owns) cudaFree(A->d);
   delete A;
   return GPS_OK;
 }

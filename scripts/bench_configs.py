@@ -1,0 +1,125 @@
+#!/usr/bin/env python
+"""Per-config throughput sweep on one GPU.
+
+Writes one JSON object per line to stdout and to profiles/configs_<tag>.jsonl:
+iterations/s and A-stream GB/s of the device-resident power loop (fixed
+iteration count, tol = 0), for the single-unit and block formulations at the
+BASELINE shapes that fit one B200.  Data: Gaussian (the timing harness's
+distribution, reference bench.py:245-246) generated on the device.
+"""
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def gauss(torch, p, n, seed):
+    g = torch.Generator(device="cuda")
+    g.manual_seed(seed)
+    return torch.randn((n, p), generator=g, device="cuda", dtype=torch.float32)
+
+
+def time_su(gps, torch, A, penalty, gamma, iters, warmup=3):
+    from paper_1312_6182_b200 import _native
+
+    loop = gps.single_unit.PowerLoop(A, penalty, gamma, 0.0, iters + warmup + 1)
+    i = int(np.argmax(A.norms))
+    loop.start(A.column(i) / A.norms[i])
+    L = _native.lib()
+    for _ in range(warmup):
+        _native.check(L.gps_su_enqueue(loop.handle, 7))
+    torch.cuda.synchronize()
+    A.context.sync()
+    t0 = time.perf_counter()
+    for _ in range(iters):
+        _native.check(L.gps_su_enqueue(loop.handle, 7))
+    A.context.sync()
+    return (time.perf_counter() - t0) / iters
+
+
+def time_bk(gps, torch, A, penalty, m, gamma, mu, iters, warmup=2):
+    from paper_1312_6182_b200 import _native
+    from paper_1312_6182_b200.block import BlockLoop, _top_m_columns
+
+    loop = BlockLoop(A, penalty, m, gamma, mu, 0.0, iters + warmup + 1)
+    loop.start_columns(_top_m_columns(np.asarray(A.norms), m))
+    L = _native.lib()
+    for _ in range(warmup):
+        _native.check(L.gps_bk_enqueue_sweep(loop.handle))
+        _native.check(L.gps_bk_enqueue_step(loop.handle))
+    A.context.sync()
+    t0 = time.perf_counter()
+    for _ in range(iters):
+        _native.check(L.gps_bk_enqueue_sweep(loop.handle))
+        _native.check(L.gps_bk_enqueue_step(loop.handle))
+    A.context.sync()
+    d, it, c = (_native.C.c_int() for _ in range(3))
+    _native.check(L.gps_bk_poll(loop.handle, _native.C.byref(d), _native.C.byref(it), _native.C.byref(c)))
+    assert not d.value, "block loop stopped early"
+    return (time.perf_counter() - t0) / iters, (m + loop_mg(A) - 1) // loop_mg(A)
+
+
+def loop_mg(A):
+    return 4 if (A.dtype == np.float32 and A.p <= 4096) else 2
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--tag", default="r1")
+    ap.add_argument("--only", default="")
+    args = ap.parse_args()
+    import torch
+
+    import paper_1312_6182_b200 as gps
+
+    out = []
+
+    def emit(rec):
+        print(json.dumps(rec), flush=True)
+        out.append(rec)
+
+    def su_rows(p, n, seed, iters):
+        At = gauss(torch, p, n, seed)
+        A = gps.DataMatrix.from_device(At.data_ptr(), p, n, owner=At)
+        del At
+        top = float(A.norms.max())
+        for pen, gamma in (("l1", 0.1 * top), ("l0", (0.1 * top) ** 2)):
+            t = time_su(gps, torch, A, pen, gamma, iters)
+            emit({"config": f"SL{pen[1]}", "p": p, "n": n, "iters_per_s": 1 / t, "ms_per_iter": t * 1e3,
+                  "a_stream_gbs": p * n * 4 / t / 1e9, "reads_per_iter": 1})
+        return A
+
+    def bk_rows(A, m, iters, mu=None):
+        top = float(A.norms.max())
+        mu = np.ones(m) if mu is None else mu
+        for pen, g in (("l1", 0.1 * top), ("l0", (0.1 * top) ** 2)):
+            t, reads = time_bk(gps, torch, A, pen, m, np.full(m, g), mu, iters)
+            emit({"config": f"BL{pen[1]} m={m}", "p": A.p, "n": A.n, "iters_per_s": 1 / t, "ms_per_iter": t * 1e3,
+                  "reads_per_iter": reads, "a_stream_gbs": A.p * A.n * 4 * reads / t / 1e9})
+
+    if args.only in ("", "c5"):
+        for n in (100_000, 250_000, 500_000, 1 << 20, 1 << 21, 1 << 22, 1 << 23):
+            A = su_rows(4096, n, n, 20 if n >= (1 << 21) else 50)
+            bk_rows(A, 10, 5 if n >= (1 << 22) else 10)
+            del A
+            torch.cuda.empty_cache()
+    if args.only in ("", "c4"):
+        At = gauss(torch, 8192, 1 << 21, 4)
+        A = gps.DataMatrix.from_device(At.data_ptr(), 8192, 1 << 21, owner=At)
+        del At
+        bk_rows(A, 64, 2, mu=np.linspace(1.0, 0.5, 64))
+        del A
+    with open(os.path.join(ROOT, "profiles", f"configs_{args.tag}.jsonl"), "w") as fh:
+        for rec in out:
+            fh.write(json.dumps(rec) + "\n")
+
+
+if __name__ == "__main__":
+    main()
