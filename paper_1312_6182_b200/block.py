@@ -4,8 +4,8 @@ block.py.
 Each iteration runs ceil(m/MG) fused block sweeps (K1b: dots, per-component
 mu scaling and threshold, objective, rank-MG update of the register-resident
 G partial -- one read of A per group of MG components instead of the
-reference's 2m reads) followed by the device polar step (Gram + one-CTA
-Jacobi eigensolver + Newton-Schulz polish; block.py:135-149), with the
+reference's 2m reads) followed by the device polar step (Householder QR of
+G, one-sided Jacobi SVD of R, X = Q U V'; block.py:135-149), with the
 history and stopping rule on the device.  Initialisation is device
 CholeskyQR2 (positive-diagonal R == the reference's sign-fixed QR).
 """
@@ -172,6 +172,15 @@ class BlockLoop:
 
     def run(self, poll_every=8):
         _native.check(_native.lib().gps_bk_run(self.handle, poll_every), "block loop")
+        X, history, converged, W, rank_fail, rank = self.result()
+        if rank_fail:
+            err = RankDeficiencyError(rank, self.m, iteration=len(history) - 1)
+            err.history = history
+            raise err
+        return X, history, converged, W
+
+    def result(self):
+        """(X, history, converged, W, rank_fail, rank) of the finished loop."""
         A, m = self.A, self.m
         X = np.empty((A.p, m), order="F")
         hist = np.empty(self.max_iter + 1)
@@ -180,12 +189,7 @@ class BlockLoop:
         _native.check(_native.lib().gps_bk_result(
             self.handle, X.ctypes.data_as(_native._dp), _native.dptr(hist), _native.C.byref(nh),
             _native.C.byref(conv), W.ctypes.data_as(_native._dp), _native.C.byref(rfail), _native.C.byref(rank)))
-        history = hist[: nh.value].tolist()
-        if rfail.value:
-            err = RankDeficiencyError(rank.value, m, iteration=nh.value - 1)
-            err.history = history
-            raise err
-        return X, history, bool(conv.value), W
+        return X, hist[: nh.value].tolist(), bool(conv.value), W, bool(rfail.value), rank.value
 
 
 def _top_m_columns(norms, m):

@@ -23,6 +23,8 @@ import numpy as np
 
 from . import _native
 from .core import RunReport, SparseLoadings
+from .block import BlockLoop, RankDeficiencyError, _as_stiefel_values
+from .core import StiefelPoint
 from .single_unit import PowerLoop, _check_unit, _random_unit
 
 
@@ -76,10 +78,9 @@ class DeviceShardLoop:
         return self.loop.result()
 
 
-def run_sharded_loop(loop, x0, all_reduce, poll_every=8, max_iter=1000):
-    """Drive a shard loop to its stopping rule: per iteration sweep ->
-    all_reduce(exchange) -> step; poll the control block every chunk."""
-    loop.start(x0)
+def run_sharded_loop(loop, all_reduce, poll_every=8, max_iter=1000):
+    """Drive a started shard loop to its stopping rule: per iteration sweep
+    -> all_reduce(exchange) -> step; poll the control block every chunk."""
     for _ in range(max_iter // poll_every + 2):
         for _ in range(poll_every):
             loop.enqueue_sweep()
@@ -183,7 +184,8 @@ def solve_single_unit_sharded(A_local, config, offset, n_global, comm=None, loop
         x0, _ = global_max_norm_start(A_local.norms, offset, A_local.column, comm, A_local.p, device)
     factory = loop_factory or DeviceShardLoop
     loop = factory(A_local, config.penalty, gamma, config.tol, config.max_iter)
-    x, history, converged, w_local = run_sharded_loop(loop, x0, comm.all_reduce_sum, poll_every, config.max_iter)
+    loop.start(x0)
+    x, history, converged, w_local = run_sharded_loop(loop, comm.all_reduce_sum, poll_every, config.max_iter)
     s2 = comm.sum_scalar(float(w_local @ w_local), device)
     z_local = w_local / np.sqrt(s2) if s2 > 0 else w_local
     z = _gather_ragged(comm, z_local, offset, n_global, device)
@@ -203,3 +205,111 @@ def _gather_ragged(comm, z_local, offset, n_global, device):
         o, k = int(part[0]), int(part[1])
         z[o:o + k] = part[2:2 + k]
     return z
+
+
+# ------------------------------------------------------------------ block
+
+
+class DeviceBlockShardLoop:
+    """BlockLoop on this rank's shard with a torch-owned exchange buffer
+    ([groups][MG*ld + 4]: per-group G partials, f, nnz)."""
+
+    def __init__(self, A_local, penalty, m, gamma, mu, tol, max_iter):
+        import torch
+
+        self.loop = BlockLoop(A_local, penalty, m, gamma, mu, tol, max_iter)
+        n_exch = _native.C.c_int64()
+        _native.check(_native.lib().gps_bk_exchange(self.loop.handle, None, _native.C.byref(n_exch)))
+        dev = torch.device("cuda", A_local.context.device)
+        self.buf = torch.zeros(n_exch.value, dtype=torch.float64, device=dev)
+        _native.check(_native.lib().gps_bk_set_exchange(self.loop.handle, _native.C.c_void_p(self.buf.data_ptr())))
+        stream = torch.cuda.current_stream(dev)
+        if stream.cuda_stream == 0:
+            stream = torch.cuda.Stream(dev)
+            torch.cuda.set_stream(stream)
+        A_local.context.set_stream(stream.cuda_stream)
+
+    def start(self, M, orthonormalize):
+        (self.loop.start_qr if orthonormalize else self.loop.start_user)(M)
+
+    def enqueue_sweep(self):
+        _native.check(_native.lib().gps_bk_enqueue_sweep(self.loop.handle))
+
+    def exchange(self):
+        return self.buf
+
+    def enqueue_step(self):
+        _native.check(_native.lib().gps_bk_enqueue_step(self.loop.handle))
+
+    def poll(self):
+        d, it, cv = _native.C.c_int(), _native.C.c_int(), _native.C.c_int()
+        _native.check(_native.lib().gps_bk_poll(self.loop.handle, _native.C.byref(d), _native.C.byref(it),
+                                                _native.C.byref(cv)))
+        return bool(d.value), it.value, bool(cv.value)
+
+    def result(self):
+        return self.loop.result()
+
+
+def global_top_m_columns(norms_local, offset, column_fn, comm, m, p, device="cpu"):
+    """block.py:157-158 across shards: the m largest norms, ties to the lowest
+    GLOBAL index (stable argsort of -norms); returns M (p x m), identical on
+    every rank (owners fill their columns, one sum all-reduce)."""
+    k = min(m, len(norms_local))
+    loc = np.argsort(-np.asarray(norms_local), kind="stable")[:k]
+    cand = np.full(2 * m, -1.0)
+    cand[:k] = np.asarray(norms_local)[loc]
+    cand[m:m + k] = offset + loc
+    allc = comm.all_gather_vec(cand, device)
+    pairs = [(c[i], int(c[m + i])) for c in allc for i in range(m) if c[m + i] >= 0]
+    pairs.sort(key=lambda t: (-t[0], t[1]))
+    chosen = [g for _, g in pairs[:m]]
+    M = np.zeros((p, m))
+    n_local = len(norms_local)
+    for j, g in enumerate(chosen):
+        if offset <= g < offset + n_local:
+            M[:, j] = column_fn(g - offset)
+    import torch
+
+    t = torch.as_tensor(M.ravel(order="F")).to(device)
+    comm.dist.all_reduce(t, op=comm.dist.ReduceOp.SUM, group=comm.group)
+    return t.cpu().numpy().reshape((p, m), order="F"), chosen
+
+
+def solve_block_sharded(A_local, config, offset, n_global, comm=None, loop_factory=None, device="cpu",
+                        poll_every=8):
+    """Sharded drop-in for solve_block (block.py:190-235).  Returns
+    (SparseLoadings over all n_global columns, RunReport) on every rank and
+    raises RankDeficiencyError identically on every rank."""
+    comm = comm or Comm()
+    if config.mode != "block":
+        raise ValueError("solve_block requires mode='block'")
+    p, m = A_local.p, config.m
+    if not 1 <= m <= min(p, n_global):
+        raise ValueError(f"need 1 <= m <= min(p, n) = {min(p, n_global)}, got m={m}")
+    start = time.perf_counter()
+    if config.init == "random_orthonormal":
+        M, ortho = np.random.default_rng(config.seed).standard_normal((p, m)), True
+    elif config.init == "max_norm_column":
+        M, _ = global_top_m_columns(A_local.norms, offset, A_local.column, comm, m, p, device)
+        ortho = True
+    else:
+        M = StiefelPoint(_as_stiefel_values(config.x0, p, m)).values
+        ortho = False
+    factory = loop_factory or DeviceBlockShardLoop
+    loop = factory(A_local, config.penalty, m, config.gamma, config.mu, config.tol, config.max_iter)
+    loop.start(M, ortho)
+    X, history, converged, W_local, rank_fail, rank = run_sharded_loop(loop, comm.all_reduce_sum, poll_every,
+                                                                      config.max_iter)
+    if rank_fail:
+        err = RankDeficiencyError(rank, m, iteration=len(history) - 1)
+        err.history = history
+        raise err
+    s2 = comm.all_gather_vec(np.einsum("ij,ij->j", W_local, W_local), device)
+    tot = np.sum(s2, axis=0)
+    Z_local = np.where(tot[None, :] > 0, W_local / np.sqrt(np.where(tot > 0, tot, 1.0))[None, :], 0.0)
+    Z = np.column_stack([_gather_ragged(comm, np.ascontiguousarray(Z_local[:, j]), offset, n_global, device)
+                         for j in range(m)])
+    loadings = SparseLoadings(Z)
+    return loadings, RunReport(history, len(history) - 1, time.perf_counter() - start,
+                               loadings.nnz_per_component(), converged, [history])

@@ -87,6 +87,68 @@ class HostShard:
         return self.values[:, i].copy()
 
 
+class OracleBlockShardLoop:
+    """Test-side restatement of the device block loop semantics on a shard."""
+
+    def __init__(self, A_local, penalty, m, gamma, mu, tol, max_iter):
+        self.A = A_local.values
+        self.penalty, self.m, self.tol, self.max_iter = penalty, m, tol, max_iter
+        self.gamma = np.broadcast_to(np.asarray(gamma, float), (m,)).copy()
+        self.mu = np.broadcast_to(np.asarray(mu, float), (m,)).copy()
+        self.buf = torch.zeros(self.A.shape[0] * m + 2, dtype=torch.float64)
+
+    def start(self, M, orthonormalize):
+        if orthonormalize:
+            Q, R = np.linalg.qr(M)
+            self.X = Q * np.sign(np.diagonal(R))
+        else:
+            self.X = np.array(M)
+        self.k, self.done, self.conv, self.f_prev, self.hist = 0, False, False, 0.0, []
+        self.rank_fail, self.rank = False, 0
+        self.W = np.zeros((self.A.shape[1], self.m))
+
+    def enqueue_sweep(self):
+        if self.done:
+            return
+        C = self.A.T @ self.X
+        self.W = np.column_stack([oracle.threshold(self.mu[j] * C[:, j], self.gamma[j], self.penalty)
+                                  for j in range(self.m)])
+        f = oracle.block_objective(C, self.gamma, self.mu, self.penalty)
+        G = self.A @ self.W
+        self.buf.copy_(torch.from_numpy(np.concatenate([G.ravel(order="F"), [f, 0.0]])))
+
+    def exchange(self):
+        return self.buf
+
+    def enqueue_step(self):
+        if self.done:
+            return
+        v = self.buf.numpy()
+        p = self.A.shape[0]
+        f = float(v[p * self.m])
+        self.hist.append(f)
+        if self.k >= 1 and abs(f - self.f_prev) < self.tol * max(abs(self.f_prev), 1e-30):
+            self.done, self.conv = True, True
+            return
+        if self.k >= self.max_iter:
+            self.done = True
+            return
+        G = v[: p * self.m].reshape((p, self.m), order="F") * (2.0 * self.mu)[None, :]
+        try:
+            self.X = oracle.polar(G)
+        except oracle.OracleRankDeficiency as err:
+            self.done, self.rank_fail, self.rank = True, True, err.rank
+            return
+        self.f_prev = f
+        self.k += 1
+
+    def poll(self):
+        return self.done, self.k, self.conv
+
+    def result(self):
+        return self.X, list(self.hist), self.conv, self.W, self.rank_fail, self.rank
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -171,3 +233,55 @@ def test_global_max_norm_tie_breaks_to_lowest_index():
         x0, val = out[rank]
         assert val == 5.0
         np.testing.assert_allclose(x0, [0.6, 0.8, 0.0])  # global column 1 (rank 0), not column 2
+
+
+def _block_worker(rank, port, case, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    try:
+        from paper_1312_6182_b200 import RankDeficiencyError, SolverConfig
+        from paper_1312_6182_b200.distributed import Comm, column_partition, solve_block_sharded
+
+        A = case["A"]
+        off, cnt = column_partition(A.shape[1], WORLD)[rank]
+        shard = HostShard(A[:, off:off + cnt])
+        cfg = SolverConfig(penalty=case["penalty"], mode="block", m=case["m"], gamma=case["gamma"],
+                           mu=case["mu"], **case.get("cfg", {}))
+        try:
+            loadings, report = solve_block_sharded(shard, cfg, off, A.shape[1], comm=Comm(),
+                                                   loop_factory=OracleBlockShardLoop, poll_every=3)
+            out[rank] = ("ok", loadings.values.copy(), list(report.objective_history), report.converged)
+        except RankDeficiencyError as err:
+            out[rank] = ("rank", err.rank, err.iteration, list(err.history))
+    finally:
+        dist.destroy_process_group()
+
+
+BLOCK_CASES = {
+    "bl1_maxnorm": dict(seed=4, shape=(30, 201), penalty="l1", m=3, mu=1.0, rule=lambda nm: 0.1 * nm),
+    "bl0_mu_random": dict(seed=5, shape=(25, 150), penalty="l0", m=4, mu=[1.0, 0.9, 0.8, 0.7],
+                          rule=lambda nm: (0.12 * nm) ** 2, cfg=dict(init="random_orthonormal", seed=2)),
+}
+
+
+@pytest.mark.parametrize("name", sorted(BLOCK_CASES))
+def test_sharded_block_solve_matches_oracle(name):
+    spec = BLOCK_CASES[name]
+    A = np.random.default_rng(spec["seed"]).standard_normal(spec["shape"])
+    gamma = float(spec["rule"](np.linalg.norm(A, axis=0).max()))
+    case = {"A": A, "penalty": spec["penalty"], "gamma": gamma, "m": spec["m"], "mu": spec["mu"],
+            "cfg": spec.get("cfg", {})}
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_block_worker, args=(_free_port(), case, out), nprocs=WORLD, join=True)
+    cfg = dict(spec.get("cfg", {}))
+    init = cfg.pop("init", "max_norm_column")
+    Z_ref, hist_ref, conv_ref, _ = oracle.block_solve(A, spec["m"], gamma, spec["mu"], spec["penalty"],
+                                                      init=init, **cfg)
+    for rank in range(WORLD):
+        status, Z, hist, conv = out[rank]
+        assert status == "ok"
+        assert conv == conv_ref and len(hist) == len(hist_ref)
+        np.testing.assert_allclose(hist, hist_ref, rtol=1e-12, atol=1e-14)
+        assert np.array_equal(Z != 0, Z_ref != 0)
+        np.testing.assert_allclose(Z, Z_ref, rtol=1e-9, atol=1e-12)
