@@ -17,6 +17,7 @@
 
 #include "../../include/gpspca_b200.h"
 #include "bk_kernels.cuh"
+#include "wide_kernels.cuh"
 
 using namespace gps;
 
@@ -93,6 +94,7 @@ namespace {
 using SweepFn = void (*)(SweepArgs);
 
 struct SweepPlan {
+  bool wide = false;  // p beyond the fused kernels' coverage: W1 + W2 fallback
   SweepFn fn = nullptr;
   int gs = 0, rv = 0, ng = 0;
   int cols_per_stage = 0, stages = 0;
@@ -145,9 +147,11 @@ int make_plan(const gps_matrix* A, int mode, SweepPlan& plan) {
     if (mode == kDotOnly) ok = pick_kernel<double, kDotOnly>(ld, plan.fn, plan.gs, plan.rv);
     if (mode == kCoef) ok = pick_kernel<double, kCoef>(ld, plan.fn, plan.gs, plan.rv);
   }
-  if (!ok)
-    return fail(GPS_E_UNSUPPORTED, "p=%lld exceeds the fused sweep coverage (%d rows for %s)",
-                (long long)A->p, A->dtype == GPS_F32 ? 8192 : 4096, A->dtype == GPS_F32 ? "fp32" : "fp64");
+  if (!ok) {
+    plan.wide = true;
+    plan.grid = static_cast<int>(std::min<int64_t>(int64_t(A->ctx->num_sms) * 2, A->n));
+    return GPS_OK;
+  }
   const size_t esz = A->dtype == GPS_F32 ? 4 : 8;
   plan.ng = kSweepWorkers / plan.gs;
   plan.cols_per_stage = plan.ng * sweep_cols_per_group(plan.rv);
@@ -165,7 +169,76 @@ int make_plan(const gps_matrix* A, int mode, SweepPlan& plan) {
   return ensure_smem_attr(reinterpret_cast<const void*>(plan.fn), plan.smem);
 }
 
-int launch_sweep(gps_matrix* A, const SweepPlan& plan, SweepArgs args) {
+// Wide-p fallback launch (csrc/wide_kernels.cuh): W1 dots/threshold, then W2
+// accumulation over the active columns; same outputs as the fused kernels.
+struct WideLaunch {
+  int grid, mode, mg, penalty;
+  const double* X;
+  int64_t x_cstride, x_par_stride;
+  const double* coef;
+  int coef_threshold;
+  WideParams prm;
+  double* wbuf;
+  double* c_out;
+  double* w_out;
+  int64_t w_cstride, w_par_stride;
+  double* part_s;
+  double* part_g;
+  const GpsCtl* ctl;
+};
+
+template <typename TA, int MG>
+void launch_wide_t(gps_matrix* A, const WideLaunch& w) {
+  gps_ctx* ctx = A->ctx;
+  const int ld = static_cast<int>(A->ld), p = static_cast<int>(A->p);
+  wide_dots_kernel<TA, MG><<<w.grid, kWideThreads, 0, ctx->stream>>>(
+      static_cast<const TA*>(A->d), A->n, ld, p, w.mode, w.penalty, w.X, w.x_cstride, w.coef, w.coef_threshold,
+      w.prm, w.wbuf, w.c_out, w.w_out, w.w_cstride, w.part_s, w.ctl, w.x_par_stride, w.w_par_stride);
+  ctx->launches++;
+  if (w.mode != kDotOnly) {
+    dim3 g2(w.grid, static_cast<unsigned>((A->ld + kWideRows - 1) / kWideRows));
+    wide_accum_kernel<TA, MG><<<g2, kWideThreads, 0, ctx->stream>>>(static_cast<const TA*>(A->d), A->n, ld, w.wbuf,
+                                                                     w.w_cstride, w.part_g, w.ctl);
+    ctx->launches++;
+  }
+}
+
+int launch_wide(gps_matrix* A, const WideLaunch& w) {
+  if (w.mg == 1) {
+    if (A->dtype == GPS_F32) launch_wide_t<float, 1>(A, w);
+    else launch_wide_t<double, 1>(A, w);
+  } else {
+    if (A->dtype == GPS_F32) launch_wide_t<float, 2>(A, w);
+    else launch_wide_t<double, 2>(A, w);
+  }
+  GPS_CHECK_LAUNCH("wide sweep launch");
+  return GPS_OK;
+}
+
+int launch_sweep(gps_matrix* A, const SweepPlan& plan, SweepArgs args, int mode, double* wbuf) {
+  if (plan.wide) {
+    WideLaunch w{};
+    w.grid = plan.grid;
+    w.mode = mode;
+    w.mg = 1;
+    w.penalty = args.penalty;
+    w.X = args.x;
+    w.x_cstride = 0;
+    w.x_par_stride = args.x_stride;
+    w.coef = args.coef;
+    w.coef_threshold = args.coef_threshold;
+    w.prm.gamma[0] = args.gamma;
+    w.prm.mu[0] = 1.0;
+    w.wbuf = wbuf;
+    w.c_out = args.c_out;
+    w.w_out = args.w_out;
+    w.w_cstride = A->n;
+    w.w_par_stride = args.w_stride;
+    w.part_s = args.part_s;
+    w.part_g = args.part_g;
+    w.ctl = args.ctl;
+    return launch_wide(A, w);
+  }
   args.A = A->d;
   args.n = A->n;
   args.ld = static_cast<int>(A->ld);
@@ -188,14 +261,14 @@ int launch_reduce(gps_ctx* ctx, const double* part_g, const double* part_s, int 
 }
 
 int ctx_scratch(gps_ctx* ctx, int64_t ld, int64_t nvec) {
-  const size_t need_g = size_t(ctx->num_sms) * ld;
+  const size_t need_g = size_t(2) * ctx->num_sms * ld;  // wide fallback grid is 2 x SMs
   if (ctx->part_g_elems < need_g) {
     if (ctx->part_g) cudaFree(ctx->part_g);
     ctx->part_g = nullptr;
     GPS_CUDA(cudaMalloc(&ctx->part_g, need_g * sizeof(double)));
     ctx->part_g_elems = need_g;
   }
-  if (!ctx->part_s) GPS_CUDA(cudaMalloc(&ctx->part_s, size_t(ctx->num_sms) * 4 * sizeof(double)));
+  if (!ctx->part_s) GPS_CUDA(cudaMalloc(&ctx->part_s, size_t(2) * ctx->num_sms * 4 * sizeof(double)));
   if (ctx->dvec_elems < size_t(nvec)) {
     if (ctx->dvec) cudaFree(ctx->dvec);
     ctx->dvec = nullptr;
@@ -248,6 +321,7 @@ __global__ void gather_columns_kernel(const TA* __restrict__ A, int64_t ld, cons
 
 struct gps_su {
   gps_matrix* A = nullptr;
+  gps_ctx* ctx = nullptr;  // destroy must not touch A (it may already be gone)
   int penalty = 0;
   double gamma = 0, tol = 1e-6;
   int max_iter = 1000;
@@ -264,6 +338,7 @@ struct gps_su {
   int graph_iters = 0;
   SweepPlan plan;
   bool exch_external = false;
+  double* wbuf = nullptr;  // wide-p fallback weights (n)
   double* defl = nullptr;  // [defl_cap][ld] previous components (implicit deflation)
   int defl_k = 0, defl_cap = 0;
 };
@@ -605,8 +680,8 @@ static int one_shot(gps_matrix* A, int mode, const double* x, const double* coef
   SweepPlan plan;
   int rc = make_plan(A, mode, plan);
   if (rc) return rc;
-  // dvec layout: [x (ld)] [coef or c (n)] [exch (ld + 4)] [w (n)]
-  rc = ctx_scratch(ctx, A->ld, A->ld + A->n + A->ld + 4 + A->n);
+  // dvec layout: [x (ld)] [coef or c (n)] [exch (ld + 4)] [w (n)] [wide scratch (n)]
+  rc = ctx_scratch(ctx, A->ld, A->ld + A->n + A->ld + 4 + A->n + A->n);
   if (rc) return rc;
   double* dx = ctx->dvec;
   double* dn = ctx->dvec + A->ld;
@@ -628,7 +703,7 @@ static int one_shot(gps_matrix* A, int mode, const double* x, const double* coef
   args.part_s = ctx->part_s;
   args.c_out = (c_out && mode != kCoef) ? dn : nullptr;
   args.w_out = (w_out && mode == kFused) ? dw : nullptr;
-  rc = launch_sweep(A, plan, args);
+  rc = launch_sweep(A, plan, args, mode, dw + A->n);
   if (rc) return rc;
   rc = launch_reduce(ctx, ctx->part_g, ctx->part_s, plan.grid, static_cast<int>(A->ld), exch, nullptr);
   if (rc) return rc;
@@ -754,6 +829,7 @@ int gps_su_create(gps_matrix* A, int penalty, double gamma, double tol, int max_
   if (rc) return rc;
   auto* s = new gps_su();
   s->A = A;
+  s->ctx = ctx;
   s->penalty = penalty;
   s->gamma = gamma;
   s->tol = tol;
@@ -770,6 +846,7 @@ int gps_su_create(gps_matrix* A, int penalty, double gamma, double tol, int max_
   alloc(&s->part_s, size_t(plan.grid) * 4);
   alloc(&s->exch, A->ld + 4);
   alloc(&s->hist, size_t(max_iter) + 1);
+  if (plan.wide) alloc(&s->wbuf, A->n);
   if (e == cudaSuccess) e = cudaMalloc(&s->ctl, sizeof(GpsCtl));
   if (e == cudaSuccess) e = cudaMallocHost(&s->ctl_host, sizeof(GpsCtl));
   if (e == cudaSuccess) e = cudaMemsetAsync(s->x, 0, 2 * A->ld * sizeof(double), ctx->stream);
@@ -783,8 +860,8 @@ int gps_su_create(gps_matrix* A, int penalty, double gamma, double tol, int max_
 
 int gps_su_destroy(gps_su* s) {
   if (!s) return GPS_OK;
-  cudaSetDevice(s->A->ctx->device);
-  cudaStreamSynchronize(s->A->ctx->stream);
+  cudaSetDevice(s->ctx->device);
+  cudaStreamSynchronize(s->ctx->stream);
   if (s->graph) cudaGraphExecDestroy(s->graph);
   cudaFree(s->x);
   cudaFree(s->w);
@@ -794,6 +871,7 @@ int gps_su_destroy(gps_su* s) {
   cudaFree(s->hist);
   cudaFree(s->ctl);
   if (s->defl) cudaFree(s->defl);
+  if (s->wbuf) cudaFree(s->wbuf);
   if (s->ctl_host) cudaFreeHost(s->ctl_host);
   delete s;
   return GPS_OK;
@@ -823,7 +901,7 @@ static int su_enqueue_sweep_nolock(gps_su* s, int mask = 3) {
   args.w_out = s->w;
   args.w_stride = s->A->n;
   args.ctl = s->ctl;
-  if (mask & 1) rc = launch_sweep(s->A, plan, args);
+  if (mask & 1) rc = launch_sweep(s->A, plan, args, kFused, s->wbuf);
   if (rc) return rc;
   if (mask & 2)
     rc = launch_reduce(s->A->ctx, s->part_g, s->part_s, plan.grid, static_cast<int>(s->A->ld), s->exch, s->ctl);
@@ -998,6 +1076,7 @@ namespace {
 using BkFn = void (*)(BlockSweepArgs);
 
 struct BkPlan {
+  bool wide = false;
   BkFn fn = nullptr;
   int gs = 0, rv = 0, ng = 0, mg = 0, k = 0;
   int cols_per_stage = 0, stages = 0;
@@ -1042,8 +1121,12 @@ bool pick_bk(int ld, BkPlan& pl) {
 int make_bk_plan(const gps_matrix* A, BkPlan& pl) {
   const int ld = static_cast<int>(A->ld);
   const bool ok = A->dtype == GPS_F32 ? pick_bk<float, float>(ld, pl) : pick_bk<double, double>(ld, pl);
-  if (!ok)
-    return fail(GPS_E_UNSUPPORTED, "p=%lld exceeds the fused block sweep coverage", (long long)A->p);
+  if (!ok) {
+    pl.wide = true;
+    pl.mg = 2;
+    pl.grid = static_cast<int>(std::min<int64_t>(int64_t(A->ctx->num_sms) * 2, A->n));
+    return GPS_OK;
+  }
   const size_t esz = A->dtype == GPS_F32 ? 4 : 8;
   pl.ng = kSweepWorkers / pl.gs;
   pl.k = bk_cols_per_group(pl.rv);
@@ -1081,6 +1164,7 @@ constexpr int kMaxBlockM = 64;
 
 struct gps_bk {
   gps_matrix* A = nullptr;
+  gps_ctx* ctx = nullptr;  // destroy must not touch A
   int penalty = 0, m = 0, mg = 0, ngroups = 0;
   std::vector<double> gamma, mu;  // length m_pad (padded: gamma 0, mu 1)
   double tol = 1e-6;
@@ -1095,6 +1179,7 @@ struct gps_bk {
   double* G = nullptr;      // [m][ld]
   double* Tm = nullptr;     // [m][ld]
   double* mu_dev = nullptr; // m
+  double* wbuf = nullptr;   // wide-p fallback weights [mg][n]
   double* hist = nullptr;
   GpsCtl* ctl = nullptr;
   GpsCtl* ctl_host = nullptr;
@@ -1130,9 +1215,33 @@ int bk_launch_group(gps_bk* s, int g, bool with_ctl, int write_w) {
   a.cols_per_stage = pl.cols_per_stage;
   a.num_stages = pl.stages;
   a.total_stages = pl.total_stages;
-  pl.fn<<<pl.grid, kSweepThreads, pl.smem, A->ctx->stream>>>(a);
-  A->ctx->launches++;
-  GPS_CHECK_LAUNCH("bk_sweep_kernel launch");
+  if (pl.wide) {
+    WideLaunch w{};
+    w.grid = pl.grid;
+    w.mode = kFused;
+    w.mg = pl.mg;
+    w.penalty = a.penalty;
+    w.X = a.X;
+    w.x_cstride = A->ld;
+    w.x_par_stride = a.x_stride;
+    for (int j = 0; j < 4; ++j) {
+      w.prm.gamma[j] = a.gamma[j];
+      w.prm.mu[j] = a.mu[j];
+    }
+    w.wbuf = s->wbuf;
+    w.w_out = a.w_out;
+    w.w_cstride = A->n;
+    w.w_par_stride = a.w_stride;
+    w.part_s = a.part_s;
+    w.part_g = a.part_g;
+    w.ctl = a.ctl;
+    int rc = launch_wide(A, w);
+    if (rc) return rc;
+  } else {
+    pl.fn<<<pl.grid, kSweepThreads, pl.smem, A->ctx->stream>>>(a);
+    A->ctx->launches++;
+    GPS_CHECK_LAUNCH("bk_sweep_kernel launch");
+  }
   double* ex = s->exch + size_t(g) * s->exch_stride();
   return launch_reduce(A->ctx, a.part_g, a.part_s, pl.grid, pl.mg * static_cast<int>(A->ld), ex,
                        with_ctl ? s->ctl : nullptr);
@@ -1203,6 +1312,7 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
   if (rc) return rc;
   auto* s = new gps_bk();
   s->A = A;
+  s->ctx = ctx;
   s->penalty = penalty;
   s->m = m;
   s->mg = pl.mg;
@@ -1230,6 +1340,7 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
   alloc((void**)&s->Tm, size_t(m) * ld * sizeof(double));
   alloc((void**)&s->mu_dev, size_t(m) * sizeof(double));
   alloc((void**)&s->hist, (size_t(max_iter) + 1) * sizeof(double));
+  if (pl.wide) alloc((void**)&s->wbuf, size_t(pl.mg) * n * sizeof(double));
   alloc((void**)&s->ctl, sizeof(GpsCtl));
   alloc((void**)&s->rank_dev, sizeof(int));
   if (e == cudaSuccess) e = cudaMallocHost(&s->ctl_host, sizeof(GpsCtl));
@@ -1247,8 +1358,8 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
 
 int gps_bk_destroy(gps_bk* s) {
   if (!s) return GPS_OK;
-  cudaSetDevice(s->A->ctx->device);
-  cudaStreamSynchronize(s->A->ctx->stream);
+  cudaSetDevice(s->ctx->device);
+  cudaStreamSynchronize(s->ctx->stream);
   if (s->graph) cudaGraphExecDestroy(s->graph);
   cudaFree(s->X);
   cudaFree(s->W);
@@ -1258,6 +1369,7 @@ int gps_bk_destroy(gps_bk* s) {
   cudaFree(s->G);
   cudaFree(s->Tm);
   cudaFree(s->mu_dev);
+  if (s->wbuf) cudaFree(s->wbuf);
   cudaFree(s->hist);
   cudaFree(s->ctl);
   cudaFree(s->rank_dev);

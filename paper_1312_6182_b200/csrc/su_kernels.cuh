@@ -422,7 +422,6 @@ __global__ void __launch_bounds__(256) su_reduce_kernel(const double* __restrict
 // (implicit deflation, single_unit.py:287-296: g = (I - x_l x_l') ... g in
 // component order), so A is never rewritten.
 constexpr int kStepThreads = 1024;
-constexpr int kStepRows = 8;  // ld <= kStepThreads * kStepRows
 
 __device__ __forceinline__ double block_sum_1024(double v, double* red) {
   v = warp_sum(v);
@@ -437,7 +436,7 @@ __device__ __forceinline__ double block_sum_1024(double v, double* red) {
   return red[32];
 }
 
-__global__ void __launch_bounds__(kStepThreads) su_step_kernel(const double* __restrict__ exch, int ld,
+__global__ void __launch_bounds__(kStepThreads) su_step_kernel(const double* exch, int ld,
                                                               double* __restrict__ xbuf, int64_t x_stride,
                                                               double* __restrict__ hist, GpsCtl* ctl,
                                                               double tol, int max_iter,
@@ -464,30 +463,19 @@ __global__ void __launch_bounds__(kStepThreads) su_step_kernel(const double* __r
     }
     return;
   }
-  double g[kStepRows];
-#pragma unroll
-  for (int j = 0; j < kStepRows; ++j) {
-    const int r = tid + j * kStepThreads;
-    g[j] = r < ld ? exch[r] : 0.0;
-  }
+  // g lives in the exchange vector (global, L2-resident); projections and
+  // the normalisation are strided block loops, so any ld is handled.
+  double* g = const_cast<double*>(exch);
   for (int l = 0; l < defl_k; ++l) {
     const double* xl = defl_X + size_t(l) * ld;
     double t = 0.0;
-#pragma unroll
-    for (int j = 0; j < kStepRows; ++j) {
-      const int r = tid + j * kStepThreads;
-      if (r < ld) t = fma(xl[r], g[j], t);
-    }
+    for (int r = tid; r < ld; r += kStepThreads) t = fma(xl[r], g[r], t);
     const double d = block_sum_1024(t, red);
-#pragma unroll
-    for (int j = 0; j < kStepRows; ++j) {
-      const int r = tid + j * kStepThreads;
-      if (r < ld) g[j] = fma(-d, xl[r], g[j]);
-    }
+    for (int r = tid; r < ld; r += kStepThreads) g[r] = fma(-d, xl[r], g[r]);
+    __syncthreads();
   }
   double t = 0.0;
-#pragma unroll
-  for (int j = 0; j < kStepRows; ++j) t = fma(g[j], g[j], t);
+  for (int r = tid; r < ld; r += kStepThreads) t = fma(g[r], g[r], t);
   const double nrm = sqrt(block_sum_1024(t, red));
   if (nrm == 0.0) {
     if (tid == 0) {
@@ -498,11 +486,7 @@ __global__ void __launch_bounds__(kStepThreads) su_step_kernel(const double* __r
     return;
   }
   double* xn = xbuf + ((k + 1) & 1) * x_stride;
-#pragma unroll
-  for (int j = 0; j < kStepRows; ++j) {
-    const int r = tid + j * kStepThreads;
-    if (r < ld) xn[r] = g[j] / nrm;
-  }
+  for (int r = tid; r < ld; r += kStepThreads) xn[r] = g[r] / nrm;
   if (tid == 0) {
     ctl->f_prev = f;
     ctl->gnorm = nrm;

@@ -257,3 +257,46 @@ class TestLargeShapes:
         assert len(ho) == len(r1.objective_history)
         np.testing.assert_allclose(r1.objective_history, ho, rtol=1e-9)
         np.testing.assert_allclose(z1.values[:, 0], zo, rtol=1e-7, atol=1e-9)
+
+
+class TestWideP:
+    """p beyond the fused kernels' register coverage (8192 fp32 / 4096 fp64)
+    runs the two-pass wide fallback; results must match the oracle exactly
+    as the fused path does."""
+
+    @pytest.mark.parametrize("p,dtype", [(9000, np.float32), (4500, np.float64)])
+    @pytest.mark.parametrize("penalty", ["l1", "l0"])
+    def test_solve_matches_oracle(self, p, dtype, penalty):
+        rng = np.random.default_rng(p)
+        A32 = rng.standard_normal((p, 1500)).astype(np.float32)
+        A64 = A32.astype(np.float64)
+        gamma = 0.1 * float(np.linalg.norm(A64, axis=0).max())
+        gamma = gamma if penalty == "l1" else gamma ** 2
+        loadings, report = gps.solve_single_unit(gps.DataMatrix(A32.astype(dtype), dtype=dtype),
+                                                 gps.SolverConfig(penalty=penalty, gamma=gamma))
+        z, hist, conv, _ = oracle.su_solve(A64, gamma, penalty)
+        assert report.iterations == len(hist) - 1
+        np.testing.assert_allclose(report.objective_history, hist, rtol=1e-9)
+        np.testing.assert_allclose(loadings.values[:, 0], z, rtol=1e-8, atol=1e-10)
+
+    def test_kernel_seam_wide(self):
+        rng = np.random.default_rng(1)
+        A = rng.standard_normal((8300, 700))
+        x = rng.standard_normal(8300)
+        x /= np.linalg.norm(x)
+        coef = rng.standard_normal(700)
+        D = gps.DataMatrix(A.astype(np.float32))
+        A32 = A.astype(np.float32).astype(np.float64)
+        np.testing.assert_allclose(gps.par_matvec_t(D, x), A32.T @ x, rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(gps.par_gram_apply(D, coef), A32 @ coef, rtol=1e-11, atol=1e-10)
+
+    def test_block_wide_matches_oracle(self):
+        rng = np.random.default_rng(2)
+        A = rng.standard_normal((4200, 900))
+        gamma = 0.1 * float(np.linalg.norm(A, axis=0).max())
+        cfg = gps.SolverConfig(penalty="l1", mode="block", m=3, gamma=gamma)
+        loadings, report = gps.solve_block(gps.DataMatrix(A), cfg)
+        Z, hist, conv, _ = oracle.block_solve(A, 3, gamma, 1.0, "l1")
+        assert report.iterations == len(hist) - 1
+        np.testing.assert_allclose(report.objective_history, hist, rtol=1e-9)
+        np.testing.assert_allclose(loadings.values, Z, rtol=1e-7, atol=1e-9)
