@@ -12,7 +12,7 @@ import threading
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libgpspca_b200.so")
+LIB_PATH = os.environ.get("GPSPCA_LIB", os.path.join(_PKG, "libgpspca_b200.so"))
 
 GPS_OK, GPS_E_ARG, GPS_E_RANK, GPS_E_OOM, GPS_E_CUDA, GPS_E_UNSUPPORTED = range(6)
 F32, F64 = 0, 1

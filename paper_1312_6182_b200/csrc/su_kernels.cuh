@@ -69,7 +69,10 @@ constexpr int kSweepLag = 1;                          // update of stage t runs 
 
 // Columns a group handles per stage: 4 (2 when a thread owns 8 vectors of a
 // column, to keep a stage <= 64 KB).
-__host__ __device__ constexpr int sweep_cols_per_group(int rv) { return rv >= 8 ? 2 : 4; }
+#ifndef GPS_SWEEP_K
+#define GPS_SWEEP_K 4
+#endif
+__host__ __device__ constexpr int sweep_cols_per_group(int rv) { return rv >= 8 ? 2 : GPS_SWEEP_K; }
 
 // Shared scratch after the ring (doubles): red[D][NG][K][NW] warp partials,
 // wsm[D][NG][K] thresholded weights, sc[NG*K][3] reducer scalars; then the
