@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -18,6 +19,10 @@
 #include "../../include/gpspca_b200.h"
 #include "bk_kernels.cuh"
 #include "wide_kernels.cuh"
+#include "tc_kernels.cuh"
+#include "polar_kernels.cuh"
+
+#include <cudaTypedefs.h>
 
 using namespace gps;
 
@@ -252,9 +257,10 @@ int launch_sweep(gps_matrix* A, const SweepPlan& plan, SweepArgs args, int mode,
 }
 
 int launch_reduce(gps_ctx* ctx, const double* part_g, const double* part_s, int nparts, int ld, double* exch,
-                  const GpsCtl* ctl) {
+                  const GpsCtl* ctl, int nparts_s = -1) {
   const int blocks = (ld + 255) / 256 + 1;
-  su_reduce_kernel<<<blocks, 256, 0, ctx->stream>>>(part_g, part_s, nparts, ld, exch, ctl);
+  su_reduce_kernel<<<blocks, 256, 0, ctx->stream>>>(part_g, part_s, nparts, ld, exch, ctl,
+                                                    nparts_s < 0 ? nparts : nparts_s);
   ctx->launches++;
   GPS_CHECK_LAUNCH("su_reduce_kernel launch");
   return GPS_OK;
@@ -1153,6 +1159,10 @@ int ensure_polar_attrs() {
       err = cudaFuncSetAttribute(polar_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (err == cudaSuccess)
       err = cudaFuncSetAttribute(cholqr2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (err == cudaSuccess)
+      err = cudaFuncSetAttribute(bk_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (err == cudaSuccess)
+      err = cudaFuncSetAttribute(chol_stage_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   });
   if (err != cudaSuccess) return cuda_fail(err, "cudaFuncSetAttribute(polar)");
   return GPS_OK;
@@ -1180,12 +1190,27 @@ struct gps_bk {
   double* Tm = nullptr;     // [m][ld]
   double* mu_dev = nullptr; // m
   double* wbuf = nullptr;   // wide-p fallback weights [mg][n]
+  // tensor-core path (fp32 A, m >= 16): split X, column activity, TMA maps
+  bool tc = false;
+  int tc_grid = 0, tc_gx = 0, tc_tiles = 0;
+  float* xhi = nullptr;
+  float* xlo = nullptr;
+  unsigned char* colmask = nullptr;
+  double* part_s_tc = nullptr;
+  CUtensorMap tmA, tmXh, tmXl;
+  // multi-CTA CholeskyQR2 polar (large p*m)
+  bool big_polar = false;
+  PolarCtl* pc = nullptr;
+  double* gram_part = nullptr;
+  double* R1 = nullptr;
+  double* Sm = nullptr;
   double* hist = nullptr;
   GpsCtl* ctl = nullptr;
   GpsCtl* ctl_host = nullptr;
   int* rank_dev = nullptr;
   cudaGraphExec_t graph = nullptr;
   int graph_iters = 0;
+  int64_t graph_launches = 0;
   size_t m_pad() const { return size_t(ngroups) * mg; }
   size_t exch_stride() const { return size_t(mg) * A->ld + 4; }
 };
@@ -1247,7 +1272,65 @@ int bk_launch_group(gps_bk* s, int g, bool with_ctl, int write_w) {
                        with_ctl ? s->ctl : nullptr);
 }
 
+// ---- tensor-core path helpers
+int tma_encode_2d(CUtensorMap* map, const void* base, uint64_t dim0, uint64_t dim1, uint64_t stride1_bytes,
+                  uint32_t box0, uint32_t box1) {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  if (!fn) return fail(GPS_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {dim0, dim1};
+  const cuuint64_t strides[1] = {stride1_bytes};
+  const cuuint32_t box[2] = {box0, box1};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(GPS_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
+  return GPS_OK;
+}
+
+int bk_enqueue_tc(gps_bk* s, bool with_ctl) {
+  gps_matrix* A = s->A;
+  gps_ctx* ctx = A->ctx;
+  const GpsCtl* ctl = with_ctl ? s->ctl : nullptr;
+  const int ld = static_cast<int>(A->ld), np = s->mg;
+  tc_split_x_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(s->X, int64_t(s->m_pad()) * ld, s->m, np, ld, s->xhi,
+                                                            s->xlo, ctl);
+  ctx->launches++;
+  TcDotsArgs a{};
+  a.n = A->n;
+  a.ld = ld;
+  a.m = s->m;
+  a.n_pad = np;
+  a.penalty = s->penalty;
+  a.mu = s->mu_dev;
+  a.w_out = s->W;
+  a.w_stride = int64_t(s->m_pad()) * A->n;
+  a.colmask = s->colmask;
+  a.part_s = s->part_s_tc;
+  a.ctl = ctl;
+  a.num_tiles = s->tc_tiles;
+  a.gamma = s->mu_dev + s->m;  // gamma stored after mu in mu_dev
+  tc_dots_kernel<<<s->tc_grid, kTcThreads, tc_smem_bytes(np), ctx->stream>>>(s->tmA, s->tmXh, s->tmXl, a);
+  ctx->launches++;
+  dim3 g2(s->tc_gx, static_cast<unsigned>((A->ld + kTcUpdRows - 1) / kTcUpdRows),
+          static_cast<unsigned>((s->m + kTcUpdComps - 1) / kTcUpdComps));
+  tc_update_kernel<<<g2, 256, 0, ctx->stream>>>(static_cast<const float*>(A->d), A->n, ld, s->m, s->colmask, s->W,
+                                                 int64_t(s->m_pad()) * A->n, np, s->part_g, ctl);
+  ctx->launches++;
+  GPS_CHECK_LAUNCH("tensor-core block sweep launch");
+  return launch_reduce(ctx, s->part_g, s->part_s_tc, s->tc_gx, np * ld, s->exch, ctl, s->tc_grid);
+}
+
 int bk_enqueue_sweeps(gps_bk* s, bool with_ctl) {
+  if (s->tc) return bk_enqueue_tc(s, with_ctl);
   for (int g = 0; g < s->ngroups; ++g) {
     int rc = bk_launch_group(s, g, with_ctl, 1);
     if (rc) return rc;
@@ -1257,11 +1340,32 @@ int bk_enqueue_sweeps(gps_bk* s, bool with_ctl) {
 
 int bk_enqueue_step(gps_bk* s) {
   gps_ctx* ctx = s->A->ctx;
-  bk_step_kernel<<<1, kPolarThreads, polar_smem_bytes(s->m), ctx->stream>>>(
-      s->exch, s->ngroups, s->mg, static_cast<int>(s->A->ld), static_cast<int>(s->A->p), s->m, s->mu_dev, s->X,
-      int64_t(s->m_pad()) * s->A->ld, s->G, s->Tm, s->hist, s->ctl, s->tol, s->max_iter, s->rank_dev);
-  ctx->launches++;
-  GPS_CHECK_LAUNCH("bk_step_kernel launch");
+  const int ld = static_cast<int>(s->A->ld), p = static_cast<int>(s->A->p), m = s->m;
+  const int64_t xs = int64_t(s->m_pad()) * s->A->ld;
+  if (!s->big_polar) {
+    bk_step_kernel<<<1, kPolarThreads, polar_smem_bytes(m), ctx->stream>>>(
+        s->exch, s->ngroups, s->mg, ld, p, m, s->mu_dev, s->X, xs, s->G, s->Tm, s->hist, s->ctl, s->tol,
+        s->max_iter, s->rank_dev);
+    ctx->launches++;
+    GPS_CHECK_LAUNCH("bk_step_kernel launch");
+    return GPS_OK;
+  }
+  // head -> assemble G -> CholeskyQR2 (gram, chol, apply) x 2 -> X = Q1 S -> finish
+  bk_head_kernel<<<1, 32, 0, ctx->stream>>>(s->exch, s->ngroups, s->mg, ld, s->hist, s->ctl, s->tol, s->max_iter,
+                                            s->pc, m);
+  bk_assemble_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(s->exch, s->mg, ld, m, s->mu_dev, s->G, s->pc);
+  gram_partial_kernel<<<kGramBlocks, kGramThreads, 0, ctx->stream>>>(s->G, ld, p, m, s->gram_part, s->pc);
+  chol_stage_kernel<<<1, 256, chol_smem_bytes(m), ctx->stream>>>(s->gram_part, kGramBlocks, m, p, 1, s->R1, s->Sm,
+                                                                 s->pc);
+  apply_right_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(s->G, s->Sm, ld, m, s->Tm, s->pc, nullptr, 0);
+  gram_partial_kernel<<<kGramBlocks, kGramThreads, 0, ctx->stream>>>(s->Tm, ld, p, m, s->gram_part, s->pc);
+  chol_stage_kernel<<<1, 256, chol_smem_bytes(m), ctx->stream>>>(s->gram_part, kGramBlocks, m, p, 2, s->R1, s->Sm,
+                                                                 s->pc);
+  apply_right_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(s->Tm, s->Sm, ld, m, s->X, s->pc, s->ctl, xs);
+  bk_finish_kernel<<<1, kPolarThreads, polar_smem_bytes(m), ctx->stream>>>(s->G, s->X, xs, ld, p, m, s->ctl, s->pc,
+                                                                           s->rank_dev);
+  ctx->launches += 9;
+  GPS_CHECK_LAUNCH("block polar step launch");
   return GPS_OK;
 }
 
@@ -1310,11 +1414,20 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
   BkPlan pl;
   rc = make_bk_plan(A, pl);
   if (rc) return rc;
+  const char* no_tc = std::getenv("GPSPCA_NO_TC");
+  const bool tc = A->dtype == GPS_F32 && m >= kTcMinM && !(no_tc && no_tc[0] == '1');
   auto* s = new gps_bk();
   s->A = A;
   s->ctx = ctx;
   s->penalty = penalty;
   s->m = m;
+  s->tc = tc;
+  if (tc) {
+    pl.mg = (m + 15) / 16 * 16;  // MMA N
+    s->tc_tiles = static_cast<int>(ceil_div(A->n, kTcTileM));
+    s->tc_grid = std::min(ctx->num_sms, s->tc_tiles);
+    s->tc_gx = static_cast<int>(std::min<int64_t>(32, A->n));
+  }
   s->mg = pl.mg;
   s->ngroups = (m + pl.mg - 1) / pl.mg;
   s->plan = pl;
@@ -1333,24 +1446,53 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
   const size_t ld = A->ld, n = A->n, mp = s->m_pad();
   alloc((void**)&s->X, 2 * mp * ld * sizeof(double));
   alloc((void**)&s->W, 2 * mp * n * sizeof(double));
-  alloc((void**)&s->part_g, size_t(s->ngroups) * pl.grid * pl.mg * ld * sizeof(double));
+  alloc((void**)&s->part_g, size_t(s->ngroups) * (tc ? s->tc_gx : pl.grid) * pl.mg * ld * sizeof(double));
   alloc((void**)&s->part_s, size_t(s->ngroups) * pl.grid * 4 * sizeof(double));
   alloc((void**)&s->exch, size_t(s->ngroups) * s->exch_stride() * sizeof(double));
   alloc((void**)&s->G, size_t(m) * ld * sizeof(double));
   alloc((void**)&s->Tm, size_t(m) * ld * sizeof(double));
-  alloc((void**)&s->mu_dev, size_t(m) * sizeof(double));
+  alloc((void**)&s->mu_dev, size_t(2) * m * sizeof(double));  // mu, then gamma (tensor-core path)
   alloc((void**)&s->hist, (size_t(max_iter) + 1) * sizeof(double));
   if (pl.wide) alloc((void**)&s->wbuf, size_t(pl.mg) * n * sizeof(double));
+  s->big_polar = size_t(ld) * m >= (size_t(1) << 15) && !std::getenv("GPSPCA_HH_POLAR");
+  if (s->big_polar) {
+    alloc((void**)&s->pc, sizeof(PolarCtl));
+    alloc((void**)&s->gram_part, size_t(kGramBlocks) * m * m * sizeof(double));
+    alloc((void**)&s->R1, size_t(m) * m * sizeof(double));
+    alloc((void**)&s->Sm, size_t(m) * m * sizeof(double));
+  }
+  if (tc) {
+    alloc((void**)&s->xhi, mp * ld * sizeof(float));
+    alloc((void**)&s->xlo, mp * ld * sizeof(float));
+    alloc((void**)&s->colmask, n);
+    alloc((void**)&s->part_s_tc, size_t(s->tc_grid) * 4 * sizeof(double));
+  }
   alloc((void**)&s->ctl, sizeof(GpsCtl));
   alloc((void**)&s->rank_dev, sizeof(int));
   if (e == cudaSuccess) e = cudaMallocHost(&s->ctl_host, sizeof(GpsCtl));
   if (e == cudaSuccess) e = cudaMemsetAsync(s->X, 0, 2 * mp * ld * sizeof(double), ctx->stream);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(s->mu_dev, mu, size_t(m) * sizeof(double), cudaMemcpyHostToDevice, ctx->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(s->mu_dev + m, gamma, size_t(m) * sizeof(double), cudaMemcpyHostToDevice, ctx->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
   if (e != cudaSuccess) {
     gps_bk_destroy(s);
     return cuda_fail(e, "gps_bk_create allocation");
+  }
+  if (tc) {
+    rc = tma_encode_2d(&s->tmA, A->d, A->ld, A->n, A->ld * 4, kTcKChunk, kTcTileM);
+    if (rc == GPS_OK) rc = tma_encode_2d(&s->tmXh, s->xhi, A->ld, mp, A->ld * 4, kTcKChunk, s->mg);
+    if (rc == GPS_OK) rc = tma_encode_2d(&s->tmXl, s->xlo, A->ld, mp, A->ld * 4, kTcKChunk, s->mg);
+    if (rc == GPS_OK) {
+      cudaError_t ea = cudaFuncSetAttribute(tc_dots_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            int(tc_smem_bytes(s->mg)));
+      if (ea != cudaSuccess) rc = cuda_fail(ea, "cudaFuncSetAttribute(tc_dots)");
+    }
+    if (rc) {
+      gps_bk_destroy(s);
+      return rc;
+    }
   }
   *out = s;
   return GPS_OK;
@@ -1370,6 +1512,14 @@ int gps_bk_destroy(gps_bk* s) {
   cudaFree(s->Tm);
   cudaFree(s->mu_dev);
   if (s->wbuf) cudaFree(s->wbuf);
+  if (s->xhi) cudaFree(s->xhi);
+  if (s->xlo) cudaFree(s->xlo);
+  if (s->colmask) cudaFree(s->colmask);
+  if (s->part_s_tc) cudaFree(s->part_s_tc);
+  if (s->pc) cudaFree(s->pc);
+  if (s->gram_part) cudaFree(s->gram_part);
+  if (s->R1) cudaFree(s->R1);
+  if (s->Sm) cudaFree(s->Sm);
   cudaFree(s->hist);
   cudaFree(s->ctl);
   cudaFree(s->rank_dev);
@@ -1473,6 +1623,7 @@ int gps_bk_run(gps_bk* s, int poll_every) {
       rc = bk_enqueue_sweeps(s, true);
       if (rc == GPS_OK) rc = bk_enqueue_step(s);
     }
+    s->graph_launches = ctx->launches - before;  // kernels per captured chunk
     ctx->launches = before;
     cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
     if (rc) {
@@ -1488,7 +1639,7 @@ int gps_bk_run(gps_bk* s, int poll_every) {
   const int max_chunks = (s->max_iter + 1 + poll_every - 1) / poll_every + 1;
   for (int c = 0; c < max_chunks; ++c) {
     GPS_CUDA(cudaGraphLaunch(s->graph, ctx->stream));
-    ctx->launches += int64_t(2 * s->ngroups + 1) * poll_every;
+    ctx->launches += s->graph_launches;
     GPS_CUDA(cudaMemcpyAsync(s->ctl_host, s->ctl, sizeof(GpsCtl), cudaMemcpyDeviceToHost, ctx->stream));
     GPS_CUDA(cudaStreamSynchronize(ctx->stream));
     if (s->ctl_host->done) return GPS_OK;

@@ -400,7 +400,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) su_sweep_kernel(const SweepA
 __global__ void __launch_bounds__(256) su_reduce_kernel(const double* __restrict__ part_g,
                                                         const double* __restrict__ part_s, int nparts,
                                                         int ld, double* __restrict__ exch,
-                                                        const GpsCtl* ctl) {
+                                                        const GpsCtl* ctl, int nparts_s) {
   if (ctl != nullptr && ctl->done) return;
   const int row_blocks = (ld + 255) / 256;
   if (blockIdx.x < row_blocks) {
@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(256) su_reduce_kernel(const double* __restrict
     exch[r] = t;
   } else if (threadIdx.x < 4) {
     double t = 0.0;
-    for (int b = 0; b < nparts; ++b) t += part_s[size_t(b) * 4 + threadIdx.x];
+    for (int b = 0; b < nparts_s; ++b) t += part_s[size_t(b) * 4 + threadIdx.x];
     exch[ld + threadIdx.x] = t;
   }
 }

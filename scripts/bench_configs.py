@@ -63,11 +63,17 @@ def time_bk(gps, torch, A, penalty, m, gamma, mu, iters, warmup=2):
     d, it, c = (_native.C.c_int() for _ in range(3))
     _native.check(L.gps_bk_poll(loop.handle, _native.C.byref(d), _native.C.byref(it), _native.C.byref(c)))
     assert not d.value, "block loop stopped early"
-    return (time.perf_counter() - t0) / iters, (m + loop_mg(A) - 1) // loop_mg(A)
+    return (time.perf_counter() - t0) / iters, full_reads(A, m)
 
 
-def loop_mg(A):
-    return 4 if (A.dtype == np.float32 and A.p <= 4096) else 2
+def full_reads(A, m):
+    """Full passes over A per block iteration: one for the tensor-core path
+    (fp32, m >= 16: tc_dots reads A once; tc_update re-reads only the active
+    columns), else one per group of MG components."""
+    if A.dtype == np.float32 and m >= 16:
+        return 1
+    mg = 4 if (A.dtype == np.float32 and A.p <= 4096) else 2
+    return (m + mg - 1) // mg
 
 
 def main():
