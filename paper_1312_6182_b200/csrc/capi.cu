@@ -1193,6 +1193,7 @@ struct gps_bk {
   // tensor-core path (fp32 A, m >= 16): split X, column activity, TMA maps
   bool tc = false;
   int tc_grid = 0, tc_gx = 0, tc_tiles = 0;
+  int tc_rings[3] = {kTcAStages, kTcLoStages, kTcXStages};
   float* xhi = nullptr;
   float* xlo = nullptr;
   unsigned char* colmask = nullptr;
@@ -1318,13 +1319,27 @@ int bk_enqueue_tc(gps_bk* s, bool with_ctl) {
   a.ctl = ctl;
   a.num_tiles = s->tc_tiles;
   a.gamma = s->mu_dev + s->m;  // gamma stored after mu in mu_dev
-  tc_dots_kernel<<<s->tc_grid, kTcThreads, tc_smem_bytes(np), ctx->stream>>>(s->tmA, s->tmXh, s->tmXl, a);
+  a.a_stages = s->tc_rings[0];
+  a.lo_stages = s->tc_rings[1];
+  a.x_stages = s->tc_rings[2];
+  {
+    static const char* sg = getenv("GPSPCA_TC_SEG");  // tuning experiments only
+    a.seg_chunks = sg && atoi(sg) > 0 ? atoi(sg) : kTcSegChunks;
+  }
+  {
+    static const char* pr = getenv("GPSPCA_TC_PROBE");  // timing experiments only
+    a.probe = pr ? atoi(pr) : 0;
+  }
+  tc_dots_kernel<<<s->tc_grid, kTcThreads, tc_smem_bytes(np, a.a_stages, a.lo_stages, a.x_stages), ctx->stream>>>(
+      s->tmA, s->tmXh, s->tmXl, a);
   ctx->launches++;
   dim3 g2(s->tc_gx, static_cast<unsigned>((A->ld + kTcUpdRows - 1) / kTcUpdRows),
           static_cast<unsigned>((s->m + kTcUpdComps - 1) / kTcUpdComps));
-  tc_update_kernel<<<g2, 256, 0, ctx->stream>>>(static_cast<const float*>(A->d), A->n, ld, s->m, s->colmask, s->W,
-                                                 int64_t(s->m_pad()) * A->n, np, s->part_g, ctl);
-  ctx->launches++;
+  if (!(a.probe & 16)) {
+    tc_update_kernel<<<g2, 256, 0, ctx->stream>>>(static_cast<const float*>(A->d), A->n, ld, s->m, s->colmask,
+                                                   s->W, int64_t(s->m_pad()) * A->n, np, s->part_g, ctl);
+    ctx->launches++;
+  }
   GPS_CHECK_LAUNCH("tensor-core block sweep launch");
   return launch_reduce(ctx, s->part_g, s->part_s_tc, s->tc_gx, np * ld, s->exch, ctl, s->tc_grid);
 }
@@ -1484,9 +1499,18 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
     rc = tma_encode_2d(&s->tmA, A->d, A->ld, A->n, A->ld * 4, kTcKChunk, kTcTileM);
     if (rc == GPS_OK) rc = tma_encode_2d(&s->tmXh, s->xhi, A->ld, mp, A->ld * 4, kTcKChunk, s->mg);
     if (rc == GPS_OK) rc = tma_encode_2d(&s->tmXl, s->xlo, A->ld, mp, A->ld * 4, kTcKChunk, s->mg);
+    if (const char* rings = getenv("GPSPCA_TC_RINGS")) {  // tuning experiments: "A,lo,X"
+      int r[3];
+      if (sscanf(rings, "%d,%d,%d", &r[0], &r[1], &r[2]) == 3 && r[0] >= 2 && r[1] >= 1 && r[2] >= 1 &&
+          r[0] <= kTcMaxStages && r[1] <= 4 && r[2] <= kTcMaxStages)
+        for (int i = 0; i < 3; ++i) s->tc_rings[i] = r[i];
+    }
+    if (rc == GPS_OK && tc_smem_bytes(s->mg, s->tc_rings[0], s->tc_rings[1], s->tc_rings[2]) > 227 * 1024)
+      rc = fail(GPS_E_ARG, "tensor-core ring configuration exceeds shared memory");
     if (rc == GPS_OK) {
-      cudaError_t ea = cudaFuncSetAttribute(tc_dots_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            int(tc_smem_bytes(s->mg)));
+      cudaError_t ea = cudaFuncSetAttribute(
+          tc_dots_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+          int(tc_smem_bytes(s->mg, s->tc_rings[0], s->tc_rings[1], s->tc_rings[2])));
       if (ea != cudaSuccess) rc = cuda_fail(ea, "cudaFuncSetAttribute(tc_dots)");
     }
     if (rc) {
@@ -1792,3 +1816,18 @@ int gps_orthonormalize(gps_ctx* ctx, const double* M, int64_t p, int m, double* 
 }
 
 }  // extern "C"
+
+// Tuning diagnostics (not part of the public header): per-role cycle
+// counters of tc_dots_kernel when GPSPCA_TC_PROBE has bit 64 set.  reset
+// clears them; otherwise copies up to n counters into out.
+extern "C" int gpsdbg_tc_profile(unsigned long long* out, int n, int reset) {
+  if (reset) {
+    unsigned long long z[16] = {};
+    return cudaMemcpyToSymbol(gps::g_tc_prof, z, sizeof(z)) == cudaSuccess ? GPS_OK : GPS_E_CUDA;
+  }
+  if (!out || n < 1) return GPS_E_ARG;
+  return cudaMemcpyFromSymbol(out, gps::g_tc_prof, sizeof(unsigned long long) * size_t(std::min(n, 16))) ==
+                 cudaSuccess
+             ? GPS_OK
+             : GPS_E_CUDA;
+}

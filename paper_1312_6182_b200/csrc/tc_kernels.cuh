@@ -14,8 +14,8 @@
 //               column activity flag.  A is read from HBM once.
 // T2 tc_update: G_j = sum over ACTIVE columns of w_ij a_i (fp64), row chunks
 //               x component groups; reads only the active columns again.
-// Roles of T1 (12 warps): w0 TMA producer, w1 MMA issuer (+TMEM owner),
-// w4-7 epilogue (warp % 4 selects the TMEM lane quarter), w8-11 converters.
+// Roles of T1 (12 warps): w0 A producer (TMA), w1 MMA issuer (+TMEM owner),
+// w2 X producer (TMA), w4-7 epilogue (warp % 4 selects the TMEM lane quarter), w8-11 converters.
 #pragma once
 
 #include <cuda.h>
@@ -26,12 +26,15 @@ namespace gps {
 
 constexpr int kTcTileM = 128;    // columns of A per tile (MMA M)
 constexpr int kTcKChunk = 32;    // rows of A per stage (128 bytes of fp32)
-constexpr int kTcStages = 4;
+constexpr int kTcAStages = 10;  // default A ring depth (HBM stream)
+constexpr int kTcLoStages = 2;  // default TMEM A_hi / A_lo slots (converter output)
+constexpr int kTcXStages = 3;   // default X_hi | X_lo ring depth (L2-resident)
+constexpr int kTcMaxStages = 16;
 constexpr int kTcThreads = 384;  // 12 warps
 constexpr int kTcMaxN = 64;
 constexpr int kTcMinM = 16;      // block solves with m >= 16 (fp32 A) take this path
 constexpr int kTcConvThreads = 128;  // converter warps 8-11
-constexpr int kTcSegChunks = 2;  // TMEM accumulation segment: 2 chunks = 64 rows, drained to fp64
+constexpr int kTcSegChunks = 4;  // TMEM accumulation segment: 4 chunks = 128 rows, drained to fp64
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
   asm volatile(
@@ -69,6 +72,26 @@ __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t a, uint64_t 
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+// Warp-converged forms: every lane executes the call with identical
+// operands and elect.sync picks the issuing lane inside the asm, so the
+// compiler keeps descriptors in uniform registers (a single-thread branch
+// instead costs a per-instruction R2UR + waterfall loop, ~90 clocks/MMA).
+__device__ __forceinline__ void umma_tf32_warp(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_warp(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
       : "memory");
 }
 
@@ -132,14 +155,87 @@ struct TcDotsArgs {
   double* part_s;          // [grid][4]
   const GpsCtl* ctl;
   int num_tiles;
+  int a_stages, lo_stages, x_stages;  // ring depths (<= kTcMaxStages)
+  int seg_chunks;                     // chunks per TMEM accumulation segment
+  int probe;  // timing experiments: 1 no A_lo, 2 one MMA, 4 no TMEM drain, 8 no X loads,
+              // 16 no update, 32 no TMEM stores, 64 cycle accounting
 };
 
-__host__ __device__ inline size_t tc_stage_bytes(int n_pad) {
-  return size_t(2) * kTcTileM * kTcKChunk * 4 + size_t(2) * n_pad * kTcKChunk * 4;
+// Operand staging of T1.  Shared memory is the scarce resource (every
+// tcgen05.mma operand read from shared memory, every TMA write and every
+// converter access share its ~128 B/clock), so A passes through it once:
+//   A ring    SA x 16 KB in shared memory (TMA, evict-first) -> converters
+//   A_hi/A_lo SL slots x 64 TMEM columns, written by the converters with
+//             tcgen05.st, read by the MMAs as the TMEM-resident A operand
+//   X ring    SX x (X_hi | X_lo) chunk in shared memory (TMA, evict-last)
+// TMEM: columns [0, 4 NP) = 2 accumulator buffers of [A X_hi | A_hi X_lo],
+// columns [256, 256 + 64 SL) = the A_hi / A_lo slots; 512 columns allocated.
+constexpr uint32_t kTcTmemCols = 512;
+constexpr uint32_t kTcTmemAOff = 256;
+__host__ __device__ inline size_t tc_a_bytes() { return size_t(kTcTileM) * kTcKChunk * 4; }
+__host__ __device__ inline size_t tc_x_bytes(int n_pad) { return size_t(n_pad) * kTcKChunk * 4; }
+__host__ __device__ inline size_t tc_smem_bytes(int n_pad, int sa, int sl, int sx) {
+  (void)sl;
+  return 1024 /*align slack*/ + sa * tc_a_bytes() + sx * 2 * tc_x_bytes(n_pad) + 4096 /*barriers, params*/;
 }
-__host__ __device__ inline size_t tc_smem_bytes(int n_pad) {
-  return 1024 /*align slack*/ + kTcStages * tc_stage_bytes(n_pad) + 4096 /*barriers, params*/;
+
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar,
+                                                 uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, "
+      "%4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y), "l"(policy)
+      : "memory");
 }
+
+// tcgen05.mma with the A operand in TMEM (M = 128 lanes, K = 8 columns).
+__device__ __forceinline__ void umma_tf32_ts_warp(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                                  uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// Optional per-role cycle accounting (tuning diagnostics, TcDotsArgs::probe & 64).
+__device__ unsigned long long g_tc_prof[16];
+struct TcProf {
+  bool on;
+  long long t;
+  __device__ __forceinline__ void start() {
+    if (on) t = clock64();
+  }
+  __device__ __forceinline__ void stop(unsigned long long& acc) {
+    if (on) acc += static_cast<unsigned long long>(clock64() - t);
+  }
+};
+
+// Ring cursor: slot index and the phase parity of its current use.
+struct TcRing {
+  int slot = 0;
+  uint32_t ph = 0;
+  __device__ __forceinline__ void next(int n) {
+    if (++slot == n) {
+      slot = 0;
+      ph ^= 1u;
+    }
+  }
+};
 
 __global__ void __launch_bounds__(kTcThreads, 1)
     tc_dots_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmXh,
@@ -150,14 +246,19 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int NP = a.n_pad;
-  const size_t a_bytes = size_t(kTcTileM) * kTcKChunk * 4;   // 16 KB
-  const size_t x_bytes = size_t(NP) * kTcKChunk * 4;
-  const size_t stage_bytes = 2 * a_bytes + 2 * x_bytes;
-  unsigned char* stages = smem;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTcStages * stage_bytes);
-  uint64_t* conv = full + kTcStages;
-  uint64_t* empty = conv + kTcStages;
-  uint64_t* tfull = empty + kTcStages;  // 2 accumulator buffers
+  const int SA = a.a_stages, SL = a.lo_stages, SX = a.x_stages;
+  const int SEG = a.seg_chunks;
+  const size_t a_bytes = tc_a_bytes();  // 16 KB
+  const size_t x_bytes = tc_x_bytes(NP);
+  unsigned char* aring = smem;
+  unsigned char* xring = aring + SA * a_bytes;  // [stage][hi | lo]
+  uint64_t* a_full = reinterpret_cast<uint64_t*>(xring + SX * 2 * x_bytes);
+  uint64_t* a_empty = a_full + SA;
+  uint64_t* lo_full = a_empty + SA;  // TMEM A_hi / A_lo slots
+  uint64_t* lo_empty = lo_full + SL;
+  uint64_t* x_full = lo_empty + SL;
+  uint64_t* x_empty = x_full + SX;
+  uint64_t* tfull = x_empty + SX;  // 2 accumulator buffers
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   double* sgam = reinterpret_cast<double*>(tmem_base_slot + 4);
@@ -166,13 +267,23 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int kchunks = a.ld / kTcKChunk;
-  const uint32_t idesc = umma_idesc_tf32(kTcTileM, NP);
+  // MMA 1: A_hi [X_hi | X_lo] (N = 2 NP, the X slot holds X_hi rows then X_lo rows);
+  // MMA 2: A_lo X_hi (N = NP) accumulating into the first NP columns.
+  const uint32_t idesc2 = umma_idesc_tf32(kTcTileM, 2 * NP);
+  const uint32_t idesc1 = umma_idesc_tf32(kTcTileM, NP);
 
   if (tid == 0) {
-    for (int i = 0; i < kTcStages; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&conv[i], 4);   // 4 converter warps
-      mbar_init(&empty[i], 1);  // tcgen05.commit
+    for (int i = 0; i < SA; ++i) {
+      mbar_init(&a_full[i], 1);
+      mbar_init(&a_empty[i], 4);  // 4 converter warps have read the slot
+    }
+    for (int i = 0; i < SL; ++i) {
+      mbar_init(&lo_full[i], 4);  // 4 converter warps stored their TMEM lanes
+      mbar_init(&lo_empty[i], 1);  // tcgen05.commit
+    }
+    for (int i = 0; i < SX; ++i) {
+      mbar_init(&x_full[i], 1);
+      mbar_init(&x_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);   // tcgen05.commit
@@ -185,10 +296,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     smu[j] = a.mu[j];
   }
   if (warp == 1) {
-    // 2 accumulator buffers of NP columns; allocation is a power of two >= 32
-    const uint32_t cols = (2 * NP <= 32) ? 32 : (2 * NP <= 64) ? 64 : 128;
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_slot)),
-                 "r"(cols)
+                 "r"(kTcTmemCols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -207,96 +316,160 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int total_chunks = my_tiles * kchunks;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ producer
+    // ---------------------------------------------------------- A producer
     if (lane == 0) {
-      int stage = 0;
-      uint32_t ph = 0;
+      uint64_t policy;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+      TcRing r;
+      TcProf pf{(a.probe & 64) != 0, 0};
+      unsigned long long w0 = 0;
+      int t = int(blockIdx.x), kc = 0;
       for (int c = 0; c < total_chunks; ++c) {
-        if (c >= kTcStages) mbar_wait_sleep(&empty[stage], ph ^ 1u);
-        const int t = int(blockIdx.x) + (c / kchunks) * int(gridDim.x);
-        const int kc = c % kchunks;
-        unsigned char* st = stages + stage * stage_bytes;
-        mbar_arrive_expect_tx(&full[stage], static_cast<uint32_t>(a_bytes + 2 * x_bytes));
-        tma_load_2d(st, &tmA, kc * kTcKChunk, t * kTcTileM, &full[stage]);
-        tma_load_2d(st + 2 * a_bytes, &tmXh, kc * kTcKChunk, 0, &full[stage]);
-        tma_load_2d(st + 2 * a_bytes + x_bytes, &tmXl, kc * kTcKChunk, 0, &full[stage]);
-        if (++stage == kTcStages) {
-          stage = 0;
-          ph ^= 1u;
+        pf.start();
+        if (c >= SA) mbar_wait_sleep(&a_empty[r.slot], r.ph ^ 1u);
+        pf.stop(w0);
+        mbar_arrive_expect_tx(&a_full[r.slot], static_cast<uint32_t>(a_bytes));
+        tma_load_2d_hint(aring + r.slot * a_bytes, &tmA, kc * kTcKChunk, t * kTcTileM, &a_full[r.slot], policy);
+        r.next(SA);
+        if (++kc == kchunks) {
+          kc = 0;
+          t += int(gridDim.x);
         }
       }
+      if (pf.on) atomicAdd(&g_tc_prof[1], w0);
+    }
+  } else if (warp == 2) {
+    // ---------------------------------------------------------- X producer
+    if (lane == 0) {
+      uint64_t policy;
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(policy));
+      TcRing r;
+      TcProf pf{(a.probe & 64) != 0, 0};
+      unsigned long long w0 = 0;
+      int kc = 0;
+      for (int c = 0; c < total_chunks; ++c) {
+        pf.start();
+        if (c >= SX) mbar_wait_sleep(&x_empty[r.slot], r.ph ^ 1u);
+        pf.stop(w0);
+        const bool lx = !(a.probe & 8) || c < SX;
+        unsigned char* st = xring + r.slot * 2 * x_bytes;
+        mbar_arrive_expect_tx(&x_full[r.slot], static_cast<uint32_t>(lx ? 2 * x_bytes : 0));
+        if (lx) {
+          tma_load_2d_hint(st, &tmXh, kc * kTcKChunk, 0, &x_full[r.slot], policy);
+          tma_load_2d_hint(st + x_bytes, &tmXl, kc * kTcKChunk, 0, &x_full[r.slot], policy);
+        }
+        r.next(SX);
+        if (++kc == kchunks) kc = 0;
+      }
+      if (pf.on) atomicAdd(&g_tc_prof[2], w0);
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------- MMA issuer
-    // Accumulate kTcSegChunks chunks (256 rows of A) per TMEM segment; the
-    // epilogue drains each segment into fp64, so the tensor core's fp32
-    // accumulation never spans more than 256 rows.
-    int stage = 0;
-    uint32_t ph = 0;
+    // The whole warp runs the loop (uniform control flow and operands);
+    // elect.sync inside the asm issues each MMA / commit once.  Each TMEM
+    // segment accumulates kTcSegChunks chunks (128 rows of A); the epilogue
+    // drains it into fp64, so the tensor core's fp32 accumulation never
+    // spans more than 128 rows.
+    const uint64_t dx = umma_desc_sw128(xring);
+    const uint64_t x_step = (2 * x_bytes) >> 4;
+    TcRing rl, rx;
+    TcProf pf{(a.probe & 64) != 0, 0};
+    unsigned long long w3 = 0, w4 = 0, w5 = 0;
+    const long long t_role = clock64();
     int seg = 0;
     for (int tt = 0; tt < my_tiles; ++tt) {
-      for (int k0 = 0; k0 < kchunks; k0 += kTcSegChunks, ++seg) {
+      for (int k0 = 0; k0 < kchunks; k0 += SEG, ++seg) {
         const int b = seg & 1;
+        pf.start();
         if (seg >= 2) mbar_wait(&tempty[b], static_cast<uint32_t>(((seg - 2) >> 1) & 1));
+        pf.stop(w3);
         tc_fence_after();
-        const uint32_t dtm = tmem_base + uint32_t(b * NP);
-        const int k1 = (k0 + kTcSegChunks < kchunks) ? k0 + kTcSegChunks : kchunks;
+        const uint32_t dtm = tmem_base + uint32_t(b * 2 * NP);
+        const int k1 = (k0 + SEG < kchunks) ? k0 + SEG : kchunks;
         for (int kc = k0; kc < k1; ++kc) {
-          mbar_wait(&conv[stage], ph);
+          pf.start();
+          mbar_wait(&lo_full[rl.slot], rl.ph);
+          pf.stop(w4);
+          pf.start();
+          mbar_wait(&x_full[rx.slot], rx.ph);
+          pf.stop(w5);
           tc_fence_after();
-          unsigned char* st = stages + stage * stage_bytes;
-          if (lane == 0) {
+          const uint32_t th = tmem_base + kTcTmemAOff + uint32_t(rl.slot) * 64;  // A_hi; A_lo at +32
+          const uint64_t bx = dx + uint64_t(rx.slot) * x_step;
 #pragma unroll
-            for (int k = 0; k < kTcKChunk / 8; ++k) {
-              const uint64_t ah = umma_desc_sw128(st) + uint64_t((k * 32) >> 4);
-              const uint64_t al = umma_desc_sw128(st + a_bytes) + uint64_t((k * 32) >> 4);
-              const uint64_t bh = umma_desc_sw128(st + 2 * a_bytes) + uint64_t((k * 32) >> 4);
-              const uint64_t bl = umma_desc_sw128(st + 2 * a_bytes + x_bytes) + uint64_t((k * 32) >> 4);
-              const uint32_t first = (kc == k0 && k == 0) ? 0u : 1u;
-              umma_tf32(dtm, al, bh, idesc, first);
-              umma_tf32(dtm, ah, bl, idesc, 1u);
-              umma_tf32(dtm, ah, bh, idesc, 1u);
-            }
-            umma_commit(&empty[stage]);
-            if (kc == k1 - 1) umma_commit(&tfull[b]);
+          for (int k = 0; k < kTcKChunk / 8; ++k) {
+            const uint32_t first = (kc == k0 && k == 0) ? 0u : 1u;
+            umma_tf32_ts_warp(dtm, th + 8 * k, bx + 2 * k, idesc2, first);
+            if (!(a.probe & 2)) umma_tf32_ts_warp(dtm, th + 32 + 8 * k, bx + 2 * k, idesc1, 1u);
           }
-          __syncwarp();
-          if (++stage == kTcStages) {
-            stage = 0;
-            ph ^= 1u;
-          }
+          umma_commit_warp(&lo_empty[rl.slot]);
+          umma_commit_warp(&x_empty[rx.slot]);
+          if (kc == k1 - 1) umma_commit_warp(&tfull[b]);
+          rl.next(SL);
+          rx.next(SX);
         }
       }
     }
+    if (pf.on && lane == 0) {
+      atomicAdd(&g_tc_prof[3], w3);
+      atomicAdd(&g_tc_prof[4], w4);
+      atomicAdd(&g_tc_prof[5], w5);
+      atomicAdd(&g_tc_prof[6], static_cast<unsigned long long>(clock64() - t_role));
+    }
   } else if (warp >= 8) {
     // ---------------------------------------------------- converter warps
-    const int ct = tid - 8 * 32;  // 0..127
-    int stage = 0;
-    uint32_t ph = 0;
+    // Thread r owns tile row r (one column of A, TMEM lane r): it reads its
+    // 128-byte row out of the 128-byte-swizzled A slot (16-byte chunk c sits
+    // at c ^ (r & 7)), splits A = A_hi + A_lo with A_hi = trunc_tf32(A)
+    // (A_lo exact in fp32) and stores both halves to its TMEM lane.
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    TcRing ra, rl;
+    TcProf pf{(a.probe & 64) != 0 && warp == 8, 0};
+    unsigned long long w7 = 0, w8 = 0, w9 = 0;
+    const long long t_role = clock64();
     for (int c = 0; c < total_chunks; ++c) {
-      mbar_wait(&full[stage], ph);
-      // The MMA reads tf32 operands by dropping the low 13 mantissa bits, so
-      // A itself serves as A_hi; A_lo = A - trunc_tf32(A) is exact in fp32
-      // (two integer/FP ops per element, no conversion-pipe traffic).
-      const float* Ah = reinterpret_cast<const float*>(stages + stage * stage_bytes);
-      float* Al = reinterpret_cast<float*>(stages + stage * stage_bytes) + kTcTileM * kTcKChunk;
-#pragma unroll 4
-      for (int i = ct * 4; i < kTcTileM * kTcKChunk; i += kTcConvThreads * 4) {
-        const float4 v = *reinterpret_cast<const float4*>(Ah + i);
-        float4 l;
-        l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-        l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-        l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-        l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-        *reinterpret_cast<float4*>(Al + i) = l;
+      pf.start();
+      mbar_wait(&a_full[ra.slot], ra.ph);
+      pf.stop(w7);
+      const unsigned char* row = aring + ra.slot * a_bytes + r * 128;
+      uint32_t hi[32], lo[32];
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) {
+        const float4 v = *reinterpret_cast<const float4*>(row + ((cc ^ (r & 7)) << 4));
+        const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t h = __float_as_uint(e[u]) & 0xFFFFE000u;
+          hi[cc * 4 + u] = h;
+          lo[cc * 4 + u] = (a.probe & 1) ? 0u : __float_as_uint(e[u] - __uint_as_float(h));
+        }
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&conv[stage]);
-      if (++stage == kTcStages) {
-        stage = 0;
-        ph ^= 1u;
+      if (lane == 0) mbar_arrive(&a_empty[ra.slot]);  // the slot's bytes are in registers
+      pf.start();
+      if (c >= SL) mbar_wait(&lo_empty[rl.slot], rl.ph ^ 1u);
+      pf.stop(w8);
+      tc_fence_after();
+      const uint32_t ta = tmem_base + (uint32_t(q * 32) << 16) + kTcTmemAOff + uint32_t(rl.slot) * 64;
+      pf.start();
+      if (!(a.probe & 32)) {
+        tmem_st32(ta, hi);
+        tmem_st32(ta + 32, lo);
+        tmem_wait_st();
       }
+      pf.stop(w9);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&lo_full[rl.slot]);
+      ra.next(SA);
+      rl.next(SL);
+    }
+    if (pf.on && lane == 0) {
+      atomicAdd(&g_tc_prof[7], w7);
+      atomicAdd(&g_tc_prof[8], w8);
+      atomicAdd(&g_tc_prof[9], w9);
+      atomicAdd(&g_tc_prof[10], static_cast<unsigned long long>(clock64() - t_role));
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------ epilogue warps
@@ -304,29 +477,38 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int et = tid - 4 * 32;
     double f_acc = 0.0, nnz_acc = 0.0;
     double* wbase = a.w_out != nullptr ? a.w_out + parity * a.w_stride : nullptr;
+    TcProf pf{(a.probe & 64) != 0 && warp == 4, 0};
+    unsigned long long w11 = 0, w12 = 0;
+    const long long t_role = clock64();
     int seg = 0;
     for (int tt = 0; tt < my_tiles; ++tt) {
       const int t = int(blockIdx.x) + tt * int(gridDim.x);
       double c[kTcMaxN];
 #pragma unroll
       for (int j = 0; j < kTcMaxN; ++j) c[j] = 0.0;
-      for (int k0 = 0; k0 < kchunks; k0 += kTcSegChunks, ++seg) {
+      for (int k0 = 0; k0 < kchunks; k0 += SEG, ++seg) {
         const int b = seg & 1;
+        pf.start();
         mbar_wait(&tfull[b], static_cast<uint32_t>((seg >> 1) & 1));
+        pf.stop(w11);
+        pf.start();
         tc_fence_after();
 #pragma unroll
         for (int j0 = 0; j0 < kTcMaxN; j0 += 16) {
-          if (j0 < NP) {
-            float v[16];
-            tmem_ld16(tmem_base + (uint32_t(q * 32) << 16) + uint32_t(b * NP + j0), v);
+          if (j0 < NP && !(a.probe & 4)) {
+            float v[16], vl[16];
+            const uint32_t ta = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(b * 2 * NP + j0);
+            tmem_ld16(ta, v);
+            tmem_ld16(ta + uint32_t(NP), vl);
             tmem_wait_ld();
 #pragma unroll
-            for (int u = 0; u < 16; ++u) c[j0 + u] += static_cast<double>(v[u]);
+            for (int u = 0; u < 16; ++u) c[j0 + u] += static_cast<double>(v[u] + vl[u]);
           }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[b]);
+        pf.stop(w12);
       }
       const int64_t col = int64_t(t) * kTcTileM + q * 32 + lane;
       if (col < a.n) {
@@ -346,6 +528,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         a.colmask[col] = any ? 1 : 0;
       }
     }
+    if (pf.on && lane == 0) {
+      atomicAdd(&g_tc_prof[11], w11);
+      atomicAdd(&g_tc_prof[12], w12);
+      atomicAdd(&g_tc_prof[13], static_cast<unsigned long long>(clock64() - t_role));
+    }
     sred[et * 2 + 0] = f_acc;
     sred[et * 2 + 1] = nnz_acc;
   }
@@ -356,8 +543,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     a.part_s[size_t(blockIdx.x) * 4 + tid] = t;
   }
   if (warp == 1) {
-    const uint32_t cols = (2 * NP <= 32) ? 32 : (2 * NP <= 64) ? 64 : 128;
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(cols) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTcTmemCols)
+                 : "memory");
   }
 }
 
