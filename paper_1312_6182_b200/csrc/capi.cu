@@ -1430,7 +1430,9 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
   rc = make_bk_plan(A, pl);
   if (rc) return rc;
   const char* no_tc = std::getenv("GPSPCA_NO_TC");
-  const bool tc = A->dtype == GPS_F32 && m >= kTcMinM && !(no_tc && no_tc[0] == '1');
+  const char* tc_min_env = std::getenv("GPSPCA_TC_MIN_M");  // tuning experiments
+  const int tc_min = tc_min_env && atoi(tc_min_env) > 0 ? atoi(tc_min_env) : kTcMinM;
+  const bool tc = A->dtype == GPS_F32 && m >= tc_min && !(no_tc && no_tc[0] == '1');
   auto* s = new gps_bk();
   s->A = A;
   s->ctx = ctx;

@@ -32,7 +32,7 @@ constexpr int kTcXStages = 3;   // default X_hi | X_lo ring depth (L2-resident)
 constexpr int kTcMaxStages = 16;
 constexpr int kTcThreads = 384;  // 12 warps
 constexpr int kTcMaxN = 64;
-constexpr int kTcMinM = 16;      // block solves with m >= 16 (fp32 A) take this path
+constexpr int kTcMinM = 5;       // block solves with m >= 5 (fp32 A) take this path (one A read vs ceil(m/4))
 constexpr int kTcConvThreads = 128;  // converter warps 8-11
 constexpr int kTcSegChunks = 4;  // TMEM accumulation segment: 4 chunks = 128 rows, drained to fp64
 

@@ -229,5 +229,7 @@ class TestLargeBlock:
             G_ref = oracle.block_gradient(A64, C, g, mu, pen)
             G = gps.ascent_direction_block(A, X, g, mu, pen)
             f = (gps.objective_bl1 if pen == "l1" else gps.objective_bl0)(A, X, g, mu)
-            assert f_ref > 0 and f == pytest.approx(f_ref, rel=1e-5)
+            # fp32 storage, m >= 5: the tensor-core sweep; the fp32-mode
+            # contract is 1e-4 relative
+            assert f_ref > 0 and f == pytest.approx(f_ref, rel=1e-4)
             np.testing.assert_allclose(G, G_ref, rtol=1e-4, atol=1e-3 * np.abs(G_ref).max())

@@ -1,5 +1,5 @@
 """Large-problem block paths: the tensor-core (tcgen05, 3xTF32) sweep for
-m >= 16 with fp32 storage, and the multi-CTA CholeskyQR2 polar step for
+m >= 5 with fp32 storage, and the multi-CTA CholeskyQR2 polar step for
 large p*m, each against the fp64 oracle and against the exact paths."""
 
 import os
