@@ -1193,9 +1193,10 @@ struct gps_bk {
   // tensor-core path (fp32 A, m >= 16): split X, column activity, TMA maps
   bool tc = false;
   int tc_grid = 0, tc_gx = 0, tc_tiles = 0;
-  int tc_rings[3] = {kTcAStages, kTcLoStages, kTcXStages};
-  float* xhi = nullptr;
-  float* xlo = nullptr;
+  int tc_rings[2] = {kTcAStages, kTcXStages};  // A ring, X ring
+  int* col_exp = nullptr;                        // n scale exponents (tensor-core path)
+  __half* xhi = nullptr;  // X1 (fp16)
+  __half* xlo = nullptr;  // X2 (fp16)
   unsigned char* colmask = nullptr;
   double* part_s_tc = nullptr;
   CUtensorMap tmA, tmXh, tmXl;
@@ -1274,8 +1275,8 @@ int bk_launch_group(gps_bk* s, int g, bool with_ctl, int write_w) {
 }
 
 // ---- tensor-core path helpers
-int tma_encode_2d(CUtensorMap* map, const void* base, uint64_t dim0, uint64_t dim1, uint64_t stride1_bytes,
-                  uint32_t box0, uint32_t box1) {
+int tma_encode_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dtype, uint64_t dim0, uint64_t dim1,
+                  uint64_t stride1_bytes, uint32_t box0, uint32_t box1) {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
   std::call_once(once, [] {
@@ -1290,7 +1291,7 @@ int tma_encode_2d(CUtensorMap* map, const void* base, uint64_t dim0, uint64_t di
   const cuuint64_t strides[1] = {stride1_bytes};
   const cuuint32_t box[2] = {box0, box1};
   const cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+  CUresult r = fn(map, dtype, 2, const_cast<void*>(base), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(GPS_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
@@ -1320,8 +1321,8 @@ int bk_enqueue_tc(gps_bk* s, bool with_ctl) {
   a.num_tiles = s->tc_tiles;
   a.gamma = s->mu_dev + s->m;  // gamma stored after mu in mu_dev
   a.a_stages = s->tc_rings[0];
-  a.lo_stages = s->tc_rings[1];
-  a.x_stages = s->tc_rings[2];
+  a.x_stages = s->tc_rings[1];
+  a.col_exp = s->col_exp;
   {
     static const char* sg = getenv("GPSPCA_TC_SEG");  // tuning experiments only
     a.seg_chunks = sg && atoi(sg) > 0 ? atoi(sg) : kTcSegChunks;
@@ -1330,7 +1331,7 @@ int bk_enqueue_tc(gps_bk* s, bool with_ctl) {
     static const char* pr = getenv("GPSPCA_TC_PROBE");  // timing experiments only
     a.probe = pr ? atoi(pr) : 0;
   }
-  tc_dots_kernel<<<s->tc_grid, kTcThreads, tc_smem_bytes(np, a.a_stages, a.lo_stages, a.x_stages), ctx->stream>>>(
+  tc_dots_kernel<<<s->tc_grid, kTcThreads, tc_smem_bytes(np, a.a_stages, a.x_stages), ctx->stream>>>(
       s->tmA, s->tmXh, s->tmXl, a);
   ctx->launches++;
   dim3 g2(s->tc_gx, static_cast<unsigned>((A->ld + kTcUpdRows - 1) / kTcUpdRows),
@@ -1479,9 +1480,10 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
     alloc((void**)&s->Sm, size_t(m) * m * sizeof(double));
   }
   if (tc) {
-    alloc((void**)&s->xhi, mp * ld * sizeof(float));
-    alloc((void**)&s->xlo, mp * ld * sizeof(float));
-    alloc((void**)&s->colmask, n);
+    alloc((void**)&s->xhi, mp * ld * sizeof(__half));
+    alloc((void**)&s->xlo, mp * ld * sizeof(__half));
+    alloc((void**)&s->col_exp, n * sizeof(int));
+    alloc((void**)&s->colmask, 2 * n);
     alloc((void**)&s->part_s_tc, size_t(s->tc_grid) * 4 * sizeof(double));
   }
   alloc((void**)&s->ctl, sizeof(GpsCtl));
@@ -1498,22 +1500,33 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
     return cuda_fail(e, "gps_bk_create allocation");
   }
   if (tc) {
-    rc = tma_encode_2d(&s->tmA, A->d, A->ld, A->n, A->ld * 4, kTcKChunk, kTcTileM);
-    if (rc == GPS_OK) rc = tma_encode_2d(&s->tmXh, s->xhi, A->ld, mp, A->ld * 4, kTcKChunk, s->mg);
-    if (rc == GPS_OK) rc = tma_encode_2d(&s->tmXl, s->xlo, A->ld, mp, A->ld * 4, kTcKChunk, s->mg);
-    if (const char* rings = getenv("GPSPCA_TC_RINGS")) {  // tuning experiments: "A,lo,X"
-      int r[3];
-      if (sscanf(rings, "%d,%d,%d", &r[0], &r[1], &r[2]) == 3 && r[0] >= 2 && r[1] >= 1 && r[2] >= 1 &&
-          r[0] <= kTcMaxStages && r[1] <= 4 && r[2] <= kTcMaxStages)
-        for (int i = 0; i < 3; ++i) s->tc_rings[i] = r[i];
+    rc = tma_encode_2d(&s->tmA, A->d, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, A->ld, A->n, A->ld * 4, kTcBoxK, kTcTileM);
+    if (rc == GPS_OK)
+      rc = tma_encode_2d(&s->tmXh, s->xhi, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, A->ld, mp, A->ld * 2, kTcKChunk, s->mg);
+    if (rc == GPS_OK)
+      rc = tma_encode_2d(&s->tmXl, s->xlo, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, A->ld, mp, A->ld * 2, kTcKChunk, s->mg);
+    if (const char* rings = getenv("GPSPCA_TC_RINGS")) {  // tuning experiments: "A,X"
+      int r[2];
+      if (sscanf(rings, "%d,%d", &r[0], &r[1]) == 2 && r[0] >= 2 && r[1] >= 1 && r[0] <= kTcMaxStages &&
+          r[1] <= kTcMaxStages)
+        for (int i = 0; i < 2; ++i) s->tc_rings[i] = r[i];
     }
-    if (rc == GPS_OK && tc_smem_bytes(s->mg, s->tc_rings[0], s->tc_rings[1], s->tc_rings[2]) > 227 * 1024)
+    if (rc == GPS_OK && tc_smem_bytes(s->mg, s->tc_rings[0], s->tc_rings[1]) > 227 * 1024)
       rc = fail(GPS_E_ARG, "tensor-core ring configuration exceeds shared memory");
     if (rc == GPS_OK) {
-      cudaError_t ea = cudaFuncSetAttribute(
-          tc_dots_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-          int(tc_smem_bytes(s->mg, s->tc_rings[0], s->tc_rings[1], s->tc_rings[2])));
+      cudaError_t ea = cudaFuncSetAttribute(tc_dots_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            int(tc_smem_bytes(s->mg, s->tc_rings[0], s->tc_rings[1])));
       if (ea != cudaSuccess) rc = cuda_fail(ea, "cudaFuncSetAttribute(tc_dots)");
+    }
+    if (rc == GPS_OK) {
+      // per-column scale exponents: one pass over A per solver (A is constant)
+      tc_col_exp_kernel<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(static_cast<const float*>(A->d), A->n,
+                                                                   static_cast<int>(A->ld), static_cast<int>(A->p),
+                                                                   s->col_exp);
+      ctx->launches++;
+      cudaError_t ek = cudaGetLastError();
+      if (ek == cudaSuccess) ek = cudaStreamSynchronize(ctx->stream);
+      if (ek != cudaSuccess) rc = cuda_fail(ek, "tc_col_exp_kernel");
     }
     if (rc) {
       gps_bk_destroy(s);
@@ -1540,6 +1553,7 @@ int gps_bk_destroy(gps_bk* s) {
   if (s->wbuf) cudaFree(s->wbuf);
   if (s->xhi) cudaFree(s->xhi);
   if (s->xlo) cudaFree(s->xlo);
+  if (s->col_exp) cudaFree(s->col_exp);
   if (s->colmask) cudaFree(s->colmask);
   if (s->part_s_tc) cudaFree(s->part_s_tc);
   if (s->pc) cudaFree(s->pc);

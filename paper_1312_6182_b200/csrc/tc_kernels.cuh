@@ -1,40 +1,53 @@
 // Block GP-SPCA on the 5th-generation tensor cores (sm_100a tcgen05), for
-// m >= 16 components (p = 8192, m = 64) where the CUDA-core
-// block sweep would need ceil(m/MG) reads of A per iteration.
+// fp32 storage and m >= 5 components (m = 10, C4: p = 8192,
+// m = 64), where the CUDA-core block sweep needs ceil(m/4) reads of A.
 //
-// T0 split_x:   X (fp64) -> X_hi = tf32(X), X_lo = tf32(X - X_hi)  (fp32, [m_pad][ld])
-// T1 tc_dots:   persistent; per tile of 128 columns the correlations
-//               C_tile = A_tile' X (M = 128 columns, N = m_pad, K = p) are
-//               accumulated in TMEM by tcgen05.mma kind::tf32 in 3xTF32
-//               form (A_hi X_hi + A_hi X_lo + A_lo X_hi, ~fp32 accuracy);
-//               A and X chunks arrive by TMA (2-D tensor maps, 128-byte
-//               swizzle), A_lo is split in shared memory by converter warps,
-//               and the epilogue warps read TMEM (tcgen05.ld), apply mu_j,
-//               the threshold and the objective in fp64, write W and a per-
-//               column activity flag.  A is read from HBM once.
+// Arithmetic: "2xFP16 with power-of-two scaling".  Column i of A is scaled
+// by s_i = 2^e_i (max |a_ji| s_i in [2^14, 2^15)) and split into two fp16
+// pieces, y = a s_i = A1 + 2^-11 A2 (A2 = fp16((y - A1) 2^11)); X is split the
+// same way with the common scale 2^14 (its columns are unit vectors).  The
+// tensor core forms, with fp32 accumulation (kind::f16, 16 rows per MMA):
+//   D0 = A1 X1,  D1 = A1 X2,  D2 = A2 X1
+// and c_ij = 2^-(e_i + 14) (D0 + 2^-11 (D1 + D2)); the dropped A2 X2 term and
+// the fp16 roundings leave ~2^-22 of max|a_i| |x|, the same class as 3xTF32
+// with half its MMA instructions and half the X traffic.
+//
+// T0 split_x:   X (fp64) -> X1, X2 (fp16, [n_pad][ld])
+// T1 tc_dots:   persistent; per tile of 128 columns accumulates D0|D1|D2 in
+//               TMEM over 64-row chunks: A arrives by TMA (fp32, 128-byte
+//               swizzle), converter warps scale and split it into TMEM
+//               (tcgen05.st), both MMAs read A from TMEM and X from shared
+//               memory; epilogue warps drain TMEM segments into fp64 (every
+//               kTcSegChunks chunks), apply mu_j, the threshold and the
+//               objective, write W and a per-column activity flag.  A is read
+//               from HBM once.
 // T2 tc_update: G_j = sum over ACTIVE columns of w_ij a_i (fp64), row chunks
 //               x component groups; reads only the active columns again.
 // Roles of T1 (12 warps): w0 A producer (TMA), w1 MMA issuer (+TMEM owner),
-// w2 X producer (TMA), w4-7 epilogue (warp % 4 selects the TMEM lane quarter), w8-11 converters.
+// w2 X producer (TMA), w4-7 epilogue (warp % 4 selects the TMEM lane
+// quarter) and w12-15 (second component half), w8-11 converters.
 #pragma once
 
 #include <cuda.h>
+#include <cuda_fp16.h>
 
 #include "su_kernels.cuh"
 
 namespace gps {
 
 constexpr int kTcTileM = 128;    // columns of A per tile (MMA M)
-constexpr int kTcKChunk = 32;    // rows of A per stage (128 bytes of fp32)
-constexpr int kTcAStages = 10;  // default A ring depth (HBM stream)
-constexpr int kTcLoStages = 2;  // default TMEM A_hi / A_lo slots (converter output)
-constexpr int kTcXStages = 3;   // default X_hi | X_lo ring depth (L2-resident)
-constexpr int kTcMaxStages = 16;
-constexpr int kTcThreads = 384;  // 12 warps
+constexpr int kTcKChunk = 64;    // rows of A per chunk (two 32-row fp32 TMA boxes; one 128-byte fp16 row)
+constexpr int kTcBoxK = 32;      // rows per fp32 TMA box (128 bytes)
+constexpr int kTcAStages = 5;    // default A ring depth (32 KB stages, HBM stream)
+constexpr int kTcLoStages = 2;   // TMEM A1 / A2 slots (converter output)
+constexpr int kTcXStages = 3;    // default X1 | X2 ring depth (L2-resident)
+constexpr int kTcMaxStages = 8;
+constexpr int kTcThreads = 512;  // 16 warps
 constexpr int kTcMaxN = 64;
 constexpr int kTcMinM = 5;       // block solves with m >= 5 (fp32 A) take this path (one A read vs ceil(m/4))
-constexpr int kTcConvThreads = 128;  // converter warps 8-11
-constexpr int kTcSegChunks = 4;  // TMEM accumulation segment: 4 chunks = 128 rows, drained to fp64
+constexpr int kTcSegChunks = 2;  // TMEM accumulation segment: 2 chunks = 128 rows, drained to fp64
+constexpr int kTcAScaleExp = 14; // |a s_i| in [2^14, 2^15)
+constexpr int kTcXScaleExp = 14; // |x| <= 1 -> |x 2^14| <= 2^14
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
   asm volatile(
@@ -114,30 +127,46 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-__device__ __forceinline__ float to_tf32(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+// C0: per-column scale exponents e_i = 14 - floor(log2 max_j |a_ji|) (0 for
+// an all-zero column, clamped to [-126, 126]); warp per column.
+__global__ void tc_col_exp_kernel(const float* __restrict__ A, int64_t n, int ld, int p, int* __restrict__ col_exp) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t col = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; col < n; col += warps) {
+    const float* a = A + col * ld;
+    float mx = 0.f;
+    for (int r = lane; r < p; r += 32) mx = fmaxf(mx, fabsf(a[r]));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    // clamped so 2^e is a normal float (only data below ~2^-112 loses range)
+    if (lane == 0) col_exp[col] = mx > 0.f ? max(-126, min(126, kTcAScaleExp - ilogbf(mx))) : 0;
+  }
 }
 
-// T0: X (fp64 [m][ld], parity slot) -> X_hi / X_lo (fp32 [n_pad][ld], zero
-// padded components).
+// T0: X (fp64 [m][ld], parity slot) -> X1 / X2 (fp16 [n_pad][ld], zero
+// padded components): x 2^14 = X1 + 2^-11 X2.
 __global__ void tc_split_x_kernel(const double* __restrict__ X, int64_t x_par_stride, int m, int n_pad, int ld,
-                                  float* __restrict__ xhi, float* __restrict__ xlo, const GpsCtl* ctl) {
+                                  __half* __restrict__ x1, __half* __restrict__ x2, const GpsCtl* ctl) {
   if (ctl != nullptr && ctl->done) return;
   const int parity = ctl != nullptr ? (ctl->iter & 1) : 0;
   const double* Xp = X + parity * x_par_stride;
   for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < int64_t(n_pad) * ld;
        e += int64_t(gridDim.x) * blockDim.x) {
     const int j = static_cast<int>(e / ld);
-    const double x = j < m ? Xp[e] : 0.0;
-    const float xf = static_cast<float>(x);
-    const float hi = __uint_as_float(__float_as_uint(xf) & 0xFFFFE000u);
-    const float lo = static_cast<float>(x - static_cast<double>(hi));
-    xhi[e] = hi;
-    xlo[e] = lo;
+    const double y = j < m ? Xp[e] * double(1 << kTcXScaleExp) : 0.0;
+    const __half h = __double2half(y);
+    x1[e] = h;
+    x2[e] = __double2half((y - static_cast<double>(__half2float(h))) * 2048.0);
   }
 }
 
@@ -149,34 +178,36 @@ struct TcDotsArgs {
   int penalty;
   const double* gamma;  // m
   const double* mu;     // m
+  const int* col_exp;   // n: scale exponents of the columns
   double* w_out;        // [m_pad][n] parity slots (may be null)
   int64_t w_stride;
-  unsigned char* colmask;  // n: 1 if any w_ij != 0
+  unsigned char* colmask;  // [2][n]: 1 if any w_ij != 0 (one row per epilogue group)
   double* part_s;          // [grid][4]
   const GpsCtl* ctl;
   int num_tiles;
-  int a_stages, lo_stages, x_stages;  // ring depths (<= kTcMaxStages)
-  int seg_chunks;                     // chunks per TMEM accumulation segment
-  int probe;  // timing experiments: 1 no A_lo, 2 one MMA, 4 no TMEM drain, 8 no X loads,
-              // 16 no update, 32 no TMEM stores, 64 cycle accounting
+  int a_stages, x_stages;  // ring depths (<= kTcMaxStages)
+  int seg_chunks;          // chunks per TMEM accumulation segment
+  int probe;  // timing experiments: 2 no A2 MMA, 4 no TMEM drain, 8 no X loads, 16 no update,
+              // 32 no TMEM stores, 64 cycle accounting
 };
 
-// Operand staging of T1.  Shared memory is the scarce resource (every
-// tcgen05.mma operand read from shared memory, every TMA write and every
-// converter access share its ~128 B/clock), so A passes through it once:
-//   A ring    SA x 16 KB in shared memory (TMA, evict-first) -> converters
-//   A_hi/A_lo SL slots x 64 TMEM columns, written by the converters with
-//             tcgen05.st, read by the MMAs as the TMEM-resident A operand
-//   X ring    SX x (X_hi | X_lo) chunk in shared memory (TMA, evict-last)
-// TMEM: columns [0, 4 NP) = 2 accumulator buffers of [A X_hi | A_hi X_lo],
-// columns [256, 256 + 64 SL) = the A_hi / A_lo slots; 512 columns allocated.
+// Operand staging of T1.  Shared memory is the scarce resource (tcgen05.mma
+// shared-memory operands, TMA writes and converter reads share its ~128
+// B/clock), so A passes through it once:
+//   A ring    SA x 32 KB in shared memory (TMA, evict-first) -> converters
+//   A1 / A2   2 slots x 64 TMEM columns (32 packed fp16 pairs each), written
+//             by the converters with tcgen05.st, read by the MMAs as the
+//             TMEM-resident A operand
+//   X ring    SX x (X1 | X2) chunk in shared memory (TMA, evict-last)
+// TMEM: columns [0, 4 NP) = 2 accumulator buffers of [D0 | D1 + D2] (2 NP
+// each; D1 and D2 carry the same 2^-11 weight, so the tensor core sums them),
+// columns [256, 384) = the two A1/A2 slots.
 constexpr uint32_t kTcTmemCols = 512;
 constexpr uint32_t kTcTmemAOff = 256;
-__host__ __device__ inline size_t tc_a_bytes() { return size_t(kTcTileM) * kTcKChunk * 4; }
-__host__ __device__ inline size_t tc_x_bytes(int n_pad) { return size_t(n_pad) * kTcKChunk * 4; }
-__host__ __device__ inline size_t tc_smem_bytes(int n_pad, int sa, int sl, int sx) {
-  (void)sl;
-  return 1024 /*align slack*/ + sa * tc_a_bytes() + sx * 2 * tc_x_bytes(n_pad) + 4096 /*barriers, params*/;
+__host__ __device__ inline size_t tc_a_bytes() { return size_t(kTcTileM) * kTcKChunk * 4; }  // 32 KB
+__host__ __device__ inline size_t tc_x_bytes(int n_pad) { return size_t(n_pad) * kTcKChunk * 2; }
+__host__ __device__ inline size_t tc_smem_bytes(int n_pad, int sa, int sx) {
+  return 1024 /*align slack*/ + sa * tc_a_bytes() + sx * 2 * tc_x_bytes(n_pad) + 8192 /*barriers, params, 256 x 2 fp64 partials*/;
 }
 
 __device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar,
@@ -188,7 +219,24 @@ __device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* m
       : "memory");
 }
 
-// tcgen05.mma with the A operand in TMEM (M = 128 lanes, K = 8 columns).
+// Instruction descriptor: D f32, A/B f16, both K-major, M x N.
+__host__ __device__ constexpr uint32_t umma_idesc_f16(int M, int N) {
+  return (1u << 4) | (0u << 7) | (0u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
+}
+
+// tcgen05.mma kind::f16 with the A operand in TMEM (M = 128 lanes, K = 16 =
+// 8 columns of packed pairs), warp-converged issue.
+__device__ __forceinline__ void umma_f16_ts_warp(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                                 uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// The tf32 form (A in TMEM) is kept for the microbenchmarks.
 __device__ __forceinline__ void umma_tf32_ts_warp(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
                                                   uint32_t acc) {
   asm volatile(
@@ -210,9 +258,23 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32
       "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
       : "memory");
 }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-// Optional per-role cycle accounting (tuning diagnostics, TcDotsArgs::probe & 64).
+// Optional per-role cycle accounting (tuning diagnostics: build with
+// -DGPS_TC_PROFILE and run with TcDotsArgs::probe & 64).
+#ifdef GPS_TC_PROFILE
+constexpr bool kTcProfile = true;
+#else
+constexpr bool kTcProfile = false;
+#endif
 __device__ unsigned long long g_tc_prof[16];
 struct TcProf {
   bool on;
@@ -237,24 +299,31 @@ struct TcRing {
   }
 };
 
+// Round two floats to fp16 and pack them (k in the low half, k + 1 high).
+__device__ __forceinline__ uint32_t pack_f16x2(float k0, float k1) {
+  uint32_t d;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(k1), "f"(k0));
+  return d;
+}
+
 __global__ void __launch_bounds__(kTcThreads, 1)
-    tc_dots_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmXh,
-                   const __grid_constant__ CUtensorMap tmXl, const TcDotsArgs a) {
+    tc_dots_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX1,
+                   const __grid_constant__ CUtensorMap tmX2, const TcDotsArgs a) {
   extern __shared__ unsigned char smem_raw[];
   if (a.ctl != nullptr && a.ctl->done) return;
   const int parity = a.ctl != nullptr ? (a.ctl->iter & 1) : 0;
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int NP = a.n_pad;
-  const int SA = a.a_stages, SL = a.lo_stages, SX = a.x_stages;
+  const int SA = a.a_stages, SL = kTcLoStages, SX = a.x_stages;
   const int SEG = a.seg_chunks;
-  const size_t a_bytes = tc_a_bytes();  // 16 KB
+  const size_t a_bytes = tc_a_bytes();  // 32 KB: two 16 KB boxes (rows 0-31, 32-63)
   const size_t x_bytes = tc_x_bytes(NP);
   unsigned char* aring = smem;
-  unsigned char* xring = aring + SA * a_bytes;  // [stage][hi | lo]
+  unsigned char* xring = aring + SA * a_bytes;  // [stage][X1 | X2]
   uint64_t* a_full = reinterpret_cast<uint64_t*>(xring + SX * 2 * x_bytes);
   uint64_t* a_empty = a_full + SA;
-  uint64_t* lo_full = a_empty + SA;  // TMEM A_hi / A_lo slots
+  uint64_t* lo_full = a_empty + SA;  // TMEM A1 / A2 slots
   uint64_t* lo_empty = lo_full + SL;
   uint64_t* x_full = lo_empty + SL;
   uint64_t* x_empty = x_full + SX;
@@ -263,14 +332,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   double* sgam = reinterpret_cast<double*>(tmem_base_slot + 4);
   double* smu = sgam + kTcMaxN;
-  double* sred = smu + kTcMaxN;  // 128 x 2 scalars (f, nnz)
+  double* sred = smu + kTcMaxN;  // 256 x 2 scalars (f, nnz)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int kchunks = a.ld / kTcKChunk;
-  // MMA 1: A_hi [X_hi | X_lo] (N = 2 NP, the X slot holds X_hi rows then X_lo rows);
-  // MMA 2: A_lo X_hi (N = NP) accumulating into the first NP columns.
-  const uint32_t idesc2 = umma_idesc_tf32(kTcTileM, 2 * NP);
-  const uint32_t idesc1 = umma_idesc_tf32(kTcTileM, NP);
+  const int kchunks = (a.ld + kTcKChunk - 1) / kTcKChunk;
+  // MMA a: A1 [X1 | X2] (N = 2 NP; the X slot holds X1 rows then X2 rows);
+  // MMA b: A2 X1 (N = NP) accumulated onto the A1 X2 columns.
+  const uint32_t idesc2 = umma_idesc_f16(kTcTileM, 2 * NP);
+  const uint32_t idesc1 = umma_idesc_f16(kTcTileM, NP);
 
   if (tid == 0) {
     for (int i = 0; i < SA; ++i) {
@@ -278,7 +347,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       mbar_init(&a_empty[i], 4);  // 4 converter warps have read the slot
     }
     for (int i = 0; i < SL; ++i) {
-      mbar_init(&lo_full[i], 4);  // 4 converter warps stored their TMEM lanes
+      mbar_init(&lo_full[i], 4);   // 4 converter warps stored their TMEM lanes
       mbar_init(&lo_empty[i], 1);  // tcgen05.commit
     }
     for (int i = 0; i < SX; ++i) {
@@ -287,7 +356,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);   // tcgen05.commit
-      mbar_init(&tempty[i], 4);  // 4 epilogue warps
+      mbar_init(&tempty[i], 8);  // 8 epilogue warps
     }
     fence_mbar_init();
   }
@@ -303,8 +372,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
-    tma_prefetch(&tmXh);
-    tma_prefetch(&tmXl);
+    tma_prefetch(&tmX1);
+    tma_prefetch(&tmX2);
   }
   tc_fence_before();
   __syncthreads();
@@ -321,15 +390,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       uint64_t policy;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
       TcRing r;
-      TcProf pf{(a.probe & 64) != 0, 0};
+      TcProf pf{kTcProfile && (a.probe & 64) != 0, 0};
       unsigned long long w0 = 0;
       int t = int(blockIdx.x), kc = 0;
       for (int c = 0; c < total_chunks; ++c) {
         pf.start();
         if (c >= SA) mbar_wait_sleep(&a_empty[r.slot], r.ph ^ 1u);
         pf.stop(w0);
+        unsigned char* st = aring + r.slot * a_bytes;
         mbar_arrive_expect_tx(&a_full[r.slot], static_cast<uint32_t>(a_bytes));
-        tma_load_2d_hint(aring + r.slot * a_bytes, &tmA, kc * kTcKChunk, t * kTcTileM, &a_full[r.slot], policy);
+        tma_load_2d_hint(st, &tmA, kc * kTcKChunk, t * kTcTileM, &a_full[r.slot], policy);
+        tma_load_2d_hint(st + a_bytes / 2, &tmA, kc * kTcKChunk + kTcBoxK, t * kTcTileM, &a_full[r.slot], policy);
         r.next(SA);
         if (++kc == kchunks) {
           kc = 0;
@@ -344,7 +415,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       uint64_t policy;
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(policy));
       TcRing r;
-      TcProf pf{(a.probe & 64) != 0, 0};
+      TcProf pf{kTcProfile && (a.probe & 64) != 0, 0};
       unsigned long long w0 = 0;
       int kc = 0;
       for (int c = 0; c < total_chunks; ++c) {
@@ -355,8 +426,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         unsigned char* st = xring + r.slot * 2 * x_bytes;
         mbar_arrive_expect_tx(&x_full[r.slot], static_cast<uint32_t>(lx ? 2 * x_bytes : 0));
         if (lx) {
-          tma_load_2d_hint(st, &tmXh, kc * kTcKChunk, 0, &x_full[r.slot], policy);
-          tma_load_2d_hint(st + x_bytes, &tmXl, kc * kTcKChunk, 0, &x_full[r.slot], policy);
+          tma_load_2d_hint(st, &tmX1, kc * kTcKChunk, 0, &x_full[r.slot], policy);
+          tma_load_2d_hint(st + x_bytes, &tmX2, kc * kTcKChunk, 0, &x_full[r.slot], policy);
         }
         r.next(SX);
         if (++kc == kchunks) kc = 0;
@@ -366,14 +437,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   } else if (warp == 1) {
     // ---------------------------------------------------------- MMA issuer
     // The whole warp runs the loop (uniform control flow and operands);
-    // elect.sync inside the asm issues each MMA / commit once.  Each TMEM
-    // segment accumulates kTcSegChunks chunks (128 rows of A); the epilogue
-    // drains it into fp64, so the tensor core's fp32 accumulation never
-    // spans more than 128 rows.
+    // elect.sync inside the asm issues each MMA / commit once.  A TMEM
+    // segment accumulates SEG chunks (128 rows) before the epilogue drains
+    // it into fp64.
     const uint64_t dx = umma_desc_sw128(xring);
     const uint64_t x_step = (2 * x_bytes) >> 4;
     TcRing rl, rx;
-    TcProf pf{(a.probe & 64) != 0, 0};
+    TcProf pf{kTcProfile && (a.probe & 64) != 0, 0};
     unsigned long long w3 = 0, w4 = 0, w5 = 0;
     const long long t_role = clock64();
     int seg = 0;
@@ -394,13 +464,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           mbar_wait(&x_full[rx.slot], rx.ph);
           pf.stop(w5);
           tc_fence_after();
-          const uint32_t th = tmem_base + kTcTmemAOff + uint32_t(rl.slot) * 64;  // A_hi; A_lo at +32
+          const uint32_t ta = tmem_base + kTcTmemAOff + uint32_t(rl.slot) * 64;  // A1; A2 at +32
           const uint64_t bx = dx + uint64_t(rx.slot) * x_step;
 #pragma unroll
-          for (int k = 0; k < kTcKChunk / 8; ++k) {
+          for (int k = 0; k < kTcKChunk / 16; ++k) {
             const uint32_t first = (kc == k0 && k == 0) ? 0u : 1u;
-            umma_tf32_ts_warp(dtm, th + 8 * k, bx + 2 * k, idesc2, first);
-            if (!(a.probe & 2)) umma_tf32_ts_warp(dtm, th + 32 + 8 * k, bx + 2 * k, idesc1, 1u);
+            umma_f16_ts_warp(dtm, ta + 8 * k, bx + 2 * k, idesc2, first);
+            if (!(a.probe & 2)) umma_f16_ts_warp(dtm + NP, ta + 32 + 8 * k, bx + 2 * k, idesc1, 1u);
           }
           umma_commit_warp(&lo_empty[rl.slot]);
           umma_commit_warp(&x_empty[rx.slot]);
@@ -416,54 +486,76 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       atomicAdd(&g_tc_prof[5], w5);
       atomicAdd(&g_tc_prof[6], static_cast<unsigned long long>(clock64() - t_role));
     }
-  } else if (warp >= 8) {
+  } else if (warp >= 8 && warp < 12) {
     // ---------------------------------------------------- converter warps
     // Thread r owns tile row r (one column of A, TMEM lane r): it reads its
-    // 128-byte row out of the 128-byte-swizzled A slot (16-byte chunk c sits
-    // at c ^ (r & 7)), splits A = A_hi + A_lo with A_hi = trunc_tf32(A)
-    // (A_lo exact in fp32) and stores both halves to its TMEM lane.
+    // two 128-byte rows out of the 128-byte-swizzled A slot (16-byte chunk c
+    // of row r sits at c ^ (r & 7)), scales by 2^e_i, splits into fp16
+    // A1 + 2^-11 A2 and stores the packed pairs to its TMEM lane.
     const int q = warp & 3;
     const int r = q * 32 + lane;
     TcRing ra, rl;
-    TcProf pf{(a.probe & 64) != 0 && warp == 8, 0};
+    TcProf pf{kTcProfile && (a.probe & 64) != 0 && warp == 8, 0};
     unsigned long long w7 = 0, w8 = 0, w9 = 0;
     const long long t_role = clock64();
+    int tt = 0, kc = 0;
+    float sc = 1.f;
     for (int c = 0; c < total_chunks; ++c) {
+      if (kc == 0) {
+        const int64_t col = int64_t(int(blockIdx.x) + tt * int(gridDim.x)) * kTcTileM + r;
+        sc = __int_as_float((127 + (col < a.n ? a.col_exp[col] : 0)) << 23);  // 2^e, e in [-126, 126]
+      }
       pf.start();
       mbar_wait(&a_full[ra.slot], ra.ph);
       pf.stop(w7);
-      const unsigned char* row = aring + ra.slot * a_bytes + r * 128;
-      uint32_t hi[32], lo[32];
-#pragma unroll
-      for (int cc = 0; cc < 8; ++cc) {
-        const float4 v = *reinterpret_cast<const float4*>(row + ((cc ^ (r & 7)) << 4));
-        const float e[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint32_t h = __float_as_uint(e[u]) & 0xFFFFE000u;
-          hi[cc * 4 + u] = h;
-          lo[cc * 4 + u] = (a.probe & 1) ? 0u : __float_as_uint(e[u] - __uint_as_float(h));
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&a_empty[ra.slot]);  // the slot's bytes are in registers
       pf.start();
       if (c >= SL) mbar_wait(&lo_empty[rl.slot], rl.ph ^ 1u);
       pf.stop(w8);
       tc_fence_after();
       const uint32_t ta = tmem_base + (uint32_t(q * 32) << 16) + kTcTmemAOff + uint32_t(rl.slot) * 64;
-      pf.start();
-      if (!(a.probe & 32)) {
-        tmem_st32(ta, hi);
-        tmem_st32(ta + 32, lo);
-        tmem_wait_st();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // rows 32 h .. 32 h + 31 (one fp32 TMA box)
+        uint32_t p1[16], p2[16];
+        const unsigned char* row = aring + ra.slot * a_bytes + h * (a_bytes / 2) + r * 128;
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) {
+          const float4 v = *reinterpret_cast<const float4*>(row + ((cc ^ (r & 7)) << 4));
+          // y = a 2^e; Veltkamp split y = hi + lo with an 11-bit hi (exact
+          // in fp16 above 2^-14, i.e. 2^-28 of the column maximum); lo 2^11
+          // rounds to fp16 with 2^-22 relative error.
+          const float y[4] = {v.x * sc, v.y * sc, v.z * sc, v.w * sc};
+          float hi[4], lo[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            // _rn intrinsics: no FMA contraction, which would break the split
+            const float t = __fmul_rn(y[u], 8193.f);
+            hi[u] = __fsub_rn(t, __fsub_rn(t, y[u]));
+            lo[u] = __fmul_rn(__fsub_rn(y[u], hi[u]), 2048.f);
+          }
+          p1[cc * 2] = pack_f16x2(hi[0], hi[1]);  // packed column (k / 2) within the half
+          p1[cc * 2 + 1] = pack_f16x2(hi[2], hi[3]);
+          p2[cc * 2] = pack_f16x2(lo[0], lo[1]);
+          p2[cc * 2 + 1] = pack_f16x2(lo[2], lo[3]);
+        }
+        pf.start();
+        if (!(a.probe & 32)) {
+          tmem_st16(ta + 16 * h, p1);
+          tmem_st16(ta + 32 + 16 * h, p2);
+        }
+        pf.stop(w9);
       }
-      pf.stop(w9);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&a_empty[ra.slot]);  // the slot's bytes have been read
+      tmem_wait_st();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&lo_full[rl.slot]);
       ra.next(SA);
       rl.next(SL);
+      if (++kc == kchunks) {
+        kc = 0;
+        ++tt;
+      }
     }
     if (pf.on && lane == 0) {
       atomicAdd(&g_tc_prof[7], w7);
@@ -471,21 +563,27 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       atomicAdd(&g_tc_prof[9], w9);
       atomicAdd(&g_tc_prof[10], static_cast<unsigned long long>(clock64() - t_role));
     }
-  } else if (warp >= 4) {
+  } else if ((warp >= 4 && warp < 8) || warp >= 12) {
     // ------------------------------------------------------ epilogue warps
-    const int q = warp & 3;  // TMEM lane quarter
-    const int et = tid - 4 * 32;
+    // Two groups of 4 warps (warp % 4 selects the TMEM lane quarter = 32
+    // columns of the tile); group g owns components [32 g, 32 g + 32).
+    const int q = warp & 3;
+    const int g = warp >= 12 ? 1 : 0;
+    const int et = g * 128 + q * 32 + lane;
+    const int jbase = g * 32;
     double f_acc = 0.0, nnz_acc = 0.0;
     double* wbase = a.w_out != nullptr ? a.w_out + parity * a.w_stride : nullptr;
-    TcProf pf{(a.probe & 64) != 0 && warp == 4, 0};
+    TcProf pf{kTcProfile && (a.probe & 64) != 0 && warp == 4, 0};
     unsigned long long w11 = 0, w12 = 0;
     const long long t_role = clock64();
     int seg = 0;
     for (int tt = 0; tt < my_tiles; ++tt) {
       const int t = int(blockIdx.x) + tt * int(gridDim.x);
-      double c[kTcMaxN];
+      // per-tile sums as unevaluated fp32 pairs (TwoSum per segment: full-
+      // rate fp32 ops instead of fp64 conversions and adds)
+      float ch[32], cl[32];
 #pragma unroll
-      for (int j = 0; j < kTcMaxN; ++j) c[j] = 0.0;
+      for (int j = 0; j < 32; ++j) ch[j] = cl[j] = 0.f;
       for (int k0 = 0; k0 < kchunks; k0 += SEG, ++seg) {
         const int b = seg & 1;
         pf.start();
@@ -494,15 +592,24 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         pf.start();
         tc_fence_after();
 #pragma unroll
-        for (int j0 = 0; j0 < kTcMaxN; j0 += 16) {
+        for (int h = 0; h < 4; ++h) {
+          const int j0 = jbase + 8 * h;
           if (j0 < NP && !(a.probe & 4)) {
-            float v[16], vl[16];
+            float v0[8], v1[8];
             const uint32_t ta = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(b * 2 * NP + j0);
-            tmem_ld16(ta, v);
-            tmem_ld16(ta + uint32_t(NP), vl);
+            tmem_ld8(ta, v0);
+            tmem_ld8(ta + uint32_t(NP), v1);
             tmem_wait_ld();
 #pragma unroll
-            for (int u = 0; u < 16; ++u) c[j0 + u] += static_cast<double>(v[u] + vl[u]);
+            for (int u = 0; u < 8; ++u) {
+              const float v = fmaf(v1[u], 1.f / 2048.f, v0[u]);
+              float& hi = ch[8 * h + u];
+              const float sum = __fadd_rn(hi, v);
+              const float bv = __fsub_rn(sum, hi);
+              const float err = __fadd_rn(__fsub_rn(hi, __fsub_rn(sum, bv)), __fsub_rn(v, bv));
+              hi = sum;
+              cl[8 * h + u] += err;
+            }
           }
         }
         tc_fence_before();
@@ -512,11 +619,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
       const int64_t col = int64_t(t) * kTcTileM + q * 32 + lane;
       if (col < a.n) {
+        // undo the scales: c = D 2^-(e_i + 14)
+        const double unscale = ldexp(1.0, -(a.col_exp[col] + kTcXScaleExp));
         bool any = false;
 #pragma unroll
-        for (int j = 0; j < kTcMaxN; ++j) {
-          if (j >= a.m) break;
-          const double sj = smu[j] * c[j];
+        for (int jj = 0; jj < 32; ++jj) {
+          const int j = jbase + jj;
+          if (j >= a.m) continue;
+          const double sj = smu[j] * ((static_cast<double>(ch[jj]) + static_cast<double>(cl[jj])) * unscale);
           const double w = threshold_weight(sj, sgam[j], a.penalty);
           f_acc += objective_term(sj, sgam[j], a.penalty);
           if (w != 0.0) {
@@ -525,7 +635,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           }
           if (wbase != nullptr) wbase[size_t(j) * a.n + col] = w;
         }
-        a.colmask[col] = any ? 1 : 0;
+        a.colmask[size_t(g) * a.n + col] = any ? 1 : 0;
       }
     }
     if (pf.on && lane == 0) {
@@ -539,7 +649,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __syncthreads();
   if (tid < 2) {
     double t = 0.0;
-    for (int i = 0; i < 128; ++i) t += sred[i * 2 + tid];
+    for (int i = 0; i < 256; ++i) t += sred[i * 2 + tid];
     a.part_s[size_t(blockIdx.x) * 4 + tid] = t;
   }
   if (warp == 1) {
@@ -574,7 +684,7 @@ __global__ void __launch_bounds__(256) tc_update_kernel(const float* __restrict_
   for (int64_t base = c0; base < c1; base += 256) {
     // cheap skip of fully inactive 256-column chunks (the common case)
     const int64_t mine = base + threadIdx.x;
-    const unsigned char f = mine < c1 ? colmask[mine] : 0;
+    const unsigned char f = mine < c1 ? (colmask[mine] | colmask[n + mine]) : 0;
     if (!__syncthreads_or(f)) continue;
     flags[threadIdx.x] = f;
     __syncthreads();

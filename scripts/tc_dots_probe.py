@@ -38,7 +38,7 @@ if int(os.environ.get('GPSPCA_TC_PROBE', '0')) & 64:
     buf = (C.c_ulonglong * 16)()
     fn(buf, 16, 0)
     v = list(buf)
-    chunks = (n // 128) * (p // 32)
+    chunks = (n // 128) * ((p + 63) // 64)
     names = {1: 'A prod wait a_empty', 2: 'X prod wait x_empty', 3: 'MMA wait tempty', 4: 'MMA wait lo_full',
              5: 'MMA wait x_full', 6: 'MMA role total', 7: 'conv wait a_full', 8: 'conv wait lo_empty',
              9: 'conv tmem st', 10: 'conv role total', 11: 'epi wait tfull', 12: 'epi drain', 13: 'epi role total'}
