@@ -42,7 +42,8 @@ def nvcc_command(out=LIB, verbose=False):
            "-o", out, os.path.join(CSRC, "capi.cu")]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
-    return cmd
+    extra = os.environ.get("GPSPCA_NVCC_FLAGS", "").split()  # diagnostics builds, e.g. -DGPS_TC_PROFILE
+    return cmd[:-1] + extra + cmd[-1:]
 
 
 def build(force=False, verbose=False):

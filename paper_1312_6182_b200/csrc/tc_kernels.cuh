@@ -299,6 +299,12 @@ struct TcRing {
   }
 };
 
+__device__ __forceinline__ float4 lds_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+
 // Round two floats to fp16 and pack them (k in the low half, k + 1 high).
 __device__ __forceinline__ uint32_t pack_f16x2(float k0, float k1) {
   uint32_t d;
@@ -516,20 +522,19 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {  // rows 32 h .. 32 h + 31 (one fp32 TMA box)
         uint32_t p1[16], p2[16];
-        const unsigned char* row = aring + ra.slot * a_bytes + h * (a_bytes / 2) + r * 128;
+        const uint32_t row_s = smem_u32(aring + ra.slot * a_bytes + h * (a_bytes / 2) + r * 128);
 #pragma unroll
         for (int cc = 0; cc < 8; ++cc) {
-          const float4 v = *reinterpret_cast<const float4*>(row + ((cc ^ (r & 7)) << 4));
-          // y = a 2^e; Veltkamp split y = hi + lo with an 11-bit hi (exact
-          // in fp16 above 2^-14, i.e. 2^-28 of the column maximum); lo 2^11
-          // rounds to fp16 with 2^-22 relative error.
+          const float4 v = lds_f4(row_s + ((cc ^ (r & 7)) << 4));
+          // y = a 2^e split as y = hi + lo with hi = y rounded to 11
+          // significant bits (integer round-half-up on the bit pattern; exact
+          // in fp16 above 2^-14, i.e. 2^-28 of the column maximum) and lo
+          // exact; lo 2^11 rounds to fp16 with 2^-22 relative error.
           const float y[4] = {v.x * sc, v.y * sc, v.z * sc, v.w * sc};
           float hi[4], lo[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            // _rn intrinsics: no FMA contraction, which would break the split
-            const float t = __fmul_rn(y[u], 8193.f);
-            hi[u] = __fsub_rn(t, __fsub_rn(t, y[u]));
+            hi[u] = __uint_as_float((__float_as_uint(y[u]) + 0x1000u) & 0xFFFFE000u);
             lo[u] = __fmul_rn(__fsub_rn(y[u], hi[u]), 2048.f);
           }
           p1[cc * 2] = pack_f16x2(hi[0], hi[1]);  // packed column (k / 2) within the half
@@ -587,7 +592,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       for (int k0 = 0; k0 < kchunks; k0 += SEG, ++seg) {
         const int b = seg & 1;
         pf.start();
-        mbar_wait(&tfull[b], static_cast<uint32_t>((seg >> 1) & 1));
+        mbar_wait_sleep(&tfull[b], static_cast<uint32_t>((seg >> 1) & 1));  // off the converters' issue slots
         pf.stop(w11);
         pf.start();
         tc_fence_after();
