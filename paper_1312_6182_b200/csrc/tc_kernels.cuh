@@ -584,8 +584,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     int seg = 0;
     for (int tt = 0; tt < my_tiles; ++tt) {
       const int t = int(blockIdx.x) + tt * int(gridDim.x);
-      // per-tile sums as unevaluated fp32 pairs (TwoSum per segment: full-
-      // rate fp32 ops instead of fp64 conversions and adds)
+      // per-tile sums with Kahan compensation in fp32 (full-rate fp32 ops
+      // instead of fp64 conversions and adds)
       float ch[32], cl[32];
 #pragma unroll
       for (int j = 0; j < 32; ++j) ch[j] = cl[j] = 0.f;
@@ -607,13 +607,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             tmem_wait_ld();
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-              const float v = fmaf(v1[u], 1.f / 2048.f, v0[u]);
-              float& hi = ch[8 * h + u];
-              const float sum = __fadd_rn(hi, v);
-              const float bv = __fsub_rn(sum, hi);
-              const float err = __fadd_rn(__fsub_rn(hi, __fsub_rn(sum, bv)), __fsub_rn(v, bv));
-              hi = sum;
-              cl[8 * h + u] += err;
+              // Kahan step: ch + cl carries the running sum, cl the (negated) compensation
+              const float yk = __fsub_rn(fmaf(v1[u], 1.f / 2048.f, v0[u]), cl[8 * h + u]);
+              const float tk = __fadd_rn(ch[8 * h + u], yk);
+              cl[8 * h + u] = __fsub_rn(__fsub_rn(tk, ch[8 * h + u]), yk);
+              ch[8 * h + u] = tk;
             }
           }
         }
@@ -631,7 +629,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         for (int jj = 0; jj < 32; ++jj) {
           const int j = jbase + jj;
           if (j >= a.m) continue;
-          const double sj = smu[j] * ((static_cast<double>(ch[jj]) + static_cast<double>(cl[jj])) * unscale);
+          const double sj = smu[j] * ((static_cast<double>(ch[jj]) - static_cast<double>(cl[jj])) * unscale);
           const double w = threshold_weight(sj, sgam[j], a.penalty);
           f_acc += objective_term(sj, sgam[j], a.penalty);
           if (w != 0.0) {
