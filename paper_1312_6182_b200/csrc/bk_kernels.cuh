@@ -452,7 +452,10 @@ __device__ void onesided_jacobi(int m, PolarScratch sp, int max_sweeps) {
         a = warp_sum(a);
         b = warp_sum(b);
         g = warp_sum(g);
-        if (g != 0.0 && fabs(g) > 1e-15 * sqrt(a * b)) {
+        // rotate unless the pair is orthogonal to working precision (the
+        // computed g carries ~m eps sqrt(ab) of rounding itself; a tighter
+        // test never converges and runs every sweep to max_sweeps)
+        if (g != 0.0 && fabs(g) > double(m) * 2.220446049250313e-16 * sqrt(a * b)) {
           const double zeta = (b - a) / (2.0 * g);
           const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;

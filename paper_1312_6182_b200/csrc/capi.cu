@@ -1371,11 +1371,11 @@ int bk_enqueue_step(gps_bk* s) {
                                             s->pc, m);
   bk_assemble_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(s->exch, s->mg, ld, m, s->mu_dev, s->G, s->pc);
   gram_partial_kernel<<<kGramBlocks, kGramThreads, 0, ctx->stream>>>(s->G, ld, p, m, s->gram_part, s->pc);
-  chol_stage_kernel<<<1, 256, chol_smem_bytes(m), ctx->stream>>>(s->gram_part, kGramBlocks, m, p, 1, s->R1, s->Sm,
+  chol_stage_kernel<<<1, kPolarThreads, chol_smem_bytes(m), ctx->stream>>>(s->gram_part, kGramBlocks, m, p, 1, s->R1, s->Sm,
                                                                  s->pc);
   apply_right_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(s->G, s->Sm, ld, m, s->Tm, s->pc, nullptr, 0);
   gram_partial_kernel<<<kGramBlocks, kGramThreads, 0, ctx->stream>>>(s->Tm, ld, p, m, s->gram_part, s->pc);
-  chol_stage_kernel<<<1, 256, chol_smem_bytes(m), ctx->stream>>>(s->gram_part, kGramBlocks, m, p, 2, s->R1, s->Sm,
+  chol_stage_kernel<<<1, kPolarThreads, chol_smem_bytes(m), ctx->stream>>>(s->gram_part, kGramBlocks, m, p, 2, s->R1, s->Sm,
                                                                  s->pc);
   apply_right_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(s->Tm, s->Sm, ld, m, s->X, s->pc, s->ctl, xs);
   bk_finish_kernel<<<1, kPolarThreads, polar_smem_bytes(m), ctx->stream>>>(s->G, s->X, xs, ld, p, m, s->ctl, s->pc,

@@ -111,6 +111,121 @@ __global__ void __launch_bounds__(kGramThreads) gram_partial_kernel(const double
   }
 }
 
+// In-place Gauss-Jordan inverse with partial pivoting of the m x m
+// row-major A (destroyed) into B; fcol: m scratch.  One CTA of 1024 threads,
+// m <= 64: thread (i, g) = (tid / 16, tid % 16) owns row i, columns
+// g, g + 16, g + 32, g + 48 of both A and B.  Returns false on an exactly
+// singular pivot.
+__device__ bool gj_inverse(double* A, double* B, double* fcol, int m) {
+  const int tid = threadIdx.x;
+  const int i = tid >> 4, g = tid & 15;
+  __shared__ int s_piv;
+  if (i < m)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int c = g + 16 * k;
+      if (c < m) B[i * m + c] = (i == c) ? 1.0 : 0.0;
+    }
+  __syncthreads();
+  for (int j = 0; j < m; ++j) {
+    if (tid < 32) {  // pivot: largest |A[r][j]|, r >= j (lowest index on ties)
+      double best = -1.0;
+      int bi = j;
+      for (int r = j + tid; r < m; r += 32) {
+        const double v = fabs(A[r * m + j]);
+        if (v > best) {
+          best = v;
+          bi = r;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) {
+          best = ob;
+          bi = oi;
+        }
+      }
+      if (tid == 0) s_piv = best > 0.0 ? bi : -1;
+    }
+    __syncthreads();
+    const int pv = s_piv;
+    if (pv < 0) return false;
+    if (pv != j && tid < 2 * m) {  // swap rows j and pv
+      double* X = tid < m ? A : B;
+      const int c = tid < m ? tid : tid - m;
+      const double t = X[j * m + c];
+      X[j * m + c] = X[pv * m + c];
+      X[pv * m + c] = t;
+    }
+    __syncthreads();
+    if (tid < m) fcol[tid] = A[tid * m + j];
+    __syncthreads();
+    const double inv = 1.0 / fcol[j];
+    if (tid < 2 * m) {  // normalise the pivot row
+      if (tid < m)
+        A[j * m + tid] *= inv;
+      else
+        B[j * m + tid - m] *= inv;
+    }
+    __syncthreads();
+    if (i < m && i != j) {
+      const double f = fcol[i];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int c = g + 16 * k;
+        if (c < m) {
+          A[i * m + c] = fma(-f, A[j * m + c], A[i * m + c]);
+          B[i * m + c] = fma(-f, B[j * m + c], B[i * m + c]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  return true;
+}
+
+// Polar factor of the m x m row-major R by the Frobenius-scaled Newton
+// iteration X <- (z X + X^-T / z) / 2 (quadratic convergence; scaling
+// dropped once the step is small).  X holds the result; W, Y, fcol, red are
+// scratch.  Returns the Frobenius condition estimate |R|_F |R^-1|_F of the
+// first step (0 if R is singular).
+__device__ double newton_polar(const double* R, double* X, double* W, double* Y, double* fcol, double* red, int m) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int e = tid; e < m * m; e += nt) X[e] = R[e];
+  __syncthreads();
+  double kappa = 0.0;
+  bool scale = true;
+  for (int it = 0; it < 30; ++it) {
+    for (int e = tid; e < m * m; e += nt) W[e] = X[e];
+    __syncthreads();
+    if (!gj_inverse(W, Y, fcol, m)) return 0.0;  // Y = X^-1
+    double a = 0.0, b = 0.0;
+    for (int e = tid; e < m * m; e += nt) {
+      a = fma(X[e], X[e], a);
+      b = fma(Y[e], Y[e], b);
+    }
+    const double nx = sqrt(block_sum_any(a, red)), ny = sqrt(block_sum_any(b, red));
+    if (it == 0) kappa = nx * ny;
+    const double z = scale ? sqrt(ny / nx) : 1.0;
+    double d = 0.0;
+    for (int e = tid; e < m * m; e += nt) {  // X_new = (z X + Y^T / z) / 2
+      const int r = e / m, c = e % m;
+      const double xn = 0.5 * (z * X[e] + Y[c * m + r] / z);
+      d = fma(xn - X[e], xn - X[e], d);
+      W[e] = xn;
+    }
+    const double dn = sqrt(block_sum_any(d, red));
+    for (int e = tid; e < m * m; e += nt) X[e] = W[e];
+    __syncthreads();
+    const double rel = dn / sqrt(double(m));  // |X| -> sqrt(m) at convergence
+    if (rel < 1e-2) scale = false;
+    if (rel < 1e-14) break;
+  }
+  return kappa;
+}
+
 // Sum the Gram partials (fixed order), Cholesky G'G = R'R (upper R), and
 // invert R.  stage 1: R1 -> Rs (R1), Rinv (R1^-1).  stage 2: R2 with R = R2 R1,
 // one-sided Jacobi SVD of R, rank, then S = R2^-1 U V' (the right factor of
@@ -177,58 +292,29 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
     }
     return;
   }
-  // stage 2: Rt = R2 R1 (upper), column-major for the Jacobi SVD
+  // stage 2: R = R2 R1 (upper, row-major in W), its polar factor P by the
+  // scaled Newton iteration (the CholeskyQR2 path only runs for condition
+  // numbers far below the rank cutoff max(p, m) eps, so rank = m here), then
+  // S = R2^-1 P, the right factor of X = Q1 S.
   for (int e = tid; e < m * m; e += nt) {
     const int i = e / m, j = e % m;
     double t = 0.0;
     for (int k = i; k <= j; ++k) t += R[i * m + k] * R1g[k * m + j];
-    W[j * m + i] = (i <= j) ? t : 0.0;  // W column-major: W[col*m + row]
+    W[e] = (i <= j) ? t : 0.0;
   }
   __syncthreads();
-  PolarScratch sp;
-  sp.R = W;
-  sp.Vr = V;
-  sp.red = M;  // unused by the Jacobi routine
-  onesided_jacobi(m, sp, 60);
-  __shared__ int s_rank, s_fb;
-  if (tid == 0) {
-    double smax = 0.0, smin = 1e300;
-    double sv[64];
-    for (int j = 0; j < m; ++j) {
-      double t = 0.0;
-      for (int r = 0; r < m; ++r) t += W[j * m + r] * W[j * m + r];
-      sv[j] = sqrt(t);
-      smax = fmax(smax, sv[j]);
-      smin = fmin(smin, sv[j]);
-    }
-    const double cutoff = smax * double(p_true > m ? p_true : m) * 2.220446049250313e-16;
-    int rank = 0;
-    for (int j = 0; j < m; ++j) rank += sv[j] > cutoff;
-    s_rank = rank;
-    s_fb = !(smin > 1e-7 * smax);  // CholeskyQR2 too inaccurate: let the exact path decide
-  }
+  __shared__ double red[40];
+  __shared__ double fcol[kMaxGramM];
+  // M (m*m) receives P; V and R serve as scratch (R2 itself is no longer
+  // needed: Ri = R2^-1 is kept)
+  const double kappa = newton_polar(W, M, V, R, fcol, red, m);
   __syncthreads();
-  if (s_fb) {
+  if (!(kappa > 0.0) || kappa > 1e7 * sqrt(double(m))) {  // CholeskyQR2 too inaccurate: exact path decides
     if (tid == 0) pc->fallback = 1;
     return;
   }
-  if (tid == 0) pc->rank = s_rank;
-  // U = W / s (columns); S = R2^-1 U V'
-  for (int j = tid; j < m; j += nt) {
-    double t = 0.0;
-    for (int r = 0; r < m; ++r) t += W[j * m + r] * W[j * m + r];
-    t = sqrt(t);
-    for (int r = 0; r < m; ++r) W[j * m + r] /= t;
-  }
-  __syncthreads();
-  for (int e = tid; e < m * m; e += nt) {  // M = U V' (row-major M[r*m+c])
-    const int r = e / m, c = e % m;
-    double t = 0.0;
-    for (int k = 0; k < m; ++k) t += W[k * m + r] * V[k * m + c];
-    M[e] = t;
-  }
-  __syncthreads();
-  for (int e = tid; e < m * m; e += nt) {  // S = Ri (R2^-1) * M
+  if (tid == 0) pc->rank = m;
+  for (int e = tid; e < m * m; e += nt) {  // S = Ri (R2^-1) * P
     const int r = e / m, c = e % m;
     double t = 0.0;
     for (int k = r; k < m; ++k) t += Ri[r * m + k] * M[k * m + c];
