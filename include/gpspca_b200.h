@@ -184,6 +184,25 @@ int gps_polar(gps_ctx* ctx, const double* G, int64_t p, int m, double* X_out, in
  * reference's sign-fixed QR, block.py:162-170). */
 int gps_orthonormalize(gps_ctx* ctx, const double* M, int64_t p, int m, double* Q_out);
 
+/* ---- Recognition path ---------------------------------
+ * Y = A C for m coefficient vectors (C: n x m column-major, Y: p x m
+ * column-major, host buffers): the building block of project (pca.py:57-71,
+ * (S - mean) L with S = A) and explained_variance (pca.py:74-103).  One pass
+ * over the columns with a nonzero coefficient row, fp64 accumulation, fixed
+ * reduction order. */
+int gps_gram_apply_block(gps_matrix* A, const double* C, int m, double* Y_out);
+/* Squared row norms of a row-major rows x dim fp64 device matrix. */
+int gps_row_sqnorms(gps_ctx* ctx, const double* X_dev, int64_t rows, int dim, double* out_dev);
+/* k-NN distances (datasets.py:213-220): dist[t][r] = max((|t|^2 - 2 t.s_r) +
+ * |s_r|^2, 0) for the row-major test rows (n_test x dim) against the train
+ * rows given column-major (trainT: dim x n_train) with their squared norms;
+ * all device pointers on the context's device.  argmin_dev (optional,
+ * n_test) receives the first minimal train index per test row (np.argmin,
+ * datasets.py:255).  Blocking at return. */
+int gps_knn_distances(gps_ctx* ctx, const double* test_dev, int64_t n_test, const double* trainT_dev,
+                      int64_t n_train, int dim, const double* train_sqnorm_dev, double* dist_dev,
+                      int64_t* argmin_dev);
+
 #ifdef __cplusplus
 }
 #endif

@@ -9,8 +9,12 @@ only `tests/`, `__graft_entry__.smoke()` and `bench.py`'s CPU-baseline leg
 its CUDA library is missing.
 
 Parity status: PINNED.  `tests/golden/*.json` were produced by running the
-reference itself in the build container (`tests/golden/make_golden.py`);
-`tests/test_oracle_golden.py` checks this restatement against them.
+reference itself in the build container (`tests/golden/make_golden.py`,
+`tests/golden/make_golden_recog.py`); `tests/test_oracle_golden.py` and
+`tests/test_recognition.py` check these restatements against them.
+
+`oracle.recognition` restates the recognition path around the solver
+(projection, explained variance, k-NN, dense PCA).
 """
 
 from .gpower import *  # noqa: F401,F403

@@ -5,7 +5,8 @@ arXiv:1312.6182).
 Same public names, signatures and exceptions as the reference API
 (`/root/reference/pkg/src/gpspca/__init__.py:8-69`) for the hot path:
 single-unit l1/l0 and block l1/l0 solvers, their one-shot objectives /
-ascent directions / recovery, and the column kernel seam.  Arithmetic runs in
+ascent directions / recovery, the column kernel seam, and the recognition
+path around them (project, explained_variance, knn_classify, pca_fit).  Arithmetic runs in
 hand-written sm_100a CUDA (libgpspca_b200.so, include/gpspca_b200.h); there is
 no CPU fallback.
 """
@@ -42,6 +43,7 @@ from .single_unit import (
     solve_multi_sequential,
     solve_single_unit,
 )
+from .recognition import PcaModel, deterministic_signs, explained_variance, knn_classify, pca_fit, project
 from .block import (
     BlockState,
     RankDeficiencyError,

@@ -21,6 +21,7 @@
 #include "wide_kernels.cuh"
 #include "tc_kernels.cuh"
 #include "polar_kernels.cuh"
+#include "recog_kernels.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -1832,6 +1833,99 @@ int gps_orthonormalize(gps_ctx* ctx, const double* M, int64_t p, int m, double* 
 }
 
 }  // extern "C"
+
+// ---- Recognition path ----------------------------------
+extern "C" int gps_gram_apply_block(gps_matrix* A, const double* C, int m, double* Y_out) {
+  if (!A || !C || !Y_out) return fail(GPS_E_ARG, "NULL argument");
+  if (m < 1) return fail(GPS_E_ARG, "m must be >= 1");
+  gps_ctx* ctx = A->ctx;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  const int64_t n = A->n, ld = A->ld;
+  const int m_pad = (m + kApplyComps - 1) / kApplyComps * kApplyComps;
+  const int gx = static_cast<int>(std::min<int64_t>(kApplyGX, n));
+  double* dC = nullptr;
+  double* part = nullptr;
+  double* exch = nullptr;
+  unsigned char* mask = nullptr;
+  auto cleanup = [&] {
+    if (dC) cudaFree(dC);
+    if (part) cudaFree(part);
+    if (exch) cudaFree(exch);
+    if (mask) cudaFree(mask);
+  };
+  cudaError_t e = cudaMalloc(&dC, size_t(n) * m * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&part, size_t(gx) * m_pad * ld * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&exch, (size_t(m_pad) * ld + 4) * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&mask, size_t(n));
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dC, C, size_t(n) * m * sizeof(double), cudaMemcpyHostToDevice, ctx->stream);
+  if (e != cudaSuccess) {
+    cleanup();
+    return cuda_fail(e, "gps_gram_apply_block allocation");
+  }
+  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(n, 256), int64_t(ctx->num_sms) * 8));
+  coef_mask_kernel<<<blocks, 256, 0, ctx->stream>>>(dC, n, m, mask);
+  ctx->launches++;
+  dim3 grid(gx, static_cast<unsigned>(ceil_div(ld, kApplyRows)), static_cast<unsigned>(m_pad / kApplyComps));
+  if (A->dtype == GPS_F32)
+    block_apply_kernel<float><<<grid, 256, 0, ctx->stream>>>(static_cast<const float*>(A->d), n, int(ld), m, mask, dC,
+                                                              m_pad, part);
+  else
+    block_apply_kernel<double><<<grid, 256, 0, ctx->stream>>>(static_cast<const double*>(A->d), n, int(ld), m, mask,
+                                                               dC, m_pad, part);
+  ctx->launches++;
+  int rc = ctx_scratch(ctx, ld, 1);
+  if (rc == GPS_OK) rc = launch_reduce(ctx, part, ctx->part_s, gx, static_cast<int>(m_pad * ld), exch, nullptr, 0);
+  if (rc == GPS_OK) {
+    e = cudaMemcpy2DAsync(Y_out, size_t(A->p) * sizeof(double), exch, size_t(ld) * sizeof(double),
+                          size_t(A->p) * sizeof(double), size_t(m), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) rc = cuda_fail(e, "gps_gram_apply_block");
+  }
+  cleanup();
+  return rc;
+}
+
+extern "C" int gps_row_sqnorms(gps_ctx* ctx, const double* X_dev, int64_t rows, int dim, double* out_dev) {
+  if (!ctx || !X_dev || !out_dev) return fail(GPS_E_ARG, "NULL argument");
+  if (rows < 1 || dim < 1) return fail(GPS_E_ARG, "bad shape");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(rows, 256), int64_t(ctx->num_sms) * 8));
+  row_sqnorm_kernel<<<blocks, 256, 0, ctx->stream>>>(X_dev, rows, dim, out_dev);
+  ctx->launches++;
+  GPS_CHECK_LAUNCH("row_sqnorm_kernel launch");
+  GPS_CUDA(cudaStreamSynchronize(ctx->stream));
+  return GPS_OK;
+}
+
+extern "C" int gps_knn_distances(gps_ctx* ctx, const double* test_dev, int64_t n_test, const double* trainT_dev,
+                                 int64_t n_train, int dim, const double* train_sqnorm_dev, double* dist_dev,
+                                 int64_t* argmin_dev) {
+  if (!ctx || !test_dev || !trainT_dev || !train_sqnorm_dev || !dist_dev) return fail(GPS_E_ARG, "NULL argument");
+  if (n_test < 1 || n_train < 1 || dim < 1) return fail(GPS_E_ARG, "bad shape");
+  if (n_test > 65535 * int64_t(kKnnTileT)) return fail(GPS_E_ARG, "chunk the test rows (at most %d per call)",
+                                                       65535 * kKnnTileT);
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  double* tt = nullptr;
+  GPS_CUDA(cudaMalloc(&tt, size_t(n_test) * sizeof(double)));
+  const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(n_test, 256), int64_t(ctx->num_sms) * 8));
+  row_sqnorm_kernel<<<blocks, 256, 0, ctx->stream>>>(test_dev, n_test, dim, tt);
+  dim3 grid(static_cast<unsigned>(ceil_div(n_train, kKnnTileR)), static_cast<unsigned>(ceil_div(n_test, kKnnTileT)));
+  knn_dist_kernel<<<grid, kKnnTileR, 0, ctx->stream>>>(test_dev, n_test, trainT_dev, n_train, dim, tt,
+                                                        train_sqnorm_dev, dist_dev);
+  ctx->launches += 2;
+  if (argmin_dev) {
+    row_argmin_kernel<<<static_cast<unsigned>(n_test), 256, 0, ctx->stream>>>(dist_dev, n_train, argmin_dev);
+    ctx->launches++;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  cudaFree(tt);
+  if (e != cudaSuccess) return cuda_fail(e, "gps_knn_distances");
+  return GPS_OK;
+}
 
 // Tuning diagnostics (not part of the public header): per-role cycle
 // counters of tc_dots_kernel when GPSPCA_TC_PROBE has bit 64 set.  reset

@@ -37,3 +37,35 @@ def make_matrix(recipe):
 
 def digest(A):
     return hashlib.sha256(np.asfortranarray(A).tobytes()).hexdigest()[:16]
+
+
+# ---- recognition-path fixtures (make_golden_recog.py) ----
+
+def recog_samples(seed, n, f):
+    rng = np.random.default_rng(seed)
+    base = rng.standard_normal((n, 3)) @ rng.standard_normal((3, f)) * 2.0
+    return (base + rng.standard_normal((n, f))).astype(np.float32).astype(np.float64)
+
+
+def sparse_loadings(seed, f, m, nnz):
+    rng = np.random.default_rng(seed)
+    L = np.zeros((f, m))
+    for j in range(m):
+        idx = rng.choice(f, size=nnz, replace=False)
+        L[idx, j] = rng.standard_normal(nnz)
+        L[:, j] /= np.linalg.norm(L[:, j])
+    L[:, -1] = 0.0  # a zero component (explained_variance credits 0)
+    return L
+
+
+def knn_case(seed, r, t, dim, n_labels, dup):
+    rng = np.random.default_rng(seed)
+    train = rng.standard_normal((r, dim))
+    test = rng.standard_normal((t, dim))
+    if dup:  # exact ties: repeated train rows and test rows on train rows
+        train[5] = train[2]
+        train[r - 1] = train[2]
+        test[0] = train[2]
+        test[1] = train[r // 2 + 1]
+    labels = rng.integers(0, n_labels, size=r)
+    return train, labels, test
