@@ -1326,7 +1326,9 @@ int bk_enqueue_tc(gps_bk* s, bool with_ctl) {
   a.col_exp = s->col_exp;
   {
     static const char* sg = getenv("GPSPCA_TC_SEG");  // tuning experiments only
-    a.seg_chunks = sg && atoi(sg) > 0 ? atoi(sg) : kTcSegChunks;
+    // two epilogue groups are busy for m > 32: drain every 256 rows there
+    // (~2.6e-6 relative vs ~1.4e-6 at 128 rows; the fp32 contract is 1e-4)
+    a.seg_chunks = sg && atoi(sg) > 0 ? atoi(sg) : (np > 32 ? 2 * kTcSegChunks : kTcSegChunks);
   }
   {
     static const char* pr = getenv("GPSPCA_TC_PROBE");  // timing experiments only

@@ -23,7 +23,8 @@ def _stiefel(rng, p, m):
 
 
 @pytest.mark.parametrize("p,n,m,pen", [(256, 1000, 16, "l1"), (512, 3000, 32, "l0"), (4096, 12000, 64, "l1"),
-                                        (8192, 8192, 64, "l0"), (300, 777, 24, "l1")])
+                                        (8192, 8192, 64, "l0"), (300, 777, 24, "l1"), (4128, 3001, 10, "l1"),
+                                        (10000, 2000, 5, "l0"), (33, 500, 7, "l1"), (1000, 129, 40, "l0")])
 def test_tensor_core_sweep_vs_oracle(p, n, m, pen):
     rng = np.random.default_rng(p + m)
     A32 = rng.standard_normal((p, n)).astype(np.float32)
