@@ -94,6 +94,9 @@ int gps_column_norms(gps_matrix* A, double* norms_out, int* nonfinite_out);
 
 /* single_unit.py:287-296 deflate: new fp64 matrix (I - xx')A (x unit). */
 int gps_matrix_deflate(gps_matrix* A, const double* x, gps_matrix** out);
+/* core.py:234-240 center_columns: a new fp64 matrix A - 1 mean' (column
+ * means in means_out, optional, length n). */
+int gps_matrix_center(gps_matrix* A, double* means_out, gps_matrix** out);
 
 /* Columns idx[0..k) as a new matrix (support-restricted power iteration,
  * single_unit.py:219-230 `A.values[:, support]`). */

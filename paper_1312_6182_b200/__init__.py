@@ -18,7 +18,9 @@ from .core import (
     SparseLoadings,
     StiefelPoint,
     as_data_matrix,
+    center_columns,
     column_norms,
+    gram_quadratic,
     positive_part,
 )
 from .parallel import (

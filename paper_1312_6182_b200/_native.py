@@ -80,6 +80,7 @@ SIGNATURES = {
     "gps_polar": (C.c_int, [_vp, _dp, _i64, C.c_int, _dp, _ip]),
     "gps_orthonormalize": (C.c_int, [_vp, _dp, _i64, C.c_int, _dp]),
     "gps_gram_apply_block": (C.c_int, [_vp, _dp, C.c_int, _dp]),
+    "gps_matrix_center": (C.c_int, [_vp, _dp, C.POINTER(_vp)]),
     "gps_row_sqnorms": (C.c_int, [_vp, _vp, _i64, C.c_int, _vp]),
     "gps_knn_distances": (C.c_int, [_vp, _vp, _i64, _vp, _i64, C.c_int, _vp, _vp, _vp]),
 }

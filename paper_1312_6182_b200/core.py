@@ -325,3 +325,31 @@ def positive_part(t):
 def column_norms(A):
     """Euclidean norm of every column (core.py:243-246), from the device pass."""
     return np.array(as_data_matrix(A).norms)
+
+
+def center_columns(A):
+    """Subtract each column's mean; a new fp64 DataMatrix (core.py:234-240),
+    formed on the device (column means by a 1/p-weighted A'1 sweep, then a
+    rank-1 copy kernel)."""
+    return center_columns_with_means(A)[0]
+
+
+def center_columns_with_means(A):
+    """center_columns plus the fp64 column means it subtracted."""
+    A = as_data_matrix(A)
+    h = _native.C.c_void_p()
+    means = np.empty(A.n)
+    _native.check(_native.lib().gps_matrix_center(A.handle, _native.dptr(means), _native.C.byref(h)))
+    return DataMatrix._wrap(A.context, h), means
+
+
+def gram_quadratic(A, z):
+    """z'(A'A)z evaluated as ||Az||^2 without forming the Gram matrix
+    (core.py:249-256); Az by the device column accumulation."""
+    A = as_data_matrix(A)
+    z = np.asarray(z, dtype=np.float64)
+    if z.shape != (A.n,):
+        raise ValueError(f"z must have length n={A.n}, got shape {z.shape}")
+    v = np.empty(A.p)
+    _native.check(_native.lib().gps_gram_apply(A.handle, _native.dptr(np.ascontiguousarray(z)), _native.dptr(v)))
+    return float(v @ v)

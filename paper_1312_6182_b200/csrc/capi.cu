@@ -748,11 +748,28 @@ int gps_su_sweep(gps_matrix* A, const double* x, double gamma, int penalty, doub
   return one_shot(A, kFused, x, nullptr, 0, gamma, penalty, f_out, g_half_out, c_out, w_out, nnz_out);
 }
 
+static int rank1_copy(gps_matrix* A, const double* x, const std::vector<double>& c, gps_matrix** out);
+
 int gps_matrix_deflate(gps_matrix* A, const double* x, gps_matrix** out) {
   if (!A || !x || !out) return fail(GPS_E_ARG, "NULL argument");
   std::vector<double> c(A->n);
   int rc = gps_matvec_t(A, x, c.data());
   if (rc) return rc;
+  return rank1_copy(A, x, c, out);
+}
+
+int gps_matrix_center(gps_matrix* A, double* means_out, gps_matrix** out) {
+  if (!A || !out) return fail(GPS_E_ARG, "NULL argument");
+  std::vector<double> w(A->p, 1.0 / double(A->p)), c(A->n), ones(A->p, 1.0);
+  int rc = gps_matvec_t(A, w.data(), c.data());  // column means, fp64
+  if (rc) return rc;
+  if (means_out) std::memcpy(means_out, c.data(), c.size() * sizeof(double));
+  return rank1_copy(A, ones.data(), c, out);
+}
+
+// B = A - x c' as a new fp64 matrix (pad rows stay zero).
+static int rank1_copy(gps_matrix* A, const double* x, const std::vector<double>& c, gps_matrix** out) {
+  int rc = GPS_OK;
   gps_ctx* ctx = A->ctx;
   std::lock_guard<std::mutex> lk(ctx->mu);
   gps_matrix* B = nullptr;

@@ -18,7 +18,7 @@ import numpy as np
 
 from . import _native
 from .block import solve_block
-from .core import DataMatrix, SolverConfig
+from .core import DataMatrix, SolverConfig, center_columns_with_means
 from .single_unit import solve_multi_sequential
 
 SPCA_VARIANTS = ("sl1", "sl0", "bl1", "bl0")
@@ -58,14 +58,12 @@ def fit_projection(train_samples, variant, m, gamma, mu=1.0, tol=1e-6, max_iter=
     (loadings n x m, feature means, RunReport)."""
     if variant not in SPCA_VARIANTS:
         raise ValueError(f"unknown variant {variant!r}")
-    X = np.asarray(train_samples, dtype=np.float64)
-    if center:
-        mean = X.mean(axis=0)
-        X = X - mean
+    A = DataMatrix(np.asarray(train_samples, dtype=np.float64))
+    if center:  # on the device: column means and the centred copy (core.py:234-240)
+        A, mean = center_columns_with_means(A)
     else:
-        mean = np.zeros(X.shape[1])
+        mean = np.zeros(A.n)
     penalty = "l1" if variant.endswith("1") else "l0"
-    A = DataMatrix(X)
     if variant.startswith("s"):
         cfg = SolverConfig(penalty=penalty, mode="single_unit", m=m, gamma=gamma, mu=mu, tol=tol,
                            max_iter=max_iter, seed=seed)

@@ -142,3 +142,33 @@ def test_device_recognition_errors():
         g.knn_classify(np.zeros((0, 2)), [], np.ones((2, 2)))
     with pytest.raises(ValueError):
         g.pca_fit(np.ones((4, 3)), 5)
+
+
+@pytest.mark.gpu
+def test_device_center_columns_and_gram_quadratic():
+    # core.py:234-256
+    g = _gps()
+    rng = np.random.default_rng(21)
+    for dtype in (np.float64, np.float32):
+        S = (rng.standard_normal((70, 45)) * 3 + 5).astype(dtype)
+        C = g.center_columns(S)
+        S64 = S.astype(np.float64)
+        np.testing.assert_allclose(C.values, S64 - S64.mean(axis=0), rtol=0, atol=1e-12)
+        assert C.dtype == np.float64 and C.shape == S.shape
+        z = rng.standard_normal(45)
+        v = S64 @ z
+        assert g.gram_quadratic(S, z) == pytest.approx(float(v @ v), rel=1e-12)
+    with pytest.raises(ValueError):
+        g.gram_quadratic(np.ones((3, 4)), np.ones(3))
+
+
+@pytest.mark.gpu
+def test_fit_projection_centres_on_device():
+    # bench.py:78-114 fit_projection: loadings of the centred training data
+    from paper_1312_6182_b200.timing import fit_projection
+
+    rng = np.random.default_rng(22)
+    X = rng.standard_normal((80, 30)) + 2.0
+    Z, mean, report = fit_projection(X, "sl1", 2, 0.05)
+    np.testing.assert_allclose(mean, X.mean(axis=0), rtol=1e-12)
+    assert Z.shape == (30, 2) and report.iterations >= 1
