@@ -1391,16 +1391,18 @@ int bk_enqueue_step(gps_bk* s) {
                                             s->pc, m);
   bk_assemble_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(s->exch, s->mg, ld, m, s->mu_dev, s->G, s->pc);
   gram_partial_kernel<<<kGramBlocks, kGramThreads, 0, ctx->stream>>>(s->G, ld, p, m, s->gram_part, s->pc);
-  chol_stage_kernel<<<1, kPolarThreads, chol_smem_bytes(m), ctx->stream>>>(s->gram_part, kGramBlocks, m, p, 1, s->R1, s->Sm,
+  gram_reduce_kernel<<<(m * m + 255) / 256, 256, 0, ctx->stream>>>(s->gram_part, kGramBlocks, m * m, s->pc);
+  chol_stage_kernel<<<1, kPolarThreads, chol_smem_bytes(m), ctx->stream>>>(s->gram_part, 1, m, p, 1, s->R1, s->Sm,
                                                                  s->pc);
   apply_right_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(s->G, s->Sm, ld, m, s->Tm, s->pc, nullptr, 0);
   gram_partial_kernel<<<kGramBlocks, kGramThreads, 0, ctx->stream>>>(s->Tm, ld, p, m, s->gram_part, s->pc);
-  chol_stage_kernel<<<1, kPolarThreads, chol_smem_bytes(m), ctx->stream>>>(s->gram_part, kGramBlocks, m, p, 2, s->R1, s->Sm,
+  gram_reduce_kernel<<<(m * m + 255) / 256, 256, 0, ctx->stream>>>(s->gram_part, kGramBlocks, m * m, s->pc);
+  chol_stage_kernel<<<1, kPolarThreads, chol_smem_bytes(m), ctx->stream>>>(s->gram_part, 1, m, p, 2, s->R1, s->Sm,
                                                                  s->pc);
   apply_right_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(s->Tm, s->Sm, ld, m, s->X, s->pc, s->ctl, xs);
   bk_finish_kernel<<<1, kPolarThreads, polar_smem_bytes(m), ctx->stream>>>(s->G, s->X, xs, ld, p, m, s->ctl, s->pc,
                                                                            s->rank_dev);
-  ctx->launches += 9;
+  ctx->launches += 11;
   GPS_CHECK_LAUNCH("block polar step launch");
   return GPS_OK;
 }

@@ -111,125 +111,112 @@ __global__ void __launch_bounds__(kGramThreads) gram_partial_kernel(const double
   }
 }
 
-// In-place Gauss-Jordan inverse with partial pivoting of the m x m
-// row-major A (destroyed) into B; fcol: m scratch.  One CTA of 1024 threads,
-// m <= 64: thread (i, g) = (tid / 16, tid % 16) owns row i, columns
-// g, g + 16, g + 32, g + 48 of both A and B.  Returns false on an exactly
-// singular pivot.
-__device__ bool gj_inverse(double* A, double* B, double* fcol, int m) {
-  const int tid = threadIdx.x;
-  const int i = tid >> 4, g = tid & 15;
-  __shared__ int s_piv;
-  if (i < m)
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int c = g + 16 * k;
-      if (c < m) B[i * m + c] = (i == c) ? 1.0 : 0.0;
+// C = op(A) B for m x m row-major smem matrices (op = transpose when ta) on
+// the fp64 tensor cores: mma.sync m8n8k4 f64, one 8 x 8 tile of C per warp
+// at a time (fragments: A[lane/4][lane%4], B[lane%4][lane/4],
+// C[lane/4][2 (lane%4) + {0,1}]), k ascending.  m <= 64, any blockDim.
+__device__ void mm_small(const double* A, const double* B, double* C, int m, bool ta) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int tiles = (m + 7) >> 3;
+  const int ar = lane >> 2, ak = lane & 3;  // A fragment (row, k); B fragment is (k, col) = (ak, ar)
+  for (int tile = warp; tile < tiles * tiles; tile += nw) {
+    const int ti = tile / tiles, tj = tile % tiles;
+    const int r = ti * 8 + ar, cb = tj * 8 + ar;
+    // two independent k-chains (even / odd 4-blocks) hide the DMMA latency
+    double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+    for (int k0 = 0; k0 < m; k0 += 8) {
+      const int k = k0 + ak, kk = k + 4;
+      const double a = (r < m && k < m) ? (ta ? A[k * m + r] : A[r * m + k]) : 0.0;
+      const double b = (k < m && cb < m) ? B[k * m + cb] : 0.0;
+      const double a2 = (r < m && kk < m) ? (ta ? A[kk * m + r] : A[r * m + kk]) : 0.0;
+      const double b2 = (kk < m && cb < m) ? B[kk * m + cb] : 0.0;
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                   : "+d"(c0), "+d"(c1)
+                   : "d"(a), "d"(b));
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                   : "+d"(e0), "+d"(e1)
+                   : "d"(a2), "d"(b2));
     }
-  __syncthreads();
-  for (int j = 0; j < m; ++j) {
-    if (tid < 32) {  // pivot: largest |A[r][j]|, r >= j (lowest index on ties)
-      double best = -1.0;
-      int bi = j;
-      for (int r = j + tid; r < m; r += 32) {
-        const double v = fabs(A[r * m + j]);
-        if (v > best) {
-          best = v;
-          bi = r;
-        }
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi < bi)) {
-          best = ob;
-          bi = oi;
-        }
-      }
-      if (tid == 0) s_piv = best > 0.0 ? bi : -1;
+    c0 += e0;
+    c1 += e1;
+    const int cr = ti * 8 + (lane >> 2), cc = tj * 8 + 2 * (lane & 3);
+    if (cr < m) {
+      if (cc < m) C[cr * m + cc] = c0;
+      if (cc + 1 < m) C[cr * m + cc + 1] = c1;
     }
-    __syncthreads();
-    const int pv = s_piv;
-    if (pv < 0) return false;
-    if (pv != j && tid < 2 * m) {  // swap rows j and pv
-      double* X = tid < m ? A : B;
-      const int c = tid < m ? tid : tid - m;
-      const double t = X[j * m + c];
-      X[j * m + c] = X[pv * m + c];
-      X[pv * m + c] = t;
-    }
-    __syncthreads();
-    if (tid < m) fcol[tid] = A[tid * m + j];
-    __syncthreads();
-    const double inv = 1.0 / fcol[j];
-    if (tid < 2 * m) {  // normalise the pivot row
-      if (tid < m)
-        A[j * m + tid] *= inv;
-      else
-        B[j * m + tid - m] *= inv;
-    }
-    __syncthreads();
-    if (i < m && i != j) {
-      const double f = fcol[i];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int c = g + 16 * k;
-        if (c < m) {
-          A[i * m + c] = fma(-f, A[j * m + c], A[i * m + c]);
-          B[i * m + c] = fma(-f, B[j * m + c], B[i * m + c]);
-        }
-      }
-    }
-    __syncthreads();
   }
-  return true;
 }
 
-// Polar factor of the m x m row-major R by the Frobenius-scaled Newton
-// iteration X <- (z X + X^-T / z) / 2 (quadratic convergence; scaling
-// dropped once the step is small).  X holds the result; W, Y, fcol, red are
-// scratch.  Returns the Frobenius condition estimate |R|_F |R^-1|_F of the
-// first step (0 if R is singular).
-__device__ double newton_polar(const double* R, double* X, double* W, double* Y, double* fcol, double* red, int m) {
+// Polar factor of the well-conditioned m x m R (row-major, in X on entry,
+// the result on exit) by the Newton-Schulz iteration
+// X <- 1.5 X - 0.5 X (X'X) from X0 = R / sqrt(|R|_1 |R|_inf) (all singular values in
+// (0, 1], so it converges; quadratically once X'X ~ I).  T, U: m x m
+// scratch.  Returns false if it has not converged in max_it steps.
+__device__ bool newton_schulz_polar(double* X, double* T, double* U, double* red, int m, int max_it) {
   const int tid = threadIdx.x, nt = blockDim.x;
-  for (int e = tid; e < m * m; e += nt) X[e] = R[e];
-  __syncthreads();
-  double kappa = 0.0;
-  bool scale = true;
-  for (int it = 0; it < 30; ++it) {
-    for (int e = tid; e < m * m; e += nt) W[e] = X[e];
-    __syncthreads();
-    if (!gj_inverse(W, Y, fcol, m)) return 0.0;  // Y = X^-1
-    double a = 0.0, b = 0.0;
-    for (int e = tid; e < m * m; e += nt) {
-      a = fma(X[e], X[e], a);
-      b = fma(Y[e], Y[e], b);
+  // X0 = R / sqrt(|R|_1 |R|_inf) (>= |R|_2, and closer to it than |R|_F)
+  __shared__ double s_norm1, s_norminf;
+  if (tid < 32) {
+    double c1 = 0.0, ci = 0.0;
+    for (int j = tid; j < m; j += 32) {
+      double cs = 0.0, rs = 0.0;
+      for (int i = 0; i < m; ++i) {
+        cs += fabs(X[i * m + j]);
+        rs += fabs(X[j * m + i]);
+      }
+      c1 = fmax(c1, cs);
+      ci = fmax(ci, rs);
     }
-    const double nx = sqrt(block_sum_any(a, red)), ny = sqrt(block_sum_any(b, red));
-    if (it == 0) kappa = nx * ny;
-    const double z = scale ? sqrt(ny / nx) : 1.0;
-    double d = 0.0;
-    for (int e = tid; e < m * m; e += nt) {  // X_new = (z X + Y^T / z) / 2
-      const int r = e / m, c = e % m;
-      const double xn = 0.5 * (z * X[e] + Y[c * m + r] / z);
-      d = fma(xn - X[e], xn - X[e], d);
-      W[e] = xn;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      c1 = fmax(c1, __shfl_xor_sync(0xffffffffu, c1, o));
+      ci = fmax(ci, __shfl_xor_sync(0xffffffffu, ci, o));
     }
-    const double dn = sqrt(block_sum_any(d, red));
-    for (int e = tid; e < m * m; e += nt) X[e] = W[e];
-    __syncthreads();
-    const double rel = dn / sqrt(double(m));  // |X| -> sqrt(m) at convergence
-    if (rel < 1e-2) scale = false;
-    if (rel < 1e-14) break;
+    if (tid == 0) {
+      s_norm1 = c1;
+      s_norminf = ci;
+    }
   }
-  return kappa;
+  __syncthreads();
+  const double inv = 1.0 / sqrt(s_norm1 * s_norminf);
+  for (int e = tid; e < m * m; e += nt) X[e] *= inv;
+  __syncthreads();
+  for (int it = 0; it < max_it; ++it) {
+    mm_small(X, X, T, m, true);  // T = X'X
+    __syncthreads();
+    mm_small(X, T, U, m, false);  // U = X T
+    __syncthreads();
+    double d = 0.0;
+    for (int e = tid; e < m * m; e += nt) {
+      const double xn = fma(-0.5, U[e], 1.5 * X[e]);
+      d = fma(xn - X[e], xn - X[e], d);
+      X[e] = xn;
+    }
+    const double dn = sqrt(block_sum_any(d, red));  // (syncs)
+#ifdef GPS_POLAR_DEBUG
+    if (tid == 0) printf("newton-schulz it %d step %.3e\n", it, dn);
+#endif
+    if (dn < 1e-15 * sqrt(double(m))) return true;
+  }
+  return false;
+}
+
+// part[0][e] = sum_b part[b][e] in a fixed order, many CTAs (the one-CTA
+// stage kernel then reads a single Gram).
+__global__ void gram_reduce_kernel(double* __restrict__ part, int nparts, int mm, const PolarCtl* pc) {
+  if (!pc->active || pc->fallback) return;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= mm) return;
+  double t = 0.0;
+  for (int b = 0; b < nparts; ++b) t += part[size_t(b) * mm + e];
+  part[e] = t;
 }
 
 // Sum the Gram partials (fixed order), Cholesky G'G = R'R (upper R), and
-// invert R.  stage 1: R1 -> Rs (R1), Rinv (R1^-1).  stage 2: R2 with R = R2 R1,
-// one-sided Jacobi SVD of R, rank, then S = R2^-1 U V' (the right factor of
-// X = Q1 S) or the fallback flag.  One CTA; small m x m work in smem.
+// invert R.  stage 1: R1 -> Rs (R1), Rinv (R1^-1), or the fallback flag when
+// kappa_F(R1) > 1e7 sqrt(m).  stage 2: R2 with R = R2 R1, the polar factor
+// P of R by Newton-Schulz, then S = R2^-1 P (the right factor of X = Q1 S).
+// One CTA; small m x m work in smem.
 __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double* __restrict__ part, int nparts, int m,
                                                                   int p_true, int stage, double* __restrict__ R1g,
                                                                   double* __restrict__ Sg, PolarCtl* pc) {
@@ -241,51 +228,93 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
   double* Ri = R + m * m;       // m*m inverse
   double* W = Ri + m * m;       // m*m scratch
   double* V = W + m * m;        // m*m scratch
+#ifdef GPS_POLAR_DEBUG
+  if (tid == 0) printf("chol stage %d start %lld\n", stage, clock64());
+#endif
   __shared__ int bad;
+  __shared__ double red[40];
+  // Gram = sum of the partials in a fixed order (8 independent loads in
+  // flight per thread)
   for (int e = tid; e < m * m; e += nt) {
     double t = 0.0;
-    for (int b = 0; b < nparts; ++b) t += part[size_t(b) * m * m + e];
+    int b = 0;
+    for (; b + 8 <= nparts; b += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = part[size_t(b + u) * m * m + e];
+      t += ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
+    }
+    for (; b < nparts; ++b) t += part[size_t(b) * m * m + e];
     M[e] = t;
     R[e] = 0.0;
+    Ri[e] = 0.0;
   }
+#ifdef GPS_POLAR_DEBUG
+  if (tid == 0) printf("chol stage %d partials loaded %lld\n", stage, clock64());
+#endif
   if (tid == 0) bad = 0;
   __syncthreads();
   double dmax = 0.0;
   for (int j = 0; j < m; ++j) dmax = fmax(dmax, M[j * m + j]);
+  // Right-looking Cholesky of the upper triangle, two barriers per step:
+  // every thread derives the pivot itself; thread (a, g) = (tid / 16,
+  // tid % 16) updates row a, columns g, g + 16, ... of the trailing block.
+  const int ta = tid >> 4, tg = tid & 15;
   for (int j = 0; j < m; ++j) {
-    if (tid == 0) {
-      const double d = M[j * m + j];
-      if (!(d > 1e-28 * dmax) || !(d > 0.0)) bad = 1;
-      R[j * m + j] = d > 0.0 ? sqrt(d) : 1.0;
+    const double d = M[j * m + j];
+    if (!(d > 1e-28 * dmax) || !(d > 0.0)) {
+      if (tid == 0) bad = 1;
+      break;  // uniform: every thread reads the same d
     }
+    const double rp = rsqrt(d);  // one reciprocal square root instead of sqrt + divisions
+    for (int c = j + tid; c < m; c += nt) R[j * m + c] = (c == j) ? d * rp : M[j * m + c] * rp;
     __syncthreads();
-    if (bad) break;
-    const double piv = R[j * m + j];
-    for (int c = j + 1 + tid; c < m; c += nt) R[j * m + c] = M[j * m + c] / piv;
-    __syncthreads();
-    for (int e = tid; e < m * m; e += nt) {
-      const int a = e / m, c = e % m;
-      if (a > j && c >= a) {
-        M[a * m + c] -= R[j * m + a] * R[j * m + c];
-        M[c * m + a] = M[a * m + c];
-      }
+    if (ta > j && ta < m) {
+      const double rja = R[j * m + ta];
+      for (int c = ta + tg; c < m; c += 16) M[ta * m + c] = fma(-rja, R[j * m + c], M[ta * m + c]);
     }
     __syncthreads();
   }
+  __syncthreads();
+#ifdef GPS_POLAR_DEBUG
+  if (tid == 0) printf("chol stage %d cholesky done %lld\n", stage, clock64());
+#endif
   if (bad) {
     if (tid == 0) pc->fallback = 1;
     return;
   }
-  // Ri = R^-1 (upper): column c by back substitution, columns in parallel
-  for (int c = tid; c < m; c += nt) {
+  // Ri = R^-1 (upper) by rows from the bottom: row i of Ri needs rows > i,
+  // all its columns c >= i at once -- 16 threads per column each form a
+  // strided piece of sum_k R[i][k] Ri[k][c], combined by shuffles (fixed
+  // order); one barrier per row.
+  {
+    const int c = tid >> 4, q = tid & 15;  // 64 columns x 16 threads
     for (int i = m - 1; i >= 0; --i) {
-      double t = (i == c) ? 1.0 : 0.0;
-      for (int k = i + 1; k <= c; ++k) t -= R[i * m + k] * Ri[k * m + c];
-      Ri[i * m + c] = (i <= c) ? t / R[i * m + i] : 0.0;
+      double t = 0.0;
+      if (c < m && c >= i)
+        for (int k = i + 1 + q; k <= c; k += 16) t = fma(R[i * m + k], Ri[k * m + c], t);
+#pragma unroll
+      for (int o = 8; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (c < m && c >= i && q == 0) Ri[i * m + c] = ((i == c ? 1.0 : 0.0) - t) / R[i * m + i];
+      __syncthreads();
     }
   }
-  __syncthreads();
+#ifdef GPS_POLAR_DEBUG
+  if (tid == 0) printf("chol stage %d inverse done %lld\n", stage, clock64());
+#endif
   if (stage == 1) {
+    // kappa_F(R1) = |R1|_F |R1^-1|_F ~ kappa(G): beyond 1e7 sqrt(m) the
+    // CholeskyQR2 result is not trusted and the exact path decides (rank too)
+    double a = 0.0, b = 0.0;
+    for (int e = tid; e < m * m; e += nt) {
+      a = fma(R[e], R[e], a);
+      b = fma(Ri[e], Ri[e], b);
+    }
+    const double kap = sqrt(block_sum_any(a, red)) * sqrt(block_sum_any(b, red));
+    if (!(kap <= 1e7 * sqrt(double(m)))) {
+      if (tid == 0) pc->fallback = 1;
+      return;
+    }
     for (int e = tid; e < m * m; e += nt) {
       R1g[e] = R[e];
       Sg[e] = Ri[e];  // apply: Q1 = G R1^-1
@@ -293,9 +322,9 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
     return;
   }
   // stage 2: R = R2 R1 (upper, row-major in W), its polar factor P by the
-  // scaled Newton iteration (the CholeskyQR2 path only runs for condition
-  // numbers far below the rank cutoff max(p, m) eps, so rank = m here), then
-  // S = R2^-1 P, the right factor of X = Q1 S.
+  // Newton-Schulz iteration (the CholeskyQR2 path only runs for condition
+  // numbers far below the rank cutoff max(p, m) eps -- stage 1 checked --
+  // so rank = m here), then S = R2^-1 P, the right factor of X = Q1 S.
   for (int e = tid; e < m * m; e += nt) {
     const int i = e / m, j = e % m;
     double t = 0.0;
@@ -303,16 +332,20 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
     W[e] = (i <= j) ? t : 0.0;
   }
   __syncthreads();
-  __shared__ double red[40];
-  __shared__ double fcol[kMaxGramM];
-  // M (m*m) receives P; V and R serve as scratch (R2 itself is no longer
-  // needed: Ri = R2^-1 is kept)
-  const double kappa = newton_polar(W, M, V, R, fcol, red, m);
+#ifdef GPS_POLAR_DEBUG
+  if (tid == 0) printf("chol stage %d R2R1 done %lld\n", stage, clock64());
+#endif
+  // M receives P (starting from R2 R1); V and R (R2 itself is no longer
+  // needed: Ri = R2^-1 is kept) are scratch
+  for (int e = tid; e < m * m; e += nt) M[e] = W[e];
   __syncthreads();
-  if (!(kappa > 0.0) || kappa > 1e7 * sqrt(double(m))) {  // CholeskyQR2 too inaccurate: exact path decides
+  if (!newton_schulz_polar(M, V, R, red, m, 100)) {  // not converged: exact path decides
     if (tid == 0) pc->fallback = 1;
     return;
   }
+#ifdef GPS_POLAR_DEBUG
+  if (tid == 0) printf("chol stage %d NS done %lld\n", stage, clock64());
+#endif
   if (tid == 0) pc->rank = m;
   for (int e = tid; e < m * m; e += nt) {  // S = Ri (R2^-1) * P
     const int r = e / m, c = e % m;
