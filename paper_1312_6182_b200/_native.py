@@ -11,6 +11,12 @@ import threading
 
 import numpy as np
 
+# Load every kernel when the CUDA context is created instead of on first
+# launch: a solve should not pay module-loading latency the first time it
+# reaches a code path (only effective if nothing initialised CUDA earlier in
+# the process; set CUDA_MODULE_LOADING yourself to override).
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("GPSPCA_LIB", os.path.join(_PKG, "libgpspca_b200.so"))
 
