@@ -259,7 +259,7 @@ int launch_sweep(gps_matrix* A, const SweepPlan& plan, SweepArgs args, int mode,
 
 int launch_reduce(gps_ctx* ctx, const double* part_g, const double* part_s, int nparts, int ld, double* exch,
                   const GpsCtl* ctl, int nparts_s = -1) {
-  const int blocks = (ld + 255) / 256 + 1;
+  const int blocks = (ld + kReduceRows - 1) / kReduceRows + 1;
   su_reduce_kernel<<<blocks, 256, 0, ctx->stream>>>(part_g, part_s, nparts, ld, exch, ctl,
                                                     nparts_s < 0 ? nparts : nparts_s);
   ctx->launches++;
@@ -1494,7 +1494,13 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
   alloc((void**)&s->mu_dev, size_t(2) * m * sizeof(double));  // mu, then gamma (tensor-core path)
   alloc((void**)&s->hist, (size_t(max_iter) + 1) * sizeof(double));
   if (pl.wide) alloc((void**)&s->wbuf, size_t(pl.mg) * n * sizeof(double));
-  s->big_polar = size_t(ld) * m >= (size_t(1) << 15) && !std::getenv("GPSPCA_HH_POLAR");
+  {
+    // CholeskyQR2 polar for large p * m (the one-CTA Householder step is
+    // latency-bound there); tuning override GPSPCA_BIG_POLAR_MIN (p * m)
+    const char* th = std::getenv("GPSPCA_BIG_POLAR_MIN");
+    const size_t min_pm = th ? size_t(std::strtoull(th, nullptr, 10)) : (size_t(1) << 12);
+    s->big_polar = size_t(ld) * m >= min_pm && !std::getenv("GPSPCA_HH_POLAR");
+  }
   if (s->big_polar) {
     alloc((void**)&s->pc, sizeof(PolarCtl));
     alloc((void**)&s->gram_part, size_t(kGramBlocks) * m * m * sizeof(double));

@@ -395,22 +395,38 @@ __global__ void __launch_bounds__(kSweepThreads, 1) su_sweep_kernel(const SweepA
   }
 }
 
-// K2: sum the per-CTA partials in CTA order (deterministic), into
-// exch = [g (ld) | f | nnz | sum w^2 | 0].  Row blocks + one scalar block.
+// K2: sum the per-CTA partials into exch = [g (ld) | f | nnz | sum w^2 | 0]
+// in a fixed order (deterministic): a 256-thread block covers 32 rows with
+// 8 slices of the partial range each (coalesced 32-row loads, ~nparts/8
+// independent loads per thread), the slice sums added in slice order.
+// Row blocks + one scalar block.
+constexpr int kReduceRows = 32;
+constexpr int kReduceSlices = 8;
 __global__ void __launch_bounds__(256) su_reduce_kernel(const double* __restrict__ part_g,
                                                         const double* __restrict__ part_s, int nparts,
                                                         int ld, double* __restrict__ exch,
                                                         const GpsCtl* ctl, int nparts_s) {
   if (ctl != nullptr && ctl->done) return;
-  const int row_blocks = (ld + 255) / 256;
+  const int row_blocks = (ld + kReduceRows - 1) / kReduceRows;
   if (blockIdx.x < row_blocks) {
-    const int r = blockIdx.x * 256 + threadIdx.x;
-    if (r >= ld) return;
+    __shared__ double part[kReduceSlices][kReduceRows];
+    const int rr = threadIdx.x & (kReduceRows - 1), sl = threadIdx.x / kReduceRows;
+    const int r = blockIdx.x * kReduceRows + rr;
+    const int b0 = nparts * sl / kReduceSlices, b1 = nparts * (sl + 1) / kReduceSlices;
     double t = 0.0;
-    const double* p = part_g + r;
-#pragma unroll 8
-    for (int b = 0; b < nparts; ++b) t += p[size_t(b) * ld];
-    exch[r] = t;
+    if (r < ld) {
+      const double* p = part_g + r;
+#pragma unroll 4
+      for (int b = b0; b < b1; ++b) t += p[size_t(b) * ld];
+    }
+    part[sl][rr] = t;
+    __syncthreads();
+    if (sl == 0 && r < ld) {
+      double u = part[0][rr];
+#pragma unroll
+      for (int k = 1; k < kReduceSlices; ++k) u += part[k][rr];
+      exch[r] = u;
+    }
   } else if (threadIdx.x < 4) {
     double t = 0.0;
     for (int b = 0; b < nparts_s; ++b) t += part_s[size_t(b) * 4 + threadIdx.x];
