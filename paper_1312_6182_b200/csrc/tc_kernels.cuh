@@ -49,14 +49,6 @@ constexpr int kTcSegChunks = 2;  // TMEM accumulation segment: 2 chunks = 128 ro
 constexpr int kTcAScaleExp = 14; // |a s_i| in [2^14, 2^15)
 constexpr int kTcXScaleExp = 14; // |x| <= 1 -> |x 2^14| <= 2^14
 
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-          smem_u32(dst)),
-      "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y)
-      : "memory");
-}
-
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
@@ -74,6 +66,8 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(const void* smem_ptr) {
   return d;
 }
 
+// tf32 instruction descriptor and single-thread issue: used by the
+// microbenchmarks in scripts/ubench (the sweep itself runs kind::f16).
 // Instruction descriptor: D f32, A/B tf32, both K-major, M x N.
 __host__ __device__ constexpr uint32_t umma_idesc_tf32(int M, int N) {
   return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
@@ -88,19 +82,10 @@ __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t a, uint64_t 
       : "memory");
 }
 
-// Warp-converged forms: every lane executes the call with identical
+// Warp-converged commit: every lane executes the call with identical
 // operands and elect.sync picks the issuing lane inside the asm, so the
-// compiler keeps descriptors in uniform registers (a single-thread branch
+// compiler keeps operands in uniform registers (a single-thread branch
 // instead costs a per-instruction R2UR + waterfall loop, ~90 clocks/MMA).
-__device__ __forceinline__ void umma_tf32_warp(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
-}
 __device__ __forceinline__ void umma_commit_warp(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
@@ -236,18 +221,6 @@ __device__ __forceinline__ void umma_f16_ts_warp(uint32_t tmem_d, uint32_t tmem_
       "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
-// The tf32 form (A in TMEM) is kept for the microbenchmarks.
-__device__ __forceinline__ void umma_tf32_ts_warp(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
-                                                  uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
-}
-
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
