@@ -1130,8 +1130,13 @@ bool pick_bk(int ld, BkPlan& pl) {
     GPS_BK(256, 4, 4)
     GPS_BK(256, 8, 2)
   } else {
-    GPS_BK(32, 1, 2)
-    GPS_BK(32, 2, 2)
+    // fp64: four components per read while a thread keeps <= 4 rows
+    // (X and the G partial: 2 x 16 doubles), two beyond
+    GPS_BK(32, 1, 4)
+    GPS_BK(32, 2, 4)
+    GPS_BK(64, 2, 4)
+    GPS_BK(128, 2, 4)
+    GPS_BK(256, 2, 4)
     GPS_BK(32, 4, 2)
     GPS_BK(64, 4, 2)
     GPS_BK(128, 4, 2)
