@@ -45,6 +45,8 @@ from .single_unit import (
     solve_multi_sequential,
     solve_single_unit,
 )
+from .timing import TimingConfig, emit_report, fit_projection, run_timing_experiment
+from .timing import TimingConfig as ExperimentConfig
 from .recognition import PcaModel, deterministic_signs, explained_variance, knn_classify, pca_fit, project
 from .block import (
     BlockState,

@@ -26,9 +26,24 @@ SPCA_VARIANTS = ("sl1", "sl0", "bl1", "bl0")
 
 @dataclass
 class TimingConfig:
-    """The timing fields of the reference ExperimentConfig (bench.py:34-75)."""
+    """The reference ExperimentConfig (bench.py:34-75) as far as the timing
+    sweep reads it.  The recognition-experiment fields (dataset, split,
+    knn_k, ...) and the CPU-plan fields (workers, chunk, timing_workers) are
+    accepted so reference call sites construct it unchanged; the device
+    ignores the plan (one GPU, fixed grid) and reports workers = 1."""
 
+    dataset: str = None
+    format: str = "csv_labeled"
+    variant: str = "sl1"
     m: tuple = (5,)
+    gamma: float = 0.1
+    repetitions: int = 1
+    workers: int = 1
+    chunk: int = 256
+    knn_k: int = 1
+    split: object = None
+    report_timing: bool = True
+    timing_workers: tuple = None
     mu: float = 1.0
     seed: int = 0
     out: str = None
