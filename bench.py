@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=N_COLS, help="columns (default 2^20)")
+    ap.add_argument("--cols", "--n", dest="n", type=int, default=N_COLS, help="columns (default 2^20)")
     ap.add_argument("--p", type=int, default=P)
     ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -217,12 +217,21 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # GPSPCA_BENCH_BACKEND=gloo: functional check of the sharded path with
+    # several ranks on fewer GPUs (timings meaningless); default NCCL
+    backend = os.environ.get("GPSPCA_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local %= torch.cuda.device_count()
+        os.environ["GPSPCA_DEVICE"] = str(local)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     p, n = args.p, args.n
     offset, n_local = column_partition(n, world)[rank]
 
