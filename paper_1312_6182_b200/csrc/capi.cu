@@ -1218,6 +1218,8 @@ struct gps_bk {
   int tc_grid = 0, tc_gx = 0, tc_tiles = 0;
   int tc_rings[2] = {kTcAStages, kTcXStages};  // A ring, X ring
   int* col_exp = nullptr;                        // n scale exponents (tensor-core path)
+  float* col_nrm = nullptr;                      // n upper bounds on ||a_i|| (candidate margin)
+  int tc_ref_grid = 0;                           // T1x grid (part_s_tc entries)
   __half* xhi = nullptr;  // X1 (fp16)
   __half* xlo = nullptr;  // X2 (fp16)
   unsigned char* colmask = nullptr;
@@ -1339,13 +1341,13 @@ int bk_enqueue_tc(gps_bk* s, bool with_ctl) {
   a.w_out = s->W;
   a.w_stride = int64_t(s->m_pad()) * A->n;
   a.colmask = s->colmask;
-  a.part_s = s->part_s_tc;
   a.ctl = ctl;
   a.num_tiles = s->tc_tiles;
   a.gamma = s->mu_dev + s->m;  // gamma stored after mu in mu_dev
   a.a_stages = s->tc_rings[0];
   a.x_stages = s->tc_rings[1];
   a.col_exp = s->col_exp;
+  a.col_nrm = s->col_nrm;
   {
     static const char* sg = getenv("GPSPCA_TC_SEG");  // tuning experiments only
     // two epilogue groups are busy for m > 32: drain every 256 rows there
@@ -1359,6 +1361,22 @@ int bk_enqueue_tc(gps_bk* s, bool with_ctl) {
   tc_dots_kernel<<<s->tc_grid, kTcThreads, tc_smem_bytes(np, a.a_stages, a.x_stages), ctx->stream>>>(
       s->tmA, s->tmXh, s->tmXl, a);
   ctx->launches++;
+  {
+    const int64_t xs = int64_t(s->m_pad()) * ld, wst = int64_t(s->m_pad()) * A->n;
+    const float* Af = static_cast<const float*>(A->d);
+    const double* gam = s->mu_dev + s->m;
+#define GPS_REFINE(J)                                                                                          \
+  tc_refine_kernel<J><<<s->tc_ref_grid, 256, 0, ctx->stream>>>(Af, A->n, ld, s->m, s->X, xs, s->mu_dev, gam, \
+                                                               s->penalty, s->colmask, s->W, wst, s->part_s_tc, ctl)
+    switch (np / 8) {
+      case 2: GPS_REFINE(2); break;
+      case 4: GPS_REFINE(4); break;
+      case 6: GPS_REFINE(6); break;
+      default: GPS_REFINE(8); break;
+    }
+#undef GPS_REFINE
+    ctx->launches++;
+  }
   dim3 g2(s->tc_gx, static_cast<unsigned>((A->ld + kTcUpdRows - 1) / kTcUpdRows),
           static_cast<unsigned>((s->m + kTcUpdComps - 1) / kTcUpdComps));
   if (!(a.probe & 16)) {
@@ -1367,7 +1385,7 @@ int bk_enqueue_tc(gps_bk* s, bool with_ctl) {
     ctx->launches++;
   }
   GPS_CHECK_LAUNCH("tensor-core block sweep launch");
-  return launch_reduce(ctx, s->part_g, s->part_s_tc, s->tc_gx, np * ld, s->exch, ctl, s->tc_grid);
+  return launch_reduce(ctx, s->part_g, s->part_s_tc, s->tc_gx, np * ld, s->exch, ctl, s->tc_ref_grid);
 }
 
 int bk_enqueue_sweeps(gps_bk* s, bool with_ctl) {
@@ -1472,6 +1490,7 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
     s->tc_tiles = static_cast<int>(ceil_div(A->n, kTcTileM));
     s->tc_grid = std::min(ctx->num_sms, s->tc_tiles);
     s->tc_gx = static_cast<int>(std::min<int64_t>(32, A->n));
+    s->tc_ref_grid = static_cast<int>(std::min<int64_t>(ceil_div(A->n, kTcRefItem), int64_t(4) * ctx->num_sms));
   }
   s->mg = pl.mg;
   s->ngroups = (m + pl.mg - 1) / pl.mg;
@@ -1517,7 +1536,8 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
     alloc((void**)&s->xlo, mp * ld * sizeof(__half));
     alloc((void**)&s->col_exp, n * sizeof(int));
     alloc((void**)&s->colmask, 2 * n);
-    alloc((void**)&s->part_s_tc, size_t(s->tc_grid) * 4 * sizeof(double));
+    alloc((void**)&s->col_nrm, n * sizeof(float));
+    alloc((void**)&s->part_s_tc, size_t(s->tc_ref_grid) * 4 * sizeof(double));
   }
   alloc((void**)&s->ctl, sizeof(GpsCtl));
   alloc((void**)&s->rank_dev, sizeof(int));
@@ -1555,7 +1575,7 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
       // per-column scale exponents: one pass over A per solver (A is constant)
       tc_col_exp_kernel<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(static_cast<const float*>(A->d), A->n,
                                                                    static_cast<int>(A->ld), static_cast<int>(A->p),
-                                                                   s->col_exp);
+                                                                   s->col_exp, s->col_nrm);
       ctx->launches++;
       cudaError_t ek = cudaGetLastError();
       if (ek == cudaSuccess) ek = cudaStreamSynchronize(ctx->stream);
@@ -1587,6 +1607,7 @@ int gps_bk_destroy(gps_bk* s) {
   if (s->xhi) cudaFree(s->xhi);
   if (s->xlo) cudaFree(s->xlo);
   if (s->col_exp) cudaFree(s->col_exp);
+  if (s->col_nrm) cudaFree(s->col_nrm);
   if (s->colmask) cudaFree(s->colmask);
   if (s->part_s_tc) cudaFree(s->part_s_tc);
   if (s->pc) cudaFree(s->pc);

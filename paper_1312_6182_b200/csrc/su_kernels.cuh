@@ -427,10 +427,13 @@ __global__ void __launch_bounds__(256) su_reduce_kernel(const double* __restrict
       for (int k = 1; k < kReduceSlices; ++k) u += part[k][rr];
       exch[r] = u;
     }
-  } else if (threadIdx.x < 4) {
+  } else if (threadIdx.x < 128) {
+    // warp k sums scalar k: lane-strided partials, then the xor tree (fixed order)
+    const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double t = 0.0;
-    for (int b = 0; b < nparts_s; ++b) t += part_s[size_t(b) * 4 + threadIdx.x];
-    exch[ld + threadIdx.x] = t;
+    for (int b = lane; b < nparts_s; b += 32) t += part_s[size_t(b) * 4 + k];
+    t = warp_sum(t);
+    if (lane == 0) exch[ld + k] = t;
   }
 }
 

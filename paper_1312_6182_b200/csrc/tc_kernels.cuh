@@ -44,10 +44,11 @@ constexpr int kTcXStages = 3;    // default X1 | X2 ring depth (L2-resident)
 constexpr int kTcMaxStages = 8;
 constexpr int kTcThreads = 512;  // 16 warps
 constexpr int kTcMaxN = 64;
-constexpr int kTcMinM = 5;       // block solves with m >= 5 (fp32 A) take this path (one A read vs ceil(m/4))
+constexpr int kTcMinM = 2;       // fp32 block solves with m >= 2 take this path (one A read, exact fp64 results)
 constexpr int kTcSegChunks = 2;  // TMEM accumulation segment: 2 chunks = 128 rows, drained to fp64
 constexpr int kTcAScaleExp = 14; // |a s_i| in [2^14, 2^15)
 constexpr int kTcXScaleExp = 14; // |x| <= 1 -> |x 2^14| <= 2^14
+constexpr int kTcMarginExp = 13; // candidate margin 2^-13 ||a_i|| (16x the error bound)
 
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
@@ -123,18 +124,30 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // C0: per-column scale exponents e_i = 14 - floor(log2 max_j |a_ji|) (0 for
-// an all-zero column, clamped to [-126, 126]); warp per column.
-__global__ void tc_col_exp_kernel(const float* __restrict__ A, int64_t n, int ld, int p, int* __restrict__ col_exp) {
+// an all-zero column, clamped to [-126, 126]) and an upper bound on ||a_i||_2
+// (fp64 sum of squares, rounded up), which sizes T1's candidate margin; warp
+// per column.
+__global__ void tc_col_exp_kernel(const float* __restrict__ A, int64_t n, int ld, int p, int* __restrict__ col_exp,
+                                  float* __restrict__ col_nrm) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
   for (int64_t col = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; col < n; col += warps) {
     const float* a = A + col * ld;
     float mx = 0.f;
-    for (int r = lane; r < p; r += 32) mx = fmaxf(mx, fabsf(a[r]));
+    double ss = 0.0;
+    for (int r = lane; r < p; r += 32) {
+      const float v = a[r];
+      mx = fmaxf(mx, fabsf(v));
+      ss = fma(double(v), double(v), ss);
+    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    ss = warp_sum(ss);
     // clamped so 2^e is a normal float (only data below ~2^-112 loses range)
-    if (lane == 0) col_exp[col] = mx > 0.f ? max(-126, min(126, kTcAScaleExp - ilogbf(mx))) : 0;
+    if (lane == 0) {
+      col_exp[col] = mx > 0.f ? max(-126, min(126, kTcAScaleExp - ilogbf(mx))) : 0;
+      col_nrm[col] = __double2float_ru(sqrt(ss) * (1.0 + 0x1p-40));
+    }
   }
 }
 
@@ -164,10 +177,10 @@ struct TcDotsArgs {
   const double* gamma;  // m
   const double* mu;     // m
   const int* col_exp;   // n: scale exponents of the columns
-  double* w_out;        // [m_pad][n] parity slots (may be null)
+  const float* col_nrm; // n: upper bounds on ||a_i||_2
+  double* w_out;        // [m_pad][n] parity slots (may be null): zeroed for non-candidate columns
   int64_t w_stride;
-  unsigned char* colmask;  // [2][n]: 1 if any w_ij != 0 (one row per epilogue group)
-  double* part_s;          // [grid][4]
+  unsigned char* colmask;  // [2][n]: 1 if column i is a candidate (one row per epilogue group)
   const GpsCtl* ctl;
   int num_tiles;
   int a_stages, x_stages;  // ring depths (<= kTcMaxStages)
@@ -311,7 +324,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   double* sgam = reinterpret_cast<double*>(tmem_base_slot + 4);
   double* smu = sgam + kTcMaxN;
-  double* sred = smu + kTcMaxN;  // 256 x 2 scalars (f, nnz)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int kchunks = (a.ld + kTcKChunk - 1) / kTcKChunk;
@@ -547,9 +559,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // columns of the tile); group g owns components [32 g, 32 g + 32).
     const int q = warp & 3;
     const int g = warp >= 12 ? 1 : 0;
-    const int et = g * 128 + q * 32 + lane;
     const int jbase = g * 32;
-    double f_acc = 0.0, nnz_acc = 0.0;
     double* wbase = a.w_out != nullptr ? a.w_out + parity * a.w_stride : nullptr;
     TcProf pf{kTcProfile && (a.probe & 64) != 0 && warp == 4, 0};
     unsigned long long w11 = 0, w12 = 0;
@@ -595,23 +605,28 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
       const int64_t col = int64_t(t) * kTcTileM + q * 32 + lane;
       if (col < a.n) {
-        // undo the scales: c = D 2^-(e_i + 14)
+        // Candidate filter.  The exact c_ij (fp64) is within
+        // delta_i = 2^-kTcMarginExp ||a_i|| ||x_j|| of this estimate (the split
+        // and fp32 accumulation errors are < 2^-17 of sum_r |a_ri x_rj|, see
+        // DESIGN.md; ||x_j|| = 1), so a column none of whose components can
+        // reach the threshold with that margin is inactive (w = 0, objective
+        // term 0) for certain; every other column is recomputed exactly by T1x.
         const double unscale = ldexp(1.0, -(a.col_exp[col] + kTcXScaleExp));
-        bool any = false;
+        const double delta = ldexp(static_cast<double>(a.col_nrm[col]), -kTcMarginExp);
+        bool cand = false;
 #pragma unroll
         for (int jj = 0; jj < 32; ++jj) {
           const int j = jbase + jj;
           if (j >= a.m) continue;
-          const double sj = smu[j] * ((static_cast<double>(ch[jj]) - static_cast<double>(cl[jj])) * unscale);
-          const double w = threshold_weight(sj, sgam[j], a.penalty);
-          f_acc += objective_term(sj, sgam[j], a.penalty);
-          if (w != 0.0) {
-            nnz_acc += 1.0;
-            any = true;
-          }
-          if (wbase != nullptr) wbase[size_t(j) * a.n + col] = w;
+          const double s = smu[j] * (fabs((static_cast<double>(ch[jj]) - static_cast<double>(cl[jj])) * unscale) + delta);
+          cand |= (a.penalty == 0) ? (s >= sgam[j]) : (s * s >= sgam[j]);
         }
-        a.colmask[size_t(g) * a.n + col] = any ? 1 : 0;
+        if (!cand && wbase != nullptr) {
+#pragma unroll 4
+          for (int jj = 0; jj < 32; ++jj)
+            if (jbase + jj < a.m) wbase[size_t(jbase + jj) * a.n + col] = 0.0;
+        }
+        a.colmask[size_t(g) * a.n + col] = cand ? 1 : 0;
       }
     }
     if (pf.on && lane == 0) {
@@ -619,18 +634,156 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       atomicAdd(&g_tc_prof[12], w12);
       atomicAdd(&g_tc_prof[13], static_cast<unsigned long long>(clock64() - t_role));
     }
-    sred[et * 2 + 0] = f_acc;
-    sred[et * 2 + 1] = nnz_acc;
   }
   __syncthreads();
-  if (tid < 2) {
-    double t = 0.0;
-    for (int i = 0; i < 256; ++i) t += sred[i * 2 + tid];
-    a.part_s[size_t(blockIdx.x) * 4 + tid] = t;
-  }
   if (warp == 1) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kTcTmemCols)
                  : "memory");
+  }
+}
+
+// T1x: exact fp64 recomputation of the candidate columns T1 flagged.
+// Work items are 256-column ranges, assigned to CTAs round-robin (item b,
+// b + grid, ...) so contiguous runs of active columns spread over the grid.
+// Per item the candidates are compacted in column order and processed in
+// batches of 64: C_batch = A_batch' X in fp64 (fp32 a_ri is exact in fp64),
+// 32 rows at a time through shared memory; thread (lane, warp) owns columns
+// {lane, lane + 32} x components [warp JPT, warp JPT + JPT).  Then, per
+// (column, component): s = mu_j c_ij, w_ij = threshold(s, gamma_j) (the
+// reference's parallel.py:117-128 / block.py:80-89 rules), the objective
+// term and nnz, W written for every component of the column, and the final
+// activity mask (colmask[0][i] = any w_ij != 0, colmask[1][i] = 0) for T2.
+// f and nnz are summed per thread in a fixed order and reduced per CTA in a
+// fixed order into part_s[blockIdx.x] (deterministic run to run).
+constexpr int kTcRefItem = 256;
+constexpr int kTcRefBatch = 64;
+constexpr int kTcRefRows = 32;
+template <int JPT>
+__global__ void __launch_bounds__(256) tc_refine_kernel(const float* __restrict__ A, int64_t n, int ld, int m,
+                                                        const double* __restrict__ X, int64_t x_par_stride,
+                                                        const double* __restrict__ mu,
+                                                        const double* __restrict__ gamma, int penalty,
+                                                        unsigned char* __restrict__ colmask, double* __restrict__ W,
+                                                        int64_t w_par_stride, double* __restrict__ part_s,
+                                                        const GpsCtl* ctl) {
+  constexpr int NJ = 8 * JPT;  // padded components handled (8 warps)
+  if (ctl != nullptr && ctl->done) return;
+  const int parity = ctl != nullptr ? (ctl->iter & 1) : 0;
+  const double* Xp = X + parity * x_par_stride;
+  double* Wp = W + parity * w_par_stride;
+  __shared__ float sA[kTcRefRows][kTcRefBatch + 1];
+  __shared__ double sX[kTcRefRows][NJ + 1];
+  __shared__ int64_t cand[kTcRefItem];
+  __shared__ int wcnt[8];
+  __shared__ unsigned char act[kTcRefBatch];
+  __shared__ double red[2][8];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double mu_r[JPT], gam_r[JPT];
+#pragma unroll
+  for (int u = 0; u < JPT; ++u) {
+    const int j = warp * JPT + u;
+    mu_r[u] = j < m ? mu[j] : 1.0;
+    gam_r[u] = j < m ? gamma[j] : 0.0;
+  }
+  double f_acc = 0.0, nnz_acc = 0.0;
+  const int64_t items = (n + kTcRefItem - 1) / kTcRefItem;
+  for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+    const int64_t col = item * kTcRefItem + tid;
+    const bool flag = col < n && (colmask[col] | colmask[n + col]);
+    const unsigned bal = __ballot_sync(0xffffffffu, flag);
+    if (lane == 0) wcnt[warp] = __popc(bal);
+    __syncthreads();
+    int off = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      off += (w < warp) ? wcnt[w] : 0;
+      total += wcnt[w];
+    }
+    if (flag) cand[off + __popc(bal & ((1u << lane) - 1u))] = col;
+    if (total == 0) {
+      __syncthreads();  // wcnt reuse
+      continue;
+    }
+    if (tid < kTcRefBatch) act[tid] = 0;
+    __syncthreads();
+    for (int b0 = 0; b0 < total; b0 += kTcRefBatch) {
+      const int nb = min(kTcRefBatch, total - b0);
+      double acc[2][JPT];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int u = 0; u < JPT; ++u) acc[i][u] = 0.0;
+      for (int r0 = 0; r0 < ld; r0 += kTcRefRows) {
+        // stage A: warp w loads batch columns 8w .. 8w + 7, lane = row
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int bc = warp * 8 + c;
+          sA[lane][bc] = bc < nb ? A[cand[b0 + bc] * ld + r0 + lane] : 0.f;
+        }
+        // stage X rows r0 .. r0 + 31 of components 0 .. NJ - 1
+        for (int e = tid; e < kTcRefRows * NJ; e += 256) {
+          const int j = e >> 5, r = e & 31;
+          sX[r][j] = j < m ? Xp[size_t(j) * ld + r0 + r] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int r = 0; r < kTcRefRows; ++r) {
+          const double a0 = static_cast<double>(sA[r][lane]);
+          const double a1 = static_cast<double>(sA[r][lane + 32]);
+#pragma unroll
+          for (int u = 0; u < JPT; ++u) {
+            const double x = sX[r][warp * JPT + u];
+            acc[0][u] = fma(a0, x, acc[0][u]);
+            acc[1][u] = fma(a1, x, acc[1][u]);
+          }
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int bc = lane + 32 * i;
+        if (bc < nb) {
+          const int64_t c = cand[b0 + bc];
+          bool any = false;
+#pragma unroll
+          for (int u = 0; u < JPT; ++u) {
+            const int j = warp * JPT + u;
+            if (j < m) {
+              const double sj = mu_r[u] * acc[i][u];
+              const double w = threshold_weight(sj, gam_r[u], penalty);
+              f_acc += objective_term(sj, gam_r[u], penalty);
+              if (w != 0.0) {
+                nnz_acc += 1.0;
+                any = true;
+              }
+              Wp[size_t(j) * n + c] = w;
+            }
+          }
+          if (any) act[bc] = 1;  // benign: every writer stores 1
+        }
+      }
+      __syncthreads();
+      if (tid < nb) {
+        const int64_t c = cand[b0 + tid];
+        colmask[c] = act[tid];
+        colmask[n + c] = 0;
+        act[tid] = 0;
+      }
+      __syncthreads();
+    }
+  }
+  f_acc = warp_sum(f_acc);
+  nnz_acc = warp_sum(nnz_acc);
+  if (lane == 0) {
+    red[0][warp] = f_acc;
+    red[1][warp] = nnz_acc;
+  }
+  __syncthreads();
+  if (tid < 4) {
+    double t = 0.0;
+    if (tid < 2)
+      for (int w = 0; w < 8; ++w) t += red[tid][w];
+    part_s[size_t(blockIdx.x) * 4 + tid] = t;
   }
 }
 

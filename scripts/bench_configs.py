@@ -68,9 +68,9 @@ def time_bk(gps, torch, A, penalty, m, gamma, mu, iters, warmup=2):
 
 def full_reads(A, m):
     """Full passes over A per block iteration: one for the tensor-core path
-    (fp32, m >= 5: tc_dots reads A once; tc_update re-reads only the active
-    columns), else one per group of MG components."""
-    if A.dtype == np.float32 and m >= 5:
+    (fp32, m >= 2: tc_dots reads A once; tc_refine / tc_update re-read only
+    the candidate / active columns), else one per group of MG components."""
+    if A.dtype == np.float32 and m >= 2:
         return 1
     mg = 4 if (A.dtype == np.float32 and A.p <= 4096) else 2
     return (m + mg - 1) // mg

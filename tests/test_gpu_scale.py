@@ -64,8 +64,11 @@ def test_block_truncated_c3_slice(penalty):
     loadings, report = gps.solve_block(A, cfg)
     Z, hist, conv, X = oracle.block_solve(A64, 10, gamma, 1.0, penalty, max_iter=3)
     assert report.iterations == len(hist) - 1 == 3
-    np.testing.assert_allclose(report.objective_history, hist, rtol=2e-5)
+    np.testing.assert_allclose(report.objective_history, hist, rtol=1e-9)
     C = A64.T @ X
     diff = (loadings.values != 0) != (Z != 0)
-    assert not (diff & ~near(C, gamma, penalty, 1e-4)).any()
-    assert np.max(np.abs(loadings.values - Z)) <= 1e-3
+    # north star: identical supports except entries within 1e-6 gamma of the threshold (logged)
+    assert not (diff & ~near(C, gamma, penalty, 1e-6)).any()
+    if diff.any():
+        print(f"near-threshold support differences: {int(diff.sum())}")
+    np.testing.assert_allclose(loadings.values, Z, rtol=1e-7, atol=1e-9)
