@@ -1216,13 +1216,15 @@ struct gps_bk {
   // tensor-core path (fp32 A, m >= 16): split X, column activity, TMA maps
   bool tc = false;
   int tc_grid = 0, tc_gx = 0, tc_tiles = 0;
-  int tc_rings[2] = {kTcAStages, kTcXStages};  // A ring, X ring
+  int tc_rings[2] = {kTcAStages, kTcXStages};  // A ring, X ring (fp64: fewer, 64 KB A stages)
   int* col_exp = nullptr;                        // n scale exponents (tensor-core path)
-  float* col_nrm = nullptr;                      // n upper bounds on ||a_i|| (candidate margin)
+  float* col_delta = nullptr;                    // n candidate margins of T1
   int tc_ref_grid = 0;                           // T1x grid (part_s_tc entries)
   __half* xhi = nullptr;  // X1 (fp16)
   __half* xlo = nullptr;  // X2 (fp16)
   unsigned char* colmask = nullptr;
+  unsigned char* tflag = nullptr;     // [2 * items][8] T1 tile flags (items = ceil(n / 256))
+  unsigned char* item_act = nullptr;  // [items] any active column (T1x -> T2)
   double* part_s_tc = nullptr;
   CUtensorMap tmA, tmXh, tmXl;
   // multi-CTA CholeskyQR2 polar (large p*m)
@@ -1341,13 +1343,14 @@ int bk_enqueue_tc(gps_bk* s, bool with_ctl) {
   a.w_out = s->W;
   a.w_stride = int64_t(s->m_pad()) * A->n;
   a.colmask = s->colmask;
+  a.tflag = s->tflag;
   a.ctl = ctl;
   a.num_tiles = s->tc_tiles;
   a.gamma = s->mu_dev + s->m;  // gamma stored after mu in mu_dev
   a.a_stages = s->tc_rings[0];
   a.x_stages = s->tc_rings[1];
   a.col_exp = s->col_exp;
-  a.col_nrm = s->col_nrm;
+  a.col_delta = s->col_delta;
   {
     static const char* sg = getenv("GPSPCA_TC_SEG");  // tuning experiments only
     // two epilogue groups are busy for m > 32: drain every 256 rows there
@@ -1358,30 +1361,50 @@ int bk_enqueue_tc(gps_bk* s, bool with_ctl) {
     static const char* pr = getenv("GPSPCA_TC_PROBE");  // timing experiments only
     a.probe = pr ? atoi(pr) : 0;
   }
-  tc_dots_kernel<<<s->tc_grid, kTcThreads, tc_smem_bytes(np, a.a_stages, a.x_stages), ctx->stream>>>(
-      s->tmA, s->tmXh, s->tmXl, a);
+  const bool f64 = A->dtype == GPS_F64;
+  const int esz = f64 ? 8 : 4;
+  if (f64)
+    tc_dots_kernel<double><<<s->tc_grid, kTcThreads, tc_smem_bytes(np, a.a_stages, a.x_stages, esz), ctx->stream>>>(
+        s->tmA, s->tmXh, s->tmXl, a);
+  else
+    tc_dots_kernel<float><<<s->tc_grid, kTcThreads, tc_smem_bytes(np, a.a_stages, a.x_stages, esz), ctx->stream>>>(
+        s->tmA, s->tmXh, s->tmXl, a);
   ctx->launches++;
   {
     const int64_t xs = int64_t(s->m_pad()) * ld, wst = int64_t(s->m_pad()) * A->n;
-    const float* Af = static_cast<const float*>(A->d);
     const double* gam = s->mu_dev + s->m;
-#define GPS_REFINE(J)                                                                                          \
-  tc_refine_kernel<J><<<s->tc_ref_grid, 256, 0, ctx->stream>>>(Af, A->n, ld, s->m, s->X, xs, s->mu_dev, gam, \
-                                                               s->penalty, s->colmask, s->W, wst, s->part_s_tc, ctl)
-    switch (np / 8) {
-      case 2: GPS_REFINE(2); break;
-      case 4: GPS_REFINE(4); break;
-      case 6: GPS_REFINE(6); break;
-      default: GPS_REFINE(8); break;
+#define GPS_REFINE(TA, J)                                                                                        \
+  tc_refine_kernel<TA, J><<<s->tc_ref_grid, 256, 0, ctx->stream>>>(static_cast<const TA*>(A->d), A->n, ld, s->m, \
+                                                                   s->X, xs, s->mu_dev, gam, s->penalty,       \
+                                                                   s->colmask, s->tflag, s->item_act, s->W, wst, \
+                                                                   s->part_s_tc, ctl)
+#define GPS_REFINE_J(TA)            \
+  switch (np / 8) {                 \
+    case 2: GPS_REFINE(TA, 2); break; \
+    case 4: GPS_REFINE(TA, 4); break; \
+    case 6: GPS_REFINE(TA, 6); break; \
+    default: GPS_REFINE(TA, 8); break; \
+  }
+    if (f64) {
+      GPS_REFINE_J(double)
+    } else {
+      GPS_REFINE_J(float)
     }
+#undef GPS_REFINE_J
 #undef GPS_REFINE
     ctx->launches++;
   }
   dim3 g2(s->tc_gx, static_cast<unsigned>((A->ld + kTcUpdRows - 1) / kTcUpdRows),
           static_cast<unsigned>((s->m + kTcUpdComps - 1) / kTcUpdComps));
   if (!(a.probe & 16)) {
-    tc_update_kernel<<<g2, 256, 0, ctx->stream>>>(static_cast<const float*>(A->d), A->n, ld, s->m, s->colmask,
-                                                   s->W, int64_t(s->m_pad()) * A->n, np, s->part_g, ctl);
+    if (f64)
+      tc_update_kernel<double><<<g2, 256, 0, ctx->stream>>>(static_cast<const double*>(A->d), A->n, ld, s->m,
+                                                            s->colmask, s->item_act, s->W, int64_t(s->m_pad()) * A->n, np,
+                                                            s->part_g, ctl);
+    else
+      tc_update_kernel<float><<<g2, 256, 0, ctx->stream>>>(static_cast<const float*>(A->d), A->n, ld, s->m,
+                                                           s->colmask, s->item_act, s->W, int64_t(s->m_pad()) * A->n, np,
+                                                           s->part_g, ctl);
     ctx->launches++;
   }
   GPS_CHECK_LAUNCH("tensor-core block sweep launch");
@@ -1478,7 +1501,9 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
   const char* no_tc = std::getenv("GPSPCA_NO_TC");
   const char* tc_min_env = std::getenv("GPSPCA_TC_MIN_M");  // tuning experiments
   const int tc_min = tc_min_env && atoi(tc_min_env) > 0 ? atoi(tc_min_env) : kTcMinM;
-  const bool tc = A->dtype == GPS_F32 && m >= tc_min && !(no_tc && no_tc[0] == '1');
+  // fp32: every m (exact via T1x); fp64: m >= 2 (m = 1 keeps the CUDA-core
+  // sweep, bitwise equal to the single-unit sweep as test_block.py:115-122 asks)
+  const bool tc = m >= (A->dtype == GPS_F32 ? 1 : tc_min) && !(no_tc && no_tc[0] == '1');
   auto* s = new gps_bk();
   s->A = A;
   s->ctx = ctx;
@@ -1490,7 +1515,7 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
     s->tc_tiles = static_cast<int>(ceil_div(A->n, kTcTileM));
     s->tc_grid = std::min(ctx->num_sms, s->tc_tiles);
     s->tc_gx = static_cast<int>(std::min<int64_t>(32, A->n));
-    s->tc_ref_grid = static_cast<int>(std::min<int64_t>(ceil_div(A->n, kTcRefItem), int64_t(4) * ctx->num_sms));
+    s->tc_ref_grid = static_cast<int>(std::min<int64_t>(ceil_div(A->n, kTcRefItem), int64_t(2) * ctx->num_sms));
   }
   s->mg = pl.mg;
   s->ngroups = (m + pl.mg - 1) / pl.mg;
@@ -1536,13 +1561,16 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
     alloc((void**)&s->xlo, mp * ld * sizeof(__half));
     alloc((void**)&s->col_exp, n * sizeof(int));
     alloc((void**)&s->colmask, 2 * n);
-    alloc((void**)&s->col_nrm, n * sizeof(float));
+    alloc((void**)&s->col_delta, n * sizeof(float));
+    alloc((void**)&s->tflag, size_t(ceil_div(n, kTcRefItem)) * 16);
+    alloc((void**)&s->item_act, size_t(ceil_div(n, kTcRefItem)));
     alloc((void**)&s->part_s_tc, size_t(s->tc_ref_grid) * 4 * sizeof(double));
   }
   alloc((void**)&s->ctl, sizeof(GpsCtl));
   alloc((void**)&s->rank_dev, sizeof(int));
   if (e == cudaSuccess) e = cudaMallocHost(&s->ctl_host, sizeof(GpsCtl));
   if (e == cudaSuccess) e = cudaMemsetAsync(s->X, 0, 2 * mp * ld * sizeof(double), ctx->stream);
+  if (e == cudaSuccess && tc) e = cudaMemsetAsync(s->tflag, 0, size_t(ceil_div(n, kTcRefItem)) * 16, ctx->stream);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(s->mu_dev, mu, size_t(m) * sizeof(double), cudaMemcpyHostToDevice, ctx->stream);
   if (e == cudaSuccess)
@@ -1553,7 +1581,11 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
     return cuda_fail(e, "gps_bk_create allocation");
   }
   if (tc) {
-    rc = tma_encode_2d(&s->tmA, A->d, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, A->ld, A->n, A->ld * 4, kTcBoxK, kTcTileM);
+    const bool f64 = A->dtype == GPS_F64;
+    const int esz = f64 ? 8 : 4;
+    if (f64) s->tc_rings[0] = s->mg <= 32 ? 3 : 2;  // 64 KB A stages: fit the 227 KB of shared memory
+    rc = tma_encode_2d(&s->tmA, A->d, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, A->ld,
+                       A->n, A->ld * esz, kTcBoxBytes / esz, kTcTileM);
     if (rc == GPS_OK)
       rc = tma_encode_2d(&s->tmXh, s->xhi, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, A->ld, mp, A->ld * 2, kTcKChunk, s->mg);
     if (rc == GPS_OK)
@@ -1564,18 +1596,24 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
           r[1] <= kTcMaxStages)
         for (int i = 0; i < 2; ++i) s->tc_rings[i] = r[i];
     }
-    if (rc == GPS_OK && tc_smem_bytes(s->mg, s->tc_rings[0], s->tc_rings[1]) > 227 * 1024)
-      rc = fail(GPS_E_ARG, "tensor-core ring configuration exceeds shared memory");
+    const size_t smem = tc_smem_bytes(s->mg, s->tc_rings[0], s->tc_rings[1], esz);
+    if (rc == GPS_OK && smem > 227 * 1024) rc = fail(GPS_E_ARG, "tensor-core ring configuration exceeds shared memory");
     if (rc == GPS_OK) {
-      cudaError_t ea = cudaFuncSetAttribute(tc_dots_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            int(tc_smem_bytes(s->mg, s->tc_rings[0], s->tc_rings[1])));
+      cudaError_t ea =
+          f64 ? cudaFuncSetAttribute(tc_dots_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))
+              : cudaFuncSetAttribute(tc_dots_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (ea != cudaSuccess) rc = cuda_fail(ea, "cudaFuncSetAttribute(tc_dots)");
     }
     if (rc == GPS_OK) {
       // per-column scale exponents: one pass over A per solver (A is constant)
-      tc_col_exp_kernel<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(static_cast<const float*>(A->d), A->n,
-                                                                   static_cast<int>(A->ld), static_cast<int>(A->p),
-                                                                   s->col_exp, s->col_nrm);
+      if (f64)
+        tc_col_exp_kernel<double><<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(
+            static_cast<const double*>(A->d), A->n, static_cast<int>(A->ld), static_cast<int>(A->p), s->col_exp,
+            s->col_delta);
+      else
+        tc_col_exp_kernel<float><<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(
+            static_cast<const float*>(A->d), A->n, static_cast<int>(A->ld), static_cast<int>(A->p), s->col_exp,
+            s->col_delta);
       ctx->launches++;
       cudaError_t ek = cudaGetLastError();
       if (ek == cudaSuccess) ek = cudaStreamSynchronize(ctx->stream);
@@ -1607,7 +1645,9 @@ int gps_bk_destroy(gps_bk* s) {
   if (s->xhi) cudaFree(s->xhi);
   if (s->xlo) cudaFree(s->xlo);
   if (s->col_exp) cudaFree(s->col_exp);
-  if (s->col_nrm) cudaFree(s->col_nrm);
+  if (s->col_delta) cudaFree(s->col_delta);
+  if (s->tflag) cudaFree(s->tflag);
+  if (s->item_act) cudaFree(s->item_act);
   if (s->colmask) cudaFree(s->colmask);
   if (s->part_s_tc) cudaFree(s->part_s_tc);
   if (s->pc) cudaFree(s->pc);

@@ -1,26 +1,29 @@
-// Block GP-SPCA on the 5th-generation tensor cores (sm_100a tcgen05), for
-// fp32 storage and m >= 5 components (m = 10, C4: p = 8192,
-// m = 64), where the CUDA-core block sweep needs ceil(m/4) reads of A.
+// Block GP-SPCA on the 5th-generation tensor cores (sm_100a tcgen05) for
+// m >= 2 components (m = 10, C4: p = 8192, m = 64), fp32 or fp64
+// storage, where the CUDA-core block sweep needs ceil(m/4) (fp32) or
+// ceil(m/2) (fp64) reads of A.  The tensor cores FILTER columns; the results
+// are fp64 arithmetic on every column that can be active.
 //
-// Arithmetic: "2xFP16 with power-of-two scaling".  Column i of A is scaled
-// by s_i = 2^e_i (max |a_ji| s_i in [2^14, 2^15)) and split into two fp16
-// pieces, y = a s_i = A1 + 2^-11 A2 (A2 = fp16((y - A1) 2^11)); X is split the
-// same way with the common scale 2^14 (its columns are unit vectors).  The
-// tensor core forms, with fp32 accumulation (kind::f16, 16 rows per MMA):
-//   D0 = A1 X1,  D1 = A1 X2,  D2 = A2 X1
-// and c_ij = 2^-(e_i + 14) (D0 + 2^-11 (D1 + D2)); the dropped A2 X2 term and
-// the fp16 roundings leave ~2^-22 of max|a_i| |x|, the same class as 3xTF32
-// with half its MMA instructions and half the X traffic.
+// Filter arithmetic: column i of A is scaled by s_i = 2^e_i (max |a_ji| s_i
+// in [2^14, 2^15)) and rounded to fp16, A1 = fp16(a s_i) (11 significant
+// bits); X is split into two fp16 pieces with the common scale 2^14 (its
+// columns are unit vectors), x 2^14 = X1 + 2^-11 X2.  One tensor-core MMA per
+// 16 rows forms, with fp32 accumulation (kind::f16), D = [A1 X1 | A1 X2] and
+// c~_ij = 2^-(e_i + 14) (D0 + 2^-11 D1).  The rounding of A is bounded per
+// column exactly (||a_i - a1_i||, tc_col_exp_kernel), the rest of the error
+// by 2^-17 ||a_i||; T1 flags a column when any component can
+// reach its threshold within that margin.
 //
 // T0 split_x:   X (fp64) -> X1, X2 (fp16, [n_pad][ld])
 // T1 tc_dots:   persistent; per tile of 128 columns accumulates D0|D1|D2 in
-//               TMEM over 64-row chunks: A arrives by TMA (fp32, 128-byte
-//               swizzle), converter warps scale and split it into TMEM
-//               (tcgen05.st), both MMAs read A from TMEM and X from shared
-//               memory; epilogue warps drain TMEM segments into fp64 (every
-//               kTcSegChunks chunks), apply mu_j, the threshold and the
-//               objective, write W and a per-column activity flag.  A is read
-//               from HBM once.
+//               TMEM over 64-row chunks: A arrives by TMA (128-byte swizzle),
+//               converter warps scale and split it into TMEM (tcgen05.st),
+//               both MMAs read A from TMEM and X from shared memory; epilogue
+//               warps drain TMEM segments (every kTcSegChunks chunks) and flag
+//               the columns that can reach a threshold with the margin
+//               2^-13 ||a_i||.  A is read from HBM once.
+// T1x tc_refine: the flagged columns again, in fp64: c, thresholds, the
+//               objective, nnz, W and the activity mask.
 // T2 tc_update: G_j = sum over ACTIVE columns of w_ij a_i (fp64), row chunks
 //               x component groups; reads only the active columns again.
 // Roles of T1 (12 warps): w0 A producer (TMA), w1 MMA issuer (+TMEM owner),
@@ -37,9 +40,9 @@ namespace gps {
 
 constexpr int kTcTileM = 128;    // columns of A per tile (MMA M)
 constexpr int kTcKChunk = 64;    // rows of A per chunk (two 32-row fp32 TMA boxes; one 128-byte fp16 row)
-constexpr int kTcBoxK = 32;      // rows per fp32 TMA box (128 bytes)
+constexpr int kTcBoxBytes = 128; // inner extent of an A TMA box: 32 fp32 / 16 fp64 rows
 constexpr int kTcAStages = 5;    // default A ring depth (32 KB stages, HBM stream)
-constexpr int kTcLoStages = 2;   // TMEM A1 / A2 slots (converter output)
+constexpr int kTcLoStages = 2;   // TMEM A1 slots (converter output)
 constexpr int kTcXStages = 3;    // default X1 | X2 ring depth (L2-resident)
 constexpr int kTcMaxStages = 8;
 constexpr int kTcThreads = 512;  // 16 warps
@@ -123,30 +126,44 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-// C0: per-column scale exponents e_i = 14 - floor(log2 max_j |a_ji|) (0 for
-// an all-zero column, clamped to [-126, 126]) and an upper bound on ||a_i||_2
-// (fp64 sum of squares, rounded up), which sizes T1's candidate margin; warp
-// per column.
-__global__ void tc_col_exp_kernel(const float* __restrict__ A, int64_t n, int ld, int p, int* __restrict__ col_exp,
-                                  float* __restrict__ col_nrm) {
+// C0, once per solver: per-column scale exponents e_i = 14 - floor(log2
+// max_j |a_ji|) (0 for an all-zero column, clamped to [-126, 126]) and the
+// candidate margin of T1,
+//   delta_i = ||a_i - a1_i||_2 + 2^-kTcMarginExp ||a_i||_2     (rounded up)
+// where a1_i = 2^-e_i fp16(fp32(a_i 2^e_i)) is exactly the operand the tensor
+// cores see (the converters' rounding, reproduced here).  With unit x_j,
+// |a1_i'x_j - a_i'x_j| <= ||a_i - a1_i|| (Cauchy-Schwarz) and the rest of T1's
+// error (the 2-term split of X, fp32 accumulation) is < 2^-17 ||a_i||, 16x
+// inside the second term.  Warp per column.
+template <typename TA>
+__global__ void tc_col_exp_kernel(const TA* __restrict__ A, int64_t n, int ld, int p, int* __restrict__ col_exp,
+                                  float* __restrict__ col_delta) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
   for (int64_t col = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; col < n; col += warps) {
-    const float* a = A + col * ld;
+    const TA* a = A + col * ld;
     float mx = 0.f;
-    double ss = 0.0;
-    for (int r = lane; r < p; r += 32) {
-      const float v = a[r];
-      mx = fmaxf(mx, fabsf(v));
-      ss = fma(double(v), double(v), ss);
-    }
+    for (int r = lane; r < p; r += 32) mx = fmaxf(mx, __double2float_ru(fabs(static_cast<double>(a[r]))));
 #pragma unroll
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    ss = warp_sum(ss);
     // clamped so 2^e is a normal float (only data below ~2^-112 loses range)
+    const int e = mx > 0.f ? max(-126, min(126, kTcAScaleExp - ilogbf(mx))) : 0;
+    const float sc = __int_as_float((127 + e) << 23);
+    const double unsc = ldexp(1.0, -e);
+    double ss = 0.0, rr = 0.0;
+    for (int r = lane; r < p; r += 32) {
+      const TA v = a[r];
+      const float y = (sizeof(TA) == 4) ? static_cast<float>(v) * sc
+                                        : __double2float_rn(static_cast<double>(v) * static_cast<double>(sc));
+      const double d = static_cast<double>(v) - static_cast<double>(__half2float(__float2half_rn(y))) * unsc;
+      ss = fma(static_cast<double>(v), static_cast<double>(v), ss);
+      rr = fma(d, d, rr);
+    }
+    ss = warp_sum(ss);
+    rr = warp_sum(rr);
     if (lane == 0) {
-      col_exp[col] = mx > 0.f ? max(-126, min(126, kTcAScaleExp - ilogbf(mx))) : 0;
-      col_nrm[col] = __double2float_ru(sqrt(ss) * (1.0 + 0x1p-40));
+      col_exp[col] = e;
+      col_delta[col] = __double2float_ru((sqrt(rr) + ldexp(sqrt(ss), -kTcMarginExp)) * (1.0 + 0x1p-40));
     }
   }
 }
@@ -177,15 +194,16 @@ struct TcDotsArgs {
   const double* gamma;  // m
   const double* mu;     // m
   const int* col_exp;   // n: scale exponents of the columns
-  const float* col_nrm; // n: upper bounds on ||a_i||_2
+  const float* col_delta;  // n: candidate margins (tc_col_exp_kernel)
   double* w_out;        // [m_pad][n] parity slots (may be null): zeroed for non-candidate columns
   int64_t w_stride;
   unsigned char* colmask;  // [2][n]: 1 if column i is a candidate (one row per epilogue group)
+  unsigned char* tflag;    // [tiles][8]: any candidate in (tile, group, lane quarter)
   const GpsCtl* ctl;
   int num_tiles;
   int a_stages, x_stages;  // ring depths (<= kTcMaxStages)
   int seg_chunks;          // chunks per TMEM accumulation segment
-  int probe;  // timing experiments: 2 no A2 MMA, 4 no TMEM drain, 8 no X loads, 16 no update,
+  int probe;  // timing experiments: 4 no TMEM drain, 8 no X loads, 16 no update,
               // 32 no TMEM stores, 64 cycle accounting
 };
 
@@ -193,19 +211,19 @@ struct TcDotsArgs {
 // shared-memory operands, TMA writes and converter reads share its ~128
 // B/clock), so A passes through it once:
 //   A ring    SA x 32 KB in shared memory (TMA, evict-first) -> converters
-//   A1 / A2   2 slots x 64 TMEM columns (32 packed fp16 pairs each), written
+//   A1        2 slots x 64 TMEM columns (32 packed fp16 pairs used), written
 //             by the converters with tcgen05.st, read by the MMAs as the
 //             TMEM-resident A operand
 //   X ring    SX x (X1 | X2) chunk in shared memory (TMA, evict-last)
-// TMEM: columns [0, 4 NP) = 2 accumulator buffers of [D0 | D1 + D2] (2 NP
-// each; D1 and D2 carry the same 2^-11 weight, so the tensor core sums them),
-// columns [256, 384) = the two A1/A2 slots.
+// TMEM: columns [0, 4 NP) = 2 accumulator buffers of [D0 | D1] (2 NP
+// each), columns [256, 384) = the two A1 slots.
 constexpr uint32_t kTcTmemCols = 512;
 constexpr uint32_t kTcTmemAOff = 256;
-__host__ __device__ inline size_t tc_a_bytes() { return size_t(kTcTileM) * kTcKChunk * 4; }  // 32 KB
+// A ring stage: one 64-row chunk of a 128-column tile (32 KB fp32, 64 KB fp64)
+__host__ __device__ inline size_t tc_a_bytes(int esz) { return size_t(kTcTileM) * kTcKChunk * esz; }
 __host__ __device__ inline size_t tc_x_bytes(int n_pad) { return size_t(n_pad) * kTcKChunk * 2; }
-__host__ __device__ inline size_t tc_smem_bytes(int n_pad, int sa, int sx) {
-  return 1024 /*align slack*/ + sa * tc_a_bytes() + sx * 2 * tc_x_bytes(n_pad) + 8192 /*barriers, params, 256 x 2 fp64 partials*/;
+__host__ __device__ inline size_t tc_smem_bytes(int n_pad, int sa, int sx, int esz) {
+  return 1024 /*align slack*/ + sa * tc_a_bytes(esz) + sx * 2 * tc_x_bytes(n_pad) + 4096 /*barriers, params*/;
 }
 
 __device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar,
@@ -285,6 +303,12 @@ struct TcRing {
   }
 };
 
+__device__ __forceinline__ double2 lds_d2(uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+
 __device__ __forceinline__ float4 lds_f4(uint32_t addr) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
@@ -298,6 +322,7 @@ __device__ __forceinline__ uint32_t pack_f16x2(float k0, float k1) {
   return d;
 }
 
+template <typename TA>
 __global__ void __launch_bounds__(kTcThreads, 1)
     tc_dots_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX1,
                    const __grid_constant__ CUtensorMap tmX2, const TcDotsArgs a) {
@@ -309,13 +334,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int NP = a.n_pad;
   const int SA = a.a_stages, SL = kTcLoStages, SX = a.x_stages;
   const int SEG = a.seg_chunks;
-  const size_t a_bytes = tc_a_bytes();  // 32 KB: two 16 KB boxes (rows 0-31, 32-63)
+  constexpr int kBoxK = kTcBoxBytes / int(sizeof(TA));  // rows per A box
+  constexpr int kBoxes = kTcKChunk / kBoxK;              // boxes per 64-row chunk (2 fp32, 4 fp64)
+  const size_t a_bytes = tc_a_bytes(sizeof(TA));         // kBoxes boxes of 16 KB
   const size_t x_bytes = tc_x_bytes(NP);
   unsigned char* aring = smem;
   unsigned char* xring = aring + SA * a_bytes;  // [stage][X1 | X2]
   uint64_t* a_full = reinterpret_cast<uint64_t*>(xring + SX * 2 * x_bytes);
   uint64_t* a_empty = a_full + SA;
-  uint64_t* lo_full = a_empty + SA;  // TMEM A1 / A2 slots
+  uint64_t* lo_full = a_empty + SA;  // TMEM A1 slots
   uint64_t* lo_empty = lo_full + SL;
   uint64_t* x_full = lo_empty + SL;
   uint64_t* x_empty = x_full + SX;
@@ -327,10 +354,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int kchunks = (a.ld + kTcKChunk - 1) / kTcKChunk;
-  // MMA a: A1 [X1 | X2] (N = 2 NP; the X slot holds X1 rows then X2 rows);
-  // MMA b: A2 X1 (N = NP) accumulated onto the A1 X2 columns.
+  // one MMA per 16 rows: A1 [X1 | X2] (N = 2 NP; the X slot holds X1 rows then X2 rows)
   const uint32_t idesc2 = umma_idesc_f16(kTcTileM, 2 * NP);
-  const uint32_t idesc1 = umma_idesc_f16(kTcTileM, NP);
 
   if (tid == 0) {
     for (int i = 0; i < SA; ++i) {
@@ -390,8 +415,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         pf.stop(w0);
         unsigned char* st = aring + r.slot * a_bytes;
         mbar_arrive_expect_tx(&a_full[r.slot], static_cast<uint32_t>(a_bytes));
-        tma_load_2d_hint(st, &tmA, kc * kTcKChunk, t * kTcTileM, &a_full[r.slot], policy);
-        tma_load_2d_hint(st + a_bytes / 2, &tmA, kc * kTcKChunk + kTcBoxK, t * kTcTileM, &a_full[r.slot], policy);
+#pragma unroll
+        for (int b = 0; b < kBoxes; ++b)
+          tma_load_2d_hint(st + b * (a_bytes / kBoxes), &tmA, kc * kTcKChunk + b * kBoxK, t * kTcTileM,
+                           &a_full[r.slot], policy);
         r.next(SA);
         if (++kc == kchunks) {
           kc = 0;
@@ -455,13 +482,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           mbar_wait(&x_full[rx.slot], rx.ph);
           pf.stop(w5);
           tc_fence_after();
-          const uint32_t ta = tmem_base + kTcTmemAOff + uint32_t(rl.slot) * 64;  // A1; A2 at +32
+          const uint32_t ta = tmem_base + kTcTmemAOff + uint32_t(rl.slot) * 64;  // A1
           const uint64_t bx = dx + uint64_t(rx.slot) * x_step;
 #pragma unroll
           for (int k = 0; k < kTcKChunk / 16; ++k) {
             const uint32_t first = (kc == k0 && k == 0) ? 0u : 1u;
             umma_f16_ts_warp(dtm, ta + 8 * k, bx + 2 * k, idesc2, first);
-            if (!(a.probe & 2)) umma_f16_ts_warp(dtm + NP, ta + 32 + 8 * k, bx + 2 * k, idesc1, 1u);
           }
           umma_commit_warp(&lo_empty[rl.slot]);
           umma_commit_warp(&x_empty[rx.slot]);
@@ -481,8 +507,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // ---------------------------------------------------- converter warps
     // Thread r owns tile row r (one column of A, TMEM lane r): it reads its
     // two 128-byte rows out of the 128-byte-swizzled A slot (16-byte chunk c
-    // of row r sits at c ^ (r & 7)), scales by 2^e_i, splits into fp16
-    // A1 + 2^-11 A2 and stores the packed pairs to its TMEM lane.
+    // of row r sits at c ^ (r & 7)), scales by 2^e_i, rounds to fp16 (A1) and
+    // stores the packed pairs to its TMEM lane.
     const int q = warp & 3;
     const int r = q * 32 + lane;
     TcRing ra, rl;
@@ -505,33 +531,32 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       tc_fence_after();
       const uint32_t ta = tmem_base + (uint32_t(q * 32) << 16) + kTcTmemAOff + uint32_t(rl.slot) * 64;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {  // rows 32 h .. 32 h + 31 (one fp32 TMA box)
-        uint32_t p1[16], p2[16];
-        const uint32_t row_s = smem_u32(aring + ra.slot * a_bytes + h * (a_bytes / 2) + r * 128);
+      for (int h = 0; h < 2; ++h) {  // rows 32 h .. 32 h + 31 (one fp32 / two fp64 TMA boxes)
+        uint32_t p1[16];
+        // A1 = fp16(y), y = a 2^e (fp64 storage: y rounded to fp32 first);
+        // tc_col_exp_kernel reproduces exactly this rounding for the margin.
+        if constexpr (sizeof(TA) == 4) {
+          const uint32_t row_s = smem_u32(aring + ra.slot * a_bytes + h * (a_bytes / 2) + r * 128);
 #pragma unroll
-        for (int cc = 0; cc < 8; ++cc) {
-          const float4 v = lds_f4(row_s + ((cc ^ (r & 7)) << 4));
-          // y = a 2^e split as y = hi + lo with hi = y rounded to 11
-          // significant bits (integer round-half-up on the bit pattern; exact
-          // in fp16 above 2^-14, i.e. 2^-28 of the column maximum) and lo
-          // exact; lo 2^11 rounds to fp16 with 2^-22 relative error.
-          const float y[4] = {v.x * sc, v.y * sc, v.z * sc, v.w * sc};
-          float hi[4], lo[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            hi[u] = __uint_as_float((__float_as_uint(y[u]) + 0x1000u) & 0xFFFFE000u);
-            lo[u] = __fmul_rn(__fsub_rn(y[u], hi[u]), 2048.f);
+          for (int cc = 0; cc < 8; ++cc) {
+            const float4 v = lds_f4(row_s + ((cc ^ (r & 7)) << 4));
+            p1[cc * 2] = pack_f16x2(v.x * sc, v.y * sc);  // packed column (row / 2) within the half
+            p1[cc * 2 + 1] = pack_f16x2(v.z * sc, v.w * sc);
           }
-          p1[cc * 2] = pack_f16x2(hi[0], hi[1]);  // packed column (k / 2) within the half
-          p1[cc * 2 + 1] = pack_f16x2(hi[2], hi[3]);
-          p2[cc * 2] = pack_f16x2(lo[0], lo[1]);
-          p2[cc * 2 + 1] = pack_f16x2(lo[2], lo[3]);
+        } else {
+          const double scd = static_cast<double>(sc);
+#pragma unroll
+          for (int bq = 0; bq < 2; ++bq) {  // 16-row box 2 h + bq
+            const uint32_t row_s = smem_u32(aring + ra.slot * a_bytes + (2 * h + bq) * (a_bytes / 4) + r * 128);
+#pragma unroll
+            for (int cc = 0; cc < 8; ++cc) {  // 16-byte chunk = rows 2 cc, 2 cc + 1 of the box
+              const double2 v = lds_d2(row_s + ((cc ^ (r & 7)) << 4));
+              p1[bq * 8 + cc] = pack_f16x2(__double2float_rn(v.x * scd), __double2float_rn(v.y * scd));
+            }
+          }
         }
         pf.start();
-        if (!(a.probe & 32)) {
-          tmem_st16(ta + 16 * h, p1);
-          tmem_st16(ta + 32 + 16 * h, p2);
-        }
+        if (!(a.probe & 32)) tmem_st16(ta + 16 * h, p1);
         pf.stop(w9);
       }
       __syncwarp();
@@ -604,16 +629,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         pf.stop(w12);
       }
       const int64_t col = int64_t(t) * kTcTileM + q * 32 + lane;
+      bool cand = false;
       if (col < a.n) {
-        // Candidate filter.  The exact c_ij (fp64) is within
-        // delta_i = 2^-kTcMarginExp ||a_i|| ||x_j|| of this estimate (the split
-        // and fp32 accumulation errors are < 2^-17 of sum_r |a_ri x_rj|, see
-        // DESIGN.md; ||x_j|| = 1), so a column none of whose components can
-        // reach the threshold with that margin is inactive (w = 0, objective
-        // term 0) for certain; every other column is recomputed exactly by T1x.
+        // Candidate filter.  The exact c_ij (fp64) is within delta_i of this
+        // estimate (tc_col_exp_kernel; ||x_j|| = 1), so a column
+        // none of whose components can reach the threshold with that margin
+        // is inactive (w = 0, objective term 0) for certain; every other
+        // column is recomputed exactly by T1x.
         const double unscale = ldexp(1.0, -(a.col_exp[col] + kTcXScaleExp));
-        const double delta = ldexp(static_cast<double>(a.col_nrm[col]), -kTcMarginExp);
-        bool cand = false;
+        const double delta = static_cast<double>(a.col_delta[col]);
 #pragma unroll
         for (int jj = 0; jj < 32; ++jj) {
           const int j = jbase + jj;
@@ -628,6 +652,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         a.colmask[size_t(g) * a.n + col] = cand ? 1 : 0;
       }
+      // per (tile, group, lane quarter) flag: T1x skips tiles with none
+      const unsigned any = __ballot_sync(0xffffffffu, cand);
+      if (lane == 0) a.tflag[size_t(t) * 8 + g * 4 + q] = any != 0u ? 1 : 0;
     }
     if (pf.on && lane == 0) {
       atomicAdd(&g_tc_prof[11], w11);
@@ -643,54 +670,68 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 }
 
 // T1x: exact fp64 recomputation of the candidate columns T1 flagged.
-// Work items are 256-column ranges, assigned to CTAs round-robin (item b,
-// b + grid, ...) so contiguous runs of active columns spread over the grid.
-// Per item the candidates are compacted in column order and processed in
-// batches of 64: C_batch = A_batch' X in fp64 (fp32 a_ri is exact in fp64),
-// 32 rows at a time through shared memory; thread (lane, warp) owns columns
-// {lane, lane + 32} x components [warp JPT, warp JPT + JPT).  Then, per
+// Work items are 256-column ranges (two T1 tiles), assigned to CTAs
+// round-robin (item b, b + grid, ...) so contiguous runs of active columns
+// spread over the grid; an item whose two tiles carry no candidate flag is
+// skipped without reading its columns.  Per item the candidates are
+// compacted in column order, then
+//   - up to kTcRefSmallMax candidates: the CTA on one column at a time,
+//     threads over rows, X read straight from L2 (no block barriers in the
+//     row loop: staged chunks would serialise p / 32 latency-bound steps);
+//   - more: batches of 64, C_batch = A_batch' X through shared memory, 32
+//     rows at a time; thread (lane, warp) owns columns {lane, lane + 32} x
+//     components [warp JPT, warp JPT + JPT).
+// fp32 a_ri is exact in fp64, so c_ij is an fp64 dot product.  Then, per
 // (column, component): s = mu_j c_ij, w_ij = threshold(s, gamma_j) (the
 // reference's parallel.py:117-128 / block.py:80-89 rules), the objective
-// term and nnz, W written for every component of the column, and the final
-// activity mask (colmask[0][i] = any w_ij != 0, colmask[1][i] = 0) for T2.
-// f and nnz are summed per thread in a fixed order and reduced per CTA in a
-// fixed order into part_s[blockIdx.x] (deterministic run to run).
+// term and nnz, W written for every component of the column, the final
+// activity mask (colmask[0][i] = any w_ij != 0, colmask[1][i] = 0) and the
+// per-item activity flag item_act for T2.  f and nnz are summed per thread in
+// a fixed order and reduced per CTA in a fixed order into part_s[blockIdx.x]
+// (deterministic run to run).
 constexpr int kTcRefItem = 256;
 constexpr int kTcRefBatch = 64;
 constexpr int kTcRefRows = 32;
-template <int JPT>
-__global__ void __launch_bounds__(256) tc_refine_kernel(const float* __restrict__ A, int64_t n, int ld, int m,
+constexpr int kTcRefSmallMax = 16;
+template <typename TA, int JPT>
+__global__ void __launch_bounds__(256, 2) tc_refine_kernel(const TA* __restrict__ A, int64_t n, int ld, int m,
                                                         const double* __restrict__ X, int64_t x_par_stride,
                                                         const double* __restrict__ mu,
                                                         const double* __restrict__ gamma, int penalty,
-                                                        unsigned char* __restrict__ colmask, double* __restrict__ W,
+                                                        unsigned char* __restrict__ colmask,
+                                                        const unsigned char* __restrict__ tflag,
+                                                        unsigned char* __restrict__ item_act, double* __restrict__ W,
                                                         int64_t w_par_stride, double* __restrict__ part_s,
                                                         const GpsCtl* ctl) {
-  constexpr int NJ = 8 * JPT;  // padded components handled (8 warps)
+  constexpr int NJ = 8 * JPT;  // padded components (X is zero beyond m)
   if (ctl != nullptr && ctl->done) return;
   const int parity = ctl != nullptr ? (ctl->iter & 1) : 0;
   const double* Xp = X + parity * x_par_stride;
   double* Wp = W + parity * w_par_stride;
-  __shared__ float sA[kTcRefRows][kTcRefBatch + 1];
+  __shared__ TA sA[kTcRefRows][kTcRefBatch + 1];
   __shared__ double sX[kTcRefRows][NJ + 1];
   __shared__ int64_t cand[kTcRefItem];
+  __shared__ int ilist[256];
   __shared__ int wcnt[8];
   __shared__ unsigned char act[kTcRefBatch];
+  __shared__ int item_any;
+  __shared__ unsigned char colany[8];
+  __shared__ double wsum[8][32];
+  __shared__ double smu[NJ], sgam[NJ];
   __shared__ double red[2][8];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  double mu_r[JPT], gam_r[JPT];
-#pragma unroll
-  for (int u = 0; u < JPT; ++u) {
-    const int j = warp * JPT + u;
-    mu_r[u] = j < m ? mu[j] : 1.0;
-    gam_r[u] = j < m ? gamma[j] : 0.0;
+  for (int j = tid; j < NJ; j += 256) {
+    smu[j] = j < m ? mu[j] : 1.0;
+    sgam[j] = j < m ? gamma[j] : 0.0;
   }
   double f_acc = 0.0, nnz_acc = 0.0;
   const int64_t items = (n + kTcRefItem - 1) / kTcRefItem;
-  for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
-    const int64_t col = item * kTcRefItem + tid;
-    const bool flag = col < n && (colmask[col] | colmask[n + col]);
+  const int64_t G = gridDim.x;
+
+  // block-wide order-preserving compaction: returns the count, pos = my slot
+  auto compact = [&](bool flag, int& pos) {
     const unsigned bal = __ballot_sync(0xffffffffu, flag);
+    __syncthreads();  // previous readers of wcnt / the lists are done
     if (lane == 0) wcnt[warp] = __popc(bal);
     __syncthreads();
     int off = 0, total = 0;
@@ -699,81 +740,159 @@ __global__ void __launch_bounds__(256) tc_refine_kernel(const float* __restrict_
       off += (w < warp) ? wcnt[w] : 0;
       total += wcnt[w];
     }
-    if (flag) cand[off + __popc(bal & ((1u << lane) - 1u))] = col;
-    if (total == 0) {
-      __syncthreads();  // wcnt reuse
-      continue;
+    pos = off + __popc(bal & ((1u << lane) - 1u));
+    return total;
+  };
+
+  for (int64_t kb = 0; int64_t(blockIdx.x) + kb * G < items; kb += 256) {
+    // my items kb .. kb + 255 (item = blockIdx.x + k G): keep the flagged ones
+    const int64_t it = int64_t(blockIdx.x) + (kb + tid) * G;
+    bool ne = false;
+    if (it < items) {
+      const uint4 f = *reinterpret_cast<const uint4*>(tflag + it * 16);
+      ne = (f.x | f.y | f.z | f.w) != 0u;
+      if (!ne) item_act[it] = 0;
     }
-    if (tid < kTcRefBatch) act[tid] = 0;
+    int pos;
+    const int nitems = compact(ne, pos);
+    if (ne) ilist[pos] = tid;
     __syncthreads();
-    for (int b0 = 0; b0 < total; b0 += kTcRefBatch) {
-      const int nb = min(kTcRefBatch, total - b0);
-      double acc[2][JPT];
+    for (int ii = 0; ii < nitems; ++ii) {
+      const int64_t item = int64_t(blockIdx.x) + (kb + ilist[ii]) * G;
+      const int64_t col = item * kTcRefItem + tid;
+      const bool flag = col < n && (colmask[col] | colmask[n + col]);
+      const int total = compact(flag, pos);
+      if (flag) cand[pos] = col;
+      if (tid == 0) item_any = 0;
+      __syncthreads();
+      if (total <= kTcRefSmallMax) {
+        // ---- few candidates: the whole CTA on one column at a time, threads
+        // over rows (X straight from L2, no barriers in the row loop), then a
+        // fixed-order reduction over the 8 warps
+        for (int ci = 0; ci < total; ++ci) {
+          const int64_t c = cand[ci];
+          const TA* ac = A + c * ld;
+          if (tid == 0) colany[0] = 0;
+          constexpr int JC = NJ < 32 ? NJ : 32;  // components per pass (register budget)
+#pragma unroll 1
+          for (int jh = 0; jh < NJ; jh += JC) {
+            double acc[JC];
 #pragma unroll
-      for (int i = 0; i < 2; ++i)
+            for (int j = 0; j < JC; ++j) acc[j] = 0.0;
+            const double* xr = Xp + size_t(jh) * ld;
+#pragma unroll 2
+            for (int r = tid; r < ld; r += 256) {
+              const double av = static_cast<double>(ac[r]);
 #pragma unroll
-        for (int u = 0; u < JPT; ++u) acc[i][u] = 0.0;
-      for (int r0 = 0; r0 < ld; r0 += kTcRefRows) {
-        // stage A: warp w loads batch columns 8w .. 8w + 7, lane = row
+              for (int j = 0; j < JC; ++j) acc[j] = fma(av, xr[size_t(j) * ld + r], acc[j]);
+            }
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const int bc = warp * 8 + c;
-          sA[lane][bc] = bc < nb ? A[cand[b0 + bc] * ld + r0 + lane] : 0.f;
-        }
-        // stage X rows r0 .. r0 + 31 of components 0 .. NJ - 1
-        for (int e = tid; e < kTcRefRows * NJ; e += 256) {
-          const int j = e >> 5, r = e & 31;
-          sX[r][j] = j < m ? Xp[size_t(j) * ld + r0 + r] : 0.0;
-        }
-        __syncthreads();
-#pragma unroll 8
-        for (int r = 0; r < kTcRefRows; ++r) {
-          const double a0 = static_cast<double>(sA[r][lane]);
-          const double a1 = static_cast<double>(sA[r][lane + 32]);
+            for (int j = 0; j < JC; ++j) {
+              const double v = warp_sum(acc[j]);
+              if (lane == 0) wsum[warp][j] = v;
+            }
+            __syncthreads();
+            if (tid < JC && jh + tid < m) {
+              const int jj = jh + tid;
+              double cj = wsum[0][tid];
 #pragma unroll
-          for (int u = 0; u < JPT; ++u) {
-            const double x = sX[r][warp * JPT + u];
-            acc[0][u] = fma(a0, x, acc[0][u]);
-            acc[1][u] = fma(a1, x, acc[1][u]);
-          }
-        }
-        __syncthreads();
-      }
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int bc = lane + 32 * i;
-        if (bc < nb) {
-          const int64_t c = cand[b0 + bc];
-          bool any = false;
-#pragma unroll
-          for (int u = 0; u < JPT; ++u) {
-            const int j = warp * JPT + u;
-            if (j < m) {
-              const double sj = mu_r[u] * acc[i][u];
-              const double w = threshold_weight(sj, gam_r[u], penalty);
-              f_acc += objective_term(sj, gam_r[u], penalty);
+              for (int w = 1; w < 8; ++w) cj += wsum[w][tid];
+              const double sj = smu[jj] * cj;
+              const double w = threshold_weight(sj, sgam[jj], penalty);
+              f_acc += objective_term(sj, sgam[jj], penalty);
               if (w != 0.0) {
                 nnz_acc += 1.0;
-                any = true;
+                colany[0] = 1;  // benign: every writer stores 1
               }
-              Wp[size_t(j) * n + c] = w;
+              Wp[size_t(jj) * n + c] = w;
+            }
+            __syncthreads();
+          }
+          if (tid == 0) {
+            colmask[c] = colany[0];
+            colmask[n + c] = 0;
+            if (colany[0]) item_any = 1;
+          }
+        }
+      } else {
+        // ---- batches of 64 through shared memory
+        if (tid < kTcRefBatch) act[tid] = 0;
+        __syncthreads();
+        for (int b0 = 0; b0 < total; b0 += kTcRefBatch) {
+          const int nb = min(kTcRefBatch, total - b0);
+          const bool two = nb > 32;  // warp-uniform: second column slot in use
+          double acc[2][JPT];
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int u = 0; u < JPT; ++u) acc[i][u] = 0.0;
+          for (int r0 = 0; r0 < ld; r0 += kTcRefRows) {
+            // stage A: warp w loads batch columns 8w .. 8w + 7, lane = row
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const int bc = warp * 8 + c;
+              sA[lane][bc] = bc < nb ? A[cand[b0 + bc] * ld + r0 + lane] : TA(0);
+            }
+            // stage X rows r0 .. r0 + 31 of components 0 .. NJ - 1
+            for (int e = tid; e < kTcRefRows * NJ; e += 256) {
+              const int j = e >> 5, r = e & 31;
+              sX[r][j] = Xp[size_t(j) * ld + r0 + r];
+            }
+            __syncthreads();
+#pragma unroll 8
+            for (int r = 0; r < kTcRefRows; ++r) {
+              const double a0 = static_cast<double>(sA[r][lane]);
+#pragma unroll
+              for (int u = 0; u < JPT; ++u) acc[0][u] = fma(a0, sX[r][warp * JPT + u], acc[0][u]);
+              if (two) {
+                const double a1 = static_cast<double>(sA[r][lane + 32]);
+#pragma unroll
+                for (int u = 0; u < JPT; ++u) acc[1][u] = fma(a1, sX[r][warp * JPT + u], acc[1][u]);
+              }
+            }
+            __syncthreads();
+          }
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int bc = lane + 32 * i;
+            if (bc < nb) {
+              const int64_t c = cand[b0 + bc];
+              bool any = false;
+#pragma unroll
+              for (int u = 0; u < JPT; ++u) {
+                const int j = warp * JPT + u;
+                if (j < m) {
+                  const double sj = smu[j] * acc[i][u];
+                  const double w = threshold_weight(sj, sgam[j], penalty);
+                  f_acc += objective_term(sj, sgam[j], penalty);
+                  if (w != 0.0) {
+                    nnz_acc += 1.0;
+                    any = true;
+                  }
+                  Wp[size_t(j) * n + c] = w;
+                }
+              }
+              if (any) act[bc] = 1;  // benign: every writer stores 1
             }
           }
-          if (any) act[bc] = 1;  // benign: every writer stores 1
+          __syncthreads();
+          if (tid < nb) {
+            const int64_t c = cand[b0 + tid];
+            colmask[c] = act[tid];
+            colmask[n + c] = 0;
+            if (act[tid]) item_any = 1;
+            act[tid] = 0;
+          }
+          __syncthreads();
         }
       }
       __syncthreads();
-      if (tid < nb) {
-        const int64_t c = cand[b0 + tid];
-        colmask[c] = act[tid];
-        colmask[n + c] = 0;
-        act[tid] = 0;
-      }
-      __syncthreads();
+      if (tid == 0) item_act[item] = item_any ? 1 : 0;
     }
   }
   f_acc = warp_sum(f_acc);
   nnz_acc = warp_sum(nnz_acc);
+  __syncthreads();
   if (lane == 0) {
     red[0][warp] = f_acc;
     red[1][warp] = nnz_acc;
@@ -788,57 +907,90 @@ __global__ void __launch_bounds__(256) tc_refine_kernel(const float* __restrict_
 }
 
 // T2: sparse rank-m update on the ACTIVE columns (colmask), fp64.
-// grid (GX, ceil(ld / 1024), ceil(m / 8)); CTA (b, y, z) owns columns
-// [b n / GX, (b+1) n / GX), rows [y*1024, +1024) and components [8z, 8z+8)
-// of part_g[b] ([m_pad][ld]).
+// grid (GX, ceil(ld / 1024), ceil(m / 8)); CTA (b, y, z) owns the 256-column
+// items [b I / GX, (b+1) I / GX) (I = ceil(n / 256)), rows [y*1024, +1024)
+// and components [8z, 8z+8) of part_g[b] ([m_pad][ld]).  Items without an
+// active column (item_act, from T1x) are skipped 256 at a time.
 constexpr int kTcUpdRows = 1024;
 constexpr int kTcUpdComps = 8;
-__global__ void __launch_bounds__(256) tc_update_kernel(const float* __restrict__ A, int64_t n, int ld, int m,
+template <typename TA>
+__global__ void __launch_bounds__(256) tc_update_kernel(const TA* __restrict__ A, int64_t n, int ld, int m,
                                                         const unsigned char* __restrict__ colmask,
+                                                        const unsigned char* __restrict__ item_act,
                                                         const double* __restrict__ W, int64_t w_par_stride,
                                                         int m_pad, double* __restrict__ part_g, const GpsCtl* ctl) {
   constexpr int RPT = kTcUpdRows / 256;
   if (ctl != nullptr && ctl->done) return;
   const int parity = ctl != nullptr ? (ctl->iter & 1) : 0;
   const double* Wp = W + parity * w_par_stride;
-  const int64_t c0 = n * blockIdx.x / gridDim.x, c1 = n * (blockIdx.x + 1) / gridDim.x;
+  const int64_t items = (n + kTcRefItem - 1) / kTcRefItem;
+  const int64_t i0 = items * blockIdx.x / gridDim.x, i1 = items * (blockIdx.x + 1) / gridDim.x;
   const int r0 = blockIdx.y * kTcUpdRows;
   const int j0 = blockIdx.z * kTcUpdComps;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   double g[kTcUpdComps][RPT];
 #pragma unroll
   for (int j = 0; j < kTcUpdComps; ++j)
 #pragma unroll
     for (int k = 0; k < RPT; ++k) g[j][k] = 0.0;
-  __shared__ unsigned char flags[256];
-  for (int64_t base = c0; base < c1; base += 256) {
-    // cheap skip of fully inactive 256-column chunks (the common case)
-    const int64_t mine = base + threadIdx.x;
-    const unsigned char f = mine < c1 ? (colmask[mine] | colmask[n + mine]) : 0;
-    if (!__syncthreads_or(f)) continue;
-    flags[threadIdx.x] = f;
+  __shared__ int ilist[256];
+  __shared__ int wcnt[8];
+  __shared__ int64_t alist[kTcRefItem];
+  __shared__ double wv[kTcRefItem][kTcUpdComps];
+  for (int64_t ib = i0; ib < i1; ib += 256) {
+    const int64_t it = ib + tid;
+    const bool ne = it < i1 && item_act[it] != 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, ne);
+    if (lane == 0) wcnt[warp] = __popc(bal);
     __syncthreads();
-    const int cnt = (c1 - base) < 256 ? static_cast<int>(c1 - base) : 256;
-    for (int k = 0; k < cnt; ++k) {
-      if (!flags[k]) continue;
-      const int64_t col = base + k;
-      double w[kTcUpdComps];
+    int off = 0, nitems = 0;
 #pragma unroll
-      for (int j = 0; j < kTcUpdComps; ++j) w[j] = (j0 + j < m) ? Wp[size_t(j0 + j) * n + col] : 0.0;
-      const float* ac = A + col * ld;
+    for (int w = 0; w < 8; ++w) {
+      off += (w < warp) ? wcnt[w] : 0;
+      nitems += wcnt[w];
+    }
+    if (ne) ilist[off + __popc(bal & ((1u << lane) - 1u))] = tid;
+    __syncthreads();
+    for (int ii = 0; ii < nitems; ++ii) {
+      // the item's active columns in column order, their weights staged
+      const int64_t base = (ib + ilist[ii]) * kTcRefItem;
+      const int64_t mine = base + tid;
+      const bool f = mine < n && colmask[mine] != 0;
+      const unsigned fb = __ballot_sync(0xffffffffu, f);
+      __syncthreads();  // wcnt / alist / wv readers of the previous item are done
+      if (lane == 0) wcnt[warp] = __popc(fb);
+      __syncthreads();
+      int o2 = 0, cnt = 0;
 #pragma unroll
-      for (int kk = 0; kk < RPT; ++kk) {
-        const int r = r0 + kk * 256 + threadIdx.x;
-        const double v = r < ld ? static_cast<double>(ac[r]) : 0.0;
+      for (int w = 0; w < 8; ++w) {
+        o2 += (w < warp) ? wcnt[w] : 0;
+        cnt += wcnt[w];
+      }
+      if (f) alist[o2 + __popc(fb & ((1u << lane) - 1u))] = mine;
+      __syncthreads();
+      for (int e = tid; e < cnt * kTcUpdComps; e += 256) {
+        const int k = e / kTcUpdComps, j = e % kTcUpdComps;
+        wv[k][j] = (j0 + j < m) ? Wp[size_t(j0 + j) * n + alist[k]] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll 4
+      for (int k = 0; k < cnt; ++k) {
+        const TA* ac = A + alist[k] * ld;
 #pragma unroll
-        for (int j = 0; j < kTcUpdComps; ++j) g[j][kk] = fma(w[j], v, g[j][kk]);
+        for (int kk = 0; kk < RPT; ++kk) {
+          const int r = r0 + kk * 256 + tid;
+          const double v = r < ld ? static_cast<double>(ac[r]) : 0.0;
+#pragma unroll
+          for (int j = 0; j < kTcUpdComps; ++j) g[j][kk] = fma(wv[k][j], v, g[j][kk]);
+        }
       }
     }
-    __syncthreads();
+    __syncthreads();  // ilist / wcnt reuse
   }
   double* pg = part_g + size_t(blockIdx.x) * m_pad * ld;
 #pragma unroll
   for (int k = 0; k < RPT; ++k) {
-    const int r = r0 + k * 256 + threadIdx.x;
+    const int r = r0 + k * 256 + tid;
     if (r < ld)
 #pragma unroll
       for (int j = 0; j < kTcUpdComps; ++j)

@@ -5,7 +5,8 @@ candidate-free column counts of the last sweep.  Run plainly for the
 iteration times, and under `ncu --metrics gpu__time_duration.sum` for the
 per-kernel split.
 
-    TC_CFG=c3|c4  TC_DATA=gauss|planted  TC_ITERS=4  python scripts/tc_breakdown.py
+    TC_CFG=c3|c4  TC_DATA=gauss|planted  TC_DTYPE=f32|f64  TC_GFRAC=0.1  TC_ITERS=4 \
+        python scripts/tc_breakdown.py
 """
 import os
 import sys
@@ -55,8 +56,12 @@ def main():
         g = torch.Generator(device="cuda")
         g.manual_seed(3)
         At = torch.randn((n, p), generator=g, device="cuda", dtype=torch.float32)
-    A = gps.DataMatrix.from_device(At.data_ptr(), p, n, owner=At)
-    top = 0.1 * float(A.norms.max())
+    if os.environ.get("TC_DTYPE", "f32") == "f64":
+        At = At.double()
+        torch.cuda.empty_cache()
+    A = gps.DataMatrix.from_device(At.data_ptr(), p, n, dtype=np.float64 if At.dtype == torch.float64 else np.float32,
+                                   owner=At)
+    top = float(os.environ.get("TC_GFRAC", 0.1)) * float(A.norms.max())
     gamma = np.full(m, top if pen == "l1" else top * top)
     loop = BlockLoop(A, pen, m, gamma, mu, 0.0, iters + 1)
     loop.start_columns(_top_m_columns(np.asarray(A.norms), m))
@@ -77,7 +82,7 @@ def main():
     _native.check(L.gps_bk_run(loop.handle, 1))  # finishes the last iteration (max_iter reached)
     X, hist, conv, W, rf, rank = loop.result()
     active = int((W != 0).any(axis=1).sum())
-    print(f"{cfg} {data}: p={p} n={n} m={m} {pen}: median {np.median(times[1:] or times):.3f} ms/iteration, "
+    print(f"{cfg} {data} {A.dtype}: p={p} n={n} m={m} {pen}: median {np.median(times[1:] or times):.3f} ms/iteration, "
           f"active columns {active} ({100.0 * active / n:.2f}%), nnz {int((W != 0).sum())}, f={hist[-1]:.6g}")
 
 

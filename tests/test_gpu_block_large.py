@@ -25,10 +25,11 @@ def _stiefel(rng, p, m):
 @pytest.mark.parametrize("p,n,m,pen", [(256, 1000, 16, "l1"), (512, 3000, 32, "l0"), (4096, 12000, 64, "l1"),
                                         (8192, 8192, 64, "l0"), (300, 777, 24, "l1"), (4128, 3001, 10, "l1"),
                                         (10000, 2000, 5, "l0"), (33, 500, 7, "l1"), (1000, 129, 40, "l0")])
-def test_tensor_core_sweep_vs_oracle(p, n, m, pen):
+@pytest.mark.parametrize("dtype", [np.float32, np.float64], ids=["fp32", "fp64"])
+def test_tensor_core_sweep_vs_oracle(p, n, m, pen, dtype):
     rng = np.random.default_rng(p + m)
     A32 = rng.standard_normal((p, n)).astype(np.float32)
-    A = gps.DataMatrix(A32)
+    A = gps.DataMatrix(A32.astype(dtype), dtype=dtype)
     X = _stiefel(rng, p, m)
     gamma = np.full(m, 2.0 if pen == "l1" else 4.0)
     mu = np.linspace(1.0, 0.6, m)
@@ -42,13 +43,14 @@ def test_tensor_core_sweep_vs_oracle(p, n, m, pen):
     assert np.abs(G - G_ref).max() <= 1e-11 * np.abs(G_ref).max()
 
 
-def test_tensor_core_solve_vs_oracle():
+@pytest.mark.parametrize("dtype", [np.float32, np.float64], ids=["fp32", "fp64"])
+def test_tensor_core_solve_vs_oracle(dtype):
     rng = np.random.default_rng(5)
     A32 = rng.standard_normal((400, 5000)).astype(np.float32)
     A64 = A32.astype(np.float64)
     gamma = 0.1 * float(np.linalg.norm(A64, axis=0).max())
     cfg = gps.SolverConfig(penalty="l1", mode="block", m=16, gamma=gamma, max_iter=40)
-    loadings, report = gps.solve_block(gps.DataMatrix(A32), cfg)
+    loadings, report = gps.solve_block(gps.DataMatrix(A32.astype(dtype), dtype=dtype), cfg)
     Z, hist, conv, X = oracle.block_solve(A64, 16, gamma, 1.0, "l1", max_iter=40)
     assert report.iterations == len(hist) - 1
     np.testing.assert_allclose(report.objective_history, hist, rtol=1e-9)
