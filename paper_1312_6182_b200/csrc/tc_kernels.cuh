@@ -907,12 +907,17 @@ __global__ void __launch_bounds__(256, 2) tc_refine_kernel(const TA* __restrict_
 }
 
 // T2: sparse rank-m update on the ACTIVE columns (colmask), fp64.
-// grid (GX, ceil(ld / 1024), ceil(m / 8)); CTA (b, y, z) owns the 256-column
-// items [b I / GX, (b+1) I / GX) (I = ceil(n / 256)), rows [y*1024, +1024)
-// and components [8z, 8z+8) of part_g[b] ([m_pad][ld]).  Items without an
-// active column (item_act, from T1x) are skipped 256 at a time.
+// grid (GX, ceil(ld / 1024), ceil(m / 8)); CTA (b, y, z) owns the
+// 512-column blocks [b B / GX, (b+1) B / GX) (B = ceil(n / 512), two T1x
+// items each), rows [y*1024, +1024) and components [8z, 8z+8) of part_g[b]
+// ([m_pad][ld]).  Blocks without an active item (item_act, from T1x) are
+// skipped 256 at a time; the active columns of consecutive blocks are
+// compacted in column order into a list of up to 512 entries whose weights
+// are staged in shared memory before the FMA pass (one pass per full list,
+// so the per-block cost is one compaction, not one latency-bound pass).
 constexpr int kTcUpdRows = 1024;
 constexpr int kTcUpdComps = 8;
+constexpr int kTcUpdBlock = 512;
 template <typename TA>
 __global__ void __launch_bounds__(256) tc_update_kernel(const TA* __restrict__ A, int64_t n, int ld, int m,
                                                         const unsigned char* __restrict__ colmask,
@@ -923,8 +928,8 @@ __global__ void __launch_bounds__(256) tc_update_kernel(const TA* __restrict__ A
   if (ctl != nullptr && ctl->done) return;
   const int parity = ctl != nullptr ? (ctl->iter & 1) : 0;
   const double* Wp = W + parity * w_par_stride;
-  const int64_t items = (n + kTcRefItem - 1) / kTcRefItem;
-  const int64_t i0 = items * blockIdx.x / gridDim.x, i1 = items * (blockIdx.x + 1) / gridDim.x;
+  const int64_t nblk = (n + kTcUpdBlock - 1) / kTcUpdBlock;
+  const int64_t b0 = nblk * blockIdx.x / gridDim.x, b1 = nblk * (blockIdx.x + 1) / gridDim.x;
   const int r0 = blockIdx.y * kTcUpdRows;
   const int j0 = blockIdx.z * kTcUpdComps;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -933,60 +938,77 @@ __global__ void __launch_bounds__(256) tc_update_kernel(const TA* __restrict__ A
   for (int j = 0; j < kTcUpdComps; ++j)
 #pragma unroll
     for (int k = 0; k < RPT; ++k) g[j][k] = 0.0;
-  __shared__ int ilist[256];
+  __shared__ int blist[256];
   __shared__ int wcnt[8];
-  __shared__ int64_t alist[kTcRefItem];
-  __shared__ double wv[kTcRefItem][kTcUpdComps];
-  for (int64_t ib = i0; ib < i1; ib += 256) {
-    const int64_t it = ib + tid;
-    const bool ne = it < i1 && item_act[it] != 0;
-    const unsigned bal = __ballot_sync(0xffffffffu, ne);
-    if (lane == 0) wcnt[warp] = __popc(bal);
+  __shared__ int64_t alist[kTcUpdBlock];
+  __shared__ double wv[kTcUpdBlock][kTcUpdComps];
+  int acc = 0;  // entries in alist (block-uniform)
+
+  // block-wide exclusive scan of a per-thread count (fixed order)
+  auto scan = [&](int v, int& total) {
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    __syncthreads();  // previous readers of wcnt are done
+    if (lane == 31) wcnt[warp] = x;
     __syncthreads();
-    int off = 0, nitems = 0;
+    int off = 0;
+    total = 0;
 #pragma unroll
     for (int w = 0; w < 8; ++w) {
       off += (w < warp) ? wcnt[w] : 0;
-      nitems += wcnt[w];
+      total += wcnt[w];
     }
-    if (ne) ilist[off + __popc(bal & ((1u << lane) - 1u))] = tid;
+    return off + x - v;
+  };
+  auto flush = [&]() {
+    for (int e = tid; e < acc * kTcUpdComps; e += 256) {
+      const int k = e / kTcUpdComps, j = e % kTcUpdComps;
+      wv[k][j] = (j0 + j < m) ? Wp[size_t(j0 + j) * n + alist[k]] : 0.0;
+    }
     __syncthreads();
-    for (int ii = 0; ii < nitems; ++ii) {
-      // the item's active columns in column order, their weights staged
-      const int64_t base = (ib + ilist[ii]) * kTcRefItem;
-      const int64_t mine = base + tid;
-      const bool f = mine < n && colmask[mine] != 0;
-      const unsigned fb = __ballot_sync(0xffffffffu, f);
-      __syncthreads();  // wcnt / alist / wv readers of the previous item are done
-      if (lane == 0) wcnt[warp] = __popc(fb);
-      __syncthreads();
-      int o2 = 0, cnt = 0;
-#pragma unroll
-      for (int w = 0; w < 8; ++w) {
-        o2 += (w < warp) ? wcnt[w] : 0;
-        cnt += wcnt[w];
-      }
-      if (f) alist[o2 + __popc(fb & ((1u << lane) - 1u))] = mine;
-      __syncthreads();
-      for (int e = tid; e < cnt * kTcUpdComps; e += 256) {
-        const int k = e / kTcUpdComps, j = e % kTcUpdComps;
-        wv[k][j] = (j0 + j < m) ? Wp[size_t(j0 + j) * n + alist[k]] : 0.0;
-      }
-      __syncthreads();
 #pragma unroll 4
-      for (int k = 0; k < cnt; ++k) {
-        const TA* ac = A + alist[k] * ld;
+    for (int k = 0; k < acc; ++k) {
+      const TA* ac = A + alist[k] * ld;
 #pragma unroll
-        for (int kk = 0; kk < RPT; ++kk) {
-          const int r = r0 + kk * 256 + tid;
-          const double v = r < ld ? static_cast<double>(ac[r]) : 0.0;
+      for (int kk = 0; kk < RPT; ++kk) {
+        const int r = r0 + kk * 256 + tid;
+        const double v = r < ld ? static_cast<double>(ac[r]) : 0.0;
 #pragma unroll
-          for (int j = 0; j < kTcUpdComps; ++j) g[j][kk] = fma(wv[k][j], v, g[j][kk]);
-        }
+        for (int j = 0; j < kTcUpdComps; ++j) g[j][kk] = fma(wv[k][j], v, g[j][kk]);
       }
     }
-    __syncthreads();  // ilist / wcnt reuse
+    __syncthreads();
+    acc = 0;
+  };
+
+  for (int64_t bb = b0; bb < b1; bb += 256) {
+    const int64_t blk = bb + tid;
+    const bool ne = blk < b1 && (item_act[2 * blk] | (2 * blk + 1 < (n + kTcRefItem - 1) / kTcRefItem
+                                                          ? item_act[2 * blk + 1] : 0)) != 0;
+    int nblocks;
+    const int bpos = scan(ne ? 1 : 0, nblocks);
+    if (ne) blist[bpos] = tid;
+    __syncthreads();
+    for (int ii = 0; ii < nblocks; ++ii) {
+      // this thread's two columns of the block
+      const int64_t c0 = (bb + blist[ii]) * kTcUpdBlock + 2 * tid;
+      const bool f0 = c0 < n && colmask[c0] != 0;
+      const bool f1 = c0 + 1 < n && colmask[c0 + 1] != 0;
+      int total;
+      const int off = scan(int(f0) + int(f1), total);
+      if (acc + total > kTcUpdBlock) flush();  // block-uniform
+      if (f0) alist[acc + off] = c0;
+      if (f1) alist[acc + off + int(f0)] = c0 + 1;
+      acc += total;
+    }
+    __syncthreads();  // blist reuse
   }
+  __syncthreads();
+  flush();
   double* pg = part_g + size_t(blockIdx.x) * m_pad * ld;
 #pragma unroll
   for (int k = 0; k < RPT; ++k) {
