@@ -673,14 +673,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 // Work items are 256-column ranges (two T1 tiles), assigned to CTAs
 // round-robin (item b, b + grid, ...) so contiguous runs of active columns
 // spread over the grid; an item whose two tiles carry no candidate flag is
-// skipped without reading its columns.  Per item the candidates are
-// compacted in column order, then
-//   - up to kTcRefSmallMax candidates: the CTA on one column at a time,
-//     threads over rows, X read straight from L2 (no block barriers in the
-//     row loop: staged chunks would serialise p / 32 latency-bound steps);
-//   - more: batches of 64, C_batch = A_batch' X through shared memory, 32
-//     rows at a time; thread (lane, warp) owns columns {lane, lane + 32} x
-//     components [warp JPT, warp JPT + JPT).
+// skipped without reading its columns.  The candidates of a CTA's items are
+// compacted in column order into one list (across items), and every 64 of
+// them are processed as a batch: C_batch = A_batch' X, 32 rows at a time (A
+// through shared memory, X in registers); thread (lane, warp) owns columns
+// {lane, lane + 32} x components [warp JPT, warp JPT + JPT).  A final partial list of up to
+// kTcRefSmallMax candidates instead takes the CTA one column at a time,
+// threads over rows, X read straight from L2 without block barriers (staged
+// chunks would serialise p / 32 latency-bound steps for a handful of columns).
 // fp32 a_ri is exact in fp64, so c_ij is an fp64 dot product.  Then, per
 // (column, component): s = mu_j c_ij, w_ij = threshold(s, gamma_j) (the
 // reference's parallel.py:117-128 / block.py:80-89 rules), the objective
@@ -695,27 +695,25 @@ constexpr int kTcRefRows = 32;
 constexpr int kTcRefSmallMax = 16;
 template <typename TA, int JPT>
 __global__ void __launch_bounds__(256, 2) tc_refine_kernel(const TA* __restrict__ A, int64_t n, int ld, int m,
-                                                        const double* __restrict__ X, int64_t x_par_stride,
-                                                        const double* __restrict__ mu,
-                                                        const double* __restrict__ gamma, int penalty,
-                                                        unsigned char* __restrict__ colmask,
-                                                        const unsigned char* __restrict__ tflag,
-                                                        unsigned char* __restrict__ item_act, double* __restrict__ W,
-                                                        int64_t w_par_stride, double* __restrict__ part_s,
-                                                        const GpsCtl* ctl) {
+                                                           const double* __restrict__ X, int64_t x_par_stride,
+                                                           const double* __restrict__ mu,
+                                                           const double* __restrict__ gamma, int penalty,
+                                                           unsigned char* __restrict__ colmask,
+                                                           const unsigned char* __restrict__ tflag,
+                                                           unsigned char* __restrict__ item_act,
+                                                           double* __restrict__ W, int64_t w_par_stride,
+                                                           double* __restrict__ part_s, const GpsCtl* ctl) {
   constexpr int NJ = 8 * JPT;  // padded components (X is zero beyond m)
+  constexpr int JC = NJ < 32 ? NJ : 32;  // components per pass of the single-column mode
   if (ctl != nullptr && ctl->done) return;
   const int parity = ctl != nullptr ? (ctl->iter & 1) : 0;
   const double* Xp = X + parity * x_par_stride;
   double* Wp = W + parity * w_par_stride;
-  __shared__ TA sA[kTcRefRows][kTcRefBatch + 1];
-  __shared__ double sX[kTcRefRows][NJ + 1];
-  __shared__ int64_t cand[kTcRefItem];
+  __shared__ TA sA[2][kTcRefRows][kTcRefBatch + 1];
+  __shared__ int64_t cand[kTcRefItem + kTcRefBatch];
   __shared__ int ilist[256];
   __shared__ int wcnt[8];
   __shared__ unsigned char act[kTcRefBatch];
-  __shared__ int item_any;
-  __shared__ unsigned char colany[8];
   __shared__ double wsum[8][32];
   __shared__ double smu[NJ], sgam[NJ];
   __shared__ double red[2][8];
@@ -743,7 +741,133 @@ __global__ void __launch_bounds__(256, 2) tc_refine_kernel(const TA* __restrict_
     pos = off + __popc(bal & ((1u << lane) - 1u));
     return total;
   };
+  // final activity of column c: mask for T2, item flag (benign: writers store 1)
+  auto publish = [&](int64_t c, bool any) {
+    colmask[c] = any ? 1 : 0;
+    colmask[n + c] = 0;
+    if (any) item_act[c / kTcRefItem] = 1;
+  };
 
+  // batch mode: candidates cand[b0 .. b0 + nb), nb <= 64.  Per 32-row chunk
+  // warp w stages batch columns 8w .. 8w + 7 (lane = row) into a double-
+  // buffered shared tile and keeps its components' X rows in registers (lane
+  // = row, broadcast by shuffles); the next chunk's loads are issued before
+  // the current chunk's FMAs, one block barrier per chunk.
+  auto batch = [&](int b0, int nb) {
+    const bool two = nb > 32;  // warp-uniform: second column slot in use
+    double acc[2][JPT];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int u = 0; u < JPT; ++u) acc[i][u] = 0.0;
+    if (tid < kTcRefBatch) act[tid] = 0;
+    const double* xw = Xp + size_t(warp * JPT) * ld;
+    TA ra[8];
+    double rx[JPT];
+    auto load = [&](int r0) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int bc = warp * 8 + c;
+        ra[c] = bc < nb ? A[cand[b0 + bc] * ld + r0 + lane] : TA(0);
+      }
+#pragma unroll
+      for (int u = 0; u < JPT; ++u) rx[u] = xw[size_t(u) * ld + r0 + lane];
+    };
+    load(0);
+    int buf = 0;
+    for (int r0 = 0; r0 < ld; r0 += kTcRefRows, buf ^= 1) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) sA[buf][lane][warp * 8 + c] = ra[c];
+      double xr[JPT];
+#pragma unroll
+      for (int u = 0; u < JPT; ++u) xr[u] = rx[u];
+      __syncthreads();
+      if (r0 + kTcRefRows < ld) load(r0 + kTcRefRows);
+#pragma unroll 8
+      for (int r = 0; r < kTcRefRows; ++r) {
+        const double a0 = static_cast<double>(sA[buf][r][lane]);
+        const double a1 = two ? static_cast<double>(sA[buf][r][lane + 32]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < JPT; ++u) {
+          const double x = __shfl_sync(0xffffffffu, xr[u], r);
+          acc[0][u] = fma(a0, x, acc[0][u]);
+          if (two) acc[1][u] = fma(a1, x, acc[1][u]);
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int bc = lane + 32 * i;
+      if (bc < nb) {
+        const int64_t c = cand[b0 + bc];
+        bool any = false;
+#pragma unroll
+        for (int u = 0; u < JPT; ++u) {
+          const int j = warp * JPT + u;
+          if (j < m) {
+            const double sj = smu[j] * acc[i][u];
+            const double w = threshold_weight(sj, sgam[j], penalty);
+            f_acc += objective_term(sj, sgam[j], penalty);
+            if (w != 0.0) {
+              nnz_acc += 1.0;
+              any = true;
+            }
+            Wp[size_t(j) * n + c] = w;
+          }
+        }
+        if (any) act[bc] = 1;  // benign: every writer stores 1
+      }
+    }
+    __syncthreads();
+    if (tid < nb) publish(cand[b0 + tid], act[tid] != 0);
+    __syncthreads();
+  };
+
+  // single-column mode: the CTA on cand[ci], threads over rows
+  auto single = [&](int ci) {
+    const int64_t c = cand[ci];
+    const TA* ac = A + c * ld;
+    if (tid == 0) act[0] = 0;
+#pragma unroll 1
+    for (int jh = 0; jh < NJ; jh += JC) {
+      double acc[JC];
+#pragma unroll
+      for (int j = 0; j < JC; ++j) acc[j] = 0.0;
+      const double* xr = Xp + size_t(jh) * ld;
+#pragma unroll 2
+      for (int r = tid; r < ld; r += 256) {
+        const double av = static_cast<double>(ac[r]);
+#pragma unroll
+        for (int j = 0; j < JC; ++j) acc[j] = fma(av, xr[size_t(j) * ld + r], acc[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < JC; ++j) {
+        const double v = warp_sum(acc[j]);
+        if (lane == 0) wsum[warp][j] = v;
+      }
+      __syncthreads();
+      if (tid < JC && jh + tid < m) {
+        const int jj = jh + tid;
+        double cj = wsum[0][tid];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) cj += wsum[w][tid];
+        const double sj = smu[jj] * cj;
+        const double w = threshold_weight(sj, sgam[jj], penalty);
+        f_acc += objective_term(sj, sgam[jj], penalty);
+        if (w != 0.0) {
+          nnz_acc += 1.0;
+          act[0] = 1;  // benign: every writer stores 1
+        }
+        Wp[size_t(jj) * n + c] = w;
+      }
+      __syncthreads();
+    }
+    if (tid == 0) publish(c, act[0] != 0);
+    __syncthreads();
+  };
+
+  int pending = 0;  // candidates in cand[0 .. pending) (block-uniform)
   for (int64_t kb = 0; int64_t(blockIdx.x) + kb * G < items; kb += 256) {
     // my items kb .. kb + 255 (item = blockIdx.x + k G): keep the flagged ones
     const int64_t it = int64_t(blockIdx.x) + (kb + tid) * G;
@@ -751,7 +875,7 @@ __global__ void __launch_bounds__(256, 2) tc_refine_kernel(const TA* __restrict_
     if (it < items) {
       const uint4 f = *reinterpret_cast<const uint4*>(tflag + it * 16);
       ne = (f.x | f.y | f.z | f.w) != 0u;
-      if (!ne) item_act[it] = 0;
+      item_act[it] = 0;  // set to 1 when one of its candidates turns out active
     }
     int pos;
     const int nitems = compact(ne, pos);
@@ -762,133 +886,25 @@ __global__ void __launch_bounds__(256, 2) tc_refine_kernel(const TA* __restrict_
       const int64_t col = item * kTcRefItem + tid;
       const bool flag = col < n && (colmask[col] | colmask[n + col]);
       const int total = compact(flag, pos);
-      if (flag) cand[pos] = col;
-      if (tid == 0) item_any = 0;
+      if (flag) cand[pending + pos] = col;
+      pending += total;
       __syncthreads();
-      if (total <= kTcRefSmallMax) {
-        // ---- few candidates: the whole CTA on one column at a time, threads
-        // over rows (X straight from L2, no barriers in the row loop), then a
-        // fixed-order reduction over the 8 warps
-        for (int ci = 0; ci < total; ++ci) {
-          const int64_t c = cand[ci];
-          const TA* ac = A + c * ld;
-          if (tid == 0) colany[0] = 0;
-          constexpr int JC = NJ < 32 ? NJ : 32;  // components per pass (register budget)
-#pragma unroll 1
-          for (int jh = 0; jh < NJ; jh += JC) {
-            double acc[JC];
-#pragma unroll
-            for (int j = 0; j < JC; ++j) acc[j] = 0.0;
-            const double* xr = Xp + size_t(jh) * ld;
-#pragma unroll 2
-            for (int r = tid; r < ld; r += 256) {
-              const double av = static_cast<double>(ac[r]);
-#pragma unroll
-              for (int j = 0; j < JC; ++j) acc[j] = fma(av, xr[size_t(j) * ld + r], acc[j]);
-            }
-#pragma unroll
-            for (int j = 0; j < JC; ++j) {
-              const double v = warp_sum(acc[j]);
-              if (lane == 0) wsum[warp][j] = v;
-            }
-            __syncthreads();
-            if (tid < JC && jh + tid < m) {
-              const int jj = jh + tid;
-              double cj = wsum[0][tid];
-#pragma unroll
-              for (int w = 1; w < 8; ++w) cj += wsum[w][tid];
-              const double sj = smu[jj] * cj;
-              const double w = threshold_weight(sj, sgam[jj], penalty);
-              f_acc += objective_term(sj, sgam[jj], penalty);
-              if (w != 0.0) {
-                nnz_acc += 1.0;
-                colany[0] = 1;  // benign: every writer stores 1
-              }
-              Wp[size_t(jj) * n + c] = w;
-            }
-            __syncthreads();
-          }
-          if (tid == 0) {
-            colmask[c] = colany[0];
-            colmask[n + c] = 0;
-            if (colany[0]) item_any = 1;
-          }
-        }
-      } else {
-        // ---- batches of 64 through shared memory
-        if (tid < kTcRefBatch) act[tid] = 0;
+      if (pending >= kTcRefBatch) {
+        const int full = pending / kTcRefBatch * kTcRefBatch;
+        for (int b0 = 0; b0 < full; b0 += kTcRefBatch) batch(b0, kTcRefBatch);
+        // move the remainder (< 64) to the front
+        const int64_t keep = tid < pending - full ? cand[full + tid] : 0;
         __syncthreads();
-        for (int b0 = 0; b0 < total; b0 += kTcRefBatch) {
-          const int nb = min(kTcRefBatch, total - b0);
-          const bool two = nb > 32;  // warp-uniform: second column slot in use
-          double acc[2][JPT];
-#pragma unroll
-          for (int i = 0; i < 2; ++i)
-#pragma unroll
-            for (int u = 0; u < JPT; ++u) acc[i][u] = 0.0;
-          for (int r0 = 0; r0 < ld; r0 += kTcRefRows) {
-            // stage A: warp w loads batch columns 8w .. 8w + 7, lane = row
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-              const int bc = warp * 8 + c;
-              sA[lane][bc] = bc < nb ? A[cand[b0 + bc] * ld + r0 + lane] : TA(0);
-            }
-            // stage X rows r0 .. r0 + 31 of components 0 .. NJ - 1
-            for (int e = tid; e < kTcRefRows * NJ; e += 256) {
-              const int j = e >> 5, r = e & 31;
-              sX[r][j] = Xp[size_t(j) * ld + r0 + r];
-            }
-            __syncthreads();
-#pragma unroll 8
-            for (int r = 0; r < kTcRefRows; ++r) {
-              const double a0 = static_cast<double>(sA[r][lane]);
-#pragma unroll
-              for (int u = 0; u < JPT; ++u) acc[0][u] = fma(a0, sX[r][warp * JPT + u], acc[0][u]);
-              if (two) {
-                const double a1 = static_cast<double>(sA[r][lane + 32]);
-#pragma unroll
-                for (int u = 0; u < JPT; ++u) acc[1][u] = fma(a1, sX[r][warp * JPT + u], acc[1][u]);
-              }
-            }
-            __syncthreads();
-          }
-#pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            const int bc = lane + 32 * i;
-            if (bc < nb) {
-              const int64_t c = cand[b0 + bc];
-              bool any = false;
-#pragma unroll
-              for (int u = 0; u < JPT; ++u) {
-                const int j = warp * JPT + u;
-                if (j < m) {
-                  const double sj = smu[j] * acc[i][u];
-                  const double w = threshold_weight(sj, sgam[j], penalty);
-                  f_acc += objective_term(sj, sgam[j], penalty);
-                  if (w != 0.0) {
-                    nnz_acc += 1.0;
-                    any = true;
-                  }
-                  Wp[size_t(j) * n + c] = w;
-                }
-              }
-              if (any) act[bc] = 1;  // benign: every writer stores 1
-            }
-          }
-          __syncthreads();
-          if (tid < nb) {
-            const int64_t c = cand[b0 + tid];
-            colmask[c] = act[tid];
-            colmask[n + c] = 0;
-            if (act[tid]) item_any = 1;
-            act[tid] = 0;
-          }
-          __syncthreads();
-        }
+        if (tid < pending - full) cand[tid] = keep;
+        pending -= full;
+        __syncthreads();
       }
-      __syncthreads();
-      if (tid == 0) item_act[item] = item_any ? 1 : 0;
     }
+  }
+  if (pending > kTcRefSmallMax) {
+    batch(0, pending);
+  } else {
+    for (int ci = 0; ci < pending; ++ci) single(ci);
   }
   f_acc = warp_sum(f_acc);
   nnz_acc = warp_sum(nnz_acc);

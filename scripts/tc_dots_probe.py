@@ -1,5 +1,6 @@
-"""Time the tensor-core block sweep (tc_split_x + tc_dots [+ update] + reduce)
-at the C4 shape under GPSPCA_TC_PROBE variants (timing experiments only)."""
+"""Time the tensor-core block sweep (tc_split_x + tc_dots + tc_refine +
+tc_update + reduce) at the C4 shape (TC_P / TC_N / TC_M override it) under
+GPSPCA_TC_PROBE variants (timing experiments only)."""
 import os
 import subprocess
 import sys
@@ -15,7 +16,7 @@ import torch
 import paper_1312_6182_b200 as gps
 from paper_1312_6182_b200 import _native
 from paper_1312_6182_b200.block import BlockLoop, _top_m_columns
-p, n, m = 8192, int(os.environ.get('TC_N', 1 << 20)), int(os.environ.get('TC_M', 64))
+p, n, m = int(os.environ.get('TC_P', 8192)), int(os.environ.get('TC_N', 1 << 20)), int(os.environ.get('TC_M', 64))
 g = torch.Generator(device='cuda'); g.manual_seed(4)
 At = torch.randn((n, p), generator=g, device='cuda', dtype=torch.float32)
 A = gps.DataMatrix.from_device(At.data_ptr(), p, n, owner=At)
@@ -44,7 +45,7 @@ if int(os.environ.get('GPSPCA_TC_PROBE', '0')) & 64:
              9: 'conv tmem st', 10: 'conv role total', 11: 'epi wait tfull', 12: 'epi drain', 13: 'epi role total'}
     for k, nm in names.items():
         print(f"  {nm:22s} {v[k] / chunks:8.1f} clk/chunk")
-print(f"probe={os.environ.get('GPSPCA_TC_PROBE','0'):>3} n={n} m={m}: sweep {t*1e3:.3f} ms  A-stream {p*n*4/t/1e9:.0f} GB/s")
+print(f"probe={os.environ.get('GPSPCA_TC_PROBE','0'):>3} p={p} n={n} m={m}: sweep {t*1e3:.3f} ms  A-stream {p*n*4/t/1e9:.0f} GB/s")
 """ % ROOT
 
 if os.environ.get("TC_INLINE"):
