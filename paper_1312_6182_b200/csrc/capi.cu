@@ -1394,17 +1394,26 @@ int bk_enqueue_tc(gps_bk* s, bool with_ctl) {
 #undef GPS_REFINE
     ctx->launches++;
   }
-  dim3 g2(s->tc_gx, static_cast<unsigned>((A->ld + kTcUpdRows - 1) / kTcUpdRows),
-          static_cast<unsigned>((s->m + kTcUpdComps - 1) / kTcUpdComps));
   if (!(a.probe & 16)) {
-    if (f64)
-      tc_update_kernel<double><<<g2, 256, 0, ctx->stream>>>(static_cast<const double*>(A->d), A->n, ld, s->m,
-                                                            s->colmask, s->item_act, s->W, int64_t(s->m_pad()) * A->n, np,
-                                                            s->part_g, ctl);
-    else
-      tc_update_kernel<float><<<g2, 256, 0, ctx->stream>>>(static_cast<const float*>(A->d), A->n, ld, s->m,
-                                                           s->colmask, s->item_act, s->W, int64_t(s->m_pad()) * A->n, np,
-                                                           s->part_g, ctl);
+    const int64_t wst = int64_t(s->m_pad()) * A->n;
+#define GPS_UPDATE(TA, J)                                                                                     \
+  tc_update_kernel<TA, J><<<dim3(s->tc_gx, static_cast<unsigned>(ceil_div(A->ld, tc_upd_rows<J>()))), 256, 0, \
+                            ctx->stream>>>(static_cast<const TA*>(A->d), A->n, ld, s->m, s->colmask, s->item_act,  \
+                                           s->W, wst, np, s->part_g, ctl)
+#define GPS_UPDATE_J(TA)               \
+  switch (np / 8) {                    \
+    case 2: GPS_UPDATE(TA, 2); break;  \
+    case 4: GPS_UPDATE(TA, 4); break;  \
+    case 6: GPS_UPDATE(TA, 6); break;  \
+    default: GPS_UPDATE(TA, 8); break; \
+  }
+    if (f64) {
+      GPS_UPDATE_J(double)
+    } else {
+      GPS_UPDATE_J(float)
+    }
+#undef GPS_UPDATE_J
+#undef GPS_UPDATE
     ctx->launches++;
   }
   GPS_CHECK_LAUNCH("tensor-core block sweep launch");

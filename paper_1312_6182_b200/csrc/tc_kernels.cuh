@@ -922,42 +922,53 @@ __global__ void __launch_bounds__(256, 2) tc_refine_kernel(const TA* __restrict_
   }
 }
 
-// T2: sparse rank-m update on the ACTIVE columns (colmask), fp64.
-// grid (GX, ceil(ld / 1024), ceil(m / 8)); CTA (b, y, z) owns the
-// 512-column blocks [b B / GX, (b+1) B / GX) (B = ceil(n / 512), two T1x
-// items each), rows [y*1024, +1024) and components [8z, 8z+8) of part_g[b]
-// ([m_pad][ld]).  Blocks without an active item (item_act, from T1x) are
-// skipped 256 at a time; the active columns of consecutive blocks are
-// compacted in column order into a list of up to 512 entries whose weights
-// are staged in shared memory before the FMA pass (one pass per full list,
-// so the per-block cost is one compaction, not one latency-bound pass).
-constexpr int kTcUpdRows = 1024;
-constexpr int kTcUpdComps = 8;
+// T2: sparse rank-m update on the ACTIVE columns (colmask), fp64:
+// G_partial[b] = sum over active i in range b of a_i w_i' -- a DGEMM-shaped
+// product A_act W_act with A_act's columns gathered on the fly.
+// grid (GX, ceil(ld / R)); CTA (b, y) owns the 512-column blocks
+// [b B / GX, (b+1) B / GX) (B = ceil(n / 512), two T1x items each), rows
+// [y R, y R + R) and all components.  Warp w owns components
+// [w JPT, w JPT + JPT), lane l rows y R + l + 32 t (t < TR = 32 / JPT), so a
+// thread keeps TR x JPT accumulators and R = 32 TR.  Blocks without an active
+// item (item_act, from T1x) are skipped 256 at a time; the active columns of
+// consecutive blocks are compacted in column order into a list of up to 512,
+// which is then consumed K (8, or 4 when R = 512) columns at a time: the A
+// tile (R rows x K columns) and the W tile (K x m_pad) are staged in shared memory, the next
+// tile's loads are issued before the current tile's FMAs (one barrier per
+// tile), and every A element is read once per CTA.  Sums run in column
+// order: deterministic run to run.
 constexpr int kTcUpdBlock = 512;
-template <typename TA>
+template <int JPT>
+__host__ __device__ constexpr int tc_upd_rows() { return 32 * (32 / JPT); }
+template <typename TA, int JPT>
 __global__ void __launch_bounds__(256) tc_update_kernel(const TA* __restrict__ A, int64_t n, int ld, int m,
                                                         const unsigned char* __restrict__ colmask,
                                                         const unsigned char* __restrict__ item_act,
                                                         const double* __restrict__ W, int64_t w_par_stride,
                                                         int m_pad, double* __restrict__ part_g, const GpsCtl* ctl) {
-  constexpr int RPT = kTcUpdRows / 256;
+  constexpr int TR = 32 / JPT;          // rows per lane
+  constexpr int R = 32 * TR;            // rows per CTA
+  constexpr int NJ = 8 * JPT;           // components (= m_pad)
+  constexpr int K = R > 256 ? 4 : 8;    // list columns per staged tile (shared memory <= 48 KB)
+  constexpr int AL = R * K / 256;       // A tile elements loaded per thread
+  constexpr int WL = (K * NJ + 255) / 256;
   if (ctl != nullptr && ctl->done) return;
   const int parity = ctl != nullptr ? (ctl->iter & 1) : 0;
   const double* Wp = W + parity * w_par_stride;
   const int64_t nblk = (n + kTcUpdBlock - 1) / kTcUpdBlock;
   const int64_t b0 = nblk * blockIdx.x / gridDim.x, b1 = nblk * (blockIdx.x + 1) / gridDim.x;
-  const int r0 = blockIdx.y * kTcUpdRows;
-  const int j0 = blockIdx.z * kTcUpdComps;
+  const int r0 = blockIdx.y * R;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  double g[kTcUpdComps][RPT];
+  double g[TR][JPT];
 #pragma unroll
-  for (int j = 0; j < kTcUpdComps; ++j)
+  for (int t = 0; t < TR; ++t)
 #pragma unroll
-    for (int k = 0; k < RPT; ++k) g[j][k] = 0.0;
+    for (int u = 0; u < JPT; ++u) g[t][u] = 0.0;
   __shared__ int blist[256];
   __shared__ int wcnt[8];
   __shared__ int64_t alist[kTcUpdBlock];
-  __shared__ double wv[kTcUpdBlock][kTcUpdComps];
+  __shared__ double sA[2][K][R];
+  __shared__ double sW[2][K][NJ];
   int acc = 0;  // entries in alist (block-uniform)
 
   // block-wide exclusive scan of a per-thread count (fixed order)
@@ -980,24 +991,52 @@ __global__ void __launch_bounds__(256) tc_update_kernel(const TA* __restrict__ A
     }
     return off + x - v;
   };
-  auto flush = [&]() {
-    for (int e = tid; e < acc * kTcUpdComps; e += 256) {
-      const int k = e / kTcUpdComps, j = e % kTcUpdComps;
-      wv[k][j] = (j0 + j < m) ? Wp[size_t(j0 + j) * n + alist[k]] : 0.0;
+  // A tile element e: list column e / R, row e % R; W tile element e: column
+  // e / NJ, component e % NJ (zero past the list or past m)
+  double ra[AL], rw[WL];
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int i = 0; i < AL; ++i) {
+      const int e = tid + 256 * i, kk = e / R, r = r0 + e % R;
+      ra[i] = (k0 + kk < acc && r < ld) ? static_cast<double>(A[alist[k0 + kk] * ld + r]) : 0.0;
     }
-    __syncthreads();
-#pragma unroll 4
-    for (int k = 0; k < acc; ++k) {
-      const TA* ac = A + alist[k] * ld;
 #pragma unroll
-      for (int kk = 0; kk < RPT; ++kk) {
-        const int r = r0 + kk * 256 + tid;
-        const double v = r < ld ? static_cast<double>(ac[r]) : 0.0;
+    for (int i = 0; i < WL; ++i) {
+      const int e = tid + 256 * i, kk = e / NJ, j = e % NJ;
+      rw[i] = (e < K * NJ && k0 + kk < acc && j < m) ? Wp[size_t(j) * n + alist[k0 + kk]] : 0.0;
+    }
+  };
+  auto flush = [&]() {
+    if (acc == 0) return;
+    load(0);
+    int buf = 0;
+    for (int k0 = 0; k0 < acc; k0 += K, buf ^= 1) {
 #pragma unroll
-        for (int j = 0; j < kTcUpdComps; ++j) g[j][kk] = fma(wv[k][j], v, g[j][kk]);
+      for (int i = 0; i < AL; ++i) {
+        const int e = tid + 256 * i;
+        sA[buf][e / R][e % R] = ra[i];
+      }
+#pragma unroll
+      for (int i = 0; i < WL; ++i) {
+        const int e = tid + 256 * i;
+        if (e < K * NJ) sW[buf][e / NJ][e % NJ] = rw[i];
+      }
+      __syncthreads();
+      if (k0 + K < acc) load(k0 + K);
+#pragma unroll
+      for (int kk = 0; kk < K; ++kk) {
+        double wv[JPT];
+#pragma unroll
+        for (int u = 0; u < JPT; ++u) wv[u] = sW[buf][kk][warp * JPT + u];
+#pragma unroll
+        for (int t = 0; t < TR; ++t) {
+          const double v = sA[buf][kk][lane + 32 * t];
+#pragma unroll
+          for (int u = 0; u < JPT; ++u) g[t][u] = fma(wv[u], v, g[t][u]);
+        }
       }
     }
-    __syncthreads();
+    __syncthreads();  // tiles and alist consumed
     acc = 0;
   };
 
@@ -1027,12 +1066,11 @@ __global__ void __launch_bounds__(256) tc_update_kernel(const TA* __restrict__ A
   flush();
   double* pg = part_g + size_t(blockIdx.x) * m_pad * ld;
 #pragma unroll
-  for (int k = 0; k < RPT; ++k) {
-    const int r = r0 + k * 256 + tid;
+  for (int t = 0; t < TR; ++t) {
+    const int r = r0 + lane + 32 * t;
     if (r < ld)
 #pragma unroll
-      for (int j = 0; j < kTcUpdComps; ++j)
-        if (j0 + j < m_pad) pg[size_t(j0 + j) * ld + r] = g[j][k];
+      for (int u = 0; u < JPT; ++u) pg[size_t(warp * JPT + u) * ld + r] = g[t][u];
   }
 }
 
