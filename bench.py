@@ -270,12 +270,19 @@ def run_ours(args):
     ctx.set_stream(stream.cuda_stream)
     total = args.warmup + args.steps
     loop = gps.single_unit.PowerLoop(A, "l0", gamma, 0.0, total + 1)
-    exch = None
+    exch = px = None
     if world > 1:
         cnt = _native.C.c_int64()
         _native.check(_native.lib().gps_su_exchange(loop.handle, None, _native.C.byref(cnt)))
         exch = torch.zeros(cnt.value, dtype=torch.float64, device=dev)
         _native.check(_native.lib().gps_su_set_exchange(loop.handle, _native.C.c_void_p(exch.data_ptr())))
+        # the per-iteration exchange: one peer-memory all-reduce kernel per
+        # rank over NVLink when every rank has its own peer-capable GPU, else
+        # the torch.distributed all-reduce (gloo emulation on one GPU, NCCL)
+        from paper_1312_6182_b200.distributed import PeerExchange, peer_exchange_available
+
+        px = PeerExchange(ctx, comm, exch.numel()) if peer_exchange_available(comm, dev) else None
+        exchange = px.all_reduce if px is not None else comm.all_reduce_sum
     loop.start(x0)
     L = _native.lib()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -288,7 +295,7 @@ def run_ours(args):
             ev[i][1].record(stream)
         _native.check(L.gps_su_enqueue(loop.handle, 2))
         if exch is not None:
-            comm.all_reduce_sum(exch)
+            exchange(exch)
         _native.check(L.gps_su_enqueue(loop.handle, 4))
 
     for _ in range(args.warmup):
@@ -391,6 +398,9 @@ def run_ours(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": WORKLOAD, "p": p, "n": n, "storage": "f32 (A), f64 accumulate",
                        "penalty": "l0", "gamma": gamma, "parallelism": f"column-shard x{world}",
+                       "exchange": ("none" if world == 1 else
+                                    "peer-memory all-reduce kernel (gps_px)" if px is not None else
+                                    f"torch.distributed all_reduce ({backend})"),
                        "l2": "no flush: A (16 GiB) >> L2 (126 MB)"},
             "a_stream_gbs": stream_gbs,
             "a_stream_frac_of_8tbs": stream_gbs / world / 8000.0,

@@ -183,6 +183,30 @@ int gps_bk_sweep(gps_matrix* A, const double* X, int m, const double* gamma, con
 /* block.py:135-149 polar_projection on the device: X = G (G'G)^{-1/2};
  * GPS_E_RANK (rank in *rank_out) when rank(G) < m by the reference rule. */
 int gps_polar(gps_ctx* ctx, const double* G, int64_t p, int m, double* X_out, int* rank_out);
+
+/* ---- peer-memory all-reduce of the sharded loops ------------------------
+ * the one exchange per power iteration of the column-sharded
+ * solves (the sum over ranks of the exchange vector, gps_su_exchange /
+ * gps_bk_exchange), done by ONE kernel per rank over NVLink peer memory (the
+ * reference has no multi-GPU path; this replaces an NCCL all-reduce).  One
+ * process per GPU: each rank creates a gps_px with the same world / count,
+ * exports its buffer with gps_px_ipc_handle (gps_px_handle_size() bytes),
+ * the caller exchanges the handles (e.g. torch.distributed.all_gather_object)
+ * and opens every peer's.  gps_px_allreduce enqueues buf (count doubles,
+ * device) <- sum over ranks in rank order (identical on every rank) on the
+ * context's stream; every rank must issue the same sequence of calls. */
+typedef struct gps_px gps_px;
+int gps_px_create(gps_ctx* ctx, int world, int rank, int64_t count, gps_px** out);
+int gps_px_handle_size(void);
+int gps_px_ipc_handle(gps_px* px, void* handle);
+int gps_px_open(gps_px* px, int peer, const void* handle);
+int gps_px_allreduce(gps_px* px, double* buf);
+int gps_px_destroy(gps_px* px);
+/* Test harness: `world` ranks emulated on the context's device as one
+ * cooperative kernel; per round k the rank vectors are in (world x count,
+ * rank-major) times (k + 1); out receives every round's results
+ * (rounds x world x count). */
+int gps_px_emulate(gps_ctx* ctx, int world, int64_t count, int rounds, const double* in, double* out);
 /* Device CholeskyQR2 of M (p x m): Q with positive-diagonal R (= the
  * reference's sign-fixed QR, block.py:162-170). */
 int gps_orthonormalize(gps_ctx* ctx, const double* M, int64_t p, int m, double* Q_out);

@@ -89,6 +89,13 @@ SIGNATURES = {
     "gps_matrix_center": (C.c_int, [_vp, _dp, C.POINTER(_vp)]),
     "gps_row_sqnorms": (C.c_int, [_vp, _vp, _i64, C.c_int, _vp]),
     "gps_knn_distances": (C.c_int, [_vp, _vp, _i64, _vp, _i64, C.c_int, _vp, _vp, _vp]),
+    "gps_px_create": (C.c_int, [_vp, C.c_int, C.c_int, _i64, C.POINTER(_vp)]),
+    "gps_px_handle_size": (C.c_int, []),
+    "gps_px_ipc_handle": (C.c_int, [_vp, _vp]),
+    "gps_px_open": (C.c_int, [_vp, C.c_int, _vp]),
+    "gps_px_allreduce": (C.c_int, [_vp, _vp]),
+    "gps_px_destroy": (C.c_int, [_vp]),
+    "gps_px_emulate": (C.c_int, [_vp, C.c_int, _i64, C.c_int, _dp, _dp]),
 }
 
 

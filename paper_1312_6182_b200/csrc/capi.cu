@@ -22,6 +22,7 @@
 #include "tc_kernels.cuh"
 #include "polar_kernels.cuh"
 #include "recog_kernels.cuh"
+#include "px_kernels.cuh"
 
 #include <cudaTypedefs.h>
 
@@ -89,6 +90,10 @@ struct gps_matrix {
   bool norms_valid = false;
   int nonfinite = 0;
   std::vector<double> norms;
+  // tensor-core filter operands of the block path (tc_col_exp_kernel), built
+  // on first use and kept with the matrix (A is immutable)
+  int* tc_col_exp = nullptr;
+  float* tc_col_delta = nullptr;
 };
 
 
@@ -565,6 +570,8 @@ int gps_matrix_destroy(gps_matrix* A) {
   cudaSetDevice(A->ctx->device);
   cudaStreamSynchronize(A->ctx->stream);
   if (A->owns) cudaFree(A->d);
+  if (A->tc_col_exp) cudaFree(A->tc_col_exp);
+  if (A->tc_col_delta) cudaFree(A->tc_col_delta);
   delete A;
   return GPS_OK;
 }
@@ -1217,8 +1224,8 @@ struct gps_bk {
   bool tc = false;
   int tc_grid = 0, tc_gx = 0, tc_tiles = 0;
   int tc_rings[2] = {kTcAStages, kTcXStages};  // A ring, X ring (fp64: fewer, 64 KB A stages)
-  int* col_exp = nullptr;                        // n scale exponents (tensor-core path)
-  float* col_delta = nullptr;                    // n candidate margins of T1
+  int* col_exp = nullptr;                        // n scale exponents (tensor-core path; owned by A)
+  float* col_delta = nullptr;                    // n candidate margins of T1 (owned by A)
   int tc_ref_grid = 0;                           // T1x grid (part_s_tc entries)
   __half* xhi = nullptr;  // X1 (fp16)
   __half* xlo = nullptr;  // X2 (fp16)
@@ -1568,9 +1575,7 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
   if (tc) {
     alloc((void**)&s->xhi, mp * ld * sizeof(__half));
     alloc((void**)&s->xlo, mp * ld * sizeof(__half));
-    alloc((void**)&s->col_exp, n * sizeof(int));
     alloc((void**)&s->colmask, 2 * n);
-    alloc((void**)&s->col_delta, n * sizeof(float));
     alloc((void**)&s->tflag, size_t(ceil_div(n, kTcRefItem)) * 16);
     alloc((void**)&s->item_act, size_t(ceil_div(n, kTcRefItem)));
     alloc((void**)&s->part_s_tc, size_t(s->tc_ref_grid) * 4 * sizeof(double));
@@ -1613,21 +1618,34 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
               : cudaFuncSetAttribute(tc_dots_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (ea != cudaSuccess) rc = cuda_fail(ea, "cudaFuncSetAttribute(tc_dots)");
     }
-    if (rc == GPS_OK) {
-      // per-column scale exponents: one pass over A per solver (A is constant)
-      if (f64)
-        tc_col_exp_kernel<double><<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(
-            static_cast<const double*>(A->d), A->n, static_cast<int>(A->ld), static_cast<int>(A->p), s->col_exp,
-            s->col_delta);
-      else
-        tc_col_exp_kernel<float><<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(
-            static_cast<const float*>(A->d), A->n, static_cast<int>(A->ld), static_cast<int>(A->p), s->col_exp,
-            s->col_delta);
-      ctx->launches++;
-      cudaError_t ek = cudaGetLastError();
+    if (rc == GPS_OK && A->tc_col_exp == nullptr) {
+      // per-column scale exponents and candidate margins: two passes over A,
+      // once per matrix (A is immutable), kept with it
+      cudaError_t ek = cudaMalloc((void**)&A->tc_col_exp, n * sizeof(int));
+      if (ek == cudaSuccess) ek = cudaMalloc((void**)&A->tc_col_delta, n * sizeof(float));
+      if (ek == cudaSuccess) {
+        if (f64)
+          tc_col_exp_kernel<double><<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(
+              static_cast<const double*>(A->d), A->n, static_cast<int>(A->ld), static_cast<int>(A->p), A->tc_col_exp,
+              A->tc_col_delta);
+        else
+          tc_col_exp_kernel<float><<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(
+              static_cast<const float*>(A->d), A->n, static_cast<int>(A->ld), static_cast<int>(A->p), A->tc_col_exp,
+              A->tc_col_delta);
+        ctx->launches++;
+        ek = cudaGetLastError();
+      }
       if (ek == cudaSuccess) ek = cudaStreamSynchronize(ctx->stream);
-      if (ek != cudaSuccess) rc = cuda_fail(ek, "tc_col_exp_kernel");
+      if (ek != cudaSuccess) {
+        cudaFree(A->tc_col_exp);
+        cudaFree(A->tc_col_delta);
+        A->tc_col_exp = nullptr;
+        A->tc_col_delta = nullptr;
+        rc = cuda_fail(ek, "tc_col_exp_kernel");
+      }
     }
+    s->col_exp = A->tc_col_exp;
+    s->col_delta = A->tc_col_delta;
     if (rc) {
       gps_bk_destroy(s);
       return rc;
@@ -1653,8 +1671,6 @@ int gps_bk_destroy(gps_bk* s) {
   if (s->wbuf) cudaFree(s->wbuf);
   if (s->xhi) cudaFree(s->xhi);
   if (s->xlo) cudaFree(s->xlo);
-  if (s->col_exp) cudaFree(s->col_exp);
-  if (s->col_delta) cudaFree(s->col_delta);
   if (s->tflag) cudaFree(s->tflag);
   if (s->item_act) cudaFree(s->item_act);
   if (s->colmask) cudaFree(s->colmask);
@@ -1858,6 +1874,152 @@ int gps_bk_sweep(gps_matrix* A, const double* X, int m, const double* gamma, con
   }
   gps_bk_destroy(s);
   return rc;
+}
+
+// ------------------------------------------------- peer-memory all-reduce
+
+struct gps_px {
+  gps_ctx* ctx = nullptr;
+  PxView view{};
+  void* local = nullptr;
+  void* opened[kPxMaxWorld] = {};
+};
+
+namespace {
+size_t px_bytes(int world, int64_t count, size_t* flags_off, size_t* state_off) {
+  const int nch = px_nchunks(count);
+  const size_t a = (px_slots_bytes(world, count) + 255) / 256 * 256;
+  const size_t b = (px_flags_bytes(world, nch) + 255) / 256 * 256;
+  if (flags_off) *flags_off = a;
+  if (state_off) *state_off = a + b;
+  return a + b + 256;
+}
+void px_bind(PxView& v, int q, void* base, size_t flags_off) {
+  v.slots[q] = static_cast<double*>(base);
+  v.flags[q] = reinterpret_cast<unsigned long long*>(static_cast<char*>(base) + flags_off);
+}
+}  // namespace
+
+int gps_px_create(gps_ctx* ctx, int world, int rank, int64_t count, gps_px** out) {
+  if (!ctx || !out) return fail(GPS_E_ARG, "NULL argument");
+  if (world < 1 || world > kPxMaxWorld) return fail(GPS_E_UNSUPPORTED, "world=%d outside [1, %d]", world, kPxMaxWorld);
+  if (rank < 0 || rank >= world || count < 1) return fail(GPS_E_ARG, "bad rank / count");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  size_t foff = 0, soff = 0;
+  const size_t bytes = px_bytes(world, count, &foff, &soff);
+  auto* px = new gps_px();
+  px->ctx = ctx;
+  cudaError_t e = cudaMalloc(&px->local, bytes);
+  if (e == cudaSuccess) e = cudaMemsetAsync(px->local, 0, bytes, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) {
+    if (px->local) cudaFree(px->local);
+    delete px;
+    return cuda_fail(e, "gps_px_create");
+  }
+  px->view.world = world;
+  px->view.rank = rank;
+  px->view.count = count;
+  px->view.nchunks = px_nchunks(count);
+  px->view.state = reinterpret_cast<PxState*>(static_cast<char*>(px->local) + soff);
+  px_bind(px->view, rank, px->local, foff);
+  *out = px;
+  return GPS_OK;
+}
+
+int gps_px_handle_size(void) { return static_cast<int>(sizeof(cudaIpcMemHandle_t)); }
+
+int gps_px_ipc_handle(gps_px* px, void* handle) {
+  if (!px || !handle) return fail(GPS_E_ARG, "NULL argument");
+  GPS_CUDA(cudaSetDevice(px->ctx->device));
+  cudaIpcMemHandle_t h;
+  GPS_CUDA(cudaIpcGetMemHandle(&h, px->local));
+  std::memcpy(handle, &h, sizeof(h));
+  return GPS_OK;
+}
+
+int gps_px_open(gps_px* px, int peer, const void* handle) {
+  if (!px || !handle) return fail(GPS_E_ARG, "NULL argument");
+  if (peer < 0 || peer >= px->view.world) return fail(GPS_E_ARG, "peer %d outside the world", peer);
+  if (peer == px->view.rank) return GPS_OK;
+  GPS_CUDA(cudaSetDevice(px->ctx->device));
+  if (px->opened[peer]) return fail(GPS_E_ARG, "peer %d already open", peer);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  void* base = nullptr;
+  GPS_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  size_t foff = 0;
+  px_bytes(px->view.world, px->view.count, &foff, nullptr);
+  px->opened[peer] = base;
+  px_bind(px->view, peer, base, foff);
+  return GPS_OK;
+}
+
+int gps_px_allreduce(gps_px* px, double* buf) {
+  if (!px || !buf) return fail(GPS_E_ARG, "NULL argument");
+  for (int q = 0; q < px->view.world; ++q)
+    if (!px->view.slots[q]) return fail(GPS_E_ARG, "peer %d not opened", q);
+  gps_ctx* ctx = px->ctx;
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  px_allreduce_kernel<<<px->view.nchunks, 256, 0, ctx->stream>>>(px->view, buf);
+  ctx->launches++;
+  GPS_CHECK_LAUNCH("px_allreduce_kernel launch");
+  return GPS_OK;
+}
+
+int gps_px_destroy(gps_px* px) {
+  if (!px) return GPS_OK;
+  cudaSetDevice(px->ctx->device);
+  cudaStreamSynchronize(px->ctx->stream);
+  for (int q = 0; q < kPxMaxWorld; ++q)
+    if (px->opened[q]) cudaIpcCloseMemHandle(px->opened[q]);
+  cudaFree(px->local);
+  delete px;
+  return GPS_OK;
+}
+
+int gps_px_emulate(gps_ctx* ctx, int world, int64_t count, int rounds, const double* in, double* out) {
+  if (!ctx || !in || !out) return fail(GPS_E_ARG, "NULL argument");
+  if (world < 1 || world > kPxMaxWorld || count < 1 || rounds < 1) return fail(GPS_E_ARG, "bad arguments");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  size_t foff = 0, soff = 0;
+  const size_t bytes = px_bytes(world, count, &foff, &soff);
+  const int nch = px_nchunks(count);
+  char* bufs = nullptr;
+  double* vecs = nullptr;
+  cudaError_t e = cudaMalloc(&bufs, bytes * world);
+  if (e == cudaSuccess) e = cudaMalloc(&vecs, size_t(world) * count * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemsetAsync(bufs, 0, bytes * world, ctx->stream);
+  PxEmu emu{};
+  for (int r = 0; r < world; ++r) {
+    PxView& v = emu.view[r];
+    v.world = world;
+    v.rank = r;
+    v.count = count;
+    v.nchunks = nch;
+    v.state = reinterpret_cast<PxState*>(bufs + bytes * r + soff);
+    for (int q = 0; q < world; ++q) px_bind(v, q, bufs + bytes * q, foff);
+    emu.vecs[r] = vecs + size_t(r) * count;
+  }
+  std::vector<double> scaled(size_t(world) * count);
+  for (int k = 0; k < rounds && e == cudaSuccess; ++k) {
+    for (size_t i = 0; i < scaled.size(); ++i) scaled[i] = in[i] * double(k + 1);
+    e = cudaMemcpyAsync(vecs, scaled.data(), scaled.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream);
+    void* args[] = {&emu};
+    if (e == cudaSuccess)
+      e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(px_emulate_kernel), dim3(nch, world), dim3(256),
+                                      args, 0, ctx->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(out + size_t(k) * world * count, vecs, scaled.size() * sizeof(double),
+                          cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  }
+  cudaFree(bufs);
+  cudaFree(vecs);
+  if (e != cudaSuccess) return cuda_fail(e, "gps_px_emulate");
+  return GPS_OK;
 }
 
 int gps_polar(gps_ctx* ctx, const double* G, int64_t p, int m, double* X_out, int* rank_out) {

@@ -11,11 +11,18 @@ activation limit, an all-gather of (max norm, global index) for the
 max-norm-column start plus a broadcast of the winning column, and a sum
 all-reduce of ||w||^2 for the recovery normalisation.
 
-Plumbing is torch.distributed (NCCL on GPUs over NVLink; gloo in the CPU
-tests); the arithmetic is libgpspca_b200 on each rank's device.  The loop
-driver is written against a small "shard loop" protocol so the CPU tests
-can drive it with gloo and a test-side loop.
+The per-iteration all-reduce runs on the devices as ONE libgpspca_b200
+kernel per rank over NVLink peer memory (PeerExchange, gps_px_*: every rank
+pushes its exchange vector into every peer's symmetric buffer, then sums
+the ranks' vectors in rank order) when every GPU pair has peer access;
+otherwise (or with GPSPCA_EXCHANGE=nccl) it is a torch.distributed
+all-reduce.  The per-solve collectives and the handle exchange are
+torch.distributed (NCCL on GPUs; gloo in the CPU tests).  The loop driver is
+written against a small "shard loop" protocol so the CPU tests can drive it
+with gloo and a test-side loop.
 """
+
+import os
 
 import time
 
@@ -44,6 +51,7 @@ class DeviceShardLoop:
         import torch
 
         self.A = A_local
+        self.A_context = A_local.context
         self.loop = PowerLoop(A_local, penalty, gamma, tol, max_iter)
         n_exch = _native.C.c_int64()
         _native.check(_native.lib().gps_su_exchange(self.loop.handle, None, _native.C.byref(n_exch)))
@@ -76,6 +84,68 @@ class DeviceShardLoop:
 
     def result(self):
         return self.loop.result()
+
+
+class PeerExchange:
+    """Sum all-reduce of a device float64 vector of fixed length over NVLink
+    peer memory (gps_px_*), one kernel per rank; identical result, summed in
+    rank order, on every rank.  Collective construction: every rank of the
+    group builds it with the same count."""
+
+    def __init__(self, context, comm, count):
+        import torch.distributed as dist
+
+        L = _native.lib()
+        self.count = int(count)
+        h = _native._vp()
+        _native.check(L.gps_px_create(context.handle, comm.world, comm.rank, self.count, _native.C.byref(h)),
+                      "gps_px_create")
+        self.handle = h
+        size = L.gps_px_handle_size()
+        mine = (_native.C.c_char * size)()
+        _native.check(L.gps_px_ipc_handle(h, mine), "gps_px_ipc_handle")
+        handles = [None] * comm.world
+        dist.all_gather_object(handles, bytes(mine), group=comm.group)
+        for peer, hb in enumerate(handles):
+            buf = (_native.C.c_char * size).from_buffer_copy(hb)
+            _native.check(L.gps_px_open(h, peer, buf), "gps_px_open")
+
+    def all_reduce(self, t):
+        assert t.numel() == self.count and t.dtype.is_floating_point and t.element_size() == 8
+        _native.check(_native.lib().gps_px_allreduce(self.handle, _native._vp(t.data_ptr())), "gps_px_allreduce")
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and _native._lib is not None:
+            _native.lib().gps_px_destroy(h)
+            self.handle = None
+
+
+def peer_exchange_available(comm, device):
+    """Peer-memory all-reduce applies: every rank on its OWN CUDA device (two
+    ranks spinning on one GPU could wait on each other forever), world in
+    [2, 8], every pair of those devices with peer access, and not disabled by
+    GPSPCA_EXCHANGE=nccl.  Decided identically on every rank."""
+    import torch
+
+    if os.environ.get("GPSPCA_EXCHANGE", "").lower() == "nccl" or not 2 <= comm.world <= 8:
+        return False
+    dev = device.index if isinstance(device, torch.device) and device.type == "cuda" else None
+    devs = [None] * comm.world
+    comm.dist.all_gather_object(devs, dev, group=comm.group)
+    if any(d is None for d in devs) or len(set(devs)) != comm.world:
+        return False
+    return all(torch.cuda.can_device_access_peer(a, b) for a in devs for b in devs if a != b)
+
+
+def loop_all_reduce(loop, comm, device):
+    """The per-iteration exchange of a device shard loop: PeerExchange when
+    available, else the torch.distributed all-reduce."""
+    if hasattr(loop, "A_context") and peer_exchange_available(comm, device):
+        px = PeerExchange(loop.A_context, comm, loop.exchange().numel())
+        loop.px = px  # lifetime: the loop's
+        return px.all_reduce
+    return comm.all_reduce_sum
 
 
 def run_sharded_loop(loop, all_reduce, poll_every=8, max_iter=1000):
@@ -185,7 +255,8 @@ def solve_single_unit_sharded(A_local, config, offset, n_global, comm=None, loop
     factory = loop_factory or DeviceShardLoop
     loop = factory(A_local, config.penalty, gamma, config.tol, config.max_iter)
     loop.start(x0)
-    x, history, converged, w_local = run_sharded_loop(loop, comm.all_reduce_sum, poll_every, config.max_iter)
+    x, history, converged, w_local = run_sharded_loop(loop, loop_all_reduce(loop, comm, device), poll_every,
+                                                      config.max_iter)
     s2 = comm.sum_scalar(float(w_local @ w_local), device)
     z_local = w_local / np.sqrt(s2) if s2 > 0 else w_local
     z = _gather_ragged(comm, z_local, offset, n_global, device)
@@ -218,6 +289,7 @@ class DeviceBlockShardLoop:
         import torch
 
         self.loop = BlockLoop(A_local, penalty, m, gamma, mu, tol, max_iter)
+        self.A_context = A_local.context
         n_exch = _native.C.c_int64()
         _native.check(_native.lib().gps_bk_exchange(self.loop.handle, None, _native.C.byref(n_exch)))
         dev = torch.device("cuda", A_local.context.device)
@@ -299,8 +371,8 @@ def solve_block_sharded(A_local, config, offset, n_global, comm=None, loop_facto
     factory = loop_factory or DeviceBlockShardLoop
     loop = factory(A_local, config.penalty, m, config.gamma, config.mu, config.tol, config.max_iter)
     loop.start(M, ortho)
-    X, history, converged, W_local, rank_fail, rank = run_sharded_loop(loop, comm.all_reduce_sum, poll_every,
-                                                                      config.max_iter)
+    X, history, converged, W_local, rank_fail, rank = run_sharded_loop(loop, loop_all_reduce(loop, comm, device),
+                                                                      poll_every, config.max_iter)
     if rank_fail:
         err = RankDeficiencyError(rank, m, iteration=len(history) - 1)
         err.history = history

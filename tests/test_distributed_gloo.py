@@ -285,3 +285,27 @@ def test_sharded_block_solve_matches_oracle(name):
         np.testing.assert_allclose(hist, hist_ref, rtol=1e-12, atol=1e-14)
         assert np.array_equal(Z != 0, Z_ref != 0)
         np.testing.assert_allclose(Z, Z_ref, rtol=1e-9, atol=1e-12)
+
+
+def _px_decision_worker(rank, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    try:
+        import torch
+
+        from paper_1312_6182_b200.distributed import Comm, peer_exchange_available
+
+        comm = Comm()
+        # CPU ranks, and ranks sharing one GPU index, never take the peer-memory path
+        # (spinning ranks on one device could wait on each other); all ranks agree
+        out[rank] = (peer_exchange_available(comm, "cpu"),
+                     peer_exchange_available(comm, torch.device("cpu")))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_exchange_decision_on_cpu_ranks():
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_px_decision_worker, args=(_free_port(), out), nprocs=WORLD, join=True)
+    assert all(out[r] == (False, False) for r in range(WORLD))
