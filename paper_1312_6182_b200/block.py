@@ -233,6 +233,7 @@ def solve_block(A, config, plan=DEFAULT_PLAN, poll_every=8):
         StiefelPoint(_as_stiefel_values(config.x0, p, m))  # block.py:197 + core.py:118-129
         loop.start_user(config.x0)
     X, history, converged, W = loop.run(poll_every)
+    StiefelPoint(X)  # every polar output is a StiefelPoint in the reference (block.py:149, core.py:118-129)
     loadings = SparseLoadings(_recover_block(W))
     return loadings, RunReport(
         objective_history=history,

@@ -377,6 +377,7 @@ def solve_block_sharded(A_local, config, offset, n_global, comm=None, loop_facto
         err = RankDeficiencyError(rank, m, iteration=len(history) - 1)
         err.history = history
         raise err
+    StiefelPoint(X)  # block.py:149, core.py:118-129
     s2 = comm.all_gather_vec(np.einsum("ij,ij->j", W_local, W_local), device)
     tot = np.sum(s2, axis=0)
     Z_local = np.where(tot[None, :] > 0, W_local / np.sqrt(np.where(tot > 0, tot, 1.0))[None, :], 0.0)
