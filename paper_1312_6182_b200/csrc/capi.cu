@@ -1310,7 +1310,8 @@ int bk_launch_group(gps_bk* s, int g, bool with_ctl, int write_w) {
 
 // ---- tensor-core path helpers
 int tma_encode_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dtype, uint64_t dim0, uint64_t dim1,
-                  uint64_t stride1_bytes, uint32_t box0, uint32_t box1) {
+                  uint64_t stride1_bytes, uint32_t box0, uint32_t box1,
+                  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B) {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
   std::call_once(once, [] {
@@ -1326,7 +1327,7 @@ int tma_encode_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dtype,
   const cuuint32_t box[2] = {box0, box1};
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, dtype, 2, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(GPS_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
   return GPS_OK;
@@ -1598,8 +1599,14 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
     const bool f64 = A->dtype == GPS_F64;
     const int esz = f64 ? 8 : 4;
     if (f64) s->tc_rings[0] = s->mg <= 32 ? 3 : 2;  // 64 KB A stages: fit the 227 KB of shared memory
+    CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    if (const char* pr = getenv("GPSPCA_TC_APROMO"))  // timing experiments: 0 / 64 / 128 / 256
+      promo = atoi(pr) == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+              : atoi(pr) == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+              : atoi(pr) == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
     rc = tma_encode_2d(&s->tmA, A->d, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, A->ld,
-                       A->n, A->ld * esz, kTcBoxBytes / esz, kTcTileM);
+                       A->n, A->ld * esz, kTcBoxBytes / esz, kTcTileM, promo);
     if (rc == GPS_OK)
       rc = tma_encode_2d(&s->tmXh, s->xhi, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, A->ld, mp, A->ld * 2, kTcKChunk, s->mg);
     if (rc == GPS_OK)

@@ -69,7 +69,11 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
 // so it is marked evict-first to keep partials / iterates resident.
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t pol;
+#ifdef GPS_STREAM_EVICT_NORMAL  // diagnostics build: A-stream experiments
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+#else
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#endif
   return pol;
 }
 

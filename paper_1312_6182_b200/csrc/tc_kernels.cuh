@@ -203,7 +203,8 @@ struct TcDotsArgs {
   int num_tiles;
   int a_stages, x_stages;  // ring depths (<= kTcMaxStages)
   int seg_chunks;          // chunks per TMEM accumulation segment
-  int probe;  // timing experiments: 4 no TMEM drain, 8 no X loads, 16 no update,
+  int probe;  // timing experiments: 4 no TMEM drain, 8 no X loads, 16 no update, 128 A loads with the
+              // evict_first hint,
               // 32 no TMEM stores, 64 cycle accounting
 };
 
@@ -232,6 +233,14 @@ __device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* m
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, "
       "%4}], [%2], %5;" ::"r"(smem_u32(dst)),
       "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y)
       : "memory");
 }
 
@@ -416,9 +425,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         unsigned char* st = aring + r.slot * a_bytes;
         mbar_arrive_expect_tx(&a_full[r.slot], static_cast<uint32_t>(a_bytes));
 #pragma unroll
-        for (int b = 0; b < kBoxes; ++b)
-          tma_load_2d_hint(st + b * (a_bytes / kBoxes), &tmA, kc * kTcKChunk + b * kBoxK, t * kTcTileM,
-                           &a_full[r.slot], policy);
+        for (int b = 0; b < kBoxes; ++b) {
+          // no L2 cache hint: evict_first on these 2-D boxes measured 2.5-3.5 % slower at
+          // C3 / C4 (probe 128 restores it for experiments)
+          if (a.probe & 128)
+            tma_load_2d_hint(st + b * (a_bytes / kBoxes), &tmA, kc * kTcKChunk + b * kBoxK, t * kTcTileM,
+                             &a_full[r.slot], policy);
+          else
+            tma_load_2d(st + b * (a_bytes / kBoxes), &tmA, kc * kTcKChunk + b * kBoxK, t * kTcTileM, &a_full[r.slot]);
+        }
         r.next(SA);
         if (++kc == kchunks) {
           kc = 0;
