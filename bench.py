@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--p", type=int, default=P)
     ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-block", action="store_true", help="skip the C3 / C4 block lines (N=1 only)")
     return ap.parse_args()
 
 
@@ -219,6 +220,51 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ our arm
+
+def block_configs(torch, gps, ctx, dev, iters=(10, 5)):
+    """BASELINE C3 (BL1 m = 10, 4096 x 2^21) and C4 (BL0 m = 64 with mu,
+    8192 x 2^21) on this GPU: iterations/s of the device-resident block loop
+    (tensor-core filter, fp64 recomputation, T2, polar step; tol = 0 so every
+    timed iteration is a real one), CUDA events on the loop's stream, Gaussian
+    A generated on the device (A >> L2, no flush needed)."""
+    from paper_1312_6182_b200 import _native
+    from paper_1312_6182_b200.block import BlockLoop, _top_m_columns
+
+    out = {}
+    stream = torch.cuda.Stream(dev)
+    for name, p, n, m, pen, mu, k in (("C3", 4096, 1 << 21, 10, "l1", np.ones(10), iters[0]),
+                                      ("C4", 8192, 1 << 21, 64, "l0", np.linspace(1.0, 0.5, 64), iters[1])):
+        g = torch.Generator(device=dev)
+        g.manual_seed(7)
+        At = torch.randn((n, p), generator=g, device=dev, dtype=torch.float32)
+        A = gps.DataMatrix.from_device(At.data_ptr(), p, n, owner=At, device=dev.index)
+        top = 0.1 * float(A.norms.max())
+        gamma = np.full(m, top if pen == "l1" else top * top)
+        loop = BlockLoop(A, pen, m, gamma, mu, 0.0, k + 4)
+        loop.start_columns(_top_m_columns(np.asarray(A.norms), m))
+        torch.cuda.synchronize()
+        ctx.set_stream(stream.cuda_stream)
+        L = _native.lib()
+        for _ in range(2):
+            _native.check(L.gps_bk_enqueue_sweep(loop.handle))
+            _native.check(L.gps_bk_enqueue_step(loop.handle))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k):
+            _native.check(L.gps_bk_enqueue_sweep(loop.handle))
+            _native.check(L.gps_bk_enqueue_step(loop.handle))
+        e1.record(stream)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / k
+        ctx.set_stream(None)
+        out[name] = {"workload": f"{'BL1' if pen == 'l1' else 'BL0'} m={m}{' with mu' if name == 'C4' else ''}, "
+                                 f"p={p} n=2^21 fp32, gamma=0.1*max||a_i||{'^2' if pen == 'l0' else ''}",
+                     "iters_per_s": 1e3 / ms, "ms_per_iter": ms, "a_stream_gbs": p * n * 4 / (ms / 1e3) / 1e9,
+                     "iterations_timed": k}
+        del loop, A, At
+        torch.cuda.empty_cache()
+    return out
+
 
 def run_ours(args):
     import torch
@@ -387,6 +433,10 @@ def run_ours(args):
     else:
         del At
 
+    block = None
+    if world == 1 and not args.no_block:
+        block = block_configs(torch, gps, ctx, dev)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline_entry(p, n)
@@ -413,6 +463,7 @@ def run_ours(args):
             "clocks": clocks.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "block_configs": block,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
