@@ -79,7 +79,61 @@ struct gps_ctx {
   size_t part_g_elems = 0;
   double* dvec = nullptr;  // generic device vector scratch
   size_t dvec_elems = 0;
+  // pinned control-block slots for the solvers' polls (one cudaMallocHost per
+  // context instead of one per solve); guarded by ctl_mu, not mu
+  std::mutex ctl_mu;
+  GpsCtl* ctl_pinned = nullptr;
+  std::vector<int> ctl_free;
 };
+
+namespace {
+constexpr int kCtlSlots = 256;
+// A pinned GpsCtl for a solver: a context slot, or its own allocation when
+// all slots are taken.
+cudaError_t ctl_host_acquire(gps_ctx* ctx, GpsCtl** out) {
+  {
+    std::lock_guard<std::mutex> lk(ctx->ctl_mu);
+    if (!ctx->ctl_pinned && cudaMallocHost(&ctx->ctl_pinned, kCtlSlots * sizeof(GpsCtl)) == cudaSuccess)
+      for (int i = kCtlSlots - 1; i >= 0; --i) ctx->ctl_free.push_back(i);
+    if (!ctx->ctl_free.empty()) {
+      *out = ctx->ctl_pinned + ctx->ctl_free.back();
+      ctx->ctl_free.pop_back();
+      return cudaSuccess;
+    }
+  }
+  return cudaMallocHost(out, sizeof(GpsCtl));
+}
+void ctl_host_release(gps_ctx* ctx, GpsCtl* c) {
+  if (!c) return;
+  std::lock_guard<std::mutex> lk(ctx->ctl_mu);
+  if (ctx->ctl_pinned && c >= ctx->ctl_pinned && c < ctx->ctl_pinned + kCtlSlots)
+    ctx->ctl_free.push_back(static_cast<int>(c - ctx->ctl_pinned));
+  else
+    cudaFreeHost(c);
+}
+}  // namespace
+
+// Device memory of the library's objects (matrices, solver state, scratch)
+// comes from the device's default stream-ordered pool, which keeps freed
+// blocks up to kPoolKeepBytes for reuse: a solve's setup and teardown then
+// cost no cudaMalloc / cudaFree round trips (they dominated small solves:
+// 2-25 ms create, 1-110 ms destroy).  Allocation is ordered on the legacy
+// stream and completed before return; a free first synchronizes the device
+// (as cudaFree does), so it never races a kernel on another stream.
+// (The peer-memory all-reduce keeps plain cudaMalloc: IPC needs it.)
+constexpr uint64_t kPoolKeepBytes = uint64_t(8) << 30;
+template <typename T>
+cudaError_t gps_malloc(T** p, size_t bytes) {
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(p), bytes, 0);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+  return e;
+}
+inline cudaError_t gps_free(void* p) {
+  if (!p) return cudaSuccess;
+  cudaError_t e = cudaDeviceSynchronize();  // the guarantee cudaFree gave: no kernel still uses p
+  cudaError_t f = cudaFreeAsync(p, 0);
+  return e != cudaSuccess ? e : f;
+}
 
 struct gps_matrix {
   gps_ctx* ctx = nullptr;
@@ -275,16 +329,16 @@ int launch_reduce(gps_ctx* ctx, const double* part_g, const double* part_s, int 
 int ctx_scratch(gps_ctx* ctx, int64_t ld, int64_t nvec) {
   const size_t need_g = size_t(2) * ctx->num_sms * ld;  // wide fallback grid is 2 x SMs
   if (ctx->part_g_elems < need_g) {
-    if (ctx->part_g) cudaFree(ctx->part_g);
+    if (ctx->part_g) gps_free(ctx->part_g);
     ctx->part_g = nullptr;
-    GPS_CUDA(cudaMalloc(&ctx->part_g, need_g * sizeof(double)));
+    GPS_CUDA(gps_malloc(&ctx->part_g, need_g * sizeof(double)));
     ctx->part_g_elems = need_g;
   }
-  if (!ctx->part_s) GPS_CUDA(cudaMalloc(&ctx->part_s, size_t(2) * ctx->num_sms * 4 * sizeof(double)));
+  if (!ctx->part_s) GPS_CUDA(gps_malloc(&ctx->part_s, size_t(2) * ctx->num_sms * 4 * sizeof(double)));
   if (ctx->dvec_elems < size_t(nvec)) {
-    if (ctx->dvec) cudaFree(ctx->dvec);
+    if (ctx->dvec) gps_free(ctx->dvec);
     ctx->dvec = nullptr;
-    GPS_CUDA(cudaMalloc(&ctx->dvec, size_t(nvec) * sizeof(double)));
+    GPS_CUDA(gps_malloc(&ctx->dvec, size_t(nvec) * sizeof(double)));
     ctx->dvec_elems = nvec;
   }
   return GPS_OK;
@@ -387,6 +441,11 @@ int gps_ctx_create(int device, gps_ctx** out) {
     return cuda_fail(e, "cudaStreamCreate");
   }
   ctx->own_stream = true;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = kPoolKeepBytes;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
   *out = ctx;
   return GPS_OK;
 }
@@ -395,9 +454,10 @@ int gps_ctx_destroy(gps_ctx* ctx) {
   if (!ctx) return GPS_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  if (ctx->part_g) cudaFree(ctx->part_g);
-  if (ctx->part_s) cudaFree(ctx->part_s);
-  if (ctx->dvec) cudaFree(ctx->dvec);
+  if (ctx->part_g) gps_free(ctx->part_g);
+  if (ctx->part_s) gps_free(ctx->part_s);
+  if (ctx->dvec) gps_free(ctx->dvec);
+  if (ctx->ctl_pinned) cudaFreeHost(ctx->ctl_pinned);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return GPS_OK;
@@ -442,15 +502,15 @@ static int matrix_alloc(gps_ctx* ctx, int64_t p, int64_t n, int dtype, gps_matri
   A->ld = ceil_div(p, 32) * 32;
   const size_t esz = dtype == GPS_F32 ? 4 : 8;
   const size_t bytes = size_t(A->ld) * size_t(n) * esz;
-  cudaError_t e = cudaMalloc(&A->d, bytes);
+  cudaError_t e = gps_malloc(&A->d, bytes);
   if (e != cudaSuccess) {
     delete A;
-    return cuda_fail(e, "cudaMalloc(A)");
+    return cuda_fail(e, "gps_malloc(A)");
   }
   if (A->ld != p) {
     e = cudaMemsetAsync(A->d, 0, bytes, ctx->stream);
     if (e != cudaSuccess) {
-      cudaFree(A->d);
+      gps_free(A->d);
       delete A;
       return cuda_fail(e, "cudaMemset(A)");
     }
@@ -477,7 +537,7 @@ int gps_matrix_create(gps_ctx* ctx, const void* host, int64_t p, int64_t n, int6
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
   if (e != cudaSuccess) {
-    cudaFree(A->d);
+    gps_free(A->d);
     delete A;
     return cuda_fail(e, "upload A");
   }
@@ -498,7 +558,7 @@ int gps_matrix_create_device(gps_ctx* ctx, const void* dev_src, int64_t p, int64
                                     ctx->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
   if (e != cudaSuccess) {
-    cudaFree(A->d);
+    gps_free(A->d);
     delete A;
     return cuda_fail(e, "copy A (device)");
   }
@@ -537,7 +597,7 @@ int gps_matrix_create_rowmajor(gps_ctx* ctx, const void* host, int64_t p, int64_
   int64_t rows = std::max<int64_t>(1, (int64_t(256) << 20) / (n * esz));
   rows = std::min<int64_t>(rows, p);
   void* stage = nullptr;
-  cudaError_t e = cudaMalloc(&stage, size_t(rows) * n * esz);
+  cudaError_t e = gps_malloc(&stage, size_t(rows) * n * esz);
   for (int64_t r0 = 0; e == cudaSuccess && r0 < p; r0 += rows) {
     const int64_t rb = std::min<int64_t>(rows, p - r0);
     e = cudaMemcpyAsync(stage, static_cast<const char*>(host) + size_t(r0) * n * esz, size_t(rb) * n * esz,
@@ -555,9 +615,9 @@ int gps_matrix_create_rowmajor(gps_ctx* ctx, const void* host, int64_t p, int64_
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-  if (stage) cudaFree(stage);
+  if (stage) gps_free(stage);
   if (e != cudaSuccess) {
-    cudaFree(A->d);
+    gps_free(A->d);
     delete A;
     return cuda_fail(e, "upload A (row-major)");
   }
@@ -569,9 +629,9 @@ int gps_matrix_destroy(gps_matrix* A) {
   if (!A) return GPS_OK;
   cudaSetDevice(A->ctx->device);
   cudaStreamSynchronize(A->ctx->stream);
-  if (A->owns) cudaFree(A->d);
-  if (A->tc_col_exp) cudaFree(A->tc_col_exp);
-  if (A->tc_col_delta) cudaFree(A->tc_col_delta);
+  if (A->owns) gps_free(A->d);
+  if (A->tc_col_exp) gps_free(A->tc_col_exp);
+  if (A->tc_col_delta) gps_free(A->tc_col_delta);
   delete A;
   return GPS_OK;
 }
@@ -783,7 +843,7 @@ static int rank1_copy(gps_matrix* A, const double* x, const std::vector<double>&
   rc = matrix_alloc(ctx, A->p, A->n, GPS_F64, &B);
   if (rc) return rc;
   double* dxc = nullptr;
-  cudaError_t e = cudaMalloc(&dxc, (A->ld + A->n) * sizeof(double));
+  cudaError_t e = gps_malloc(&dxc, (A->ld + A->n) * sizeof(double));
   if (e == cudaSuccess) e = cudaMemsetAsync(dxc, 0, A->ld * sizeof(double), ctx->stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(dxc, x, A->p * sizeof(double), cudaMemcpyHostToDevice, ctx->stream);
   if (e == cudaSuccess)
@@ -800,9 +860,9 @@ static int rank1_copy(gps_matrix* A, const double* x, const std::vector<double>&
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-  if (dxc) cudaFree(dxc);
+  if (dxc) gps_free(dxc);
   if (e != cudaSuccess) {
-    cudaFree(B->d);
+    gps_free(B->d);
     delete B;
     return cuda_fail(e, "gps_matrix_deflate");
   }
@@ -820,7 +880,7 @@ int gps_matrix_gather(gps_matrix* A, const int64_t* idx, int64_t k, gps_matrix**
   int rc = matrix_alloc(ctx, A->p, k, A->dtype, &B);
   if (rc) return rc;
   int64_t* didx = nullptr;
-  cudaError_t e = cudaMalloc(&didx, k * sizeof(int64_t));
+  cudaError_t e = gps_malloc(&didx, k * sizeof(int64_t));
   if (e == cudaSuccess) e = cudaMemcpyAsync(didx, idx, k * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream);
   if (e == cudaSuccess) {
     const int blocks = static_cast<int>(std::min<int64_t>(k, int64_t(ctx->num_sms) * 16));
@@ -834,9 +894,9 @@ int gps_matrix_gather(gps_matrix* A, const int64_t* idx, int64_t k, gps_matrix**
     e = cudaGetLastError();
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-  if (didx) cudaFree(didx);
+  if (didx) gps_free(didx);
   if (e != cudaSuccess) {
-    cudaFree(B->d);
+    gps_free(B->d);
     delete B;
     return cuda_fail(e, "gps_matrix_gather");
   }
@@ -869,7 +929,7 @@ int gps_su_create(gps_matrix* A, int penalty, double gamma, double tol, int max_
   s->plan = plan;
   cudaError_t e = cudaSuccess;
   auto alloc = [&](double** p, size_t elems) {
-    if (e == cudaSuccess) e = cudaMalloc(p, elems * sizeof(double));
+    if (e == cudaSuccess) e = gps_malloc(p, elems * sizeof(double));
   };
   alloc(&s->x, 2 * A->ld);
   alloc(&s->w, 2 * A->n);
@@ -878,8 +938,8 @@ int gps_su_create(gps_matrix* A, int penalty, double gamma, double tol, int max_
   alloc(&s->exch, A->ld + 4);
   alloc(&s->hist, size_t(max_iter) + 1);
   if (plan.wide) alloc(&s->wbuf, A->n);
-  if (e == cudaSuccess) e = cudaMalloc(&s->ctl, sizeof(GpsCtl));
-  if (e == cudaSuccess) e = cudaMallocHost(&s->ctl_host, sizeof(GpsCtl));
+  if (e == cudaSuccess) e = gps_malloc(&s->ctl, sizeof(GpsCtl));
+  if (e == cudaSuccess) e = ctl_host_acquire(ctx, &s->ctl_host);
   if (e == cudaSuccess) e = cudaMemsetAsync(s->x, 0, 2 * A->ld * sizeof(double), ctx->stream);
   if (e != cudaSuccess) {
     gps_su_destroy(s);
@@ -894,16 +954,16 @@ int gps_su_destroy(gps_su* s) {
   cudaSetDevice(s->ctx->device);
   cudaStreamSynchronize(s->ctx->stream);
   if (s->graph) cudaGraphExecDestroy(s->graph);
-  cudaFree(s->x);
-  cudaFree(s->w);
-  cudaFree(s->part_g);
-  cudaFree(s->part_s);
-  if (!s->exch_external) cudaFree(s->exch);
-  cudaFree(s->hist);
-  cudaFree(s->ctl);
-  if (s->defl) cudaFree(s->defl);
-  if (s->wbuf) cudaFree(s->wbuf);
-  if (s->ctl_host) cudaFreeHost(s->ctl_host);
+  gps_free(s->x);
+  gps_free(s->w);
+  gps_free(s->part_g);
+  gps_free(s->part_s);
+  if (!s->exch_external) gps_free(s->exch);
+  gps_free(s->hist);
+  gps_free(s->ctl);
+  if (s->defl) gps_free(s->defl);
+  if (s->wbuf) gps_free(s->wbuf);
+  ctl_host_release(s->ctx, s->ctl_host);
   delete s;
   return GPS_OK;
 }
@@ -954,9 +1014,9 @@ int gps_su_set_deflation(gps_su* s, const double* X, int k) {
   std::lock_guard<std::mutex> lk(ctx->mu);
   GPS_CUDA(cudaSetDevice(ctx->device));
   if (k > s->defl_cap) {
-    if (s->defl) cudaFree(s->defl);
+    if (s->defl) gps_free(s->defl);
     s->defl = nullptr;
-    GPS_CUDA(cudaMalloc(&s->defl, size_t(k) * s->A->ld * sizeof(double)));
+    GPS_CUDA(gps_malloc(&s->defl, size_t(k) * s->A->ld * sizeof(double)));
     s->defl_cap = k;
     if (s->graph) cudaGraphExecDestroy(s->graph);  // captured pointer changed
     s->graph = nullptr;
@@ -998,7 +1058,7 @@ int gps_su_enqueue(gps_su* s, int mask) {
 
 int gps_su_set_exchange(gps_su* s, void* dev_ptr) {
   if (!s || !dev_ptr) return fail(GPS_E_ARG, "NULL argument");
-  if (!s->exch_external) cudaFree(s->exch);
+  if (!s->exch_external) gps_free(s->exch);
   s->exch = static_cast<double*>(dev_ptr);
   s->exch_external = true;
   if (s->graph) cudaGraphExecDestroy(s->graph);
@@ -1518,9 +1578,19 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
   const char* no_tc = std::getenv("GPSPCA_NO_TC");
   const char* tc_min_env = std::getenv("GPSPCA_TC_MIN_M");  // tuning experiments
   const int tc_min = tc_min_env && atoi(tc_min_env) > 0 ? atoi(tc_min_env) : kTcMinM;
-  // fp32: every m (exact via T1x); fp64: m >= 2 (m = 1 keeps the CUDA-core
-  // sweep, bitwise equal to the single-unit sweep as test_block.py:115-122 asks)
-  const bool tc = m >= (A->dtype == GPS_F32 ? 1 : tc_min) && !(no_tc && no_tc[0] == '1');
+  // fp32: every m (exact via T1x).  fp64: the CUDA-core sweep is exact too
+  // and reads A ceil(m / 2) times; the tensor-core filter reads it once but
+  // adds ~60 us of fixed per-iteration work (T0, T1x, T2 launches), so it is
+  // taken when the saved reads outweigh that: (ceil(m/2) - 1) p n 8 bytes >=
+  // GPSPCA_TC_F64_MIN_BYTES (default 384 MiB, ~60 us of HBM).  m = 1 keeps
+  // the CUDA-core sweep, bitwise equal to the single-unit sweep
+  // (test_block.py:115-122).
+  bool tc = m >= (A->dtype == GPS_F32 ? 1 : tc_min) && !(no_tc && no_tc[0] == '1');
+  if (tc && A->dtype == GPS_F64) {
+    const char* mb = std::getenv("GPSPCA_TC_F64_MIN_BYTES");
+    const double min_bytes = mb ? std::strtod(mb, nullptr) : double(384ull << 20);
+    tc = double((m + 1) / 2 - 1) * double(A->p) * double(A->n) * 8.0 >= min_bytes;
+  }
   auto* s = new gps_bk();
   s->A = A;
   s->ctx = ctx;
@@ -1547,7 +1617,7 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
   }
   cudaError_t e = cudaSuccess;
   auto alloc = [&](void** p, size_t bytes) {
-    if (e == cudaSuccess) e = cudaMalloc(p, bytes);
+    if (e == cudaSuccess) e = gps_malloc(p, bytes);
   };
   const size_t ld = A->ld, n = A->n, mp = s->m_pad();
   alloc((void**)&s->X, 2 * mp * ld * sizeof(double));
@@ -1583,7 +1653,7 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
   }
   alloc((void**)&s->ctl, sizeof(GpsCtl));
   alloc((void**)&s->rank_dev, sizeof(int));
-  if (e == cudaSuccess) e = cudaMallocHost(&s->ctl_host, sizeof(GpsCtl));
+  if (e == cudaSuccess) e = ctl_host_acquire(ctx, &s->ctl_host);
   if (e == cudaSuccess) e = cudaMemsetAsync(s->X, 0, 2 * mp * ld * sizeof(double), ctx->stream);
   if (e == cudaSuccess && tc) e = cudaMemsetAsync(s->tflag, 0, size_t(ceil_div(n, kTcRefItem)) * 16, ctx->stream);
   if (e == cudaSuccess)
@@ -1628,8 +1698,8 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
     if (rc == GPS_OK && A->tc_col_exp == nullptr) {
       // per-column scale exponents and candidate margins: two passes over A,
       // once per matrix (A is immutable), kept with it
-      cudaError_t ek = cudaMalloc((void**)&A->tc_col_exp, n * sizeof(int));
-      if (ek == cudaSuccess) ek = cudaMalloc((void**)&A->tc_col_delta, n * sizeof(float));
+      cudaError_t ek = gps_malloc((void**)&A->tc_col_exp, n * sizeof(int));
+      if (ek == cudaSuccess) ek = gps_malloc((void**)&A->tc_col_delta, n * sizeof(float));
       if (ek == cudaSuccess) {
         if (f64)
           tc_col_exp_kernel<double><<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(
@@ -1644,8 +1714,8 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
       }
       if (ek == cudaSuccess) ek = cudaStreamSynchronize(ctx->stream);
       if (ek != cudaSuccess) {
-        cudaFree(A->tc_col_exp);
-        cudaFree(A->tc_col_delta);
+        gps_free(A->tc_col_exp);
+        gps_free(A->tc_col_delta);
         A->tc_col_exp = nullptr;
         A->tc_col_delta = nullptr;
         rc = cuda_fail(ek, "tc_col_exp_kernel");
@@ -1667,29 +1737,29 @@ int gps_bk_destroy(gps_bk* s) {
   cudaSetDevice(s->ctx->device);
   cudaStreamSynchronize(s->ctx->stream);
   if (s->graph) cudaGraphExecDestroy(s->graph);
-  cudaFree(s->X);
-  cudaFree(s->W);
-  cudaFree(s->part_g);
-  cudaFree(s->part_s);
-  if (!s->exch_external) cudaFree(s->exch);
-  cudaFree(s->G);
-  cudaFree(s->Tm);
-  cudaFree(s->mu_dev);
-  if (s->wbuf) cudaFree(s->wbuf);
-  if (s->xhi) cudaFree(s->xhi);
-  if (s->xlo) cudaFree(s->xlo);
-  if (s->tflag) cudaFree(s->tflag);
-  if (s->item_act) cudaFree(s->item_act);
-  if (s->colmask) cudaFree(s->colmask);
-  if (s->part_s_tc) cudaFree(s->part_s_tc);
-  if (s->pc) cudaFree(s->pc);
-  if (s->gram_part) cudaFree(s->gram_part);
-  if (s->R1) cudaFree(s->R1);
-  if (s->Sm) cudaFree(s->Sm);
-  cudaFree(s->hist);
-  cudaFree(s->ctl);
-  cudaFree(s->rank_dev);
-  if (s->ctl_host) cudaFreeHost(s->ctl_host);
+  gps_free(s->X);
+  gps_free(s->W);
+  gps_free(s->part_g);
+  gps_free(s->part_s);
+  if (!s->exch_external) gps_free(s->exch);
+  gps_free(s->G);
+  gps_free(s->Tm);
+  gps_free(s->mu_dev);
+  if (s->wbuf) gps_free(s->wbuf);
+  if (s->xhi) gps_free(s->xhi);
+  if (s->xlo) gps_free(s->xlo);
+  if (s->tflag) gps_free(s->tflag);
+  if (s->item_act) gps_free(s->item_act);
+  if (s->colmask) gps_free(s->colmask);
+  if (s->part_s_tc) gps_free(s->part_s_tc);
+  if (s->pc) gps_free(s->pc);
+  if (s->gram_part) gps_free(s->gram_part);
+  if (s->R1) gps_free(s->R1);
+  if (s->Sm) gps_free(s->Sm);
+  gps_free(s->hist);
+  gps_free(s->ctl);
+  gps_free(s->rank_dev);
+  ctl_host_release(s->ctx, s->ctl_host);
   delete s;
   return GPS_OK;
 }
@@ -1753,7 +1823,7 @@ int gps_bk_exchange(gps_bk* s, void** dev_ptr, int64_t* count) {
 
 int gps_bk_set_exchange(gps_bk* s, void* dev_ptr) {
   if (!s || !dev_ptr) return fail(GPS_E_ARG, "NULL argument");
-  if (!s->exch_external) cudaFree(s->exch);
+  if (!s->exch_external) gps_free(s->exch);
   s->exch = static_cast<double*>(dev_ptr);
   s->exch_external = true;
   if (s->graph) cudaGraphExecDestroy(s->graph);
@@ -2040,8 +2110,8 @@ int gps_polar(gps_ctx* ctx, const double* G, int64_t p, int m, double* X_out, in
   const int64_t ld = ceil_div(p, 32) * 32;
   double* buf = nullptr;
   int* rk = nullptr;
-  cudaError_t e = cudaMalloc(&buf, size_t(3) * m * ld * sizeof(double));
-  if (e == cudaSuccess) e = cudaMalloc(&rk, sizeof(int));
+  cudaError_t e = gps_malloc(&buf, size_t(3) * m * ld * sizeof(double));
+  if (e == cudaSuccess) e = gps_malloc(&rk, sizeof(int));
   if (e == cudaSuccess) e = cudaMemsetAsync(buf, 0, size_t(3) * m * ld * sizeof(double), ctx->stream);
   if (e == cudaSuccess)
     e = cudaMemcpy2DAsync(buf, ld * sizeof(double), G, p * sizeof(double), p * sizeof(double), m,
@@ -2058,8 +2128,8 @@ int gps_polar(gps_ctx* ctx, const double* G, int64_t p, int m, double* X_out, in
     e = cudaMemcpy2DAsync(X_out, p * sizeof(double), buf + m * ld, ld * sizeof(double), p * sizeof(double), m,
                           cudaMemcpyDeviceToHost, ctx->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-  cudaFree(buf);
-  cudaFree(rk);
+  gps_free(buf);
+  gps_free(rk);
   if (e != cudaSuccess) return cuda_fail(e, "gps_polar");
   if (rank_out) *rank_out = rank;
   if (rank < m) return fail(GPS_E_RANK, "gradient has numerical rank %d < %d", rank, m);
@@ -2076,8 +2146,8 @@ int gps_orthonormalize(gps_ctx* ctx, const double* M, int64_t p, int m, double* 
   const int64_t ld = ceil_div(p, 32) * 32;
   double* buf = nullptr;
   int* st = nullptr;
-  cudaError_t e = cudaMalloc(&buf, size_t(2) * m * ld * sizeof(double));
-  if (e == cudaSuccess) e = cudaMalloc(&st, sizeof(int));
+  cudaError_t e = gps_malloc(&buf, size_t(2) * m * ld * sizeof(double));
+  if (e == cudaSuccess) e = gps_malloc(&st, sizeof(int));
   if (e == cudaSuccess) e = cudaMemsetAsync(buf, 0, size_t(2) * m * ld * sizeof(double), ctx->stream);
   if (e == cudaSuccess)
     e = cudaMemcpy2DAsync(buf, ld * sizeof(double), M, p * sizeof(double), p * sizeof(double), m,
@@ -2094,8 +2164,8 @@ int gps_orthonormalize(gps_ctx* ctx, const double* M, int64_t p, int m, double* 
     e = cudaMemcpy2DAsync(Q_out, p * sizeof(double), buf + m * ld, ld * sizeof(double), p * sizeof(double), m,
                           cudaMemcpyDeviceToHost, ctx->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-  cudaFree(buf);
-  cudaFree(st);
+  gps_free(buf);
+  gps_free(st);
   if (e != cudaSuccess) return cuda_fail(e, "gps_orthonormalize");
   if (status != 0)
     return fail(GPS_E_ARG,
@@ -2120,15 +2190,15 @@ extern "C" int gps_gram_apply_block(gps_matrix* A, const double* C, int m, doubl
   double* exch = nullptr;
   unsigned char* mask = nullptr;
   auto cleanup = [&] {
-    if (dC) cudaFree(dC);
-    if (part) cudaFree(part);
-    if (exch) cudaFree(exch);
-    if (mask) cudaFree(mask);
+    if (dC) gps_free(dC);
+    if (part) gps_free(part);
+    if (exch) gps_free(exch);
+    if (mask) gps_free(mask);
   };
-  cudaError_t e = cudaMalloc(&dC, size_t(n) * m * sizeof(double));
-  if (e == cudaSuccess) e = cudaMalloc(&part, size_t(gx) * m_pad * ld * sizeof(double));
-  if (e == cudaSuccess) e = cudaMalloc(&exch, (size_t(m_pad) * ld + 4) * sizeof(double));
-  if (e == cudaSuccess) e = cudaMalloc(&mask, size_t(n));
+  cudaError_t e = gps_malloc(&dC, size_t(n) * m * sizeof(double));
+  if (e == cudaSuccess) e = gps_malloc(&part, size_t(gx) * m_pad * ld * sizeof(double));
+  if (e == cudaSuccess) e = gps_malloc(&exch, (size_t(m_pad) * ld + 4) * sizeof(double));
+  if (e == cudaSuccess) e = gps_malloc(&mask, size_t(n));
   if (e == cudaSuccess) e = cudaMemcpyAsync(dC, C, size_t(n) * m * sizeof(double), cudaMemcpyHostToDevice, ctx->stream);
   if (e != cudaSuccess) {
     cleanup();
@@ -2180,7 +2250,7 @@ extern "C" int gps_knn_distances(gps_ctx* ctx, const double* test_dev, int64_t n
   std::lock_guard<std::mutex> lk(ctx->mu);
   GPS_CUDA(cudaSetDevice(ctx->device));
   double* tt = nullptr;
-  GPS_CUDA(cudaMalloc(&tt, size_t(n_test) * sizeof(double)));
+  GPS_CUDA(gps_malloc(&tt, size_t(n_test) * sizeof(double)));
   const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(n_test, 256), int64_t(ctx->num_sms) * 8));
   row_sqnorm_kernel<<<blocks, 256, 0, ctx->stream>>>(test_dev, n_test, dim, tt);
   dim3 grid(static_cast<unsigned>(ceil_div(n_train, kKnnTileR)), static_cast<unsigned>(ceil_div(n_test, kKnnTileT)));
@@ -2193,7 +2263,7 @@ extern "C" int gps_knn_distances(gps_ctx* ctx, const double* test_dev, int64_t n
   }
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-  cudaFree(tt);
+  gps_free(tt);
   if (e != cudaSuccess) return cuda_fail(e, "gps_knn_distances");
   return GPS_OK;
 }

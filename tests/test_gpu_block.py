@@ -31,8 +31,11 @@ def random_stiefel(rng, p, m):
     return Q * np.sign(np.diagonal(R))
 
 
+@pytest.mark.parametrize("f64_path", ["cuda_core", "tc"])
 @pytest.mark.parametrize("case", BLOCK_CASES, ids=[c["name"] for c in BLOCK_CASES])
-def test_solve_block_golden_fp64(case):
+def test_solve_block_golden_fp64(case, f64_path, monkeypatch):
+    # small fp64 problems take the CUDA-core sweep by default; force each path
+    monkeypatch.setenv("GPSPCA_TC_F64_MIN_BYTES", "1e30" if f64_path == "cuda_core" else "0")
     A = gps.DataMatrix(case_matrix(case), dtype=np.float64)
     cfg = _cfg(case)
     if "rank_error" in case:

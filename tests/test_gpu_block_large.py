@@ -26,7 +26,8 @@ def _stiefel(rng, p, m):
                                         (8192, 8192, 64, "l0"), (300, 777, 24, "l1"), (4128, 3001, 10, "l1"),
                                         (10000, 2000, 5, "l0"), (33, 500, 7, "l1"), (1000, 129, 40, "l0")])
 @pytest.mark.parametrize("dtype", [np.float32, np.float64], ids=["fp32", "fp64"])
-def test_tensor_core_sweep_vs_oracle(p, n, m, pen, dtype):
+def test_tensor_core_sweep_vs_oracle(p, n, m, pen, dtype, monkeypatch):
+    monkeypatch.setenv("GPSPCA_TC_F64_MIN_BYTES", "0")  # fp64: the tensor-core path at every size
     rng = np.random.default_rng(p + m)
     A32 = rng.standard_normal((p, n)).astype(np.float32)
     A = gps.DataMatrix(A32.astype(dtype), dtype=dtype)
@@ -44,7 +45,8 @@ def test_tensor_core_sweep_vs_oracle(p, n, m, pen, dtype):
 
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64], ids=["fp32", "fp64"])
-def test_tensor_core_solve_vs_oracle(dtype):
+def test_tensor_core_solve_vs_oracle(dtype, monkeypatch):
+    monkeypatch.setenv("GPSPCA_TC_F64_MIN_BYTES", "0")
     rng = np.random.default_rng(5)
     A32 = rng.standard_normal((400, 5000)).astype(np.float32)
     A64 = A32.astype(np.float64)

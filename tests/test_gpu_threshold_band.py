@@ -36,7 +36,11 @@ def near_threshold_instance(p, n, m, gamma, mu, penalty, seed):
 @pytest.mark.parametrize("dtype", [np.float32, np.float64], ids=["fp32", "fp64"])
 @pytest.mark.parametrize("penalty", ["l1", "l0"])
 @pytest.mark.parametrize("m", [3, 10, 64])
-def test_every_column_near_threshold(dtype, penalty, m):
+@pytest.mark.parametrize("f64_path", ["tc", "cuda_core"])
+def test_every_column_near_threshold(dtype, penalty, m, f64_path, monkeypatch):
+    if dtype == np.float32 and f64_path == "cuda_core":
+        pytest.skip("fp32 storage always takes the tensor-core filter")
+    monkeypatch.setenv("GPSPCA_TC_F64_MIN_BYTES", "0" if f64_path == "tc" else "1e30")
     p, n = 512, 3000
     mu = np.linspace(1.0, 0.6, m)
     gamma = np.full(m, 2.0 if penalty == "l1" else 4.0)
