@@ -1533,8 +1533,34 @@ int bk_enqueue_step(gps_bk* s) {
 // Orthonormalise M (device, [m][ld]) into X slot 0 with CholeskyQR2.
 int bk_qr_into_x(gps_bk* s, double* Mdev) {
   gps_ctx* ctx = s->A->ctx;
+  const int ld = static_cast<int>(s->A->ld), p = static_cast<int>(s->A->p), m = s->m;
+  if (s->big_polar) {
+    // large p m: the multi-CTA CholeskyQR2 stages of the polar step, twice
+    // (Q1 = M R1^-1 into Tm, Q = Q1 R2^-1 into X slot 0; the positive
+    // diagonal of R gives the reference's sign-fixed Q, block.py:162-170).
+    // A Cholesky breakdown or kappa_F(R1) > 1e7 sqrt(m) hands over to the
+    // one-CTA kernel below, which also owns the rank-deficiency decision.
+    const PolarCtl on{1, 0, 0, 0};
+    GPS_CUDA(cudaMemcpyAsync(s->pc, &on, sizeof(PolarCtl), cudaMemcpyHostToDevice, ctx->stream));
+    const double* in = Mdev;
+    double* outs[2] = {s->Tm, s->X};
+    for (int pass = 0; pass < 2; ++pass) {
+      gram_partial_kernel<<<kGramBlocks, kGramThreads, 0, ctx->stream>>>(in, ld, p, m, s->gram_part, s->pc);
+      gram_reduce_kernel<<<(m * m + 255) / 256, 256, 0, ctx->stream>>>(s->gram_part, kGramBlocks, m * m, s->pc);
+      chol_stage_kernel<<<1, kPolarThreads, chol_smem_bytes(m), ctx->stream>>>(s->gram_part, 1, m, p, 1, s->R1,
+                                                                               s->Sm, s->pc);
+      apply_right_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(in, s->Sm, ld, m, outs[pass], s->pc, nullptr, 0);
+      in = outs[pass];
+    }
+    ctx->launches += 8;
+    GPS_CHECK_LAUNCH("CholeskyQR2 init launch");
+    PolarCtl got{};
+    GPS_CUDA(cudaMemcpyAsync(&got, s->pc, sizeof(PolarCtl), cudaMemcpyDeviceToHost, ctx->stream));
+    GPS_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (!got.fallback) return GPS_OK;
+  }
   cholqr2_kernel<<<1, kPolarThreads, size_t(2) * s->m * s->m * sizeof(double) + 64, ctx->stream>>>(
-      Mdev, s->X, static_cast<int>(s->A->ld), s->m, s->rank_dev);
+      Mdev, s->X, ld, s->m, s->rank_dev);
   ctx->launches++;
   GPS_CHECK_LAUNCH("cholqr2_kernel launch");
   int st = 0;
