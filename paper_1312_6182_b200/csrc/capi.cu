@@ -144,7 +144,7 @@ struct gps_matrix {
   bool norms_valid = false;
   int nonfinite = 0;
   std::vector<double> norms;
-  // tensor-core filter operands of the block path (tc_col_exp_kernel), built
+  // tensor-core filter operands of the block path (tc_col_delta_kernel), built
   // on first use and kept with the matrix (A is immutable)
   int* tc_col_exp = nullptr;
   float* tc_col_delta = nullptr;
@@ -674,32 +674,44 @@ int gps_matrix_column(gps_matrix* A, int64_t i, double* out) {
   return GPS_OK;
 }
 
+namespace {
+// The K0 pass (caller holds ctx->mu): column norms, the finiteness flag and
+// the tensor-core scale exponents, once per matrix.
+int matrix_norms_locked(gps_matrix* A) {
+  if (A->norms_valid) return GPS_OK;
+  gps_ctx* ctx = A->ctx;
+  int rc = ctx_scratch(ctx, A->ld, A->n + 1);
+  if (rc) return rc;
+  if (!A->tc_col_exp) GPS_CUDA(gps_malloc(&A->tc_col_exp, size_t(A->n) * sizeof(int)));
+  int* flag = reinterpret_cast<int*>(ctx->dvec + A->n);
+  GPS_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
+  const int blocks = ctx->num_sms * 8;
+  if (A->dtype == GPS_F32)
+    column_norms_kernel<float><<<blocks, 256, 0, ctx->stream>>>(static_cast<const float*>(A->d), A->n,
+                                                                static_cast<int>(A->ld), ctx->dvec, flag,
+                                                                A->tc_col_exp);
+  else
+    column_norms_kernel<double><<<blocks, 256, 0, ctx->stream>>>(static_cast<const double*>(A->d), A->n,
+                                                                 static_cast<int>(A->ld), ctx->dvec, flag,
+                                                                 A->tc_col_exp);
+  ctx->launches++;
+  GPS_CHECK_LAUNCH("column_norms_kernel launch");
+  A->norms.resize(A->n);
+  GPS_CUDA(cudaMemcpyAsync(A->norms.data(), ctx->dvec, A->n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  GPS_CUDA(cudaMemcpyAsync(&A->nonfinite, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  GPS_CUDA(cudaStreamSynchronize(ctx->stream));
+  A->norms_valid = true;
+  return GPS_OK;
+}
+}  // namespace
+
 int gps_column_norms(gps_matrix* A, double* norms_out, int* nonfinite_out) {
   if (!A) return fail(GPS_E_ARG, "matrix is NULL");
   gps_ctx* ctx = A->ctx;
   std::lock_guard<std::mutex> lk(ctx->mu);
   GPS_CUDA(cudaSetDevice(ctx->device));
-  if (!A->norms_valid) {
-    int rc = ctx_scratch(ctx, A->ld, A->n + 1);
-    if (rc) return rc;
-    int* flag = reinterpret_cast<int*>(ctx->dvec + A->n);
-    GPS_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
-    const int blocks = ctx->num_sms * 8;
-    if (A->dtype == GPS_F32)
-      column_norms_kernel<float><<<blocks, 256, 0, ctx->stream>>>(static_cast<const float*>(A->d), A->n,
-                                                                  static_cast<int>(A->ld), ctx->dvec, flag);
-    else
-      column_norms_kernel<double><<<blocks, 256, 0, ctx->stream>>>(static_cast<const double*>(A->d), A->n,
-                                                                   static_cast<int>(A->ld), ctx->dvec, flag);
-    ctx->launches++;
-    GPS_CHECK_LAUNCH("column_norms_kernel launch");
-    A->norms.resize(A->n);
-    GPS_CUDA(cudaMemcpyAsync(A->norms.data(), ctx->dvec, A->n * sizeof(double), cudaMemcpyDeviceToHost,
-                             ctx->stream));
-    GPS_CUDA(cudaMemcpyAsync(&A->nonfinite, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    GPS_CUDA(cudaStreamSynchronize(ctx->stream));
-    A->norms_valid = true;
-  }
+  int rc = matrix_norms_locked(A);
+  if (rc) return rc;
   if (norms_out) std::memcpy(norms_out, A->norms.data(), A->n * sizeof(double));
   if (nonfinite_out) *nonfinite_out = A->nonfinite;
   return GPS_OK;
@@ -1721,30 +1733,28 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
               : cudaFuncSetAttribute(tc_dots_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (ea != cudaSuccess) rc = cuda_fail(ea, "cudaFuncSetAttribute(tc_dots)");
     }
-    if (rc == GPS_OK && A->tc_col_exp == nullptr) {
-      // per-column scale exponents and candidate margins: two passes over A,
-      // once per matrix (A is immutable), kept with it
-      cudaError_t ek = gps_malloc((void**)&A->tc_col_exp, n * sizeof(int));
-      if (ek == cudaSuccess) ek = gps_malloc((void**)&A->tc_col_delta, n * sizeof(float));
-      if (ek == cudaSuccess) {
+    if (rc == GPS_OK && A->tc_col_delta == nullptr) {
+      // candidate margins: one pass over A once per matrix (the scale
+      // exponents come from the matrix's norms pass), kept with it
+      rc = matrix_norms_locked(A);
+      cudaError_t ek = rc == GPS_OK ? gps_malloc(&A->tc_col_delta, n * sizeof(float)) : cudaSuccess;
+      if (rc == GPS_OK && ek == cudaSuccess) {
         if (f64)
-          tc_col_exp_kernel<double><<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(
+          tc_col_delta_kernel<double><<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(
               static_cast<const double*>(A->d), A->n, static_cast<int>(A->ld), static_cast<int>(A->p), A->tc_col_exp,
               A->tc_col_delta);
         else
-          tc_col_exp_kernel<float><<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(
+          tc_col_delta_kernel<float><<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(
               static_cast<const float*>(A->d), A->n, static_cast<int>(A->ld), static_cast<int>(A->p), A->tc_col_exp,
               A->tc_col_delta);
         ctx->launches++;
         ek = cudaGetLastError();
+        if (ek == cudaSuccess) ek = cudaStreamSynchronize(ctx->stream);
       }
-      if (ek == cudaSuccess) ek = cudaStreamSynchronize(ctx->stream);
-      if (ek != cudaSuccess) {
-        gps_free(A->tc_col_exp);
+      if (rc == GPS_OK && ek != cudaSuccess) {
         gps_free(A->tc_col_delta);
-        A->tc_col_exp = nullptr;
         A->tc_col_delta = nullptr;
-        rc = cuda_fail(ek, "tc_col_exp_kernel");
+        rc = cuda_fail(ek, "tc_col_delta_kernel");
       }
     }
     s->col_exp = A->tc_col_exp;

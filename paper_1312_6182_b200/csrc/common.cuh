@@ -65,6 +65,10 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
   while (!mbar_try_wait(bar, parity)) __nanosleep(40);
 }
 
+// Tensor-core filter scale: column i is scaled by 2^e_i with max|a_i| 2^e_i in
+// [2^14, 2^15) (the norms pass computes e_i, tc_kernels.cuh uses it).
+constexpr int kTcAScaleExp = 14;
+
 // L2 policy: A is streamed exactly once per sweep and is far larger than L2,
 // so it is marked evict-first to keep partials / iterates resident.
 __device__ __forceinline__ uint64_t policy_evict_first() {

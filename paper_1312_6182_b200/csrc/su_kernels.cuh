@@ -520,7 +520,8 @@ __global__ void __launch_bounds__(kStepThreads) su_step_kernel(const double* exc
 // (core.py:36-47 finiteness check, core.py:243-246 norms).  Warp per column.
 template <typename TA>
 __global__ void __launch_bounds__(256) column_norms_kernel(const TA* __restrict__ A, int64_t n, int ld,
-                                                           double* __restrict__ norms, int* nonfinite) {
+                                                           double* __restrict__ norms, int* nonfinite,
+                                                           int* __restrict__ col_exp = nullptr) {
   constexpr int VN = Vec16<TA>::N;
   using V = typename Vec16<TA>::T;
   const int lane = threadIdx.x & 31;
@@ -531,6 +532,7 @@ __global__ void __launch_bounds__(256) column_norms_kernel(const TA* __restrict_
   for (int64_t col = warp; col < n; col += nwarps) {
     const V* cp = reinterpret_cast<const V*>(A + col * ld);
     double acc = 0.0;
+    float mx = 0.f;
 #pragma unroll 4
     for (int v = lane; v < nv; v += 32) {
       V q = __ldcs(cp + v);
@@ -541,10 +543,16 @@ __global__ void __launch_bounds__(256) column_norms_kernel(const TA* __restrict_
         const double d = static_cast<double>(e[u]);
         bad |= !isfinite(d);
         acc = fma(d, d, acc);
+        mx = fmaxf(mx, __double2float_ru(fabs(d)));
       }
     }
     acc = warp_sum(acc);
     if (lane == 0) norms[col] = sqrt(acc);
+    if (col_exp != nullptr) {  // the tensor-core filter's per-column scale exponent (tc_kernels.cuh)
+#pragma unroll
+      for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      if (lane == 0) col_exp[col] = mx > 0.f ? max(-126, min(126, kTcAScaleExp - ilogbf(mx))) : 0;
+    }
   }
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(nonfinite, 1);
 }

@@ -10,7 +10,7 @@
 // columns are unit vectors), x 2^14 = X1 + 2^-11 X2.  One tensor-core MMA per
 // 16 rows forms, with fp32 accumulation (kind::f16), D = [A1 X1 | A1 X2] and
 // c~_ij = 2^-(e_i + 14) (D0 + 2^-11 D1).  The rounding of A is bounded per
-// column exactly (||a_i - a1_i||, tc_col_exp_kernel), the rest of the error
+// column exactly (||a_i - a1_i||, tc_col_delta_kernel), the rest of the error
 // by 2^-17 ||a_i||; T1 flags a column when any component can
 // reach its threshold within that margin.
 //
@@ -49,7 +49,6 @@ constexpr int kTcThreads = 512;  // 16 warps
 constexpr int kTcMaxN = 64;
 constexpr int kTcMinM = 2;       // fp32 block solves with m >= 2 take this path (one A read, exact fp64 results)
 constexpr int kTcSegChunks = 2;  // TMEM accumulation segment: 2 chunks = 128 rows, drained to fp64
-constexpr int kTcAScaleExp = 14; // |a s_i| in [2^14, 2^15)
 constexpr int kTcXScaleExp = 14; // |x| <= 1 -> |x 2^14| <= 2^14
 constexpr int kTcMarginExp = 13; // candidate margin 2^-13 ||a_i|| (16x the error bound)
 
@@ -126,28 +125,23 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-// C0, once per solver: per-column scale exponents e_i = 14 - floor(log2
-// max_j |a_ji|) (0 for an all-zero column, clamped to [-126, 126]) and the
-// candidate margin of T1,
+// C0, once per matrix: the candidate margin of T1,
 //   delta_i = ||a_i - a1_i||_2 + 2^-kTcMarginExp ||a_i||_2     (rounded up)
 // where a1_i = 2^-e_i fp16(fp32(a_i 2^e_i)) is exactly the operand the tensor
-// cores see (the converters' rounding, reproduced here).  With unit x_j,
-// |a1_i'x_j - a_i'x_j| <= ||a_i - a1_i|| (Cauchy-Schwarz) and the rest of T1's
-// error (the 2-term split of X, fp32 accumulation) is < 2^-17 ||a_i||, 16x
-// inside the second term.  Warp per column.
+// cores see (the converters' rounding, reproduced here) and e_i = 14 -
+// floor(log2 max_j |a_ji|) (0 for an all-zero column, clamped to
+// [-126, 126]) comes from the matrix's norms pass (column_norms_kernel).
+// With unit x_j, |a1_i'x_j - a_i'x_j| <= ||a_i - a1_i|| (Cauchy-Schwarz) and
+// the rest of T1's error (the 2-term split of X, fp32 accumulation) is
+// < 2^-17 ||a_i||, 16x inside the second term.  Warp per column.
 template <typename TA>
-__global__ void tc_col_exp_kernel(const TA* __restrict__ A, int64_t n, int ld, int p, int* __restrict__ col_exp,
-                                  float* __restrict__ col_delta) {
+__global__ void tc_col_delta_kernel(const TA* __restrict__ A, int64_t n, int ld, int p,
+                                    const int* __restrict__ col_exp, float* __restrict__ col_delta) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
   for (int64_t col = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; col < n; col += warps) {
     const TA* a = A + col * ld;
-    float mx = 0.f;
-    for (int r = lane; r < p; r += 32) mx = fmaxf(mx, __double2float_ru(fabs(static_cast<double>(a[r]))));
-#pragma unroll
-    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    // clamped so 2^e is a normal float (only data below ~2^-112 loses range)
-    const int e = mx > 0.f ? max(-126, min(126, kTcAScaleExp - ilogbf(mx))) : 0;
+    const int e = col_exp[col];
     const float sc = __int_as_float((127 + e) << 23);
     const double unsc = ldexp(1.0, -e);
     double ss = 0.0, rr = 0.0;
@@ -161,10 +155,7 @@ __global__ void tc_col_exp_kernel(const TA* __restrict__ A, int64_t n, int ld, i
     }
     ss = warp_sum(ss);
     rr = warp_sum(rr);
-    if (lane == 0) {
-      col_exp[col] = e;
-      col_delta[col] = __double2float_ru((sqrt(rr) + ldexp(sqrt(ss), -kTcMarginExp)) * (1.0 + 0x1p-40));
-    }
+    if (lane == 0) col_delta[col] = __double2float_ru((sqrt(rr) + ldexp(sqrt(ss), -kTcMarginExp)) * (1.0 + 0x1p-40));
   }
 }
 
@@ -194,7 +185,7 @@ struct TcDotsArgs {
   const double* gamma;  // m
   const double* mu;     // m
   const int* col_exp;   // n: scale exponents of the columns
-  const float* col_delta;  // n: candidate margins (tc_col_exp_kernel)
+  const float* col_delta;  // n: candidate margins (tc_col_delta_kernel)
   double* w_out;        // [m_pad][n] parity slots (may be null): zeroed for non-candidate columns
   int64_t w_stride;
   unsigned char* colmask;  // [2][n]: 1 if column i is a candidate (one row per epilogue group)
@@ -549,7 +540,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       for (int h = 0; h < 2; ++h) {  // rows 32 h .. 32 h + 31 (one fp32 / two fp64 TMA boxes)
         uint32_t p1[16];
         // A1 = fp16(y), y = a 2^e (fp64 storage: y rounded to fp32 first);
-        // tc_col_exp_kernel reproduces exactly this rounding for the margin.
+        // tc_col_delta_kernel reproduces exactly this rounding for the margin.
         if constexpr (sizeof(TA) == 4) {
           const uint32_t row_s = smem_u32(aring + ra.slot * a_bytes + h * (a_bytes / 2) + r * 128);
 #pragma unroll
@@ -647,7 +638,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       bool cand = false;
       if (col < a.n) {
         // Candidate filter.  The exact c_ij (fp64) is within delta_i of this
-        // estimate (tc_col_exp_kernel; ||x_j|| = 1), so a column
+        // estimate (tc_col_delta_kernel; ||x_j|| = 1), so a column
         // none of whose components can reach the threshold with that margin
         // is inactive (w = 0, objective term 0) for certain; every other
         // column is recomputed exactly by T1x.
