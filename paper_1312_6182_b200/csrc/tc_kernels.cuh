@@ -42,7 +42,10 @@ constexpr int kTcTileM = 128;    // columns of A per tile (MMA M)
 constexpr int kTcKChunk = 64;    // rows of A per chunk (two 32-row fp32 TMA boxes; one 128-byte fp16 row)
 constexpr int kTcBoxBytes = 128; // inner extent of an A TMA box: 32 fp32 / 16 fp64 rows
 constexpr int kTcAStages = 5;    // default A ring depth (32 KB stages, HBM stream)
-constexpr int kTcLoStages = 2;   // TMEM A1 slots (converter output)
+#ifndef GPS_TC_LO_STAGES
+#define GPS_TC_LO_STAGES 2
+#endif
+constexpr int kTcLoStages = GPS_TC_LO_STAGES;  // TMEM A1 slots (converter output; <= 4: columns 256..511)
 constexpr int kTcXStages = 3;    // default X1 | X2 ring depth (L2-resident)
 constexpr int kTcMaxStages = 8;
 constexpr int kTcThreads = 512;  // 16 warps
