@@ -322,13 +322,16 @@ def run_ours(args):
         _native.check(_native.lib().gps_su_exchange(loop.handle, None, _native.C.byref(cnt)))
         exch = torch.zeros(cnt.value, dtype=torch.float64, device=dev)
         _native.check(_native.lib().gps_su_set_exchange(loop.handle, _native.C.c_void_p(exch.data_ptr())))
-        # the per-iteration exchange: one peer-memory all-reduce kernel per
-        # rank over NVLink when every rank has its own peer-capable GPU, else
-        # the torch.distributed all-reduce (gloo emulation on one GPU, NCCL)
+        # the per-iteration exchange: fused into the loop's K2 reduction kernel
+        # over NVLink peer memory when every rank has its own peer-capable
+        # GPU, else the torch.distributed all-reduce (gloo emulation on one
+        # GPU, NCCL)
         from paper_1312_6182_b200.distributed import PeerExchange, peer_exchange_available
 
         px = PeerExchange(ctx, comm, exch.numel()) if peer_exchange_available(comm, dev) else None
-        exchange = px.all_reduce if px is not None else comm.all_reduce_sum
+        if px is not None:
+            _native.check(_native.lib().gps_su_attach_px(loop.handle, px.handle))
+        exchange = (lambda t: None) if px is not None else comm.all_reduce_sum
     loop.start(x0)
     L = _native.lib()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -449,7 +452,7 @@ def run_ours(args):
             "config": {"workload": WORKLOAD, "p": p, "n": n, "storage": "f32 (A), f64 accumulate",
                        "penalty": "l0", "gamma": gamma, "parallelism": f"column-shard x{world}",
                        "exchange": ("none" if world == 1 else
-                                    "peer-memory all-reduce kernel (gps_px)" if px is not None else
+                                    "K2 fused with a peer-memory all-reduce (gps_px)" if px is not None else
                                     f"torch.distributed all_reduce ({backend})"),
                        "l2": "no flush: A (16 GiB) >> L2 (126 MB)"},
             "a_stream_gbs": stream_gbs,

@@ -202,11 +202,24 @@ int gps_px_ipc_handle(gps_px* px, void* handle);
 int gps_px_open(gps_px* px, int peer, const void* handle);
 int gps_px_allreduce(gps_px* px, double* buf);
 int gps_px_destroy(gps_px* px);
+/* Fuse the exchange into the loop's cross-CTA reduction (K2): with a peer
+ * exchange attached (count = gps_su_exchange's count, or ONE group's
+ * exchange vector for gps_bk: gps_bk_exchange's count / groups), the K2 kernel
+ * itself reduces this rank's partials, stores them into every rank's slots,
+ * and sums the ranks' vectors in rank order into the exchange vector -- no
+ * separate all-reduce call.  NULL detaches. */
+int gps_su_attach_px(gps_su* s, gps_px* px);
+int gps_bk_attach_px(gps_bk* s, gps_px* px);
+int gps_bk_exchange_stride(gps_bk* s, int64_t* stride); /* one group's exchange length */
 /* Test harness: `world` ranks emulated on the context's device as one
  * cooperative kernel; per round k the rank vectors are in (world x count,
  * rank-major) times (k + 1); out receives every round's results
  * (rounds x world x count). */
 int gps_px_emulate(gps_ctx* ctx, int world, int64_t count, int rounds, const double* in, double* out);
+/* Same for the fused K2: per rank, partials part_g (nparts x rows) and
+ * part_s (nparts_s x 4), rank-major; exch_out: rounds x world x (rows + 4). */
+int gps_px_emulate_reduce(gps_ctx* ctx, int world, int rows, int nparts, int nparts_s, int rounds,
+                          const double* part_g, const double* part_s, double* exch_out);
 /* Device CholeskyQR2 of M (p x m): Q with positive-diagonal R (= the
  * reference's sign-fixed QR, block.py:162-170). */
 int gps_orthonormalize(gps_ctx* ctx, const double* M, int64_t p, int m, double* Q_out);

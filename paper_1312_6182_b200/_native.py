@@ -96,6 +96,10 @@ SIGNATURES = {
     "gps_px_allreduce": (C.c_int, [_vp, _vp]),
     "gps_px_destroy": (C.c_int, [_vp]),
     "gps_px_emulate": (C.c_int, [_vp, C.c_int, _i64, C.c_int, _dp, _dp]),
+    "gps_su_attach_px": (C.c_int, [_vp, _vp]),
+    "gps_bk_attach_px": (C.c_int, [_vp, _vp]),
+    "gps_bk_exchange_stride": (C.c_int, [_vp, _i64p]),
+    "gps_px_emulate_reduce": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp, _dp]),
 }
 
 

@@ -154,6 +154,13 @@ struct gps_matrix {
 
 // ------------------------------------------------------------- dispatch
 
+struct gps_px {
+  gps_ctx* ctx = nullptr;
+  PxView view{};
+  void* local = nullptr;
+  void* opened[kPxMaxWorld] = {};
+};
+
 namespace {
 
 using SweepFn = void (*)(SweepArgs);
@@ -317,7 +324,18 @@ int launch_sweep(gps_matrix* A, const SweepPlan& plan, SweepArgs args, int mode,
 }
 
 int launch_reduce(gps_ctx* ctx, const double* part_g, const double* part_s, int nparts, int ld, double* exch,
-                  const GpsCtl* ctl, int nparts_s = -1) {
+                  const GpsCtl* ctl, int nparts_s = -1, const gps_px* px = nullptr) {
+  if (px != nullptr) {
+    // K2 fused with the peer-memory all-reduce (px_kernels.cuh)
+    if (px->view.count != int64_t(ld) + 4) return fail(GPS_E_ARG, "peer exchange sized for %lld, reduce has %d + 4",
+                                                      static_cast<long long>(px->view.count), ld);
+    su_reduce_px_kernel<<<px_uniform_chunks(ld) + 1, 256, 0, ctx->stream>>>(part_g, part_s, nparts, ld, exch, ctl,
+                                                                            nparts_s < 0 ? nparts : nparts_s,
+                                                                            px->view);
+    ctx->launches++;
+    GPS_CHECK_LAUNCH("su_reduce_px_kernel launch");
+    return GPS_OK;
+  }
   const int blocks = (ld + kReduceRows - 1) / kReduceRows + 1;
   su_reduce_kernel<<<blocks, 256, 0, ctx->stream>>>(part_g, part_s, nparts, ld, exch, ctl,
                                                     nparts_s < 0 ? nparts : nparts_s);
@@ -386,6 +404,7 @@ __global__ void gather_columns_kernel(const TA* __restrict__ A, int64_t ld, cons
 }  // namespace
 
 struct gps_su {
+  const gps_px* px = nullptr;  // peer-memory exchange fused into K2 (sharded loops)
   gps_matrix* A = nullptr;
   gps_ctx* ctx = nullptr;  // destroy must not touch A (it may already be gone)
   int penalty = 0;
@@ -1007,7 +1026,8 @@ static int su_enqueue_sweep_nolock(gps_su* s, int mask = 3) {
   if (mask & 1) rc = launch_sweep(s->A, plan, args, kFused, s->wbuf);
   if (rc) return rc;
   if (mask & 2)
-    rc = launch_reduce(s->A->ctx, s->part_g, s->part_s, plan.grid, static_cast<int>(s->A->ld), s->exch, s->ctl);
+    rc = launch_reduce(s->A->ctx, s->part_g, s->part_s, plan.grid, static_cast<int>(s->A->ld), s->exch, s->ctl, -1,
+                       s->px);
   return rc;
 }
 
@@ -1275,6 +1295,7 @@ constexpr int kMaxBlockM = 64;
 }  // namespace
 
 struct gps_bk {
+  const gps_px* px = nullptr;  // peer-memory exchange fused into K2 (sharded loops)
   gps_matrix* A = nullptr;
   gps_ctx* ctx = nullptr;  // destroy must not touch A
   int penalty = 0, m = 0, mg = 0, ngroups = 0;
@@ -1377,7 +1398,7 @@ int bk_launch_group(gps_bk* s, int g, bool with_ctl, int write_w) {
   }
   double* ex = s->exch + size_t(g) * s->exch_stride();
   return launch_reduce(A->ctx, a.part_g, a.part_s, pl.grid, pl.mg * static_cast<int>(A->ld), ex,
-                       with_ctl ? s->ctl : nullptr);
+                       with_ctl ? s->ctl : nullptr, -1, s->px);
 }
 
 // ---- tensor-core path helpers
@@ -1497,7 +1518,7 @@ int bk_enqueue_tc(gps_bk* s, bool with_ctl) {
     ctx->launches++;
   }
   GPS_CHECK_LAUNCH("tensor-core block sweep launch");
-  return launch_reduce(ctx, s->part_g, s->part_s_tc, s->tc_gx, np * ld, s->exch, ctl, s->tc_ref_grid);
+  return launch_reduce(ctx, s->part_g, s->part_s_tc, s->tc_gx, np * ld, s->exch, ctl, s->tc_ref_grid, s->px);
 }
 
 int bk_enqueue_sweeps(gps_bk* s, bool with_ctl) {
@@ -1991,13 +2012,6 @@ int gps_bk_sweep(gps_matrix* A, const double* X, int m, const double* gamma, con
 
 // ------------------------------------------------- peer-memory all-reduce
 
-struct gps_px {
-  gps_ctx* ctx = nullptr;
-  PxView view{};
-  void* local = nullptr;
-  void* opened[kPxMaxWorld] = {};
-};
-
 namespace {
 size_t px_bytes(int world, int64_t count, size_t* flags_off, size_t* state_off) {
   const int nch = px_nchunks(count);
@@ -2075,7 +2089,7 @@ int gps_px_allreduce(gps_px* px, double* buf) {
     if (!px->view.slots[q]) return fail(GPS_E_ARG, "peer %d not opened", q);
   gps_ctx* ctx = px->ctx;
   GPS_CUDA(cudaSetDevice(ctx->device));
-  px_allreduce_kernel<<<px->view.nchunks, 256, 0, ctx->stream>>>(px->view, buf);
+  px_allreduce_kernel<<<px_uniform_chunks(px->view.count), 256, 0, ctx->stream>>>(px->view, buf);
   ctx->launches++;
   GPS_CHECK_LAUNCH("px_allreduce_kernel launch");
   return GPS_OK;
@@ -2122,7 +2136,8 @@ int gps_px_emulate(gps_ctx* ctx, int world, int64_t count, int rounds, const dou
     e = cudaMemcpyAsync(vecs, scaled.data(), scaled.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream);
     void* args[] = {&emu};
     if (e == cudaSuccess)
-      e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(px_emulate_kernel), dim3(nch, world), dim3(256),
+      e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(px_emulate_kernel),
+                                      dim3(px_uniform_chunks(count), world), dim3(256),
                                       args, 0, ctx->stream);
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(out + size_t(k) * world * count, vecs, scaled.size() * sizeof(double),
@@ -2132,6 +2147,87 @@ int gps_px_emulate(gps_ctx* ctx, int world, int64_t count, int rounds, const dou
   cudaFree(bufs);
   cudaFree(vecs);
   if (e != cudaSuccess) return cuda_fail(e, "gps_px_emulate");
+  return GPS_OK;
+}
+
+int gps_su_attach_px(gps_su* s, gps_px* px) {
+  if (!s) return fail(GPS_E_ARG, "NULL argument");
+  if (px && px->view.count != s->A->ld + 4) return fail(GPS_E_ARG, "peer exchange must hold ld + 4 doubles");
+  s->px = px;
+  if (s->graph) cudaGraphExecDestroy(s->graph);
+  s->graph = nullptr;
+  return GPS_OK;
+}
+
+int gps_bk_exchange_stride(gps_bk* s, int64_t* stride) {
+  if (!s || !stride) return fail(GPS_E_ARG, "NULL argument");
+  *stride = int64_t(s->exch_stride());
+  return GPS_OK;
+}
+
+int gps_bk_attach_px(gps_bk* s, gps_px* px) {
+  if (!s) return fail(GPS_E_ARG, "NULL argument");
+  if (px && px->view.count != int64_t(s->exch_stride()))
+    return fail(GPS_E_ARG, "peer exchange must hold one group's exchange vector (%zu doubles)", s->exch_stride());
+  s->px = px;
+  if (s->graph) cudaGraphExecDestroy(s->graph);
+  s->graph = nullptr;
+  return GPS_OK;
+}
+
+int gps_px_emulate_reduce(gps_ctx* ctx, int world, int rows, int nparts, int nparts_s, int rounds,
+                          const double* part_g, const double* part_s, double* exch_out) {
+  if (!ctx || !part_g || !part_s || !exch_out) return fail(GPS_E_ARG, "NULL argument");
+  if (world < 1 || world > kPxMaxWorld || rows < 1 || nparts < 1 || nparts_s < 1 || rounds < 1)
+    return fail(GPS_E_ARG, "bad arguments");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  const int64_t count = int64_t(rows) + 4;
+  size_t foff = 0, soff = 0;
+  const size_t bytes = px_bytes(world, count, &foff, &soff);
+  const size_t ng = size_t(nparts) * rows, ns = size_t(nparts_s) * 4;
+  char* bufs = nullptr;
+  double *dg = nullptr, *ds = nullptr, *dx = nullptr;
+  cudaError_t e = cudaMalloc(&bufs, bytes * world);
+  if (e == cudaSuccess) e = cudaMalloc(&dg, ng * world * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&ds, ns * world * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&dx, size_t(count) * world * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemsetAsync(bufs, 0, bytes * world, ctx->stream);
+  PxReduceEmu emu{};
+  for (int r = 0; r < world; ++r) {
+    PxView& v = emu.view[r];
+    v.world = world;
+    v.rank = r;
+    v.count = count;
+    v.nchunks = px_nchunks(count);
+    v.state = reinterpret_cast<PxState*>(bufs + bytes * r + soff);
+    for (int q = 0; q < world; ++q) px_bind(v, q, bufs + bytes * q, foff);
+    emu.part_g[r] = dg + ng * r;
+    emu.part_s[r] = ds + ns * r;
+    emu.exch[r] = dx + size_t(count) * r;
+  }
+  std::vector<double> hg(ng * world), hs(ns * world);
+  for (int k = 0; k < rounds && e == cudaSuccess; ++k) {
+    for (size_t i = 0; i < hg.size(); ++i) hg[i] = part_g[i] * double(k + 1);
+    for (size_t i = 0; i < hs.size(); ++i) hs[i] = part_s[i] * double(k + 1);
+    e = cudaMemcpyAsync(dg, hg.data(), hg.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(ds, hs.data(), hs.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream);
+    int a_np = nparts, a_rows = rows, a_ns = nparts_s;
+    void* args[] = {&emu, &a_np, &a_rows, &a_ns};
+    if (e == cudaSuccess)
+      e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(px_reduce_emulate_kernel),
+                                      dim3(px_uniform_chunks(rows) + 1, world), dim3(256), args, 0, ctx->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(exch_out + size_t(k) * world * count, dx, size_t(count) * world * sizeof(double),
+                          cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  }
+  cudaFree(bufs);
+  cudaFree(dg);
+  cudaFree(ds);
+  cudaFree(dx);
+  if (e != cudaSuccess) return cuda_fail(e, "gps_px_emulate_reduce");
   return GPS_OK;
 }
 

@@ -24,7 +24,7 @@
 // issues only after finishing its own epoch e sums.
 #pragma once
 
-#include "common.cuh"
+#include "su_kernels.cuh"
 
 namespace gps {
 
@@ -55,7 +55,10 @@ __host__ __device__ inline size_t px_slots_bytes(int world, int64_t count) {
 __host__ __device__ inline size_t px_flags_bytes(int world, int nchunks) {
   return size_t(world) * nchunks * sizeof(unsigned long long);
 }
-__host__ __device__ inline int px_nchunks(int64_t count) { return int((count + kPxChunk - 1) / kPxChunk); }
+// flag slots per rank: the uniform chunks of px_allreduce_kernel, plus one
+// (the fused reduction's scalar chunk)
+__host__ __device__ inline int px_nchunks(int64_t count) { return int((count + kPxChunk - 1) / kPxChunk) + 1; }
+__host__ __device__ inline int px_uniform_chunks(int64_t count) { return int((count + kPxChunk - 1) / kPxChunk); }
 
 __device__ __forceinline__ void px_store_release_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -66,28 +69,26 @@ __device__ __forceinline__ unsigned long long px_load_acquire_sys(const unsigned
   return v;
 }
 
-// CTA body: chunk c of rank v.rank at epoch e; vec is the rank's local vector.
-__device__ __forceinline__ void px_chunk(const PxView& v, double* vec, int c, unsigned long long e) {
-  const int par = static_cast<int>(e & 1ull);
-  const int64_t lo = int64_t(c) * kPxChunk;
-  const int64_t hi = lo + kPxChunk < v.count ? lo + kPxChunk : v.count;
-  // 1. push the chunk to every rank (self included)
-  for (int q = 0; q < v.world; ++q) {
-    double* dst = v.slots[q] + (size_t(par) * v.world + v.rank) * v.count;
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) dst[i] = vec[i];
-  }
+// Publish chunk c of this rank's epoch-e data: fence (system scope) and
+// release-store flags[rank][c] = e at every rank.
+__device__ __forceinline__ void px_signal(const PxView& v, int c, unsigned long long e) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();
     for (int q = 0; q < v.world; ++q) px_store_release_sys(v.flags[q] + size_t(v.rank) * v.nchunks + c, e);
   }
-  // 2. wait for every rank's chunk at this rank
+}
+// Wait until every rank published chunk c at this rank, then write the
+// rank-order sum of elements [lo, hi) into vec.
+__device__ __forceinline__ void px_gather(const PxView& v, double* vec, int c, int64_t lo, int64_t hi,
+                                          unsigned long long e) {
+  const int par = static_cast<int>(e & 1ull);
   if (threadIdx.x < v.world) {
     const unsigned long long* f = v.flags[v.rank] + size_t(threadIdx.x) * v.nchunks + c;
     while (px_load_acquire_sys(f) < e) __nanosleep(64);
   }
   __syncthreads();
-  // 3. fixed rank-order sum (L2 loads: the slots are written by peers)
+  // fixed rank-order sum (L2 loads: the slots are written by peers)
   const double* own = v.slots[v.rank] + size_t(par) * v.world * v.count;
   for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
     double s = __ldcg(own + i);
@@ -95,14 +96,28 @@ __device__ __forceinline__ void px_chunk(const PxView& v, double* vec, int c, un
     vec[i] = s;
   }
 }
+// Element i of this rank's epoch-e vector into slots[e&1][rank][i] at every rank.
+__device__ __forceinline__ void px_put(const PxView& v, int64_t i, double x, unsigned long long e) {
+  const int par = static_cast<int>(e & 1ull);
+  for (int q = 0; q < v.world; ++q) v.slots[q][(size_t(par) * v.world + v.rank) * v.count + i] = x;
+}
+
+// CTA body: chunk c of rank v.rank at epoch e; vec is the rank's local vector.
+__device__ __forceinline__ void px_chunk(const PxView& v, double* vec, int c, unsigned long long e) {
+  const int64_t lo = int64_t(c) * kPxChunk;
+  const int64_t hi = lo + kPxChunk < v.count ? lo + kPxChunk : v.count;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) px_put(v, i, vec[i], e);
+  px_signal(v, c, e);
+  px_gather(v, vec, c, lo, hi, e);
+}
 
 // Epoch bookkeeping: every CTA reads the epoch before it finishes; the last
 // CTA to finish publishes it for the next launch (stream order).
-__device__ __forceinline__ void px_finish(PxState* st, int nchunks, unsigned long long e) {
+__device__ __forceinline__ void px_finish(PxState* st, unsigned long long e) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    if (atomicAdd(&st->done_ctas, 1u) == unsigned(nchunks) - 1u) {
+    if (atomicAdd(&st->done_ctas, 1u) == gridDim.x - 1u) {
       st->epoch = e;
       st->done_ctas = 0;
       __threadfence();
@@ -113,7 +128,7 @@ __device__ __forceinline__ void px_finish(PxState* st, int nchunks, unsigned lon
 __global__ void __launch_bounds__(256) px_allreduce_kernel(const PxView v, double* vec) {
   const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&v.state->epoch) + 1ull;
   px_chunk(v, vec, blockIdx.x, e);
-  px_finish(v.state, v.nchunks, e);
+  px_finish(v.state, e);
 }
 
 // Test emulation of `world` ranks on ONE device as ONE cooperative kernel
@@ -127,7 +142,82 @@ __global__ void __launch_bounds__(256) px_emulate_kernel(const PxEmu emu) {
   const PxView& v = emu.view[blockIdx.y];
   const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&v.state->epoch) + 1ull;
   px_chunk(v, emu.vecs[blockIdx.y], blockIdx.x, e);
-  px_finish(v.state, v.nchunks, e);
+  px_finish(v.state, e);
+}
+
+// ---- K2 fused with the exchange: the cross-CTA reduction of one rank's
+// sweep partials (su_reduce_kernel's rows and scalars, in the same fixed
+// order) written straight into every rank's slots, then the rank-order sum
+// into the local exchange vector -- compute and collective in one kernel.
+// Chunk c < nrc: rows [c kPxChunk, ...) of the `rows`-long partial vector,
+// 32-row sub-blocks as in su_reduce_kernel; chunk nrc: the 4 scalars at
+// offset rows.  v.count == rows + 4.
+__device__ __forceinline__ void px_reduce_chunk(const PxView& v, const double* __restrict__ part_g,
+                                                const double* __restrict__ part_s, int nparts, int rows,
+                                                int nparts_s, double* exch, int c, unsigned long long e) {
+  __shared__ double part[kReduceSlices][kReduceRows];
+  const int nrc = (rows + kPxChunk - 1) / kPxChunk;
+  if (c < nrc) {
+    const int lo = c * kPxChunk, hi = min(rows, lo + kPxChunk);
+    const int rr = threadIdx.x & (kReduceRows - 1), sl = threadIdx.x / kReduceRows;
+    const int b0 = nparts * sl / kReduceSlices, b1 = nparts * (sl + 1) / kReduceSlices;
+    for (int base = lo; base < hi; base += kReduceRows) {
+      const int r = base + rr;
+      double t = 0.0;
+      if (r < hi) {
+        const double* p = part_g + r;
+#pragma unroll 4
+        for (int b = b0; b < b1; ++b) t += p[size_t(b) * rows];
+      }
+      part[sl][rr] = t;
+      __syncthreads();
+      if (sl == 0 && r < hi) {
+        double u = part[0][rr];
+#pragma unroll
+        for (int k = 1; k < kReduceSlices; ++k) u += part[k][rr];
+        px_put(v, r, u, e);
+      }
+      __syncthreads();
+    }
+    px_signal(v, c, e);
+    px_gather(v, exch, c, lo, hi, e);
+  } else {
+    if (threadIdx.x < 128) {
+      const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      double t = 0.0;
+      for (int b = lane; b < nparts_s; b += 32) t += part_s[size_t(b) * 4 + k];
+      t = warp_sum(t);
+      if (lane == 0) px_put(v, rows + k, t, e);
+    }
+    px_signal(v, c, e);
+    px_gather(v, exch, c, rows, int64_t(rows) + 4, e);
+  }
+}
+
+__global__ void __launch_bounds__(256) su_reduce_px_kernel(const double* __restrict__ part_g,
+                                                           const double* __restrict__ part_s, int nparts, int rows,
+                                                           double* __restrict__ exch, const GpsCtl* ctl,
+                                                           int nparts_s, const PxView v) {
+  if (ctl != nullptr && ctl->done) return;  // identical on every rank (replicated step)
+  const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&v.state->epoch) + 1ull;
+  px_reduce_chunk(v, part_g, part_s, nparts, rows, nparts_s, exch, blockIdx.x, e);
+  px_finish(v.state, e);
+}
+
+// Test emulation of the fused reduction: block (c, r) runs rank r's chunk c.
+struct PxReduceEmu {
+  PxView view[kPxMaxWorld];
+  const double* part_g[kPxMaxWorld];
+  const double* part_s[kPxMaxWorld];
+  double* exch[kPxMaxWorld];
+};
+__global__ void __launch_bounds__(256) px_reduce_emulate_kernel(const PxReduceEmu emu, int nparts, int rows,
+                                                                int nparts_s) {
+  const int r = blockIdx.y;
+  const PxView& v = emu.view[r];
+  const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&v.state->epoch) + 1ull;
+  px_reduce_chunk(v, emu.part_g[r], emu.part_s[r], nparts, rows, nparts_s, emu.exch[r], blockIdx.x, e);
+  px_finish(v.state, e);
 }
 
 }  // namespace gps

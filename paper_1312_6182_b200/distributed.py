@@ -11,10 +11,11 @@ activation limit, an all-gather of (max norm, global index) for the
 max-norm-column start plus a broadcast of the winning column, and a sum
 all-reduce of ||w||^2 for the recovery normalisation.
 
-The per-iteration all-reduce runs on the devices as ONE libgpspca_b200
-kernel per rank over NVLink peer memory (PeerExchange, gps_px_*: every rank
-pushes its exchange vector into every peer's symmetric buffer, then sums
-the ranks' vectors in rank order) when every GPU pair has peer access;
+The per-iteration all-reduce runs on the devices inside the loop's own
+cross-CTA reduction kernel over NVLink peer memory (PeerExchange attached to
+the loop, gps_px_*: every rank's K2 stores its reduced exchange vector into
+every peer's symmetric buffer, then sums the ranks' vectors in rank order)
+when every GPU pair has peer access;
 otherwise (or with GPSPCA_EXCHANGE=nccl) it is a torch.distributed
 all-reduce.  The per-solve collectives and the handle exchange are
 torch.distributed (NCCL on GPUs; gloo in the CPU tests).  The loop driver is
@@ -66,6 +67,10 @@ class DeviceShardLoop:
 
     def start(self, x0):
         self.loop.start(x0)
+
+    def attach_px(self, comm):
+        self.px = PeerExchange(self.A_context, comm, self.buf.numel())  # ld + 4
+        _native.check(_native.lib().gps_su_attach_px(self.loop.handle, self.px.handle), "gps_su_attach_px")
 
     def enqueue_sweep(self):
         _native.check(_native.lib().gps_su_enqueue_sweep(self.loop.handle))
@@ -139,12 +144,14 @@ def peer_exchange_available(comm, device):
 
 
 def loop_all_reduce(loop, comm, device):
-    """The per-iteration exchange of a device shard loop: PeerExchange when
-    available, else the torch.distributed all-reduce."""
-    if hasattr(loop, "A_context") and peer_exchange_available(comm, device):
-        px = PeerExchange(loop.A_context, comm, loop.exchange().numel())
-        loop.px = px  # lifetime: the loop's
-        return px.all_reduce
+    """The per-iteration exchange of a device shard loop.  With peer access
+    between every rank's GPU, a PeerExchange is attached to the loop and the
+    loop's own cross-CTA reduction kernel (K2) performs the all-reduce --
+    compute and collective in one kernel -- so the returned callable does
+    nothing; otherwise the torch.distributed all-reduce."""
+    if hasattr(loop, "attach_px") and peer_exchange_available(comm, device):
+        loop.attach_px(comm)
+        return lambda t: None
     return comm.all_reduce_sum
 
 
@@ -303,6 +310,12 @@ class DeviceBlockShardLoop:
 
     def start(self, M, orthonormalize):
         (self.loop.start_qr if orthonormalize else self.loop.start_user)(M)
+
+    def attach_px(self, comm):
+        stride = _native.C.c_int64()
+        _native.check(_native.lib().gps_bk_exchange_stride(self.loop.handle, _native.C.byref(stride)))
+        self.px = PeerExchange(self.A_context, comm, stride.value)  # one group's exchange vector
+        _native.check(_native.lib().gps_bk_attach_px(self.loop.handle, self.px.handle), "gps_bk_attach_px")
 
     def enqueue_sweep(self):
         _native.check(_native.lib().gps_bk_enqueue_sweep(self.loop.handle))

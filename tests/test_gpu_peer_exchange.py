@@ -73,3 +73,80 @@ def test_bad_arguments():
             _native.check(_native.lib().gps_px_allreduce(h, buf.ctypes.data_as(_native._vp)))
     finally:
         _native.lib().gps_px_destroy(h)
+
+
+def k2_reference(pg, ps, rows):
+    """su_reduce_kernel's fixed order: 8 contiguous slices of the partials per
+    row summed sequentially, then the slices in order; scalars: lane-strided
+    (32 lanes) sequential sums combined by the xor butterfly."""
+    nparts = pg.shape[0]
+    out = np.empty(rows + 4)
+    slices = []
+    for sl in range(8):
+        b0, b1 = nparts * sl // 8, nparts * (sl + 1) // 8
+        t = np.zeros(rows)
+        for b in range(b0, b1):
+            t = t + pg[b]
+        slices.append(t)
+    u = slices[0].copy()
+    for k in range(1, 8):
+        u = u + slices[k]
+    out[:rows] = u
+    ns = ps.shape[0]
+    for k in range(4):
+        lanes = np.zeros(32)
+        for lane in range(32):
+            t = 0.0
+            for b in range(lane, ns, 32):
+                t = t + ps[b, k]
+            lanes[lane] = t
+        o = 16
+        while o:
+            lanes = lanes + lanes[np.arange(32) ^ o]
+            o >>= 1
+        out[rows + k] = lanes[0]
+    return out
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+@pytest.mark.parametrize("rows,nparts,nparts_s", [(4096, 148, 148), (640, 32, 296), (3 * 4096 + 96, 32, 5)])
+def test_fused_reduce_exchange_emulated(world, rows, nparts, nparts_s):
+    rng = np.random.default_rng(rows + world)
+    pg = rng.standard_normal((world, nparts, rows))
+    ps = rng.standard_normal((world, nparts_s, 4))
+    rounds = 2
+    out = np.empty((rounds, world, rows + 4))
+    ctx = _native.context(0)
+    _native.check(_native.lib().gps_px_emulate_reduce(ctx.handle, world, rows, nparts, nparts_s, rounds,
+                                                      _native.dptr(np.ascontiguousarray(pg)),
+                                                      _native.dptr(np.ascontiguousarray(ps)),
+                                                      out.ctypes.data_as(_native._dp)))
+    for k in range(rounds):
+        per_rank = [k2_reference(pg[r] * (k + 1), ps[r] * (k + 1), rows) for r in range(world)]
+        ref = rank_order_sum(per_rank)
+        for r in range(world):
+            assert np.array_equal(out[k, r], ref), (k, r)
+
+
+def test_fused_reduce_world_one_solve_matches():
+    """A world-size-1 peer exchange attached to a single-unit loop: the fused
+    K2 must reproduce the unfused solve bitwise."""
+    rng = np.random.default_rng(3)
+    A = rng.standard_normal((300, 2001)).astype(np.float32)
+    D = gps.DataMatrix(A)
+    gamma = 0.1 * float(np.asarray(D.norms).max())
+    ref_loop = gps.single_unit.PowerLoop(D, "l1", gamma, 1e-6, 200)
+    x0 = D.column(int(np.argmax(D.norms))) / float(np.max(D.norms))
+    x_ref, h_ref, c_ref, w_ref = ref_loop.run(x0)
+    L = _native.lib()
+    ctx = D.context
+    h = _native._vp()
+    _native.check(L.gps_px_create(ctx.handle, 1, 0, 320 + 4, _native.C.byref(h)))  # ld = roundup(300, 32)
+    try:
+        loop = gps.single_unit.PowerLoop(D, "l1", gamma, 1e-6, 200)
+        _native.check(L.gps_su_attach_px(loop.handle, h))
+        x, hist, conv, w = loop.run(x0)
+        assert hist == h_ref and np.array_equal(w, w_ref) and np.array_equal(x, x_ref)
+        del loop
+    finally:
+        L.gps_px_destroy(h)
