@@ -706,13 +706,13 @@ int matrix_norms_locked(gps_matrix* A) {
   GPS_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
   const int blocks = ctx->num_sms * 8;
   if (A->dtype == GPS_F32)
-    column_norms_kernel<float><<<blocks, 256, 0, ctx->stream>>>(static_cast<const float*>(A->d), A->n,
-                                                                static_cast<int>(A->ld), ctx->dvec, flag,
-                                                                A->tc_col_exp);
+    column_norms_kernel<float, true><<<blocks, 256, 0, ctx->stream>>>(static_cast<const float*>(A->d), A->n,
+                                                                      static_cast<int>(A->ld), ctx->dvec, flag,
+                                                                      A->tc_col_exp);
   else
-    column_norms_kernel<double><<<blocks, 256, 0, ctx->stream>>>(static_cast<const double*>(A->d), A->n,
-                                                                 static_cast<int>(A->ld), ctx->dvec, flag,
-                                                                 A->tc_col_exp);
+    column_norms_kernel<double, true><<<blocks, 256, 0, ctx->stream>>>(static_cast<const double*>(A->d), A->n,
+                                                                       static_cast<int>(A->ld), ctx->dvec, flag,
+                                                                       A->tc_col_exp);
   ctx->launches++;
   GPS_CHECK_LAUNCH("column_norms_kernel launch");
   A->norms.resize(A->n);

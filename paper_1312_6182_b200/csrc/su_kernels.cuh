@@ -518,7 +518,9 @@ __global__ void __launch_bounds__(kStepThreads) su_step_kernel(const double* exc
 
 // K0: column norms ||a_i|| with fp64 accumulation plus a non-finite flag
 // (core.py:36-47 finiteness check, core.py:243-246 norms).  Warp per column.
-template <typename TA>
+// WITH_EXP: also the tensor-core filter's per-column scale exponents (the
+// plain variant is the read-only stream reference of gps_bench_read_stream)
+template <typename TA, bool WITH_EXP = false>
 __global__ void __launch_bounds__(256) column_norms_kernel(const TA* __restrict__ A, int64_t n, int ld,
                                                            double* __restrict__ norms, int* nonfinite,
                                                            int* __restrict__ col_exp = nullptr) {
@@ -543,12 +545,12 @@ __global__ void __launch_bounds__(256) column_norms_kernel(const TA* __restrict_
         const double d = static_cast<double>(e[u]);
         bad |= !isfinite(d);
         acc = fma(d, d, acc);
-        mx = fmaxf(mx, __double2float_ru(fabs(d)));
+        if (WITH_EXP) mx = fmaxf(mx, __double2float_ru(fabs(d)));
       }
     }
     acc = warp_sum(acc);
     if (lane == 0) norms[col] = sqrt(acc);
-    if (col_exp != nullptr) {  // the tensor-core filter's per-column scale exponent (tc_kernels.cuh)
+    if (WITH_EXP) {  // the tensor-core filter's per-column scale exponent (tc_kernels.cuh)
 #pragma unroll
       for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
       if (lane == 0) col_exp[col] = mx > 0.f ? max(-126, min(126, kTcAScaleExp - ilogbf(mx))) : 0;
