@@ -111,49 +111,74 @@ __global__ void __launch_bounds__(kGramThreads) gram_partial_kernel(const double
   }
 }
 
-// C = op(A) B for m x m row-major smem matrices (op = transpose when ta) on
-// the fp64 tensor cores: mma.sync m8n8k4 f64, one 8 x 8 tile of C per warp
-// at a time (fragments: A[lane/4][lane%4], B[lane%4][lane/4],
-// C[lane/4][2 (lane%4) + {0,1}]), k ascending.  m <= 64, any blockDim.
-__device__ void mm_small(const double* A, const double* B, double* C, int m, bool ta) {
+// Row stride of the Newton-Schulz working matrices: ld = 4 (mod 16) doubles
+// puts the 8 rows x 4 k of an m8n8k4 fragment load in distinct banks (two
+// wavefronts per warp load, the minimum for 256 bytes); a row stride of
+// m = 64 would put all 8 rows of an A fragment in one bank (8 wavefronts).
+__host__ __device__ inline int ns_ld(int m) { return ((m + 15) & ~15) + 4; }
+
+// C = op(A) B for m x m row-major smem matrices with row stride ld (op =
+// transpose when ta) on the fp64 tensor cores: mma.sync m8n8k4 f64, a warp
+// owns two horizontally adjacent 8 x 8 tiles of C at a time so each A
+// fragment feeds two DMMAs (fragments: A[lane/4][lane%4], B[lane%4][lane/4],
+// C[lane/4][2 (lane%4) + {0,1}]), k ascending in two chains (even / odd
+// 4-blocks) per tile.  m <= 64, any blockDim.
+__device__ void mm_small(const double* A, const double* B, double* C, int m, int ld, bool ta) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const int tiles = (m + 7) >> 3;
+  const int tiles = (m + 7) >> 3, pairs = (tiles + 1) >> 1;
   const int ar = lane >> 2, ak = lane & 3;  // A fragment (row, k); B fragment is (k, col) = (ak, ar)
-  for (int tile = warp; tile < tiles * tiles; tile += nw) {
-    const int ti = tile / tiles, tj = tile % tiles;
-    const int r = ti * 8 + ar, cb = tj * 8 + ar;
-    // two independent k-chains (even / odd 4-blocks) hide the DMMA latency
-    double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+  for (int u = warp; u < tiles * pairs; u += nw) {
+    const int ti = u / pairs, tj = (u % pairs) * 2;
+    const int r = ti * 8 + ar, cb = tj * 8 + ar, cb2 = cb + 8;
+    double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;  // tile tj
+    double f0 = 0.0, f1 = 0.0, g0 = 0.0, g1 = 0.0;  // tile tj + 1
     for (int k0 = 0; k0 < m; k0 += 8) {
       const int k = k0 + ak, kk = k + 4;
-      const double a = (r < m && k < m) ? (ta ? A[k * m + r] : A[r * m + k]) : 0.0;
-      const double b = (k < m && cb < m) ? B[k * m + cb] : 0.0;
-      const double a2 = (r < m && kk < m) ? (ta ? A[kk * m + r] : A[r * m + kk]) : 0.0;
-      const double b2 = (kk < m && cb < m) ? B[kk * m + cb] : 0.0;
+      const double a = (r < m && k < m) ? (ta ? A[k * ld + r] : A[r * ld + k]) : 0.0;
+      const double a2 = (r < m && kk < m) ? (ta ? A[kk * ld + r] : A[r * ld + kk]) : 0.0;
+      const double b = (k < m && cb < m) ? B[k * ld + cb] : 0.0;
+      const double b2 = (kk < m && cb < m) ? B[kk * ld + cb] : 0.0;
+      const double bb = (k < m && cb2 < m) ? B[k * ld + cb2] : 0.0;
+      const double bb2 = (kk < m && cb2 < m) ? B[kk * ld + cb2] : 0.0;
       asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                    : "+d"(c0), "+d"(c1)
                    : "d"(a), "d"(b));
       asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                   : "+d"(f0), "+d"(f1)
+                   : "d"(a), "d"(bb));
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                    : "+d"(e0), "+d"(e1)
                    : "d"(a2), "d"(b2));
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                   : "+d"(g0), "+d"(g1)
+                   : "d"(a2), "d"(bb2));
     }
     c0 += e0;
     c1 += e1;
-    const int cr = ti * 8 + (lane >> 2), cc = tj * 8 + 2 * (lane & 3);
+    f0 += g0;
+    f1 += g1;
+    const int cr = ti * 8 + (lane >> 2), cc = tj * 8 + 2 * (lane & 3), cc2 = cc + 8;
     if (cr < m) {
-      if (cc < m) C[cr * m + cc] = c0;
-      if (cc + 1 < m) C[cr * m + cc + 1] = c1;
+      if (cc < m) C[cr * ld + cc] = c0;
+      if (cc + 1 < m) C[cr * ld + cc + 1] = c1;
+      if (cc2 < m) C[cr * ld + cc2] = f0;
+      if (cc2 + 1 < m) C[cr * ld + cc2 + 1] = f1;
     }
   }
 }
 
-// Polar factor of the well-conditioned m x m R (row-major, in X on entry,
-// the result on exit) by the Newton-Schulz iteration
+// Polar factor of the well-conditioned m x m R (row-major, row stride m, in
+// X on entry, the result on exit) by the Newton-Schulz iteration
 // X <- 1.5 X - 0.5 X (X'X) from X0 = R / sqrt(|R|_1 |R|_inf) (all singular values in
-// (0, 1], so it converges; quadratically once X'X ~ I).  T, U: m x m
-// scratch.  Returns false if it has not converged in max_it steps.
-__device__ bool newton_schulz_polar(double* X, double* T, double* U, double* red, int m, int max_it) {
+// (0, 1], so it converges; quadratically once X'X ~ I).  ws: 3 m ns_ld(m)
+// doubles of scratch (the iterate and two products at row stride ns_ld(m)).
+// Returns false if it has not converged in max_it steps.
+__device__ bool newton_schulz_polar(double* X, double* ws, double* red, int m, int max_it) {
   const int tid = threadIdx.x, nt = blockDim.x;
+  const int ld = ns_ld(m);
+  double* Xp = ws;
+  double* T = ws + m * ld;
+  double* U = T + m * ld;
   // X0 = R / sqrt(|R|_1 |R|_inf) (>= |R|_2, and closer to it than |R|_F)
   __shared__ double s_norm1, s_norminf;
   if (tid < 32) {
@@ -179,26 +204,31 @@ __device__ bool newton_schulz_polar(double* X, double* T, double* U, double* red
   }
   __syncthreads();
   const double inv = 1.0 / sqrt(s_norm1 * s_norminf);
-  for (int e = tid; e < m * m; e += nt) X[e] *= inv;
+  for (int e = tid; e < m * m; e += nt) Xp[(e / m) * ld + e % m] = X[e] * inv;
   __syncthreads();
-  for (int it = 0; it < max_it; ++it) {
-    mm_small(X, X, T, m, true);  // T = X'X
+  bool ok = false;
+  for (int it = 0; it < max_it && !ok; ++it) {
+    mm_small(Xp, Xp, T, m, ld, true);  // T = X'X
     __syncthreads();
-    mm_small(X, T, U, m, false);  // U = X T
+    mm_small(Xp, T, U, m, ld, false);  // U = X T
     __syncthreads();
     double d = 0.0;
     for (int e = tid; e < m * m; e += nt) {
-      const double xn = fma(-0.5, U[e], 1.5 * X[e]);
-      d = fma(xn - X[e], xn - X[e], d);
-      X[e] = xn;
+      const int o = (e / m) * ld + e % m;
+      const double xn = fma(-0.5, U[o], 1.5 * Xp[o]);
+      d = fma(xn - Xp[o], xn - Xp[o], d);
+      Xp[o] = xn;
     }
     const double dn = sqrt(block_sum_any(d, red));  // (syncs)
 #ifdef GPS_POLAR_DEBUG
     if (tid == 0) printf("newton-schulz it %d step %.3e\n", it, dn);
 #endif
-    if (dn < 1e-15 * sqrt(double(m))) return true;
+    ok = dn < 1e-15 * sqrt(double(m));
   }
-  return false;
+  if (ok)
+    for (int e = tid; e < m * m; e += nt) X[e] = Xp[(e / m) * ld + e % m];
+  __syncthreads();
+  return ok;
 }
 
 // part[0][e] = sum_b part[b][e] in a fixed order, many CTAs (the one-CTA
@@ -224,10 +254,11 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
   if (!pc->active || pc->fallback) return;
   const int tid = threadIdx.x, nt = blockDim.x;
   double* M = psm;              // m*m (row-major a*m+c)
-  double* R = psm + m * m;      // m*m upper, row-major R[i*m+j]
-  double* Ri = R + m * m;       // m*m inverse
-  double* W = Ri + m * m;       // m*m scratch
-  double* V = W + m * m;        // m*m scratch
+  double* Ri = psm + m * m;     // m*m inverse
+  double* R = Ri + m * m;       // m*m upper, row-major R[i*m+j]
+  double* W = R + m * m;        // m*m scratch
+  // R, W and the rest of the allocation (3 m ns_ld(m) doubles from R) are
+  // the Newton-Schulz workspace in stage 2
 #ifdef GPS_POLAR_DEBUG
   if (tid == 0) printf("chol stage %d start %lld\n", stage, clock64());
 #endif
@@ -335,11 +366,11 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
 #ifdef GPS_POLAR_DEBUG
   if (tid == 0) printf("chol stage %d R2R1 done %lld\n", stage, clock64());
 #endif
-  // M receives P (starting from R2 R1); V and R (R2 itself is no longer
-  // needed: Ri = R2^-1 is kept) are scratch
+  // M receives P (starting from R2 R1); R onwards (R2 itself is no longer
+  // needed: Ri = R2^-1 is kept) is scratch
   for (int e = tid; e < m * m; e += nt) M[e] = W[e];
   __syncthreads();
-  if (!newton_schulz_polar(M, V, R, red, m, 100)) {  // not converged: exact path decides
+  if (!newton_schulz_polar(M, R, red, m, 100)) {  // not converged: exact path decides
     if (tid == 0) pc->fallback = 1;
     return;
   }
@@ -413,6 +444,9 @@ __global__ void __launch_bounds__(kPolarThreads) bk_finish_kernel(double* G, dou
   }
 }
 
-__host__ __device__ inline size_t chol_smem_bytes(int m) { return size_t(5) * m * m * sizeof(double) + 64; }
+// M, Ri, then max(3 m^2, the Newton-Schulz workspace) from R
+__host__ __device__ inline size_t chol_smem_bytes(int m) {
+  return (size_t(2) * m * m + size_t(3) * m * ns_ld(m)) * sizeof(double) + 64;
+}
 
 }  // namespace gps

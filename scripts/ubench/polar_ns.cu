@@ -13,21 +13,23 @@ using namespace gps;
 
 __global__ void __launch_bounds__(kPolarThreads) probe(const double* Rin, int m, long long* stamps, double* out) {
   extern __shared__ double sm[];
-  double* X = sm;
-  double* T = X + m * m;
-  double* U = T + m * m;
+  const int ld = ns_ld(m);
+  double* X = sm;  // row stride ld for the products, m for newton_schulz_polar
+  double* T = X + m * ld;
+  double* U = T + m * ld;
+  double* ws = U + m * ld;
   __shared__ double red[40];
   const int tid = threadIdx.x;
-  for (int e = tid; e < m * m; e += blockDim.x) X[e] = Rin[e];
+  for (int e = tid; e < m * m; e += blockDim.x) X[(e / m) * ld + e % m] = Rin[e];
   __syncthreads();
   long long t0 = clock64();
   for (int r = 0; r < 10; ++r) {
-    mm_small(X, X, T, m, true);
+    mm_small(X, X, T, m, ld, true);
     __syncthreads();
   }
   long long t1 = clock64();
   for (int r = 0; r < 10; ++r) {
-    mm_small(X, T, U, m, false);
+    mm_small(X, T, U, m, ld, false);
     __syncthreads();
   }
   long long t2 = clock64();
@@ -37,7 +39,7 @@ __global__ void __launch_bounds__(kPolarThreads) probe(const double* Rin, int m,
   for (int e = tid; e < m * m; e += blockDim.x) X[e] = Rin[e];
   __syncthreads();
   long long t4 = clock64();
-  const bool ok = newton_schulz_polar(X, T, U, red, m, 100);
+  const bool ok = newton_schulz_polar(X, ws, red, m, 100);
   __syncthreads();
   long long t5 = clock64();
   if (tid == 0) {
@@ -65,7 +67,7 @@ int main() {
   cudaMalloc(&dout, 8);
   cudaMalloc(&dst, 8 * 8);
   cudaMemcpy(dR, R.data(), m * m * 8, cudaMemcpyHostToDevice);
-  const int smem = 3 * m * m * 8;
+  const int smem = 6 * m * ns_ld(m) * 8;
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   for (int rep = 0; rep < 3; ++rep) {
     cudaEvent_t a, b;
@@ -97,7 +99,7 @@ int main() {
   cudaMalloc(&dS, m * m * 8);
   cudaMalloc(&pc, sizeof(PolarCtl));
   cudaMemcpy(dG, Gm.data(), m * m * 8, cudaMemcpyHostToDevice);
-  const int ssm = 5 * m * m * 8;
+  const int ssm = int(chol_smem_bytes(m));
   cudaFuncSetAttribute(chol_stage_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm);
   for (int rep = 0; rep < 3; ++rep)
     for (int stage = 1; stage <= 2; ++stage) {
