@@ -18,6 +18,20 @@
 
 namespace gps {
 
+// Phase clock stamps of chol_stage_kernel for scripts/ubench (diagnostics
+// builds only).
+#ifdef GPS_POLAR_STAMPS
+__device__ long long g_polar_stamps[8];
+#define GPS_STAMP(i)                                   \
+  do {                                                 \
+    if (threadIdx.x == 0) g_polar_stamps[i] = clock64(); \
+  } while (0)
+#else
+#define GPS_STAMP(i) \
+  do {               \
+  } while (0)
+#endif
+
 struct PolarCtl {
   int active;    // this iteration computes a polar step
   int fallback;  // CholeskyQR2 unusable -> Householder path
@@ -259,6 +273,7 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
   double* W = R + m * m;        // m*m scratch
   // R, W and the rest of the allocation (3 m ns_ld(m) doubles from R) are
   // the Newton-Schulz workspace in stage 2
+  GPS_STAMP(0);
 #ifdef GPS_POLAR_DEBUG
   if (tid == 0) printf("chol stage %d start %lld\n", stage, clock64());
 #endif
@@ -280,6 +295,7 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
     R[e] = 0.0;
     Ri[e] = 0.0;
   }
+  GPS_STAMP(1);
 #ifdef GPS_POLAR_DEBUG
   if (tid == 0) printf("chol stage %d partials loaded %lld\n", stage, clock64());
 #endif
@@ -307,6 +323,7 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
     __syncthreads();
   }
   __syncthreads();
+  GPS_STAMP(2);
 #ifdef GPS_POLAR_DEBUG
   if (tid == 0) printf("chol stage %d cholesky done %lld\n", stage, clock64());
 #endif
@@ -314,22 +331,29 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
     if (tid == 0) pc->fallback = 1;
     return;
   }
-  // Ri = R^-1 (upper) by rows from the bottom: row i of Ri needs rows > i,
-  // all its columns c >= i at once -- 16 threads per column each form a
-  // strided piece of sum_k R[i][k] Ri[k][c], combined by shuffles (fixed
-  // order); one barrier per row.
+  // Ri = R^-1 (upper) by back substitution, one half-warp per column c:
+  // row i of column c needs only rows > i of the same column, so the 16
+  // threads each form a strided piece of sum_k R[i][k] Ri[k][c], combine it
+  // by shuffles (fixed order) and sync at warp level -- no block barrier per
+  // row.  Both half-warps of a warp walk the same rows (from the warp's
+  // larger live column down) so the shuffles stay warp-uniform.
   {
     const int c = tid >> 4, q = tid & 15;  // 64 columns x 16 threads
-    for (int i = m - 1; i >= 0; --i) {
-      double t = 0.0;
-      if (c < m && c >= i)
-        for (int k = i + 1 + q; k <= c; k += 16) t = fma(R[i * m + k], Ri[k * m + c], t);
+    if ((c & ~1) < m) {
+      for (int i = min(c | 1, m - 1); i >= 0; --i) {
+        const bool act = c < m && c >= i;
+        double t = 0.0;
+        if (act)
+          for (int k = i + 1 + q; k <= c; k += 16) t = fma(R[i * m + k], Ri[k * m + c], t);
 #pragma unroll
-      for (int o = 8; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-      if (c < m && c >= i && q == 0) Ri[i * m + c] = ((i == c ? 1.0 : 0.0) - t) / R[i * m + i];
-      __syncthreads();
+        for (int o = 8; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (act && q == 0) Ri[i * m + c] = ((i == c ? 1.0 : 0.0) - t) / R[i * m + i];
+        __syncwarp();
+      }
     }
+    __syncthreads();
   }
+  GPS_STAMP(3);
 #ifdef GPS_POLAR_DEBUG
   if (tid == 0) printf("chol stage %d inverse done %lld\n", stage, clock64());
 #endif
@@ -350,6 +374,7 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
       R1g[e] = R[e];
       Sg[e] = Ri[e];  // apply: Q1 = G R1^-1
     }
+    GPS_STAMP(6);
     return;
   }
   // stage 2: R = R2 R1 (upper, row-major in W), its polar factor P by the
@@ -363,6 +388,7 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
     W[e] = (i <= j) ? t : 0.0;
   }
   __syncthreads();
+  GPS_STAMP(4);
 #ifdef GPS_POLAR_DEBUG
   if (tid == 0) printf("chol stage %d R2R1 done %lld\n", stage, clock64());
 #endif
@@ -374,6 +400,7 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
     if (tid == 0) pc->fallback = 1;
     return;
   }
+  GPS_STAMP(5);
 #ifdef GPS_POLAR_DEBUG
   if (tid == 0) printf("chol stage %d NS done %lld\n", stage, clock64());
 #endif
@@ -384,6 +411,7 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
     for (int k = r; k < m; ++k) t += Ri[r * m + k] * M[k * m + c];
     Sg[e] = t;
   }
+  GPS_STAMP(6);
 }
 
 // Out[j][r] = sum_b In[b][r] * S[b][j]   (In, Out: [m][ld]; S row-major m x m)

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <vector>
 
+#define GPS_POLAR_STAMPS
 #include "polar_kernels.cuh"
 
 using namespace gps;
@@ -115,7 +116,13 @@ int main() {
       float ms;
       cudaEventElapsedTime(&ms, a, b);
       cudaMemcpy(&h, pc, sizeof(h), cudaMemcpyDeviceToHost);
-      printf("chol_stage %d: %.1f us fallback=%d rank=%d\n", stage, ms * 1e3, h.fallback, h.rank);
+      long long ps[8];
+      cudaMemcpyFromSymbol(ps, g_polar_stamps, sizeof(ps));
+      printf("chol_stage %d: %.1f us fallback=%d rank=%d | partials %lld, cholesky %lld, inverse %lld clk", stage, ms * 1e3,
+             h.fallback, h.rank, ps[1] - ps[0], ps[2] - ps[1], ps[3] - ps[2]);
+      if (stage == 2) printf(", R2R1 %lld, NS %lld clk", ps[4] - ps[3], ps[5] - ps[4]);
+      printf(", tail %lld, total %lld clk", ps[6] - (stage == 2 ? ps[5] : ps[3]), ps[6] - ps[0]);
+      printf("\n");
     }
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
