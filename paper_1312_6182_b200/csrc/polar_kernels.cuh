@@ -331,28 +331,31 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
     if (tid == 0) pc->fallback = 1;
     return;
   }
-  // Ri = R^-1 (upper) by back substitution, one half-warp per column c:
-  // row i of column c needs only rows > i of the same column, so the 16
-  // threads each form a strided piece of sum_k R[i][k] Ri[k][c], combine it
-  // by shuffles (fixed order) and sync at warp level -- no block barrier per
-  // row.  Both half-warps of a warp walk the same rows (from the warp's
-  // larger live column down) so the shuffles stay warp-uniform.
-  {
-    const int c = tid >> 4, q = tid & 15;  // 64 columns x 16 threads
-    if ((c & ~1) < m) {
-      for (int i = min(c | 1, m - 1); i >= 0; --i) {
-        const bool act = c < m && c >= i;
-        double t = 0.0;
-        if (act)
-          for (int k = i + 1 + q; k <= c; k += 16) t = fma(R[i * m + k], Ri[k * m + c], t);
-#pragma unroll
-        for (int o = 8; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-        if (act && q == 0) Ri[i * m + c] = ((i == c ? 1.0 : 0.0) - t) / R[i * m + i];
-        __syncwarp();
+  // Ri = R^-1 (upper) by back substitution, one thread per column c (a
+  // column needs only its own rows below, so no barrier per row), times
+  // the diagonal reciprocals formed in parallel first.  Every lane of a
+  // warp walks the same rows i and the same k range (up to the warp's last
+  // column; entries below a column's diagonal are zero), so the R reads are
+  // broadcasts and the Ri reads are conflict-free.  Measured at m = 64
+  // (scripts/ubench/polar_ns.cu, whole stage-1 kernel): 75 us, against 95 us
+  // with a half-warp per column and shuffle sums, 100 us with one block
+  // barrier per row.
+  if (tid < m) W[tid] = 1.0 / R[tid * m + tid];
+  __syncthreads();
+  if (tid < ((m + 31) & ~31)) {
+    const int c = tid, cr = min(c, m - 1), cw = min((tid | 31), m - 1);  // cr: lanes past m read a live column
+    for (int i = cw; i >= 0; --i) {
+      double t0 = 0.0, t1 = 0.0;
+      int k = i + 1;
+      for (; k + 1 <= cw; k += 2) {
+        t0 = fma(R[i * m + k], Ri[k * m + cr], t0);
+        t1 = fma(R[i * m + k + 1], Ri[(k + 1) * m + cr], t1);
       }
+      if (k <= cw) t0 = fma(R[i * m + k], Ri[k * m + cr], t0);
+      if (c < m && i <= c) Ri[i * m + c] = ((i == c ? 1.0 : 0.0) - (t0 + t1)) * W[i];
     }
-    __syncthreads();
   }
+  __syncthreads();
   GPS_STAMP(3);
 #ifdef GPS_POLAR_DEBUG
   if (tid == 0) printf("chol stage %d inverse done %lld\n", stage, clock64());
