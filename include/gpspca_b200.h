@@ -150,6 +150,12 @@ int gps_su_result(gps_su* s, double* x_out, double* hist_out, int* n_hist, int* 
                   double* w_sumsq_out);
 /* Kernel launches per power iteration of gps_su_run (instrumentation). */
 int gps_su_launches_per_iter(gps_su* s);
+/* Near-threshold log of the final sweep (north_star: support entries within
+ * 1e-6 gamma of the threshold are logged; thresholds of parallel.py:117-128):
+ * entries col * 64 + component with ||c| - gamma| <= 1e-6 gamma (l1) or
+ * |c^2 - gamma| <= 1e-6 gamma (l0); *count_out = entries found (the first
+ * min(count, cap, 8192) are copied). */
+int gps_su_band(gps_su* s, int64_t* entries_out, int cap, int* count_out);
 
 /* ---- block power iteration: block.py:190-235 ---------------------------- */
 /* m <= 64 components; gamma, mu: length m (mu_j > 0, gamma_j >= 0).  Each
@@ -176,6 +182,17 @@ int gps_bk_poll(gps_bk* s, int* done, int* iter, int* converged);
  * found rank(G) < m at iteration n_hist - 1 (block.py:215-218). */
 int gps_bk_result(gps_bk* s, double* X_out, double* hist_out, int* n_hist, int* converged, double* W_out,
                   int* rank_fail, int* rank_out);
+/* Per-iterate ||X_k'X_k - I||_F for k = 0 .. n_hist - 1 (the StiefelPoint
+ * every polar output becomes, block.py:149 / core.py:113-129; a value above
+ * 1e-10 stops the loop with status 3, the reference's ValueError), the
+ * loop status (0 running / converged / max_iter, 2 rank loss, 3 Stiefel
+ * violation) and the number of steps the exact Householder + Jacobi polar
+ * path took. */
+int gps_bk_diagnostics(gps_bk* s, double* stiefel_out, int* status_out, int* exact_steps_out);
+/* Near-threshold log of the final block sweep: entries col * 64 + j with
+ * the mu-scaled correlation s = mu_j c_ij within 1e-6 gamma_j of the
+ * threshold (block.py:80-89 rules); as gps_su_band. */
+int gps_bk_band(gps_bk* s, int64_t* entries_out, int cap, int* count_out);
 /* One-shot block sweep at X (p x m): objective (block.py:80-111), ascent
  * direction G = 2 mu_j sum_i w a_i (block.py:114-132), optional W (n x m). */
 int gps_bk_sweep(gps_matrix* A, const double* X, int m, const double* gamma, const double* mu, int penalty,
@@ -183,6 +200,12 @@ int gps_bk_sweep(gps_matrix* A, const double* X, int m, const double* gamma, con
 /* block.py:135-149 polar_projection on the device: X = G (G'G)^{-1/2};
  * GPS_E_RANK (rank in *rank_out) when rank(G) < m by the reference rule. */
 int gps_polar(gps_ctx* ctx, const double* G, int64_t p, int m, double* X_out, int* rank_out);
+/* The same polar factor through the block loop's multi-CTA step (CholeskyQR2
+ * + Newton-Schulz, Stiefel check, exact Householder + Jacobi fallback; used
+ * in the loop for p m >= 4096): ||X'X - I||_F in *stiefel_out, 1 in
+ * *exact_out when the exact path took the step. */
+int gps_polar_cholqr2(gps_ctx* ctx, const double* G, int64_t p, int m, double* X_out, int* rank_out,
+                      double* stiefel_out, int* exact_out);
 
 /* ---- peer-memory all-reduce of the sharded loops ------------------------
  * the one exchange per power iteration of the column-sharded

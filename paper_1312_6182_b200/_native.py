@@ -70,6 +70,9 @@ SIGNATURES = {
     "gps_su_poll": (C.c_int, [_vp, _ip, _ip, _ip]),
     "gps_su_result": (C.c_int, [_vp, _dp, _dp, _ip, _ip, _dp, _dp]),
     "gps_su_launches_per_iter": (C.c_int, [_vp]),
+    "gps_su_band": (C.c_int, [_vp, _i64p, C.c_int, _ip]),
+    "gps_bk_diagnostics": (C.c_int, [_vp, _dp, _ip, _ip]),
+    "gps_bk_band": (C.c_int, [_vp, _i64p, C.c_int, _ip]),
     "gps_bk_create": (C.c_int, [_vp, C.c_int, C.c_int, _dp, _dp, C.c_double, C.c_int, C.POINTER(_vp)]),
     "gps_bk_destroy": (C.c_int, [_vp]),
     "gps_bk_start": (C.c_int, [_vp, _dp]),
@@ -84,6 +87,7 @@ SIGNATURES = {
     "gps_bk_result": (C.c_int, [_vp, _dp, _dp, _ip, _ip, _dp, _ip, _ip]),
     "gps_bk_sweep": (C.c_int, [_vp, _dp, C.c_int, _dp, _dp, C.c_int, _dp, _dp, _dp]),
     "gps_polar": (C.c_int, [_vp, _dp, _i64, C.c_int, _dp, _ip]),
+    "gps_polar_cholqr2": (C.c_int, [_vp, _dp, _i64, C.c_int, _dp, _ip, _dp, _ip]),
     "gps_orthonormalize": (C.c_int, [_vp, _dp, _i64, C.c_int, _dp]),
     "gps_gram_apply_block": (C.c_int, [_vp, _dp, C.c_int, _dp]),
     "gps_matrix_center": (C.c_int, [_vp, _dp, C.POINTER(_vp)]),

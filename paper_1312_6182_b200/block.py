@@ -10,16 +10,18 @@ history and stopping rule on the device.  Initialisation is device
 CholeskyQR2 (positive-diagonal R == the reference's sign-fixed QR).
 """
 
+import os
 import time
-from dataclasses import dataclass
+from dataclasses import dataclass, replace
 
 import numpy as np
 
 from . import _native
-from .core import RunReport, SparseLoadings, StiefelPoint, as_data_matrix
+from .core import RunReport, SparseLoadings, StiefelPoint, as_data_matrix, decode_band
 from .parallel import DEFAULT_PLAN, fused_sweep
 
 BLOCK_FEASIBILITY_TOL = 1e-8  # block.py:17
+_STATUS_STIEFEL = 3  # gps_bk loop status: an iterate missed the Stiefel tolerance
 
 
 @dataclass(frozen=True)
@@ -141,6 +143,24 @@ def polar_projection(G):
     return StiefelPoint(X)
 
 
+def _polar_cholqr2(G):
+    """polar_projection through the block loop's multi-CTA step (CholeskyQR2
+    + Newton-Schulz with the Stiefel check and exact fallback, the path the
+    loop takes for p m >= 4096): (X, ||X'X - I||_F, exact path taken)."""
+    G = np.asarray(G, dtype=np.float64)
+    p, m = G.shape
+    X = np.empty((p, m), order="F")
+    rank, exact = _native.C.c_int(0), _native.C.c_int(0)
+    err = _native.C.c_double(0.0)
+    rc = _native.lib().gps_polar_cholqr2(_native.context().handle, _fortran(G).ctypes.data_as(_native._dp), p, m,
+                                         X.ctypes.data_as(_native._dp), _native.C.byref(rank), _native.C.byref(err),
+                                         _native.C.byref(exact))
+    if rc == _native.GPS_E_RANK:
+        raise RankDeficiencyError(rank.value, m)
+    _native.check(rc, "polar (CholeskyQR2 path)")
+    return X, err.value, bool(exact.value)
+
+
 class BlockLoop:
     """Device block power iteration (gps_bk) for one (A, penalty, m, gamma, mu)."""
 
@@ -173,11 +193,30 @@ class BlockLoop:
     def run(self, poll_every=8):
         _native.check(_native.lib().gps_bk_run(self.handle, poll_every), "block loop")
         X, history, converged, W, rank_fail, rank = self.result()
+        stiefel, status, _ = self.diagnostics(len(history))
+        self.stiefel_errors = stiefel
         if rank_fail:
             err = RankDeficiencyError(rank, self.m, iteration=len(history) - 1)
             err.history = history
             raise err
+        if status == _STATUS_STIEFEL:  # the reference's StiefelPoint(U @ Vt) raises here (core.py:126-129)
+            raise ValueError(f"columns not orthonormal: ||X'X - I||_F = {stiefel[-1]:.3e}")
         return X, history, converged, W
+
+    def diagnostics(self, n_hist):
+        """(per-iterate ||X'X - I||_F list, loop status, exact polar steps)."""
+        out = np.zeros(n_hist + 1)
+        status, exact = _native.C.c_int(0), _native.C.c_int(0)
+        _native.check(_native.lib().gps_bk_diagnostics(self.handle, _native.dptr(out), _native.C.byref(status),
+                                                       _native.C.byref(exact)))
+        n = n_hist + (1 if status.value == _STATUS_STIEFEL else 0)
+        return out[:n].tolist(), status.value, exact.value
+
+    def band(self):
+        """(entries, total) of the final sweep's near-threshold log."""
+        from .single_unit import _read_band
+
+        return _read_band(_native.lib().gps_bk_band, self.handle)
 
     def result(self):
         """(X, history, converged, W, rank_fail, rank) of the finished loop."""
@@ -214,6 +253,87 @@ def _recover_block(W):
     return Z
 
 
+def _init_x0(A, config, loop=None):
+    """The initial iterate (block.py:152-171) on the device: with `loop`,
+    written into the loop's X slot; without, returned as a host array."""
+    p, m = A.p, config.m
+    if config.init == "user_supplied":
+        X0 = _as_stiefel_values(config.x0, p, m)
+        StiefelPoint(X0)  # block.py:197 + core.py:118-129
+        if loop is not None:
+            loop.start_user(config.x0)
+        return X0
+    if config.init == "random_orthonormal":
+        M = np.random.default_rng(config.seed).standard_normal((p, m))
+    else:
+        idx = _top_m_columns(np.asarray(A.norms), m)
+        if loop is not None:
+            loop.start_columns(idx)
+            return None
+        M = np.column_stack([A.column(i) for i in idx])
+    if loop is not None:
+        loop.start_qr(M)
+        return None
+    Q = np.empty((p, m), order="F")
+    _native.check(_native.lib().gps_orthonormalize(_native.context().handle, _fortran(M).ctypes.data_as(_native._dp),
+                                                   p, m, Q.ctypes.data_as(_native._dp)))
+    return Q
+
+
+def _eager_requested():
+    """Trace mode: the module-level polar_projection was replaced (a caller
+    intercepting every polar step, as the reference's acceptance criterion 5
+    does, test_acceptance.py:195-228) or GPSPCA_EAGER_BLOCK=1."""
+    import sys
+
+    return (sys.modules[__name__].polar_projection is not _DEVICE_POLAR
+            or os.environ.get("GPSPCA_EAGER_BLOCK") == "1")
+
+
+def _solve_block_eager(A, config, start):
+    """block.py:190-235 step by step from the host: one device block sweep
+    per iteration (objective, G and W in one read of A) and a call of the
+    module-level polar_projection (looked up at every step, so a
+    replacement sees each G) -- the graph-captured loop's arithmetic,
+    without the graph."""
+    import sys
+
+    mod = sys.modules[__name__]
+    gamma, mu, m = config.gamma, config.mu, config.m
+    point = StiefelPoint(_init_x0(A, config))
+    stiefel = [float(np.linalg.norm(point.values.T @ point.values - np.eye(m)))]
+    f, G, W = _block_sweep(A, point.values, gamma, mu, config.penalty, want_w=True)
+    history = [f]
+    converged = False
+    iteration = 0
+    while iteration < config.max_iter:
+        try:
+            point = mod.polar_projection(G)
+        except RankDeficiencyError as err:
+            err.iteration = iteration
+            err.history = history
+            raise
+        X = point.values
+        stiefel.append(float(np.linalg.norm(X.T @ X - np.eye(m))))
+        f_new, G, W = _block_sweep(A, X, gamma, mu, config.penalty, want_w=True)
+        history.append(f_new)
+        iteration += 1
+        if abs(f_new - f) < config.tol * max(abs(f), 1e-30):
+            converged = True
+            break
+        f = f_new
+    loadings = SparseLoadings(_recover_block(W))
+    return loadings, RunReport(
+        objective_history=history,
+        iterations=len(history) - 1,
+        wall_time=time.perf_counter() - start,
+        nnz_per_component=loadings.nnz_per_component(),
+        converged=converged,
+        component_histories=[history],
+        stiefel_errors=stiefel,
+    )
+
+
 def solve_block(A, config, plan=DEFAULT_PLAN, poll_every=8):
     """config.m components jointly (block.py:190-235) -> (SparseLoadings, RunReport)."""
     A = as_data_matrix(A)
@@ -223,17 +343,15 @@ def solve_block(A, config, plan=DEFAULT_PLAN, poll_every=8):
         raise ValueError(f"need 1 <= m <= min(p, n) = {min(A.p, A.n)}, got m={config.m}")
     launches0 = A.context.launch_count
     start = time.perf_counter()
-    p, m = A.p, config.m
+    if _eager_requested():
+        loadings, report = _solve_block_eager(A, config, start)
+        return loadings, replace(report, kernel_launches=A.context.launch_count - launches0)
+    m = config.m
     loop = BlockLoop(A, config.penalty, m, config.gamma, config.mu, config.tol, config.max_iter)
-    if config.init == "random_orthonormal":
-        loop.start_qr(np.random.default_rng(config.seed).standard_normal((p, m)))
-    elif config.init == "max_norm_column":
-        loop.start_columns(_top_m_columns(np.asarray(A.norms), m))
-    else:
-        StiefelPoint(_as_stiefel_values(config.x0, p, m))  # block.py:197 + core.py:118-129
-        loop.start_user(config.x0)
+    _init_x0(A, config, loop)
     X, history, converged, W = loop.run(poll_every)
     StiefelPoint(X)  # every polar output is a StiefelPoint in the reference (block.py:149, core.py:118-129)
+    entries, total = loop.band()
     loadings = SparseLoadings(_recover_block(W))
     return loadings, RunReport(
         objective_history=history,
@@ -243,7 +361,13 @@ def solve_block(A, config, plan=DEFAULT_PLAN, poll_every=8):
         converged=converged,
         component_histories=[history],
         kernel_launches=A.context.launch_count - launches0,
+        near_threshold=decode_band(entries, m),
+        near_threshold_total=total,
+        stiefel_errors=loop.stiefel_errors,
     )
+
+
+_DEVICE_POLAR = polar_projection
 
 
 __all__ = ["BlockState", "RankDeficiencyError", "objective_bl1", "objective_bl0", "ascent_direction_block",

@@ -305,8 +305,20 @@ class SolverConfig:
 @dataclass(frozen=True)
 class RunReport:
     """Per-solve diagnostics (reference core.py:212-226) plus device
-    counters: `device_iterations` sweeps executed and the kernel launch
-    count of the solve."""
+    records the reference keeps implicitly:
+
+    - `kernel_launches`: device kernels the solve launched;
+    - `near_threshold`: per component, the column indices whose (mu-scaled)
+      correlation in the final sweep lies within 1e-6 gamma of the
+      threshold -- ||c| - gamma| <= 1e-6 gamma (l1), |c^2 - gamma| <=
+      1e-6 gamma (l0) -- the entries whose support membership is decided by
+      rounding (north_star: logged, not counted as a support mismatch);
+      `near_threshold_total` counts them (the device keeps the first 8192);
+    - `stiefel_errors` (block solves): ||X_k'X_k - I||_F of every iterate,
+      k = 0 .. iterations -- the feasibility the reference asserts by
+      building a StiefelPoint from each polar output (block.py:149,
+      core.py:113-129).
+    """
 
     objective_history: list = field(default_factory=list)
     iterations: int = 0
@@ -315,6 +327,19 @@ class RunReport:
     converged: bool = False
     component_histories: list = None
     kernel_launches: int = 0
+    near_threshold: list = None
+    near_threshold_total: int = 0
+    stiefel_errors: list = None
+
+
+BAND_COMPONENTS = 64  # entries are col * 64 + component (csrc/common.cuh BandLog)
+
+
+def decode_band(entries, m, offset=0):
+    """Per-component sorted column indices of a device near-threshold list."""
+    e = np.asarray(entries, dtype=np.int64)
+    cols, comp = e // BAND_COMPONENTS + offset, e % BAND_COMPONENTS
+    return [np.unique(cols[comp == j]) for j in range(m)]
 
 
 def positive_part(t):

@@ -30,6 +30,8 @@ struct BlockSweepArgs {
   int64_t w_stride;    // parity stride of the W buffer
   int64_t w_cstride;   // stride between components in W
   const GpsCtl* ctl;
+  BandLog* band;       // optional near-threshold log; components comp0 + j
+  int comp0;
   int cols_per_stage;
   int num_stages;
   int64_t total_stages;
@@ -187,6 +189,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) bk_sweep_kernel(const BlockS
         const double sj = a.mu[j] * c;
         double w = threshold_weight(sj, a.gamma[j], a.penalty);
         if (col < a.n) {
+          band_note(a.band, parity, col, a.comp0 + j, sj, a.gamma[j], a.penalty);
           f_acc += objective_term(sj, a.gamma[j], a.penalty);
           if (w != 0.0) nnz_acc += 1.0;
           if (wbase != nullptr) wbase[j * a.w_cstride + col] = w;
@@ -547,6 +550,62 @@ __device__ inline PolarScratch polar_scratch(double* psm, int m) {
   return sp;
 }
 
+// ||X'X - I||_F of the device iterate X ([m][ld], zero rows >= p) by one CTA
+// (fixed order; M: m*m doubles of shared scratch).  The reference builds a
+// StiefelPoint -- ||X'X - I||_F <= 1e-10 (core.py:113-129) -- from every
+// polar output (block.py:149); the loops record this per iteration.
+__device__ double gram_error_from(const double* M, int m, double* red) {
+  double t = 0.0;
+  for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+    const double d = M[e] - ((e / m == e % m) ? 1.0 : 0.0);
+    t = fma(d, d, t);
+  }
+  return sqrt(block_sum_any(t, red));
+}
+__device__ void gram_mm(const double* P, const double* Q, int ld, int m, double* M, bool symmetric);
+__device__ double stiefel_error(const double* X, int ld, int m, double* M) {
+  __shared__ double red[40];
+  __syncthreads();
+  gram_mm(X, X, ld, m, M, true);
+  __syncthreads();
+  return gram_error_from(M, m, red);
+}
+
+constexpr double kStiefelTol = 1e-10;  // core.py:22 STIEFEL_TOL
+
+// End of a block step (thread 0): rank loss stops the loop with status 2
+// (block.py:144-148, RankDeficiencyError); an iterate off the Stiefel
+// manifold stops it with status 3 (the reference's StiefelPoint raises
+// ValueError); otherwise the error is recorded, the loop advances and the
+// near-threshold list of the next sweep is cleared.
+__device__ void bk_advance(GpsCtl* ctl, int k, int m, int rank, double err, int* rank_out, BandLog* band,
+                           double* stiefel) {
+  if (rank < m) {
+    ctl->done = 1;
+    ctl->converged = 0;
+    ctl->status = 2;
+    *rank_out = rank;
+    return;
+  }
+  if (stiefel != nullptr) stiefel[k + 1] = err;
+  if (!(err <= kStiefelTol)) {
+    ctl->done = 1;
+    ctl->converged = 0;
+    ctl->status = 3;
+    return;
+  }
+  if (band != nullptr) band->count[(k + 1) & 1] = 0;
+  ctl->iter = k + 1;
+}
+
+// One-CTA record of X_0's Stiefel error (init; block.py:202).
+__global__ void __launch_bounds__(kPolarThreads) stiefel_error_kernel(const double* X, int ld, int m,
+                                                                      double* out) {
+  extern __shared__ double psm[];
+  const double e = stiefel_error(X, ld, m, psm);
+  if (threadIdx.x == 0) *out = e;
+}
+
 // Block power step (block.py:211-226) on the reduced exchange vectors of the
 // ng groups: exch layout [ng][MG*ld + 4].  History, stopping rule, then
 // G_j = 2 mu_j sum(...) and X_{k+1} = polar(G); rank loss stops the loop with
@@ -556,7 +615,8 @@ __global__ void __launch_bounds__(kPolarThreads) bk_step_kernel(const double* __
                                                                double* __restrict__ Xbuf, int64_t x_stride,
                                                                double* __restrict__ Gbuf, double* __restrict__ Tbuf,
                                                                double* __restrict__ hist, GpsCtl* ctl, double tol,
-                                                               int max_iter, int* rank_out) {
+                                                               int max_iter, int* rank_out, BandLog* band,
+                                                               double* __restrict__ stiefel) {
   extern __shared__ double psm[];
   __shared__ int decision;
   if (ctl->done) return;
@@ -591,16 +651,8 @@ __global__ void __launch_bounds__(kPolarThreads) bk_step_kernel(const double* __
   __syncthreads();
   double* Xn = Xbuf + ((k + 1) & 1) * x_stride;
   const int rank = polar_device(Gbuf, Xn, ld, p_true, m, polar_scratch(psm, m));
-  if (tid == 0) {
-    if (rank < m) {
-      ctl->done = 1;
-      ctl->converged = 0;
-      ctl->status = 2;
-      *rank_out = rank;
-    } else {
-      ctl->iter = k + 1;
-    }
-  }
+  const double err = rank < m ? 0.0 : stiefel_error(Xn, ld, m, psm);
+  if (tid == 0) bk_advance(ctl, k, m, rank, err, rank_out, band, stiefel);
 }
 
 // One-shot polar (block.py:135-149 polar_projection) on device buffers.
@@ -630,8 +682,9 @@ __device__ void gram_mm(const double* P, const double* Q, int ld, int m, double*
 
 // CholeskyQR2 (block.py:152-171 init): Q = M R^{-1} with R from the Cholesky
 // factor of M'M, applied twice; R has a positive diagonal, so Q equals the
-// reference's sign-fixed Householder Q.  status_out: 0 ok, 1 rank deficient
-// by the reference rule |r_jj| <= m eps max(1, max |r_ii|).
+// reference's sign-fixed Householder Q.  status_out: 0 ok, 1 not decided
+// here (Cholesky breakdown or r_jj spread > 1e6): the caller runs the
+// Householder QR, which applies the reference's rank rule.
 __global__ void __launch_bounds__(kPolarThreads) cholqr2_kernel(double* Mbuf, double* Q, int ld, int m,
                                                                 int* status_out) {
   extern __shared__ double psm[];
@@ -662,10 +715,16 @@ __global__ void __launch_bounds__(kPolarThreads) cholqr2_kernel(double* Mbuf, do
         }
       }
       if (!bad && pass == 0) {
-        double mx = 1.0;
-        for (int j = 0; j < m; ++j) mx = fmax(mx, fabs(Gm[j * m + j]));
-        for (int j = 0; j < m; ++j)
-          if (fabs(Gm[j * m + j]) <= m * 2.220446049250313e-16 * mx) bad = 1;
+        // trust the Gram-based factor only well inside Cholesky's range:
+        // near kappa(M) ~ 1e8 rounding can make a pivot of an exactly
+        // rank-deficient M positive, so r_jj spread beyond 1e6 hands the
+        // decision to the Householder path (hh_init_kernel)
+        double mx = 0.0, mn = INFINITY;
+        for (int j = 0; j < m; ++j) {
+          mx = fmax(mx, fabs(Gm[j * m + j]));
+          mn = fmin(mn, fabs(Gm[j * m + j]));
+        }
+        if (!(mn > 1e-6 * mx)) bad = 1;
       }
       for (int i = 0; i < m * m; ++i) Rt[i] = Gm[i];
     }
@@ -687,6 +746,51 @@ __global__ void __launch_bounds__(kPolarThreads) cholqr2_kernel(double* Mbuf, do
     __syncthreads();
   }
   if (tid == 0) *status_out = 0;
+}
+
+// Householder QR initialisation (block.py:162-170 exactly): R's diagonal
+// decides rank deficiency by the reference rule |r_jj| <= m eps
+// max(1, max_i |r_ii|) (status 1 -> ValueError), otherwise
+// Q = H_1 ... H_m [I; 0] diag(sign r_jj), the reference's sign-fixed Q.
+// Used when CholeskyQR2 breaks down or misses the Stiefel tolerance
+// (kappa(M) beyond ~1e8), where the Gram-based rank test would reject
+// matrices the reference accepts.  M is destroyed (reflectors).
+__global__ void __launch_bounds__(kPolarThreads) hh_init_kernel(double* M, double* Q, int ld, int p_true, int m,
+                                                                int* status_out) {
+  extern __shared__ double psm[];
+  PolarScratch sp = polar_scratch(psm, m);
+  const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+  householder_qr(M, ld, p_true, m, sp);
+  __shared__ int bad;
+  if (tid == 0) {
+    double mx = 1.0;
+    for (int j = 0; j < m; ++j) mx = fmax(mx, fabs(sp.R[j * m + j]));
+    int b = 0;
+    for (int j = 0; j < m; ++j)
+      if (fabs(sp.R[j * m + j]) <= m * 2.220446049250313e-16 * mx) b = 1;
+    bad = b;
+    *status_out = b;
+  }
+  __syncthreads();
+  if (bad) return;
+  for (size_t e = tid; e < size_t(m) * ld; e += nt) {
+    const int c = static_cast<int>(e / ld), r = static_cast<int>(e % ld);
+    const double d = sp.R[c * m + c];
+    Q[e] = (r == c) ? (d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0)) : 0.0;
+  }
+  __syncthreads();
+  for (int j = m - 1; j >= 0; --j) {
+    const double* hj = M + size_t(j) * ld;
+    const double tj = sp.tau[j];
+    for (int c = warp; c < m; c += nw) {
+      double* qc = Q + size_t(c) * ld;
+      double w = 0.0;
+      for (int r = j + lane; r < p_true; r += 32) w = fma(hj[r], qc[r], w);
+      w = warp_sum(w) * tj;
+      for (int r = j + lane; r < p_true; r += 32) qc[r] = fma(-w, hj[r], qc[r]);
+    }
+    __syncthreads();
+  }
 }
 
 }  // namespace gps

@@ -128,6 +128,24 @@ cudaError_t gps_malloc(T** p, size_t bytes) {
   if (e == cudaSuccess) e = cudaStreamSynchronize(0);
   return e;
 }
+inline cudaError_t gps_free(void* p);
+
+// Near-threshold log of a loop object (common.cuh BandLog): the device
+// header plus [2][cap] entries, cleared at every start.
+constexpr unsigned kBandCap = 8192;
+cudaError_t band_alloc(BandLog** band, long long** entries, cudaStream_t st) {
+  cudaError_t e = gps_malloc(entries, size_t(2) * kBandCap * sizeof(long long));
+  if (e == cudaSuccess) e = gps_malloc(band, sizeof(BandLog));
+  if (e != cudaSuccess) return e;
+  const BandLog h{{0u, 0u}, kBandCap, 0u, *entries};
+  e = cudaMemcpyAsync(*band, &h, sizeof(BandLog), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // h is a stack object
+  return e;
+}
+inline cudaError_t band_clear(BandLog* band, cudaStream_t st) {
+  return cudaMemsetAsync(band, 0, 2 * sizeof(unsigned), st);
+}
+
 inline cudaError_t gps_free(void* p) {
   if (!p) return cudaSuccess;
   cudaError_t e = cudaDeviceSynchronize();  // the guarantee cudaFree gave: no kernel still uses p
@@ -197,13 +215,17 @@ bool pick_kernel(int ld, SweepFn& fn, int& gs, int& rv) {
 }
 
 std::mutex g_attr_mu;
-std::set<const void*> g_attr_done;
+std::set<std::pair<int, const void*>> g_attr_done;  // (device, function)
 
-int ensure_smem_attr(const void* fn, size_t smem) {
+// Raise a kernel's dynamic shared-memory limit to the full budget once per
+// device (every caller sizes its launch <= kSmemBudget).
+int ensure_smem_attr(const void* fn, size_t /*smem*/) {
+  int dev = 0;
+  GPS_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lk(g_attr_mu);
-  if (g_attr_done.count(fn)) return GPS_OK;
+  if (g_attr_done.count({dev, fn})) return GPS_OK;
   GPS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
-  g_attr_done.insert(fn);
+  g_attr_done.insert({dev, fn});
   return GPS_OK;
 }
 
@@ -301,6 +323,8 @@ int launch_sweep(gps_matrix* A, const SweepPlan& plan, SweepArgs args, int mode,
     w.coef_threshold = args.coef_threshold;
     w.prm.gamma[0] = args.gamma;
     w.prm.mu[0] = 1.0;
+    w.prm.band = mode == kFused ? args.band : nullptr;
+    w.prm.comp0 = 0;
     w.wbuf = wbuf;
     w.c_out = args.c_out;
     w.w_out = args.w_out;
@@ -426,6 +450,8 @@ struct gps_su {
   double* wbuf = nullptr;  // wide-p fallback weights (n)
   double* defl = nullptr;  // [defl_cap][ld] previous components (implicit deflation)
   int defl_k = 0, defl_cap = 0;
+  BandLog* band = nullptr;          // near-threshold log (common.cuh)
+  long long* band_entries = nullptr;
 };
 
 // ------------------------------------------------------------------ API
@@ -970,6 +996,7 @@ int gps_su_create(gps_matrix* A, int penalty, double gamma, double tol, int max_
   alloc(&s->hist, size_t(max_iter) + 1);
   if (plan.wide) alloc(&s->wbuf, A->n);
   if (e == cudaSuccess) e = gps_malloc(&s->ctl, sizeof(GpsCtl));
+  if (e == cudaSuccess) e = band_alloc(&s->band, &s->band_entries, ctx->stream);
   if (e == cudaSuccess) e = ctl_host_acquire(ctx, &s->ctl_host);
   if (e == cudaSuccess) e = cudaMemsetAsync(s->x, 0, 2 * A->ld * sizeof(double), ctx->stream);
   if (e != cudaSuccess) {
@@ -994,6 +1021,8 @@ int gps_su_destroy(gps_su* s) {
   gps_free(s->ctl);
   if (s->defl) gps_free(s->defl);
   if (s->wbuf) gps_free(s->wbuf);
+  if (s->band) gps_free(s->band);
+  if (s->band_entries) gps_free(s->band_entries);
   ctl_host_release(s->ctx, s->ctl_host);
   delete s;
   return GPS_OK;
@@ -1006,6 +1035,7 @@ int gps_su_start(gps_su* s, const double* x0) {
   GPS_CUDA(cudaMemcpyAsync(s->x, x0, s->A->p * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   std::memset(s->ctl_host, 0, sizeof(GpsCtl));
   GPS_CUDA(cudaMemcpyAsync(s->ctl, s->ctl_host, sizeof(GpsCtl), cudaMemcpyHostToDevice, ctx->stream));
+  GPS_CUDA(band_clear(s->band, ctx->stream));
   GPS_CUDA(cudaStreamSynchronize(ctx->stream));  // x0 / ctl_host are caller / reused buffers
   return GPS_OK;
 }
@@ -1023,6 +1053,7 @@ static int su_enqueue_sweep_nolock(gps_su* s, int mask = 3) {
   args.w_out = s->w;
   args.w_stride = s->A->n;
   args.ctl = s->ctl;
+  args.band = s->band;
   if (mask & 1) rc = launch_sweep(s->A, plan, args, kFused, s->wbuf);
   if (rc) return rc;
   if (mask & 2)
@@ -1034,7 +1065,7 @@ static int su_enqueue_sweep_nolock(gps_su* s, int mask = 3) {
 static int su_enqueue_step_nolock(gps_su* s) {
   gps_ctx* ctx = s->A->ctx;
   su_step_kernel<<<1, kStepThreads, 0, ctx->stream>>>(s->exch, static_cast<int>(s->A->ld), s->x, s->A->ld, s->hist,
-                                                      s->ctl, s->tol, s->max_iter, s->defl, s->defl_k);
+                                                      s->ctl, s->tol, s->max_iter, s->defl, s->defl_k, s->band);
   ctx->launches++;
   GPS_CHECK_LAUNCH("su_step_kernel launch");
   return GPS_OK;
@@ -1272,21 +1303,25 @@ int make_bk_plan(const gps_matrix* A, BkPlan& pl) {
   return ensure_smem_attr(reinterpret_cast<const void*>(pl.fn), pl.smem);
 }
 
+// Dynamic shared-memory limits are per (device context, function): the
+// caches below are keyed by device so a second device in the same process
+// gets its own attributes (every launch runs after cudaSetDevice).
 int ensure_polar_attrs() {
-  static std::once_flag once;
-  static cudaError_t err = cudaSuccess;
-  std::call_once(once, [] {
-    err = cudaFuncSetAttribute(bk_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (err == cudaSuccess)
-      err = cudaFuncSetAttribute(polar_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (err == cudaSuccess)
-      err = cudaFuncSetAttribute(cholqr2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (err == cudaSuccess)
-      err = cudaFuncSetAttribute(bk_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (err == cudaSuccess)
-      err = cudaFuncSetAttribute(chol_stage_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  });
-  if (err != cudaSuccess) return cuda_fail(err, "cudaFuncSetAttribute(polar)");
+  int dev = 0;
+  GPS_CUDA(cudaGetDevice(&dev));
+  static std::mutex mu;
+  static std::set<int> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count(dev)) return GPS_OK;
+  const void* fns[] = {reinterpret_cast<const void*>(bk_step_kernel), reinterpret_cast<const void*>(polar_kernel),
+                       reinterpret_cast<const void*>(cholqr2_kernel), reinterpret_cast<const void*>(bk_finish_kernel),
+                       reinterpret_cast<const void*>(chol_stage_kernel), reinterpret_cast<const void*>(hh_init_kernel),
+                       reinterpret_cast<const void*>(stiefel_error_kernel)};
+  for (const void* fn : fns) {
+    cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (err != cudaSuccess) return cuda_fail(err, "cudaFuncSetAttribute(polar)");
+  }
+  done.insert(dev);
   return GPS_OK;
 }
 
@@ -1337,6 +1372,9 @@ struct gps_bk {
   GpsCtl* ctl = nullptr;
   GpsCtl* ctl_host = nullptr;
   int* rank_dev = nullptr;
+  double* stiefel = nullptr;  // ||X_k'X_k - I||_F per iterate (max_iter + 1)
+  BandLog* band = nullptr;    // near-threshold log (common.cuh)
+  long long* band_entries = nullptr;
   cudaGraphExec_t graph = nullptr;
   int graph_iters = 0;
   int64_t graph_launches = 0;
@@ -1366,6 +1404,8 @@ int bk_launch_group(gps_bk* s, int g, bool with_ctl, int write_w) {
   a.w_stride = int64_t(s->m_pad()) * A->n;
   a.w_cstride = A->n;
   a.ctl = with_ctl ? s->ctl : nullptr;
+  a.band = with_ctl ? s->band : nullptr;
+  a.comp0 = g * pl.mg;
   a.cols_per_stage = pl.cols_per_stage;
   a.num_stages = pl.stages;
   a.total_stages = pl.total_stages;
@@ -1382,6 +1422,8 @@ int bk_launch_group(gps_bk* s, int g, bool with_ctl, int write_w) {
       w.prm.gamma[j] = a.gamma[j];
       w.prm.mu[j] = a.mu[j];
     }
+    w.prm.band = a.band;
+    w.prm.comp0 = a.comp0;
     w.wbuf = s->wbuf;
     w.w_out = a.w_out;
     w.w_cstride = A->n;
@@ -1478,7 +1520,7 @@ int bk_enqueue_tc(gps_bk* s, bool with_ctl) {
   tc_refine_kernel<TA, J><<<s->tc_ref_grid, 256, 0, ctx->stream>>>(static_cast<const TA*>(A->d), A->n, ld, s->m, \
                                                                    s->X, xs, s->mu_dev, gam, s->penalty,       \
                                                                    s->colmask, s->tflag, s->item_act, s->W, wst, \
-                                                                   s->part_s_tc, ctl)
+                                                                   s->part_s_tc, ctl, ctl ? s->band : nullptr)
 #define GPS_REFINE_J(TA)            \
   switch (np / 8) {                 \
     case 2: GPS_REFINE(TA, 2); break; \
@@ -1530,6 +1572,42 @@ int bk_enqueue_sweeps(gps_bk* s, bool with_ctl) {
   return GPS_OK;
 }
 
+// The multi-CTA polar step (polar_kernels.cuh) on G ([m][ld]): CholeskyQR2
+// (gram, chol, apply) x 2, the Newton-Schulz polar factor of R inside the
+// second stage, X_{k+1} = Q1 S into X's parity slot, the Gram of X_{k+1},
+// and bk_finish (Stiefel check, exact fallback, rank decision, advance).
+struct CholQr2Polar {
+  double *G, *Tm, *X;
+  int64_t xs;
+  double *gram_part, *R1, *Sm;
+  PolarCtl* pc;
+  GpsCtl* ctl;
+  int* rank_dev;
+  BandLog* band;
+  double* stiefel;
+};
+
+int enqueue_cholqr2_polar(gps_ctx* ctx, const CholQr2Polar& q, int ld, int p, int m) {
+  gram_partial_kernel<<<kGramBlocks, kGramThreads, 0, ctx->stream>>>(q.G, ld, p, m, q.gram_part, q.pc);
+  gram_reduce_kernel<<<(m * m + 255) / 256, 256, 0, ctx->stream>>>(q.gram_part, kGramBlocks, m * m, q.pc);
+  chol_stage_kernel<<<1, kPolarThreads, chol_smem_bytes(m), ctx->stream>>>(q.gram_part, 1, m, p, 1, q.R1, q.Sm,
+                                                                           q.pc);
+  apply_right_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(q.G, q.Sm, ld, m, q.Tm, q.pc, nullptr, 0);
+  gram_partial_kernel<<<kGramBlocks, kGramThreads, 0, ctx->stream>>>(q.Tm, ld, p, m, q.gram_part, q.pc);
+  gram_reduce_kernel<<<(m * m + 255) / 256, 256, 0, ctx->stream>>>(q.gram_part, kGramBlocks, m * m, q.pc);
+  chol_stage_kernel<<<1, kPolarThreads, chol_smem_bytes(m), ctx->stream>>>(q.gram_part, 1, m, p, 2, q.R1, q.Sm,
+                                                                           q.pc);
+  apply_right_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(q.Tm, q.Sm, ld, m, q.X, q.pc, q.ctl, q.xs);
+  // Gram of the new iterate: bk_finish checks it against the Stiefel tolerance
+  gram_partial_kernel<<<kGramBlocks, kGramThreads, 0, ctx->stream>>>(q.X, ld, p, m, q.gram_part, q.pc, q.ctl, q.xs);
+  gram_reduce_kernel<<<(m * m + 255) / 256, 256, 0, ctx->stream>>>(q.gram_part, kGramBlocks, m * m, q.pc);
+  bk_finish_kernel<<<1, kPolarThreads, polar_smem_bytes(m), ctx->stream>>>(
+      q.G, q.X, q.xs, ld, p, m, q.ctl, q.pc, q.rank_dev, q.gram_part, q.band, q.stiefel);
+  ctx->launches += 11;
+  GPS_CHECK_LAUNCH("block polar step launch");
+  return GPS_OK;
+}
+
 int bk_enqueue_step(gps_bk* s) {
   gps_ctx* ctx = s->A->ctx;
   const int ld = static_cast<int>(s->A->ld), p = static_cast<int>(s->A->p), m = s->m;
@@ -1537,42 +1615,38 @@ int bk_enqueue_step(gps_bk* s) {
   if (!s->big_polar) {
     bk_step_kernel<<<1, kPolarThreads, polar_smem_bytes(m), ctx->stream>>>(
         s->exch, s->ngroups, s->mg, ld, p, m, s->mu_dev, s->X, xs, s->G, s->Tm, s->hist, s->ctl, s->tol,
-        s->max_iter, s->rank_dev);
+        s->max_iter, s->rank_dev, s->band, s->stiefel);
     ctx->launches++;
     GPS_CHECK_LAUNCH("bk_step_kernel launch");
     return GPS_OK;
   }
-  // head -> assemble G -> CholeskyQR2 (gram, chol, apply) x 2 -> X = Q1 S -> finish
+  // head -> assemble G -> CholeskyQR2 polar
   bk_head_kernel<<<1, 32, 0, ctx->stream>>>(s->exch, s->ngroups, s->mg, ld, s->hist, s->ctl, s->tol, s->max_iter,
                                             s->pc, m);
   bk_assemble_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(s->exch, s->mg, ld, m, s->mu_dev, s->G, s->pc);
-  gram_partial_kernel<<<kGramBlocks, kGramThreads, 0, ctx->stream>>>(s->G, ld, p, m, s->gram_part, s->pc);
-  gram_reduce_kernel<<<(m * m + 255) / 256, 256, 0, ctx->stream>>>(s->gram_part, kGramBlocks, m * m, s->pc);
-  chol_stage_kernel<<<1, kPolarThreads, chol_smem_bytes(m), ctx->stream>>>(s->gram_part, 1, m, p, 1, s->R1, s->Sm,
-                                                                 s->pc);
-  apply_right_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(s->G, s->Sm, ld, m, s->Tm, s->pc, nullptr, 0);
-  gram_partial_kernel<<<kGramBlocks, kGramThreads, 0, ctx->stream>>>(s->Tm, ld, p, m, s->gram_part, s->pc);
-  gram_reduce_kernel<<<(m * m + 255) / 256, 256, 0, ctx->stream>>>(s->gram_part, kGramBlocks, m * m, s->pc);
-  chol_stage_kernel<<<1, kPolarThreads, chol_smem_bytes(m), ctx->stream>>>(s->gram_part, 1, m, p, 2, s->R1, s->Sm,
-                                                                 s->pc);
-  apply_right_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(s->Tm, s->Sm, ld, m, s->X, s->pc, s->ctl, xs);
-  bk_finish_kernel<<<1, kPolarThreads, polar_smem_bytes(m), ctx->stream>>>(s->G, s->X, xs, ld, p, m, s->ctl, s->pc,
-                                                                           s->rank_dev);
-  ctx->launches += 11;
-  GPS_CHECK_LAUNCH("block polar step launch");
-  return GPS_OK;
+  ctx->launches += 2;
+  CholQr2Polar cq{s->G, s->Tm, s->X, xs, s->gram_part, s->R1, s->Sm, s->pc, s->ctl, s->rank_dev, s->band, s->stiefel};
+  return enqueue_cholqr2_polar(ctx, cq, ld, p, m);
 }
 
-// Orthonormalise M (device, [m][ld]) into X slot 0 with CholeskyQR2.
+int bk_record_x0(gps_bk* s, double* err_out);
+
+// Orthonormalise M (device, [m][ld]) into X slot 0 (block.py:162-170):
+// CholeskyQR2 (multi-CTA stages for large p m, else one CTA), accepted when
+// its Cholesky factors exist and the result meets the Stiefel tolerance --
+// then the Householder R's diagonal is far from the reference's rank cutoff
+// (a Cholesky of M'M only succeeds for kappa(M) < ~1e8, the cutoff sits at
+// kappa ~ 1 / (m eps)).  Otherwise the exact Householder QR decides rank and
+// forms the sign-fixed Q, as the reference does.
 int bk_qr_into_x(gps_bk* s, double* Mdev) {
   gps_ctx* ctx = s->A->ctx;
   const int ld = static_cast<int>(s->A->ld), p = static_cast<int>(s->A->p), m = s->m;
+  bool done = false;
+  double err = 0.0;
   if (s->big_polar) {
     // large p m: the multi-CTA CholeskyQR2 stages of the polar step, twice
     // (Q1 = M R1^-1 into Tm, Q = Q1 R2^-1 into X slot 0; the positive
     // diagonal of R gives the reference's sign-fixed Q, block.py:162-170).
-    // A Cholesky breakdown or kappa_F(R1) > 1e7 sqrt(m) hands over to the
-    // one-CTA kernel below, which also owns the rank-deficiency decision.
     const PolarCtl on{1, 0, 0, 0};
     GPS_CUDA(cudaMemcpyAsync(s->pc, &on, sizeof(PolarCtl), cudaMemcpyHostToDevice, ctx->stream));
     const double* in = Mdev;
@@ -1590,18 +1664,59 @@ int bk_qr_into_x(gps_bk* s, double* Mdev) {
     PolarCtl got{};
     GPS_CUDA(cudaMemcpyAsync(&got, s->pc, sizeof(PolarCtl), cudaMemcpyDeviceToHost, ctx->stream));
     GPS_CUDA(cudaStreamSynchronize(ctx->stream));
-    if (!got.fallback) return GPS_OK;
+    if (!got.fallback) {
+      int rc = bk_record_x0(s, &err);
+      if (rc) return rc;
+      done = err <= kStiefelTol;
+    }
   }
-  cholqr2_kernel<<<1, kPolarThreads, size_t(2) * s->m * s->m * sizeof(double) + 64, ctx->stream>>>(
-      Mdev, s->X, ld, s->m, s->rank_dev);
+  if (!done) {
+    cholqr2_kernel<<<1, kPolarThreads, size_t(2) * s->m * s->m * sizeof(double) + 64, ctx->stream>>>(
+        Mdev, s->X, ld, s->m, s->rank_dev);
+    ctx->launches++;
+    GPS_CHECK_LAUNCH("cholqr2_kernel launch");
+    int st = 0;
+    GPS_CUDA(cudaMemcpyAsync(&st, s->rank_dev, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    GPS_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (st == 0) {
+      int rc = bk_record_x0(s, &err);
+      if (rc) return rc;
+      done = err <= kStiefelTol;
+    }
+  }
+  if (!done) {
+    // exact path: Householder QR with the reference's rank rule (M is
+    // intact: the CholeskyQR2 attempts only read it)
+    GPS_CUDA(cudaMemsetAsync(s->X, 0, size_t(m) * ld * sizeof(double), ctx->stream));
+    hh_init_kernel<<<1, kPolarThreads, polar_smem_bytes(m), ctx->stream>>>(Mdev, s->X, ld, p, m, s->rank_dev);
+    ctx->launches++;
+    GPS_CHECK_LAUNCH("hh_init_kernel launch");
+    int st = 0;
+    GPS_CUDA(cudaMemcpyAsync(&st, s->rank_dev, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    GPS_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (st != 0)
+      return fail(GPS_E_ARG,
+                  "initialization columns are numerically rank deficient; use init='random_orthonormal' or reduce m");
+    int rc = bk_record_x0(s, &err);
+    if (rc) return rc;
+    if (!(err <= kStiefelTol))
+      return fail(GPS_E_ARG, "columns not orthonormal: ||X'X - I||_F = %.3e", err);
+  }
+  return GPS_OK;
+}
+
+// X_0's Stiefel error into stiefel[0] (block.py:202 builds a StiefelPoint
+// from the initial iterate); returns it.
+int bk_record_x0(gps_bk* s, double* err_out) {
+  gps_ctx* ctx = s->A->ctx;
+  stiefel_error_kernel<<<1, kPolarThreads, size_t(s->m) * s->m * sizeof(double), ctx->stream>>>(
+      s->X, static_cast<int>(s->A->ld), s->m, s->stiefel);
   ctx->launches++;
-  GPS_CHECK_LAUNCH("cholqr2_kernel launch");
-  int st = 0;
-  GPS_CUDA(cudaMemcpyAsync(&st, s->rank_dev, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  GPS_CHECK_LAUNCH("stiefel_error_kernel launch");
+  double err = 0.0;
+  GPS_CUDA(cudaMemcpyAsync(&err, s->stiefel, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   GPS_CUDA(cudaStreamSynchronize(ctx->stream));
-  if (st != 0)
-    return fail(GPS_E_ARG,
-                "initialization columns are numerically rank deficient; use init='random_orthonormal' or reduce m");
+  *err_out = err;
   return GPS_OK;
 }
 
@@ -1610,6 +1725,8 @@ int bk_reset_ctl(gps_bk* s) {
   std::memset(s->ctl_host, 0, sizeof(GpsCtl));
   GPS_CUDA(cudaMemcpyAsync(s->ctl, s->ctl_host, sizeof(GpsCtl), cudaMemcpyHostToDevice, ctx->stream));
   GPS_CUDA(cudaMemsetAsync(s->rank_dev, 0, sizeof(int), ctx->stream));
+  GPS_CUDA(band_clear(s->band, ctx->stream));
+  if (s->pc) GPS_CUDA(cudaMemsetAsync(s->pc, 0, sizeof(PolarCtl), ctx->stream));
   GPS_CUDA(cudaStreamSynchronize(ctx->stream));
   return GPS_OK;
 }
@@ -1712,6 +1829,8 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
   }
   alloc((void**)&s->ctl, sizeof(GpsCtl));
   alloc((void**)&s->rank_dev, sizeof(int));
+  alloc((void**)&s->stiefel, (size_t(max_iter) + 1) * sizeof(double));
+  if (e == cudaSuccess) e = band_alloc(&s->band, &s->band_entries, ctx->stream);
   if (e == cudaSuccess) e = ctl_host_acquire(ctx, &s->ctl_host);
   if (e == cudaSuccess) e = cudaMemsetAsync(s->X, 0, 2 * mp * ld * sizeof(double), ctx->stream);
   if (e == cudaSuccess && tc) e = cudaMemsetAsync(s->tflag, 0, size_t(ceil_div(n, kTcRefItem)) * 16, ctx->stream);
@@ -1748,12 +1867,12 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
     }
     const size_t smem = tc_smem_bytes(s->mg, s->tc_rings[0], s->tc_rings[1], esz);
     if (rc == GPS_OK && smem > 227 * 1024) rc = fail(GPS_E_ARG, "tensor-core ring configuration exceeds shared memory");
-    if (rc == GPS_OK) {
-      cudaError_t ea =
-          f64 ? cudaFuncSetAttribute(tc_dots_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem))
-              : cudaFuncSetAttribute(tc_dots_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      if (ea != cudaSuccess) rc = cuda_fail(ea, "cudaFuncSetAttribute(tc_dots)");
-    }
+    // the limit is raised to the whole budget (not this loop's size): a
+    // smaller-m loop created later must not lower it under a live larger one
+    if (rc == GPS_OK)
+      rc = ensure_smem_attr(f64 ? reinterpret_cast<const void*>(tc_dots_kernel<double>)
+                                : reinterpret_cast<const void*>(tc_dots_kernel<float>),
+                            smem);
     if (rc == GPS_OK && A->tc_col_delta == nullptr) {
       // candidate margins: one pass over A once per matrix (the scale
       // exponents come from the matrix's norms pass), kept with it
@@ -1816,6 +1935,9 @@ int gps_bk_destroy(gps_bk* s) {
   gps_free(s->hist);
   gps_free(s->ctl);
   gps_free(s->rank_dev);
+  if (s->stiefel) gps_free(s->stiefel);
+  if (s->band) gps_free(s->band);
+  if (s->band_entries) gps_free(s->band_entries);
   ctl_host_release(s->ctx, s->ctl_host);
   delete s;
   return GPS_OK;
@@ -1828,6 +1950,9 @@ int gps_bk_start(gps_bk* s, const double* X0) {
   GPS_CUDA(cudaMemsetAsync(s->X, 0, s->m_pad() * s->A->ld * sizeof(double), ctx->stream));
   GPS_CUDA(cudaMemcpy2DAsync(s->X, s->A->ld * sizeof(double), X0, s->A->p * sizeof(double), s->A->p * sizeof(double),
                              s->m, cudaMemcpyHostToDevice, ctx->stream));
+  double err = 0.0;
+  int rc = bk_record_x0(s, &err);  // the host already validated X0 (1e-8, then 1e-10)
+  if (rc) return rc;
   return bk_reset_ctl(s);
 }
 
@@ -1968,6 +2093,61 @@ int gps_bk_result(gps_bk* s, double* X_out, double* hist_out, int* n_hist, int* 
   if (rank_fail) *rank_fail = c.status == 2;
   if (rank_out) *rank_out = rank;
   return GPS_OK;
+}
+
+int gps_bk_diagnostics(gps_bk* s, double* stiefel_out, int* status_out, int* exact_steps_out) {
+  if (!s) return fail(GPS_E_ARG, "NULL argument");
+  gps_ctx* ctx = s->A->ctx;
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  GPS_CUDA(cudaMemcpyAsync(s->ctl_host, s->ctl, sizeof(GpsCtl), cudaMemcpyDeviceToHost, ctx->stream));
+  PolarCtl pc{};
+  if (s->pc) GPS_CUDA(cudaMemcpyAsync(&pc, s->pc, sizeof(PolarCtl), cudaMemcpyDeviceToHost, ctx->stream));
+  GPS_CUDA(cudaStreamSynchronize(ctx->stream));
+  const GpsCtl c = *s->ctl_host;
+  // entries 0 .. iter (iter + 1 on a Stiefel stop: the rejected iterate)
+  const int n = c.iter + 1 + (c.status == 3 ? 1 : 0);
+  if (stiefel_out)
+    GPS_CUDA(cudaMemcpyAsync(stiefel_out, s->stiefel, size_t(n) * sizeof(double), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+  GPS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (status_out) *status_out = c.status;
+  if (exact_steps_out) *exact_steps_out = s->big_polar ? pc.exact_steps : c.iter;
+  return GPS_OK;
+}
+
+}  // extern "C"
+
+namespace {
+// Final sweep's near-threshold entries (parity of the last iterate).
+int band_result(gps_ctx* ctx, const GpsCtl* ctl_dev, GpsCtl* ctl_host, const BandLog* band, const long long* entries,
+                int64_t* out, int cap, int* count) {
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  BandLog h{};
+  GPS_CUDA(cudaMemcpyAsync(ctl_host, ctl_dev, sizeof(GpsCtl), cudaMemcpyDeviceToHost, ctx->stream));
+  GPS_CUDA(cudaMemcpyAsync(&h, band, sizeof(BandLog), cudaMemcpyDeviceToHost, ctx->stream));
+  GPS_CUDA(cudaStreamSynchronize(ctx->stream));
+  const int par = ctl_host->iter & 1;
+  const unsigned got = std::min(h.count[par], h.cap);
+  const unsigned take = std::min<unsigned>(got, cap > 0 ? unsigned(cap) : 0u);
+  if (out && take)
+    GPS_CUDA(cudaMemcpyAsync(out, entries + size_t(par) * h.cap, take * sizeof(long long), cudaMemcpyDeviceToHost,
+                             ctx->stream));
+  GPS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (count) *count = static_cast<int>(h.count[par]);
+  return GPS_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int gps_su_band(gps_su* s, int64_t* entries_out, int cap, int* count_out) {
+  if (!s) return fail(GPS_E_ARG, "NULL argument");
+  return band_result(s->A->ctx, s->ctl, s->ctl_host, s->band, s->band_entries, entries_out, cap, count_out);
+}
+
+int gps_bk_band(gps_bk* s, int64_t* entries_out, int cap, int* count_out) {
+  if (!s) return fail(GPS_E_ARG, "NULL argument");
+  return band_result(s->A->ctx, s->ctl, s->ctl_host, s->band, s->band_entries, entries_out, cap, count_out);
 }
 
 int gps_bk_sweep(gps_matrix* A, const double* X, int m, const double* gamma, const double* mu, int penalty,
@@ -2268,6 +2448,72 @@ int gps_polar(gps_ctx* ctx, const double* G, int64_t p, int m, double* X_out, in
   return GPS_OK;
 }
 
+int gps_polar_cholqr2(gps_ctx* ctx, const double* G, int64_t p, int m, double* X_out, int* rank_out,
+                      double* stiefel_out, int* exact_out) {
+  if (!ctx || !G || !X_out || p < 1 || m < 1) return fail(GPS_E_ARG, "bad arguments");
+  if (m > kMaxBlockM) return fail(GPS_E_UNSUPPORTED, "m=%d > %d", m, kMaxBlockM);
+  if (m > p) return fail(GPS_E_ARG, "need m <= p");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  int rc = ensure_polar_attrs();
+  if (rc) return rc;
+  const int64_t ld = ceil_div(p, 32) * 32;
+  const size_t mld = size_t(m) * ld;
+  // one allocation: G | Tm | X[2] | gram_part | R1 | Sm | stiefel[2] | ctl | pc | rank
+  const size_t doubles = 4 * mld + size_t(kGramBlocks) * m * m + 2 * size_t(m) * m + 2;
+  char* base = nullptr;
+  const size_t bytes = doubles * sizeof(double) + sizeof(GpsCtl) + sizeof(PolarCtl) + 16;
+  GPS_CUDA(gps_malloc(&base, bytes));
+  double* d = reinterpret_cast<double*>(base);
+  CholQr2Polar q{};
+  q.G = d;
+  q.Tm = d + mld;
+  q.X = d + 2 * mld;
+  q.xs = int64_t(mld);
+  q.gram_part = d + 4 * mld;
+  q.R1 = q.gram_part + size_t(kGramBlocks) * m * m;
+  q.Sm = q.R1 + size_t(m) * m;
+  q.stiefel = q.Sm + size_t(m) * m;
+  q.ctl = reinterpret_cast<GpsCtl*>(q.stiefel + 2);
+  q.pc = reinterpret_cast<PolarCtl*>(q.ctl + 1);
+  q.rank_dev = reinterpret_cast<int*>(q.pc + 1);
+  q.band = nullptr;
+  const PolarCtl on{1, 0, m, 0};
+  cudaError_t e = cudaMemsetAsync(base, 0, bytes, ctx->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(q.pc, &on, sizeof(PolarCtl), cudaMemcpyHostToDevice, ctx->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(q.G, ld * sizeof(double), G, p * sizeof(double), p * sizeof(double), m,
+                          cudaMemcpyHostToDevice, ctx->stream);
+  if (e == cudaSuccess) rc = enqueue_cholqr2_polar(ctx, q, static_cast<int>(ld), static_cast<int>(p), m);
+  GpsCtl c{};
+  PolarCtl pcv{};
+  int rank = 0;
+  double st[2] = {0, 0};
+  if (e == cudaSuccess && rc == GPS_OK) {
+    e = cudaMemcpyAsync(&c, q.ctl, sizeof(GpsCtl), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&pcv, q.pc, sizeof(PolarCtl), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&rank, q.rank_dev, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(st, q.stiefel, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(X_out, p * sizeof(double), q.X + mld, ld * sizeof(double), p * sizeof(double), m,
+                            cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  }
+  cudaStreamSynchronize(ctx->stream);
+  gps_free(base);
+  if (rc) return rc;
+  if (e != cudaSuccess) return cuda_fail(e, "gps_polar_cholqr2");
+  if (exact_out) *exact_out = pcv.exact_steps;
+  if (stiefel_out) *stiefel_out = st[1];
+  if (c.status == 2) {
+    if (rank_out) *rank_out = rank;
+    return fail(GPS_E_RANK, "gradient has numerical rank %d < %d", rank, m);
+  }
+  if (rank_out) *rank_out = m;
+  if (c.status == 3) return fail(GPS_E_ARG, "columns not orthonormal: ||X'X - I||_F = %.3e", st[1]);
+  return GPS_OK;
+}
+
 int gps_orthonormalize(gps_ctx* ctx, const double* M, int64_t p, int m, double* Q_out) {
   if (!ctx || !M || !Q_out || p < 1 || m < 1) return fail(GPS_E_ARG, "bad arguments");
   if (m > kMaxBlockM) return fail(GPS_E_UNSUPPORTED, "m=%d > %d", m, kMaxBlockM);
@@ -2292,6 +2538,20 @@ int gps_orthonormalize(gps_ctx* ctx, const double* M, int64_t p, int m, double* 
   }
   int status = 0;
   if (e == cudaSuccess) e = cudaMemcpyAsync(&status, st, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (e == cudaSuccess && status != 0) {
+    // CholeskyQR2 broke down: the exact Householder QR decides with the
+    // reference's diagonal rule (block.py:162-168) and forms the
+    // sign-fixed Q (M in buf is intact)
+    e = cudaMemsetAsync(buf + m * ld, 0, size_t(m) * ld * sizeof(double), ctx->stream);
+    if (e == cudaSuccess) {
+      hh_init_kernel<<<1, kPolarThreads, polar_smem_bytes(m), ctx->stream>>>(buf, buf + m * ld, static_cast<int>(ld),
+                                                                            static_cast<int>(p), m, st);
+      ctx->launches++;
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&status, st, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
+  }
   if (e == cudaSuccess)
     e = cudaMemcpy2DAsync(Q_out, p * sizeof(double), buf + m * ld, ld * sizeof(double), p * sizeof(double), m,
                           cudaMemcpyDeviceToHost, ctx->stream);

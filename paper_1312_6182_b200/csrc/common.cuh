@@ -129,4 +129,31 @@ __device__ __forceinline__ T objective_term(T c, T gamma, int penalty) {
   return t > T(0) ? t : T(0);
 }
 
+// Near-threshold log (the band `north_star` asks to be logged): every
+// (column, component) whose scaled correlation s = mu_j c_ij lies within
+// 1e-6 gamma_j of the threshold -- ||s| - gamma| <= 1e-6 gamma (l1),
+// |s^2 - gamma| <= 1e-6 gamma (l0) -- is appended as col * 64 + j to the
+// list of the sweep's parity (the loops double-buffer by iteration parity
+// like W, and the step kernel that advances to iteration k + 1 clears the
+// list that sweep k + 1 fills).  At gamma = 0 there is no band: a zero
+// correlation gives w = 0 on either side of the threshold.
+struct BandLog {
+  unsigned int count[2];  // entries appended per parity (may exceed cap)
+  unsigned int cap;       // capacity per parity
+  unsigned int pad;
+  long long* entries;     // [2][cap]
+};
+constexpr double kBandRel = 1e-6;
+constexpr int kBandMaxComponents = 64;
+
+__device__ __forceinline__ void band_note(BandLog* b, int parity, int64_t col, int j, double s, double gamma,
+                                          int penalty) {
+  if (b == nullptr || !(gamma > 0.0)) return;
+  const double d = penalty == 0 ? fabs(fabs(s) - gamma) : fabs(s * s - gamma);
+  if (d <= kBandRel * gamma) {
+    const unsigned int pos = atomicAdd(&b->count[parity], 1u);
+    if (pos < b->cap) b->entries[size_t(parity) * b->cap + pos] = col * kBandMaxComponents + j;
+  }
+}
+
 }  // namespace gps

@@ -7,9 +7,10 @@
 //   Q1 = Q R2 (same again), R = R2 R1 = U S V' (one-sided Jacobi on one CTA),
 //   X = Q U V' = Q1 (R2^-1 U V').
 // The singular values of R carry the rank test of the reference.  When a
-// Cholesky breaks down or cond(R) > 1e7 (where CholeskyQR2 would lose the
-// accuracy the rank rule needs) the step falls back to the Householder path
-// on one CTA, so results keep LAPACK-grade rank decisions in every case.
+// Cholesky breaks down, kappa_F(R1) > 1e5, R2 strays from I, or the new
+// iterate misses the Stiefel tolerance (checked on its Gram), the step falls
+// back to the Householder path on one CTA, so results keep LAPACK-grade rank
+// decisions and every kept iterate is a valid StiefelPoint.
 // All kernels read a device control block; nothing is decided on the host,
 // so an iteration stays CUDA-graph capturable.
 #pragma once
@@ -33,16 +34,22 @@ __device__ long long g_polar_stamps[8];
 #endif
 
 struct PolarCtl {
-  int active;    // this iteration computes a polar step
-  int fallback;  // CholeskyQR2 unusable -> Householder path
+  int active;       // this iteration computes a polar step
+  int fallback;     // CholeskyQR2 unusable -> Householder path
   int rank;
-  int pad;
+  int exact_steps;  // diagnostics: steps the exact path took (cumulative)
 };
 
 constexpr int kMaxGramM = 64;
 constexpr int kGramBlocks = 64;
 constexpr int kGramThreads = 256;
 constexpr int kGramRows = 32;  // rows staged in smem per pass
+// CholeskyQR2 trust region: kappa_F(R1) = |R1|_F |R1^-1|_F <= 1e5 keeps the
+// first pass's loss of orthogonality (~kappa^2 u) near 1e-6, which the
+// second pass removes; beyond it, or when R2 strays from I by more than
+// 1e-4 (stage 2), the exact Householder + Jacobi path takes the step.
+constexpr double kCholQr2MaxKappa = 1e5;
+constexpr double kCholQr2MaxR2Dev = 1e-4;
 
 // Head of the block step: history and stopping rule (block.py:211-226).
 __global__ void bk_head_kernel(const double* __restrict__ exch, int ng, int mg, int ld, double* __restrict__ hist,
@@ -87,11 +94,14 @@ __global__ void bk_assemble_kernel(const double* __restrict__ exch, int mg, int 
 
 // Partial Gram matrices of Y ([m][ld], rows >= p_true zero): block b covers
 // a contiguous row range; part[b][a*m + c].  Fixed summation order.
+// With ctl given, Y is the parity slot the step is writing (X_{k+1}).
 __global__ void __launch_bounds__(kGramThreads) gram_partial_kernel(const double* __restrict__ Y, int ld, int p_true,
                                                                    int m, double* __restrict__ part,
-                                                                   const PolarCtl* pc) {
+                                                                   const PolarCtl* pc, const GpsCtl* ctl = nullptr,
+                                                                   int64_t par_stride = 0) {
   __shared__ double tile[kGramRows][kMaxGramM + 1];
   if (!pc->active || pc->fallback) return;
+  if (ctl != nullptr) Y += ((ctl->iter + 1) & 1) * par_stride;
   const int rows_per = (p_true + gridDim.x - 1) / gridDim.x;
   const int r0 = blockIdx.x * rows_per;
   const int r1 = min(p_true, r0 + rows_per);
@@ -258,7 +268,7 @@ __global__ void gram_reduce_kernel(double* __restrict__ part, int nparts, int mm
 
 // Sum the Gram partials (fixed order), Cholesky G'G = R'R (upper R), and
 // invert R.  stage 1: R1 -> Rs (R1), Rinv (R1^-1), or the fallback flag when
-// kappa_F(R1) > 1e7 sqrt(m).  stage 2: R2 with R = R2 R1, the polar factor
+// kappa_F(R1) > kCholQr2MaxKappa.  stage 2: R2 with R = R2 R1, the polar factor
 // P of R by Newton-Schulz, then S = R2^-1 P (the right factor of X = Q1 S).
 // One CTA; small m x m work in smem.
 __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double* __restrict__ part, int nparts, int m,
@@ -361,7 +371,7 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
   if (tid == 0) printf("chol stage %d inverse done %lld\n", stage, clock64());
 #endif
   if (stage == 1) {
-    // kappa_F(R1) = |R1|_F |R1^-1|_F ~ kappa(G): beyond 1e7 sqrt(m) the
+    // kappa_F(R1) = |R1|_F |R1^-1|_F ~ kappa(G): beyond kCholQr2MaxKappa the
     // CholeskyQR2 result is not trusted and the exact path decides (rank too)
     double a = 0.0, b = 0.0;
     for (int e = tid; e < m * m; e += nt) {
@@ -369,7 +379,7 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
       b = fma(Ri[e], Ri[e], b);
     }
     const double kap = sqrt(block_sum_any(a, red)) * sqrt(block_sum_any(b, red));
-    if (!(kap <= 1e7 * sqrt(double(m)))) {
+    if (!(kap <= kCholQr2MaxKappa)) {
       if (tid == 0) pc->fallback = 1;
       return;
     }
@@ -379,6 +389,20 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
     }
     GPS_STAMP(6);
     return;
+  }
+  // stage 2: Q1 = G R1^-1 is orthonormal to ~kappa^2 u when stage 1 was
+  // accurate, so R2 ~ I; a larger departure means stage 1 lost accuracy and
+  // the exact path takes the step.
+  {
+    double t = 0.0;
+    for (int e = tid; e < m * m; e += nt) {
+      const double d = R[e] - ((e / m == e % m) ? 1.0 : 0.0);
+      t = fma(d, d, t);
+    }
+    if (!(sqrt(block_sum_any(t, red)) <= kCholQr2MaxR2Dev)) {
+      if (tid == 0) pc->fallback = 1;
+      return;
+    }
   }
   // stage 2: R = R2 R1 (upper, row-major in W), its polar factor P by the
   // Newton-Schulz iteration (the CholeskyQR2 path only runs for condition
@@ -453,25 +477,39 @@ __global__ void __launch_bounds__(256) apply_right_kernel(const double* __restri
   }
 }
 
-// Fallback (exact Householder + Jacobi, one CTA) and the step's finish:
-// rank failure stops the loop (block.py:215-218), else the iterate advances.
+// Fallback (exact Householder + Jacobi, one CTA) and the step's finish.
+// On the CholeskyQR2 path `gram` holds X_{k+1}'X_{k+1} (the Gram kernels
+// ran on the new iterate): an error above the reference's Stiefel
+// tolerance (core.py:22) sends the step to the exact path as well, so a
+// CholeskyQR2 result is only ever kept when it is a valid StiefelPoint.
+// Rank failure stops the loop (block.py:215-218), else the iterate
+// advances (bk_advance).
 __global__ void __launch_bounds__(kPolarThreads) bk_finish_kernel(double* G, double* Xbuf, int64_t x_stride, int ld,
                                                                  int p_true, int m, GpsCtl* ctl, PolarCtl* pc,
-                                                                 int* rank_out) {
+                                                                 int* rank_out, const double* __restrict__ gram,
+                                                                 BandLog* band, double* __restrict__ stiefel) {
   extern __shared__ double psm[];
+  __shared__ double red[40];
   if (!pc->active) return;
   const int k = ctl->iter;
+  double* Xn = Xbuf + ((k + 1) & 1) * x_stride;
   int rank = pc->rank;
-  if (pc->fallback) rank = polar_device(G, Xbuf + ((k + 1) & 1) * x_stride, ld, p_true, m, polar_scratch(psm, m));
+  bool exact = pc->fallback != 0;
+  double err = 0.0;
+  if (!exact) {
+    err = gram_error_from(gram, m, red);
+    exact = !(err <= kStiefelTol);
+  }
+  if (exact) {
+    rank = polar_device(G, Xn, ld, p_true, m, polar_scratch(psm, m));
+    if (rank == m) err = stiefel_error(Xn, ld, m, psm);
+  }
   if (threadIdx.x == 0) {
-    if (rank < m) {
-      ctl->done = 1;
-      ctl->converged = 0;
-      ctl->status = 2;
-      *rank_out = rank;
-    } else {
-      ctl->iter = k + 1;
+    if (exact) {
+      pc->fallback = 1;
+      pc->exact_steps += 1;
     }
+    bk_advance(ctl, k, m, rank, err, rank_out, band, stiefel);
   }
 }
 

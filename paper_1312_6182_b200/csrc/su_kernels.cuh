@@ -57,6 +57,7 @@ struct SweepArgs {
   double* w_out;      // optional: thresholded weights (n), parity slot
   int64_t w_stride;
   const GpsCtl* ctl;  // optional loop control (early exit + parity)
+  BandLog* band;      // optional near-threshold log (kFused)
   int cols_per_stage; // T
   int num_stages;     // smem ring depth S
   int64_t total_stages;
@@ -246,6 +247,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) su_sweep_kernel(const SweepA
           w = (MODE == kFused) ? threshold_weight(c, a.gamma, a.penalty) : 0.0;
         }
         if (col < a.n) {
+          if (MODE == kFused) band_note(a.band, parity, col, 0, c, a.gamma, a.penalty);
           if (MODE != kCoef) f_acc += objective_term(c, a.gamma, a.penalty);
           if (w != 0.0) {
             nnz_acc += 1.0;
@@ -462,7 +464,8 @@ __global__ void __launch_bounds__(kStepThreads) su_step_kernel(const double* exc
                                                               double* __restrict__ xbuf, int64_t x_stride,
                                                               double* __restrict__ hist, GpsCtl* ctl,
                                                               double tol, int max_iter,
-                                                              const double* __restrict__ defl_X, int defl_k) {
+                                                              const double* __restrict__ defl_X, int defl_k,
+                                                              BandLog* band) {
   __shared__ double red[33];
   __shared__ int decision;
   if (ctl->done) return;
@@ -510,6 +513,7 @@ __global__ void __launch_bounds__(kStepThreads) su_step_kernel(const double* exc
   double* xn = xbuf + ((k + 1) & 1) * x_stride;
   for (int r = tid; r < ld; r += kStepThreads) xn[r] = g[r] / nrm;
   if (tid == 0) {
+    if (band != nullptr) band->count[(k + 1) & 1] = 0;  // sweep k + 1 logs afresh
     ctl->f_prev = f;
     ctl->gnorm = nrm;
     ctl->iter = k + 1;

@@ -711,7 +711,8 @@ __global__ void __launch_bounds__(256, 2) tc_refine_kernel(const TA* __restrict_
                                                            const unsigned char* __restrict__ tflag,
                                                            unsigned char* __restrict__ item_act,
                                                            double* __restrict__ W, int64_t w_par_stride,
-                                                           double* __restrict__ part_s, const GpsCtl* ctl) {
+                                                           double* __restrict__ part_s, const GpsCtl* ctl,
+                                                           BandLog* band) {
   constexpr int NJ = 8 * JPT;  // padded components (X is zero beyond m)
   constexpr int JC = NJ < 32 ? NJ : 32;  // components per pass of the single-column mode
   if (ctl != nullptr && ctl->done) return;
@@ -817,6 +818,7 @@ __global__ void __launch_bounds__(256, 2) tc_refine_kernel(const TA* __restrict_
           if (j < m) {
             const double sj = smu[j] * acc[i][u];
             const double w = threshold_weight(sj, sgam[j], penalty);
+            band_note(band, parity, c, j, sj, sgam[j], penalty);
             f_acc += objective_term(sj, sgam[j], penalty);
             if (w != 0.0) {
               nnz_acc += 1.0;
@@ -863,6 +865,7 @@ __global__ void __launch_bounds__(256, 2) tc_refine_kernel(const TA* __restrict_
         for (int w = 1; w < 8; ++w) cj += wsum[w][tid];
         const double sj = smu[jj] * cj;
         const double w = threshold_weight(sj, sgam[jj], penalty);
+        band_note(band, parity, c, jj, sj, sgam[jj], penalty);
         f_acc += objective_term(sj, sgam[jj], penalty);
         if (w != 0.0) {
           nnz_acc += 1.0;

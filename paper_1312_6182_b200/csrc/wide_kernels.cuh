@@ -21,6 +21,8 @@ constexpr int kWideRows = 2048;  // row chunk of W2 (8 rows per thread)
 struct WideParams {
   double gamma[4];
   double mu[4];
+  BandLog* band;  // near-threshold log (kFused loops), component index comp0 + j
+  int comp0;
 };
 
 template <typename TA, int MG>
@@ -62,6 +64,7 @@ __global__ void __launch_bounds__(kWideThreads) wide_dots_kernel(
         w = coef_threshold ? threshold_weight(c[0], gamma[0], penalty) : c[0];
       } else {
         const double s = mu[j] * c[j];
+        if (mode == kFused && lane == 0) band_note(prm.band, parity, col, prm.comp0 + j, s, gamma[j], penalty);
         f_acc += objective_term(s, gamma[j], penalty);
         w = mode == kFused ? threshold_weight(s, gamma[j], penalty) : 0.0;
       }

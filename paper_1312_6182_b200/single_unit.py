@@ -22,7 +22,7 @@ from dataclasses import dataclass, replace
 import numpy as np
 
 from . import _native
-from .core import RunReport, SparseLoadings, as_data_matrix, positive_part
+from .core import RunReport, SparseLoadings, as_data_matrix, decode_band, positive_part
 from .parallel import DEFAULT_PLAN, fused_sweep, par_matvec_t
 
 UNIT_NORM_TOL = 1e-9
@@ -115,6 +115,20 @@ def recover_pattern_sl0(A, x, gamma, plan=DEFAULT_PLAN):
 _RECOVER = {"l1": recover_pattern_sl1, "l0": recover_pattern_sl0}
 
 
+class Trial(tuple):
+    """(x, history, converged, w) of one loop run; `.band` holds the final
+    sweep's near-threshold entries and their total count."""
+
+    band = (np.zeros(0, dtype=np.int64), 0)
+
+
+def _read_band(fn, handle, cap=8192):
+    out = np.empty(cap, dtype=np.int64)
+    cnt = _native.C.c_int(0)
+    _native.check(fn(handle, out.ctypes.data_as(_native._i64p), cap, _native.C.byref(cnt)))
+    return out[: min(cnt.value, cap)].copy(), int(cnt.value)
+
+
 class PowerLoop:
     """Device power iteration for one (A, penalty, gamma, tol, max_iter):
     a gps_su object reused across restarts / components."""
@@ -145,10 +159,17 @@ class PowerLoop:
         _native.check(_native.lib().gps_su_start(self.handle, _native.dptr(x0)))
 
     def run(self, x0, poll_every=None):
-        """Iterate from x0 to the stopping rule; returns (x, history, converged, w)."""
+        """Iterate from x0 to the stopping rule; returns (x, history, converged, w)
+        carrying the final sweep's near-threshold list as `.band`."""
         self.start(x0)
         _native.check(_native.lib().gps_su_run(self.handle, poll_every or _poll_every()), "power loop")
-        return self.result()
+        trial = Trial(self.result())
+        trial.band = self.band()
+        return trial
+
+    def band(self):
+        """(entries, total) of the final sweep's near-threshold log."""
+        return _read_band(_native.lib().gps_su_band, self.handle)
 
     def result(self):
         A = self.A
@@ -198,12 +219,16 @@ def _initial_iterates(A, config, norms=None, column=None):
     return out
 
 
-def _solve_component(A, gamma, config, plan=DEFAULT_PLAN, loop=None, norms=None, column=None, project=None):
+def _solve_component(A, gamma, config, plan=DEFAULT_PLAN, loop=None, norms=None, column=None, project=None,
+                     info=None):
     """Shared single-component path (single_unit.py:267-284).
 
     Returns (z, history, converged, x).  `project` maps a start vector into
-    the deflated space (implicit deflation)."""
+    the deflated space (implicit deflation).  `info` (a dict), if given,
+    receives the final sweep's near-threshold list as info["band"]."""
     norms = A.norms if norms is None else norms
+    if info is not None:
+        info["band"] = Trial.band
     if gamma >= _activation_limit(norms, config.penalty):
         return np.zeros(A.n), [0.0], True, None
     loop = loop or PowerLoop(A, config.penalty, gamma, config.tol, config.max_iter)
@@ -215,8 +240,10 @@ def _solve_component(A, gamma, config, plan=DEFAULT_PLAN, loop=None, norms=None,
     if config.refine:
         from .refine import refine_support
 
-        best = refine_support(A, best, gamma, config, loop)
+        best = refine_support(A, best, gamma, config, loop, project=project)
     x, history, converged, w = best
+    if info is not None:
+        info["band"] = getattr(best, "band", Trial.band)
     return _normalized(w), history, converged, x
 
 
@@ -229,7 +256,9 @@ def solve_single_unit(A, config, plan=DEFAULT_PLAN):
         raise ValueError("solve_single_unit handles m=1; use solve_multi_sequential")
     launches0 = A.context.launch_count
     start = time.perf_counter()
-    z, history, converged, _ = _solve_component(A, float(config.gamma[0]), config, plan)
+    info = {}
+    z, history, converged, _ = _solve_component(A, float(config.gamma[0]), config, plan, info=info)
+    band, band_total = info["band"]
     loadings = SparseLoadings(z)
     return loadings, RunReport(
         objective_history=history,
@@ -239,6 +268,8 @@ def solve_single_unit(A, config, plan=DEFAULT_PLAN):
         converged=converged,
         component_histories=[history],
         kernel_launches=A.context.launch_count - launches0,
+        near_threshold=decode_band(band, 1),
+        near_threshold_total=band_total,
     )
 
 
@@ -313,7 +344,9 @@ def solve_multi_sequential(A, config, plan=DEFAULT_PLAN):
     launches0 = A.context.launch_count
     start = time.perf_counter()
     defl = _ImplicitDeflation(A)
-    columns, histories = [], []
+    info = {}
+    columns, histories, bands = [], [], []
+    band_total = 0
     converged_all = True
     loops = {}
     for j in range(config.m):
@@ -325,14 +358,18 @@ def solve_multi_sequential(A, config, plan=DEFAULT_PLAN):
         norms = _column_normed_norms(defl)
         z, history, converged, x = _solve_component(
             A, gamma, config, plan, loop=loop, norms=norms, column=defl.column,
-            project=defl.project if defl.X.shape[1] else None)
+            project=defl.project if defl.X.shape[1] else None, info=info)
         columns.append(z)
         histories.append(history)
+        entries, total = info["band"]
+        bands.append(decode_band(entries, 1)[0])
+        band_total += total
         converged_all = converged_all and converged
         if not np.any(z):
             for _ in range(j + 1, config.m):
                 columns.append(np.zeros(A.n))
                 histories.append([0.0])
+                bands.append(np.zeros(0, dtype=np.int64))
             break
         if j + 1 < config.m:
             defl.add(x)
@@ -345,6 +382,8 @@ def solve_multi_sequential(A, config, plan=DEFAULT_PLAN):
         converged=converged_all,
         component_histories=histories,
         kernel_launches=A.context.launch_count - launches0,
+        near_threshold=bands,
+        near_threshold_total=band_total,
     )
 
 

@@ -26,7 +26,7 @@ from gpspca import block as ref_block  # noqa: E402
 from gpspca.single_unit import _solve_component  # noqa: E402
 
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
-from recipes import digest, make_matrix  # noqa: E402
+from recipes import digest, make_matrix, polar_input  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 
@@ -79,7 +79,8 @@ def multi_case(name, recipe, penalty, gamma_rule, m, **cfg):
 def block_case(name, recipe, penalty, gamma_rule, m, mu=1.0, **cfg):
     A = make_matrix(recipe)
     gmax = float(gpspca.column_norms(A).max())
-    gamma = {"0.1max": 0.1 * gmax, "0.1max_sq": (0.1 * gmax) ** 2}.get(gamma_rule, gamma_rule)
+    gamma = {"0.1max": 0.1 * gmax, "0.1max_sq": (0.1 * gmax) ** 2, "0.02max": 0.02 * gmax,
+             "0.02max_sq": (0.02 * gmax) ** 2}.get(gamma_rule, gamma_rule)
     mu_list = np.broadcast_to(np.asarray(mu, dtype=np.float64), (m,)).tolist()
     config = gpspca.SolverConfig(penalty=penalty, mode="block", gamma=gamma, m=m,
                                  mu=mu_list, **cfg)
@@ -138,6 +139,94 @@ def kernel_case():
     return out
 
 
+def b64(M):
+    import base64
+
+    M = np.asfortranarray(M, dtype=np.float64)
+    return {"shape": list(M.shape), "data": base64.b64encode(M.tobytes(order="F")).decode()}
+
+
+def polar_case(name, recipe):
+    """The reference polar_projection (block.py:135-149) on a conditioned G."""
+    G = polar_input(recipe)
+    # G and X are stored bit-exactly (base64 fp64, column-major): an
+    # ill-conditioned G's polar factor moves with the last bits of G, so the
+    # input must not depend on the LAPACK build that regenerates it
+    out = {"name": name, "recipe": recipe, "sha": digest(G), "G": b64(G)}
+    try:
+        out["X"] = b64(ref_block.polar_projection(G).values)
+    except ref_block.RankDeficiencyError as err:
+        out["rank_error"] = {"rank": err.rank, "required": err.required}
+    out["s"] = np.linalg.svd(G, compute_uv=False).tolist()
+    return out
+
+
+def hard_cases():
+    """Round-2 fixtures: block solves at m = 32 / 64 (the C4 code paths:
+    m_pad = 64 tensor-core refine / update, the CholeskyQR2 + Newton-Schulz
+    polar step, CholeskyQR2 init at p m >= 4096), refine with deflation,
+    near-collinear and duplicated max-norm columns at init."""
+    lr64 = {"kind": "lowrank32", "seed": 31, "shape": [256, 4096], "rank": 64, "support": 32, "scale": 4.0}
+    c1 = {"kind": "gauss32", "seed": 0, "shape": [500, 1000]}
+    mu64 = np.linspace(1, 0.5, 64).tolist()
+    return [
+        block_case("lr64_bl0_m64_mu", lr64, "l0", "0.1max_sq", 64, mu=mu64),
+        block_case("lr64_bl0_m64_mu_random", lr64, "l0", "0.1max_sq", 64, mu=mu64,
+                   init="random_orthonormal", seed=5),
+        block_case("lr64_bl0_m64_mu_random_g02", lr64, "l0", "0.02max_sq", 64, mu=mu64,
+                   init="random_orthonormal", seed=5, max_iter=80),
+        block_case("lr64_bl1_m32", lr64, "l1", "0.1max", 32),
+        block_case("lr64_bl1_m32_random", lr64, "l1", "0.1max", 32, init="random_orthonormal", seed=6),
+        block_case("lr64_bl1_m32_random_g02", lr64, "l1", "0.02max", 32, init="random_orthonormal", seed=6,
+                   max_iter=80),
+        block_case("c1_bl1_m64", c1, "l1", "0.1max", 64, max_iter=60),
+        multi_case("c1_multi_sl1_m3_refine", c1, "l1", "0.1max", 3, refine=True),
+        multi_case("c1_multi_sl0_m3_refine", c1, "l0", "0.1max_sq", 3, refine=True),
+        block_case("nearcol_bl1_m2", {"kind": "nearcol", "seed": 41, "shape": [50, 300], "rel": 1e-9}, "l1",
+                   "0.1max", 2),
+        block_case("nearcol_bl1_m3", {"kind": "nearcol", "seed": 42, "shape": [50, 300], "rel": 1e-12}, "l1",
+                   "0.1max", 3),
+    ]
+
+
+def init_error(case_fn, *args, **kw):
+    try:
+        return case_fn(*args, **kw)
+    except ValueError as err:
+        name, recipe = args[0], args[1]
+        A = make_matrix(recipe)
+        return {"name": name, "solver": "block", "recipe": recipe, "sha": digest(A), "penalty": args[2],
+                "gamma": 0.1 * float(gpspca.column_norms(A).max()), "m": args[4], "mu": [1.0] * args[4],
+                "config": {}, "init_error": str(err)}
+
+
+def polar_cases():
+    cases = []
+    for m in (10, 64):
+        for kappa in (10.0, 1e3, 1e5, 1e7):
+            cases.append(polar_case(f"polar_m{m}_k{kappa:g}", {"seed": int(m + np.log10(kappa)),
+                                                                "p": 512 if m == 10 else 128, "m": m,
+                                                                "kappa": kappa}))
+    cases.append(polar_case("polar_rank_keep", {"seed": 90, "p": 4096, "m": 2, "s": [89.9, 4.5e-10]}))
+    cases.append(polar_case("polar_rank_drop", {"seed": 91, "p": 4096, "m": 2, "s": [89.9, 5e-11]}))
+    cases.append(polar_case("polar_rank_zero", {"seed": 92, "p": 300, "m": 10,
+                                                "s": [1.0] * 9 + [0.0]}))
+    return cases
+
+
+def main_hard():
+    cases = hard_cases()
+    cases.append(init_error(block_case, "dupcol_bl1_m2", {"kind": "nearcol", "seed": 43, "shape": [50, 300],
+                                                          "rel": 0.0}, "l1", "0.1max", 2))
+    with open(os.path.join(HERE, "solves_hard.json"), "w") as fh:
+        json.dump({"reference": "gpspca 0.1.0 @ /root/reference/pkg", "numpy": np.__version__,
+                   "cases": cases}, fh)
+    with open(os.path.join(HERE, "polar.json"), "w") as fh:
+        json.dump({"reference": "gpspca 0.1.0 @ /root/reference/pkg", "cases": polar_cases()}, fh)
+    for c in cases:
+        print(c["name"], c.get("iterations"), c.get("nnz"), "rank_error" in c, c.get("init_error"))
+
+
 def main():
     c1 = {"kind": "gauss32", "seed": 0, "shape": [500, 1000]}
     cases = [
@@ -184,4 +273,7 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if "--hard" in sys.argv:
+        main_hard()
+    else:
+        main()

@@ -23,6 +23,16 @@ def make_matrix(recipe):
             V[f * s:(f + 1) * s, f] = e / np.linalg.norm(e)
         A = (U * recipe["scale"]) @ V.T + rng.standard_normal((p, n))
         A = A.astype(np.float32)
+    elif kind == "nearcol":
+        # Gaussian with the two largest columns nearly (or exactly) collinear:
+        # a_0 scaled up, a_1 = a_0 + rel * ||a_0|| * e (built in fp64, so
+        # the matrix must be stored as fp64 to keep the perturbation)
+        rng = np.random.default_rng(recipe["seed"])
+        A = rng.standard_normal((p, n)).astype(np.float32).astype(np.float64)
+        A[:, 0] *= 10.0
+        e = rng.standard_normal(p)
+        A[:, 1] = A[:, 0] + recipe["rel"] * np.linalg.norm(A[:, 0]) * e / np.linalg.norm(e)
+        return A
     elif kind == "zeros":
         A = np.zeros((p, n), dtype=np.float32)
     elif kind == "diag":
@@ -37,6 +47,17 @@ def make_matrix(recipe):
 
 def digest(A):
     return hashlib.sha256(np.asfortranarray(A).tobytes()).hexdigest()[:16]
+
+
+def polar_input(recipe):
+    """G = U diag(s) V' with Haar-like U (p x m), V (m x m): s is
+    logspace(0, -log10 kappa, m) or an explicit list."""
+    rng = np.random.default_rng(recipe["seed"])
+    p, m = recipe["p"], recipe["m"]
+    U = np.linalg.qr(rng.standard_normal((p, m)))[0]
+    V = np.linalg.qr(rng.standard_normal((m, m)))[0]
+    s = np.asarray(recipe["s"], dtype=np.float64) if "s" in recipe else np.logspace(0, -np.log10(recipe["kappa"]), m)
+    return (U * s) @ V.T
 
 
 # ---- recognition-path fixtures (make_golden_recog.py) ----
