@@ -52,6 +52,9 @@ typedef struct gps_bk gps_bk;         /* block solver state                 */
 int gps_version(void);
 const char* gps_last_error(void);
 int gps_device_count(int* count);
+/* Free device memory of the context's GPU (parallel.py:145-157
+ * check_allocation, on HBM instead of host RAM). */
+int gps_device_free_bytes(gps_ctx* ctx, size_t* free_out);
 int gps_ctx_create(int device, gps_ctx** out);
 int gps_ctx_destroy(gps_ctx* ctx);
 /* Use a caller stream (e.g. a torch.cuda.Stream's cuda_stream; not the legacy
@@ -224,6 +227,15 @@ int gps_px_handle_size(void);
 int gps_px_ipc_handle(gps_px* px, void* handle);
 int gps_px_open(gps_px* px, int peer, const void* handle);
 int gps_px_allreduce(gps_px* px, double* buf);
+/* Bound (seconds) on every peer-flag wait of this exchange; default
+ * GPSPCA_PX_TIMEOUT_S or 60 s.  A wait that expires raises the exchange's
+ * error flag (gps_px_error) and stops the attached loop, whose run / poll
+ * then return GPS_E_CUDA instead of every GPU spinning forever. */
+int gps_px_set_timeout(gps_px* px, double seconds);
+int gps_px_error(gps_px* px, int* error_out);
+/* Test: rank 0 of a world-`world` exchange whose peers never arrive must
+ * time out after timeout_s with the error flag set (*error_out = 1). */
+int gps_px_emulate_timeout(gps_ctx* ctx, int world, int64_t count, double timeout_s, int* error_out);
 int gps_px_destroy(gps_px* px);
 /* Fuse the exchange into the loop's cross-CTA reduction (K2): with a peer
  * exchange attached (count = gps_su_exchange's count, or ONE group's

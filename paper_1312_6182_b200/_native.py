@@ -35,6 +35,7 @@ SIGNATURES = {
     "gps_version": (C.c_int, []),
     "gps_last_error": (C.c_char_p, []),
     "gps_device_count": (C.c_int, [_ip]),
+    "gps_device_free_bytes": (C.c_int, [_vp, C.POINTER(C.c_size_t)]),
     "gps_ctx_create": (C.c_int, [C.c_int, C.POINTER(_vp)]),
     "gps_ctx_destroy": (C.c_int, [_vp]),
     "gps_ctx_set_stream": (C.c_int, [_vp, _vp]),
@@ -99,6 +100,9 @@ SIGNATURES = {
     "gps_px_open": (C.c_int, [_vp, C.c_int, _vp]),
     "gps_px_allreduce": (C.c_int, [_vp, _vp]),
     "gps_px_destroy": (C.c_int, [_vp]),
+    "gps_px_set_timeout": (C.c_int, [_vp, C.c_double]),
+    "gps_px_error": (C.c_int, [_vp, _ip]),
+    "gps_px_emulate_timeout": (C.c_int, [_vp, C.c_int, _i64, C.c_double, _ip]),
     "gps_px_emulate": (C.c_int, [_vp, C.c_int, _i64, C.c_int, _dp, _dp]),
     "gps_su_attach_px": (C.c_int, [_vp, _vp]),
     "gps_bk_attach_px": (C.c_int, [_vp, _vp]),

@@ -64,6 +64,12 @@ constexpr int kSmemBudget = 227 * 1024;
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+int exchange_timeout_error() {
+  return fail(GPS_E_CUDA,
+              "peer-memory exchange timed out: a rank stopped, died or launched a different number of exchanges "
+              "(GPSPCA_PX_TIMEOUT_S)");
+}
+
 }  // namespace
 
 struct gps_ctx {
@@ -348,14 +354,15 @@ int launch_sweep(gps_matrix* A, const SweepPlan& plan, SweepArgs args, int mode,
 }
 
 int launch_reduce(gps_ctx* ctx, const double* part_g, const double* part_s, int nparts, int ld, double* exch,
-                  const GpsCtl* ctl, int nparts_s = -1, const gps_px* px = nullptr) {
+                  const GpsCtl* ctl, int nparts_s = -1, const gps_px* px = nullptr,
+                  const SuStepArgs* step = nullptr) {
   if (px != nullptr) {
     // K2 fused with the peer-memory all-reduce (px_kernels.cuh)
     if (px->view.count != int64_t(ld) + 4) return fail(GPS_E_ARG, "peer exchange sized for %lld, reduce has %d + 4",
                                                       static_cast<long long>(px->view.count), ld);
-    su_reduce_px_kernel<<<px_uniform_chunks(ld) + 1, 256, 0, ctx->stream>>>(part_g, part_s, nparts, ld, exch, ctl,
-                                                                            nparts_s < 0 ? nparts : nparts_s,
-                                                                            px->view);
+    su_reduce_px_kernel<<<px_uniform_chunks(ld) + 1, 256, 0, ctx->stream>>>(
+        part_g, part_s, nparts, ld, exch, const_cast<GpsCtl*>(ctl), nparts_s < 0 ? nparts : nparts_s, px->view,
+        step != nullptr ? *step : SuStepArgs{});
     ctx->launches++;
     GPS_CHECK_LAUNCH("su_reduce_px_kernel launch");
     return GPS_OK;
@@ -461,6 +468,15 @@ extern "C" {
 int gps_version(void) { return 1; }
 
 const char* gps_last_error(void) { return g_last_error.c_str(); }
+
+int gps_device_free_bytes(gps_ctx* ctx, size_t* free_out) {
+  if (!ctx || !free_out) return fail(GPS_E_ARG, "NULL argument");
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  size_t fr = 0, total = 0;
+  GPS_CUDA(cudaMemGetInfo(&fr, &total));
+  *free_out = fr;
+  return GPS_OK;
+}
 
 int gps_device_count(int* count) {
   if (!count) return fail(GPS_E_ARG, "count is NULL");
@@ -1040,6 +1056,20 @@ int gps_su_start(gps_su* s, const double* x0) {
   return GPS_OK;
 }
 
+static SuStepArgs su_step_args(const gps_su* s) {
+  SuStepArgs a{};
+  a.ld = static_cast<int>(s->A->ld);
+  a.xbuf = s->x;
+  a.x_stride = s->A->ld;
+  a.hist = s->hist;
+  a.tol = s->tol;
+  a.max_iter = s->max_iter;
+  a.defl_X = s->defl;
+  a.defl_k = s->defl_k;
+  a.band = s->band;
+  return a;
+}
+
 static int su_enqueue_sweep_nolock(gps_su* s, int mask = 3) {
   const SweepPlan& plan = s->plan;
   int rc = GPS_OK;
@@ -1056,16 +1086,20 @@ static int su_enqueue_sweep_nolock(gps_su* s, int mask = 3) {
   args.band = s->band;
   if (mask & 1) rc = launch_sweep(s->A, plan, args, kFused, s->wbuf);
   if (rc) return rc;
-  if (mask & 2)
+  if (mask & 2) {
+    // with a peer exchange attached the step runs in the exchange kernel's
+    // last CTA (su_reduce_px_kernel): one launch fewer per iteration
+    const SuStepArgs step = su_step_args(s);
     rc = launch_reduce(s->A->ctx, s->part_g, s->part_s, plan.grid, static_cast<int>(s->A->ld), s->exch, s->ctl, -1,
-                       s->px);
+                       s->px, s->px != nullptr ? &step : nullptr);
+  }
   return rc;
 }
 
 static int su_enqueue_step_nolock(gps_su* s) {
   gps_ctx* ctx = s->A->ctx;
-  su_step_kernel<<<1, kStepThreads, 0, ctx->stream>>>(s->exch, static_cast<int>(s->A->ld), s->x, s->A->ld, s->hist,
-                                                      s->ctl, s->tol, s->max_iter, s->defl, s->defl_k, s->band);
+  if (s->px != nullptr) return GPS_OK;  // fused into the exchange (su_enqueue_sweep_nolock)
+  su_step_kernel<<<1, kStepThreads, 0, ctx->stream>>>(s->exch, s->ctl, su_step_args(s));
   ctx->launches++;
   GPS_CHECK_LAUNCH("su_step_kernel launch");
   return GPS_OK;
@@ -1141,13 +1175,14 @@ int gps_su_poll(gps_su* s, int* done, int* iter, int* converged) {
   gps_ctx* ctx = s->A->ctx;
   GPS_CUDA(cudaMemcpyAsync(s->ctl_host, s->ctl, sizeof(GpsCtl), cudaMemcpyDeviceToHost, ctx->stream));
   GPS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (s->ctl_host->status == kStatusExchangeTimeout) return exchange_timeout_error();
   if (done) *done = s->ctl_host->done;
   if (iter) *iter = s->ctl_host->iter;
   if (converged) *converged = s->ctl_host->converged;
   return GPS_OK;
 }
 
-int gps_su_launches_per_iter(gps_su* s) { return s ? 3 : 0; }
+int gps_su_launches_per_iter(gps_su* s) { return s ? (s->px != nullptr ? 2 : 3) : 0; }
 
 int gps_su_run(gps_su* s, int poll_every) {
   if (!s) return fail(GPS_E_ARG, "NULL argument");
@@ -1181,9 +1216,10 @@ int gps_su_run(gps_su* s, int poll_every) {
   const int max_chunks = (s->max_iter + 1 + poll_every - 1) / poll_every + 1;
   for (int c = 0; c < max_chunks; ++c) {
     GPS_CUDA(cudaGraphLaunch(s->graph, ctx->stream));
-    ctx->launches += int64_t(3) * poll_every;
+    ctx->launches += int64_t(gps_su_launches_per_iter(s)) * poll_every;
     GPS_CUDA(cudaMemcpyAsync(s->ctl_host, s->ctl, sizeof(GpsCtl), cudaMemcpyDeviceToHost, ctx->stream));
     GPS_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (s->ctl_host->status == kStatusExchangeTimeout) return exchange_timeout_error();
     if (s->ctl_host->done) return GPS_OK;
   }
   return fail(GPS_E_CUDA, "power loop did not reach its stopping rule within max_iter");
@@ -2018,6 +2054,7 @@ int gps_bk_poll(gps_bk* s, int* done, int* iter, int* converged) {
   gps_ctx* ctx = s->A->ctx;
   GPS_CUDA(cudaMemcpyAsync(s->ctl_host, s->ctl, sizeof(GpsCtl), cudaMemcpyDeviceToHost, ctx->stream));
   GPS_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (s->ctl_host->status == kStatusExchangeTimeout) return exchange_timeout_error();
   if (done) *done = s->ctl_host->done;
   if (iter) *iter = s->ctl_host->iter;
   if (converged) *converged = s->ctl_host->converged;
@@ -2060,6 +2097,7 @@ int gps_bk_run(gps_bk* s, int poll_every) {
     ctx->launches += s->graph_launches;
     GPS_CUDA(cudaMemcpyAsync(s->ctl_host, s->ctl, sizeof(GpsCtl), cudaMemcpyDeviceToHost, ctx->stream));
     GPS_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (s->ctl_host->status == kStatusExchangeTimeout) return exchange_timeout_error();
     if (s->ctl_host->done) return GPS_OK;
   }
   return fail(GPS_E_CUDA, "block loop did not reach its stopping rule within max_iter");
@@ -2207,6 +2245,13 @@ void px_bind(PxView& v, int q, void* base, size_t flags_off) {
 }
 }  // namespace
 
+// Bound on every peer-flag wait: GPSPCA_PX_TIMEOUT_S seconds (default 60).
+unsigned long long px_timeout_ns() {
+  const char* t = std::getenv("GPSPCA_PX_TIMEOUT_S");
+  const double s = t ? std::strtod(t, nullptr) : 60.0;
+  return static_cast<unsigned long long>((s > 0 ? s : 60.0) * 1e9);
+}
+
 int gps_px_create(gps_ctx* ctx, int world, int rank, int64_t count, gps_px** out) {
   if (!ctx || !out) return fail(GPS_E_ARG, "NULL argument");
   if (world < 1 || world > kPxMaxWorld) return fail(GPS_E_UNSUPPORTED, "world=%d outside [1, %d]", world, kPxMaxWorld);
@@ -2229,6 +2274,7 @@ int gps_px_create(gps_ctx* ctx, int world, int rank, int64_t count, gps_px** out
   px->view.rank = rank;
   px->view.count = count;
   px->view.nchunks = px_nchunks(count);
+  px->view.timeout_ns = px_timeout_ns();
   px->view.state = reinterpret_cast<PxState*>(static_cast<char*>(px->local) + soff);
   px_bind(px->view, rank, px->local, foff);
   *out = px;
@@ -2286,6 +2332,64 @@ int gps_px_destroy(gps_px* px) {
   return GPS_OK;
 }
 
+int gps_px_set_timeout(gps_px* px, double seconds) {
+  if (!px || !(seconds > 0)) return fail(GPS_E_ARG, "bad arguments");
+  px->view.timeout_ns = static_cast<unsigned long long>(seconds * 1e9);
+  return GPS_OK;
+}
+
+int gps_px_error(gps_px* px, int* error_out) {
+  if (!px || !error_out) return fail(GPS_E_ARG, "NULL argument");
+  GPS_CUDA(cudaSetDevice(px->ctx->device));
+  unsigned int err = 0;
+  GPS_CUDA(cudaMemcpyAsync(&err, &px->view.state->error, sizeof(unsigned), cudaMemcpyDeviceToHost, px->ctx->stream));
+  GPS_CUDA(cudaStreamSynchronize(px->ctx->stream));
+  *error_out = static_cast<int>(err);
+  return GPS_OK;
+}
+
+// A rank whose peers never arrive: only rank 0's CTAs of a world-`world`
+// exchange run, so every flag wait must expire after timeout_s, raise the
+// error flag and return (the bounded-wait guarantee of px_gather).
+int gps_px_emulate_timeout(gps_ctx* ctx, int world, int64_t count, double timeout_s, int* error_out) {
+  if (!ctx || !error_out || world < 2 || world > kPxMaxWorld || count < 1 || !(timeout_s > 0))
+    return fail(GPS_E_ARG, "bad arguments");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  size_t foff = 0, soff = 0;
+  const size_t bytes = px_bytes(world, count, &foff, &soff);
+  char* bufs = nullptr;
+  double* vec = nullptr;
+  cudaError_t e = cudaMalloc(&bufs, bytes * world);
+  if (e == cudaSuccess) e = cudaMalloc(&vec, size_t(count) * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemsetAsync(bufs, 0, bytes * world, ctx->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(vec, 0, size_t(count) * sizeof(double), ctx->stream);
+  PxEmu emu{};
+  PxView& v = emu.view[0];
+  v.world = world;
+  v.rank = 0;
+  v.count = count;
+  v.nchunks = px_nchunks(count);
+  v.timeout_ns = static_cast<unsigned long long>(timeout_s * 1e9);
+  v.state = reinterpret_cast<PxState*>(bufs + soff);
+  for (int q = 0; q < world; ++q) px_bind(v, q, bufs + bytes * q, foff);
+  emu.vecs[0] = vec;
+  if (e == cudaSuccess) {
+    px_emulate_kernel<<<dim3(px_uniform_chunks(count), 1), 256, 0, ctx->stream>>>(emu);
+    ctx->launches++;
+    e = cudaGetLastError();
+  }
+  unsigned int err = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&err, &v.state->error, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                                            ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  cudaFree(bufs);
+  cudaFree(vec);
+  if (e != cudaSuccess) return cuda_fail(e, "gps_px_emulate_timeout");
+  *error_out = static_cast<int>(err);
+  return GPS_OK;
+}
+
 int gps_px_emulate(gps_ctx* ctx, int world, int64_t count, int rounds, const double* in, double* out) {
   if (!ctx || !in || !out) return fail(GPS_E_ARG, "NULL argument");
   if (world < 1 || world > kPxMaxWorld || count < 1 || rounds < 1) return fail(GPS_E_ARG, "bad arguments");
@@ -2306,6 +2410,7 @@ int gps_px_emulate(gps_ctx* ctx, int world, int64_t count, int rounds, const dou
     v.rank = r;
     v.count = count;
     v.nchunks = nch;
+    v.timeout_ns = px_timeout_ns();
     v.state = reinterpret_cast<PxState*>(bufs + bytes * r + soff);
     for (int q = 0; q < world; ++q) px_bind(v, q, bufs + bytes * q, foff);
     emu.vecs[r] = vecs + size_t(r) * count;
@@ -2380,6 +2485,7 @@ int gps_px_emulate_reduce(gps_ctx* ctx, int world, int rows, int nparts, int npa
     v.rank = r;
     v.count = count;
     v.nchunks = px_nchunks(count);
+    v.timeout_ns = px_timeout_ns();
     v.state = reinterpret_cast<PxState*>(bufs + bytes * r + soff);
     for (int q = 0; q < world; ++q) px_bind(v, q, bufs + bytes * q, foff);
     emu.part_g[r] = dg + ng * r;

@@ -34,7 +34,7 @@ constexpr int kPxChunk = 4096;  // doubles per CTA (32 KB)
 struct PxState {
   unsigned long long epoch;
   unsigned int done_ctas;
-  unsigned int pad;
+  unsigned int error;  // 1: a wait timed out (a peer stopped, died or diverged)
 };
 
 // One rank's view of the symmetric buffers: base pointers of every rank's
@@ -47,7 +47,18 @@ struct PxView {
   int rank;
   int64_t count;
   int nchunks;
+  unsigned long long timeout_ns;  // bound on every flag wait (globaltimer)
 };
+
+// Loop status written by a timed-out exchange (GpsCtl::status): the loop
+// stops and the host raises instead of every GPU spinning forever.
+constexpr int kStatusExchangeTimeout = 4;
+
+__device__ __forceinline__ unsigned long long px_now_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __host__ __device__ inline size_t px_slots_bytes(int world, int64_t count) {
   return size_t(2) * world * count * sizeof(double);
@@ -79,15 +90,30 @@ __device__ __forceinline__ void px_signal(const PxView& v, int c, unsigned long 
   }
 }
 // Wait until every rank published chunk c at this rank, then write the
-// rank-order sum of elements [lo, hi) into vec.
-__device__ __forceinline__ void px_gather(const PxView& v, double* vec, int c, int64_t lo, int64_t hi,
+// rank-order sum of elements [lo, hi) into vec.  Every wait is bounded by
+// v.timeout_ns: on expiry the error flag is raised and false returned
+// (vec untouched), so a rank that stopped, died or launched a different
+// number of exchanges cannot hang its peers.
+__device__ __forceinline__ bool px_gather(const PxView& v, double* vec, int c, int64_t lo, int64_t hi,
                                           unsigned long long e) {
+  __shared__ int s_timeout;
   const int par = static_cast<int>(e & 1ull);
+  if (threadIdx.x == 0) s_timeout = 0;
+  __syncthreads();
   if (threadIdx.x < v.world) {
     const unsigned long long* f = v.flags[v.rank] + size_t(threadIdx.x) * v.nchunks + c;
-    while (px_load_acquire_sys(f) < e) __nanosleep(64);
+    const unsigned long long t0 = px_now_ns();
+    while (px_load_acquire_sys(f) < e) {
+      if (px_now_ns() - t0 > v.timeout_ns) {
+        s_timeout = 1;
+        atomicExch(&v.state->error, 1u);
+        break;
+      }
+      __nanosleep(64);
+    }
   }
   __syncthreads();
+  if (s_timeout) return false;
   // fixed rank-order sum (L2 loads: the slots are written by peers)
   const double* own = v.slots[v.rank] + size_t(par) * v.world * v.count;
   for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
@@ -95,6 +121,7 @@ __device__ __forceinline__ void px_gather(const PxView& v, double* vec, int c, i
     for (int q = 1; q < v.world; ++q) s += __ldcg(own + size_t(q) * v.count + i);
     vec[i] = s;
   }
+  return true;
 }
 // Element i of this rank's epoch-e vector into slots[e&1][rank][i] at every rank.
 __device__ __forceinline__ void px_put(const PxView& v, int64_t i, double x, unsigned long long e) {
@@ -108,21 +135,28 @@ __device__ __forceinline__ void px_chunk(const PxView& v, double* vec, int c, un
   const int64_t hi = lo + kPxChunk < v.count ? lo + kPxChunk : v.count;
   for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) px_put(v, i, vec[i], e);
   px_signal(v, c, e);
-  px_gather(v, vec, c, lo, hi, e);
+  px_gather(v, vec, c, lo, hi, e);  // a timeout is reported through v.state->error
 }
 
 // Epoch bookkeeping: every CTA reads the epoch before it finishes; the last
-// CTA to finish publishes it for the next launch (stream order).
-__device__ __forceinline__ void px_finish(PxState* st, unsigned long long e) {
+// CTA to finish publishes it for the next launch (stream order).  Returns
+// true (block-uniform) in the last CTA, after a fence that makes every other
+// CTA's writes of this launch visible to it.
+__device__ __forceinline__ bool px_finish(PxState* st, unsigned long long e) {
+  __shared__ int s_last;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
+    s_last = 0;
     if (atomicAdd(&st->done_ctas, 1u) == gridDim.x - 1u) {
       st->epoch = e;
       st->done_ctas = 0;
       __threadfence();
+      s_last = 1;
     }
   }
+  __syncthreads();
+  return s_last != 0;
 }
 
 __global__ void __launch_bounds__(256) px_allreduce_kernel(const PxView v, double* vec) {
@@ -152,7 +186,7 @@ __global__ void __launch_bounds__(256) px_emulate_kernel(const PxEmu emu) {
 // Chunk c < nrc: rows [c kPxChunk, ...) of the `rows`-long partial vector,
 // 32-row sub-blocks as in su_reduce_kernel; chunk nrc: the 4 scalars at
 // offset rows.  v.count == rows + 4.
-__device__ __forceinline__ void px_reduce_chunk(const PxView& v, const double* __restrict__ part_g,
+__device__ __forceinline__ bool px_reduce_chunk(const PxView& v, const double* __restrict__ part_g,
                                                 const double* __restrict__ part_s, int nparts, int rows,
                                                 int nparts_s, double* exch, int c, unsigned long long e) {
   __shared__ double part[kReduceSlices][kReduceRows];
@@ -180,7 +214,7 @@ __device__ __forceinline__ void px_reduce_chunk(const PxView& v, const double* _
       __syncthreads();
     }
     px_signal(v, c, e);
-    px_gather(v, exch, c, lo, hi, e);
+    return px_gather(v, exch, c, lo, hi, e);
   } else {
     if (threadIdx.x < 128) {
       const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -190,18 +224,28 @@ __device__ __forceinline__ void px_reduce_chunk(const PxView& v, const double* _
       if (lane == 0) px_put(v, rows + k, t, e);
     }
     px_signal(v, c, e);
-    px_gather(v, exch, c, rows, int64_t(rows) + 4, e);
+    return px_gather(v, exch, c, rows, int64_t(rows) + 4, e);
   }
 }
 
+// With step.xbuf set (single-unit loops) the last CTA to finish also runs the
+// power step (K3's su_step_body, same arithmetic) on the all-reduced vector:
+// sweep partials -> exchange -> step in one launch per iteration.
 __global__ void __launch_bounds__(256) su_reduce_px_kernel(const double* __restrict__ part_g,
                                                            const double* __restrict__ part_s, int nparts, int rows,
-                                                           double* __restrict__ exch, const GpsCtl* ctl,
-                                                           int nparts_s, const PxView v) {
+                                                           double* __restrict__ exch, GpsCtl* ctl, int nparts_s,
+                                                           const PxView v, const SuStepArgs step) {
   if (ctl != nullptr && ctl->done) return;  // identical on every rank (replicated step)
   const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&v.state->epoch) + 1ull;
-  px_reduce_chunk(v, part_g, part_s, nparts, rows, nparts_s, exch, blockIdx.x, e);
-  px_finish(v.state, e);
+  const bool ok = px_reduce_chunk(v, part_g, part_s, nparts, rows, nparts_s, exch, blockIdx.x, e);
+  if (!ok && ctl != nullptr && threadIdx.x == 0) {
+    ctl->status = kStatusExchangeTimeout;
+    ctl->done = 1;
+  }
+  const bool last = px_finish(v.state, e);
+  if (last && ctl != nullptr && step.xbuf != nullptr &&
+      *reinterpret_cast<volatile unsigned int*>(&v.state->error) == 0u)
+    su_step_body(exch, ctl, step);
 }
 
 // Test emulation of the fused reduction: block (c, r) runs rank r's chunk c.

@@ -439,45 +439,80 @@ __global__ void __launch_bounds__(256) su_reduce_kernel(const double* __restrict
   }
 }
 
-// K3: one power step (single_unit.py:167-180) on the reduced exchange
-// vector: history, the relative-change stopping rule, the zero-gradient
-// fixed point, and x_{k+1} = g / ||g|| into the other parity slot.  With
-// defl_k > 0 the gradient is first projected off the previous components
-// (implicit deflation, single_unit.py:287-296: g = (I - x_l x_l') ... g in
-// component order), so A is never rewritten.
 constexpr int kStepThreads = 1024;
+constexpr int kStepLanes = 1024;  // virtual lanes of the step's reductions
 
-__device__ __forceinline__ double block_sum_1024(double v, double* red) {
-  v = warp_sum(v);
-  const int tid = threadIdx.x;
-  __syncthreads();  // red reuse
-  if ((tid & 31) == 0) red[tid >> 5] = v;
+// Sum of vl[0 .. 1024) in the order of a 1024-thread block reduction (warp
+// xor-butterflies, lane 0 of each warp, then the same over the 32 warp
+// sums), computed by any block size: the step's arithmetic is therefore
+// identical whether it runs as K3 (1024 threads) or inside the last CTA of
+// the fused exchange kernel (256 threads).
+__device__ double vlane_tree(const double* vl, double* red) {
   __syncthreads();
-  double u = tid < 32 ? red[tid] : 0.0;
-  if (tid < 32) u = warp_sum(u);
-  if (tid == 0) red[32] = u;
+  const int tid = threadIdx.x;
+  if (tid < 32) {
+    double s[32];
+#pragma unroll
+    for (int l = 0; l < 32; ++l) s[l] = vl[tid * 32 + l];
+#pragma unroll
+    for (int o = 16; o; o >>= 1)
+#pragma unroll
+      for (int l = 0; l < o; ++l) s[l] = s[l] + s[l + o];
+    red[tid] = s[0];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double s[32];
+#pragma unroll
+    for (int l = 0; l < 32; ++l) s[l] = red[l];
+#pragma unroll
+    for (int o = 16; o; o >>= 1)
+#pragma unroll
+      for (int l = 0; l < o; ++l) s[l] = s[l] + s[l + o];
+    red[32] = s[0];
+  }
   __syncthreads();
   return red[32];
 }
 
-__global__ void __launch_bounds__(kStepThreads) su_step_kernel(const double* exch, int ld,
-                                                              double* __restrict__ xbuf, int64_t x_stride,
-                                                              double* __restrict__ hist, GpsCtl* ctl,
-                                                              double tol, int max_iter,
-                                                              const double* __restrict__ defl_X, int defl_k,
-                                                              BandLog* band) {
+// sum_r a[r] b[r] over r < ld: virtual lane v accumulates r = v, v + 1024, ...
+__device__ double step_dot(const double* a, const double* b, int ld, double* vl, double* red) {
+  for (int v = threadIdx.x; v < kStepLanes; v += blockDim.x) {
+    double t = 0.0;
+    for (int r = v; r < ld; r += kStepLanes) t = fma(__ldcg(a + r), __ldcg(b + r), t);
+    vl[v] = t;
+  }
+  return vlane_tree(vl, red);
+}
+
+struct SuStepArgs {
+  int ld;
+  double* xbuf;  // [2][ld] iterate parity slots
+  int64_t x_stride;
+  double* hist;
+  double tol;
+  int max_iter;
+  const double* defl_X;  // [defl_k][ld] earlier components (implicit deflation)
+  int defl_k;
+  BandLog* band;
+};
+
+// The power step on the reduced exchange vector g = exch[0 .. ld), f =
+// exch[ld] (any block size; g is read through L2: in the fused exchange it
+// was written by other CTAs of the same launch).
+__device__ void su_step_body(double* g, GpsCtl* ctl, const SuStepArgs& a) {
+  __shared__ double vl[kStepLanes];
   __shared__ double red[33];
   __shared__ int decision;
-  if (ctl->done) return;
   const int k = ctl->iter;
-  const double f = exch[ld];
+  const double f = __ldcg(g + a.ld);
   const double f_prev = ctl->f_prev;
   const int tid = threadIdx.x;
   if (tid == 0) {
-    hist[k] = f;
+    a.hist[k] = f;
     int d = 0;  // 0 continue, 1 converged, 2 max_iter
-    if (k >= 1 && fabs(f - f_prev) < tol * fmax(fabs(f_prev), 1e-30)) d = 1;
-    else if (k >= max_iter) d = 2;
+    if (k >= 1 && fabs(f - f_prev) < a.tol * fmax(fabs(f_prev), 1e-30)) d = 1;
+    else if (k >= a.max_iter) d = 2;
     decision = d;
   }
   __syncthreads();
@@ -488,20 +523,14 @@ __global__ void __launch_bounds__(kStepThreads) su_step_kernel(const double* exc
     }
     return;
   }
-  // g lives in the exchange vector (global, L2-resident); projections and
-  // the normalisation are strided block loops, so any ld is handled.
-  double* g = const_cast<double*>(exch);
-  for (int l = 0; l < defl_k; ++l) {
-    const double* xl = defl_X + size_t(l) * ld;
-    double t = 0.0;
-    for (int r = tid; r < ld; r += kStepThreads) t = fma(xl[r], g[r], t);
-    const double d = block_sum_1024(t, red);
-    for (int r = tid; r < ld; r += kStepThreads) g[r] = fma(-d, xl[r], g[r]);
+  // projections and the normalisation are strided block loops: any ld
+  for (int l = 0; l < a.defl_k; ++l) {
+    const double* xl = a.defl_X + size_t(l) * a.ld;
+    const double d = step_dot(xl, g, a.ld, vl, red);
+    for (int r = tid; r < a.ld; r += blockDim.x) g[r] = fma(-d, xl[r], __ldcg(g + r));
     __syncthreads();
   }
-  double t = 0.0;
-  for (int r = tid; r < ld; r += kStepThreads) t = fma(g[r], g[r], t);
-  const double nrm = sqrt(block_sum_1024(t, red));
+  const double nrm = sqrt(step_dot(g, g, a.ld, vl, red));
   if (nrm == 0.0) {
     if (tid == 0) {
       ctl->done = 1;
@@ -510,14 +539,25 @@ __global__ void __launch_bounds__(kStepThreads) su_step_kernel(const double* exc
     }
     return;
   }
-  double* xn = xbuf + ((k + 1) & 1) * x_stride;
-  for (int r = tid; r < ld; r += kStepThreads) xn[r] = g[r] / nrm;
+  double* xn = a.xbuf + ((k + 1) & 1) * a.x_stride;
+  for (int r = tid; r < a.ld; r += blockDim.x) xn[r] = __ldcg(g + r) / nrm;
   if (tid == 0) {
-    if (band != nullptr) band->count[(k + 1) & 1] = 0;  // sweep k + 1 logs afresh
+    if (a.band != nullptr) a.band->count[(k + 1) & 1] = 0;  // sweep k + 1 logs afresh
     ctl->f_prev = f;
     ctl->gnorm = nrm;
     ctl->iter = k + 1;
   }
+}
+
+// K3: one power step (single_unit.py:167-180) on the reduced exchange
+// vector: history, the relative-change stopping rule, the zero-gradient
+// fixed point, and x_{k+1} = g / ||g|| into the other parity slot.  With
+// defl_k > 0 the gradient is first projected off the previous components
+// (implicit deflation, single_unit.py:287-296: g = (I - x_l x_l') ... g in
+// component order), so A is never rewritten.
+__global__ void __launch_bounds__(kStepThreads) su_step_kernel(double* exch, GpsCtl* ctl, const SuStepArgs a) {
+  if (ctl->done) return;
+  su_step_body(exch, ctl, a);
 }
 
 // K0: column norms ||a_i|| with fp64 accumulation plus a non-finite flag

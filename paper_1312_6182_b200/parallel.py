@@ -107,3 +107,69 @@ def fused_sweep(A, x, gamma, penalty, want_c=False, want_w=False):
         _native.dptr(g), _native.dptr(c) if want_c else None, _native.dptr(w) if want_w else None,
         _native.C.byref(nnz)))
     return f.value, g, c, w, nnz.value
+
+
+def check_allocation(P, N, itemsize=8):
+    """MemoryError before allocating a P x N matrix that cannot fit in the
+    current device's free memory (the reference checks host RAM for its
+    fp64 copy, parallel.py:145-157; the engine's copy lives in HBM)."""
+    needed = int(P) * int(N) * int(itemsize)
+    free = _native.C.c_size_t(0)
+    if _native.lib().gps_device_free_bytes(_native.context().handle, _native.C.byref(free)) != _native.GPS_OK:
+        return
+    if needed > free.value:
+        raise MemoryError(f"a {P}x{N} matrix needs {needed} bytes but only {free.value} are free on the device")
+
+
+def _kernel_invocation(kernel, A, rng):
+    if kernel == "matvec_t":
+        x = rng.standard_normal(A.p)
+        return lambda plan: par_matvec_t(A, x, plan)
+    if kernel == "gram_apply":
+        z = rng.standard_normal(A.n)
+        return lambda plan: par_gram_apply(A, z, plan)
+    if kernel == "threshold_accumulate":
+        x = rng.standard_normal(A.p)
+        c = par_matvec_t(A, x)
+        gamma = 0.05 * float(np.max(np.abs(c)))
+        return lambda plan: par_threshold_accumulate(A, c, gamma, "l1", plan)
+    raise ValueError(f"unknown kernel {kernel!r}; expected one of {KERNELS}")
+
+
+def measure_scaling(kernel, sizes, workers, instances=20, chunk=256, seed=0):
+    """Median wall times of one kernel-seam call over a (P, N) grid and the
+    given worker counts (parallel.py:175-215: same rows, order and
+    speedup-vs-workers=1 definition).  On the device `workers` selects
+    nothing -- the grid is fixed -- so the rows report the device call time
+    per plan and speedups near 1; the harness is kept so callers of the
+    reference's scaling table run unchanged."""
+    import time
+
+    if not sizes:
+        raise ValueError("sizes must be nonempty")
+    if instances < 1:
+        raise ValueError("instances must be >= 1")
+    if kernel not in KERNELS:
+        raise ValueError(f"unknown kernel {kernel!r}; expected one of {KERNELS}")
+    workers = sorted(set(int(w) for w in workers))
+    if 1 not in workers:
+        workers = [1] + workers
+    rows = []
+    for P, N in sorted(sizes, key=lambda s: s[1]):
+        check_allocation(P, N)
+        times = {w: [] for w in workers}
+        for instance in range(instances):
+            rng = np.random.default_rng([seed, N, instance])
+            A = as_data_matrix(rng.standard_normal((P, N)))
+            run = _kernel_invocation(kernel, A, rng)
+            for w in workers:
+                plan = KernelPlan(workers=w, chunk=chunk)
+                start = time.perf_counter()
+                run(plan)
+                times[w].append(time.perf_counter() - start)
+        base = float(np.median(times[1]))
+        for w in workers:
+            med = float(np.median(times[w]))
+            rows.append({"kernel": kernel, "N": N, "P": P, "workers": w, "median_seconds": med,
+                         "speedup": base / med if med > 0 else float("nan")})
+    return rows

@@ -150,3 +150,46 @@ def test_fused_reduce_world_one_solve_matches():
         del loop
     finally:
         L.gps_px_destroy(h)
+
+
+def test_fused_step_world_one_with_deflation():
+    """The power step fused into the exchange kernel's last CTA (one launch
+    fewer per iteration) with implicit deflation active: bitwise equal to
+    the separate K3."""
+    rng = np.random.default_rng(4)
+    A = rng.standard_normal((300, 3001)).astype(np.float32)
+    D = gps.DataMatrix(A)
+    gamma = 0.05 * float(np.asarray(D.norms).max())
+    X = np.linalg.qr(rng.standard_normal((300, 2)))[0]
+    x0 = rng.standard_normal(300)
+    x0 -= X @ (X.T @ x0)
+    x0 /= np.linalg.norm(x0)
+    ref_loop = gps.single_unit.PowerLoop(D, "l1", gamma, 1e-8, 300)
+    ref_loop.set_deflation(X)
+    x_ref, h_ref, _, w_ref = ref_loop.run(x0)
+    L = _native.lib()
+    h = _native._vp()
+    _native.check(L.gps_px_create(D.context.handle, 1, 0, 320 + 4, _native.C.byref(h)))
+    try:
+        loop = gps.single_unit.PowerLoop(D, "l1", gamma, 1e-8, 300)
+        loop.set_deflation(X)
+        _native.check(L.gps_su_attach_px(loop.handle, h))
+        assert L.gps_su_launches_per_iter(loop.handle) == 2
+        x, hist, _, w = loop.run(x0)
+        assert hist == h_ref and np.array_equal(w, w_ref) and np.array_equal(x, x_ref)
+        del loop
+    finally:
+        L.gps_px_destroy(h)
+
+
+def test_exchange_wait_is_bounded():
+    """A rank whose peers never arrive times out (error flag) instead of
+    spinning forever (px_gather's globaltimer deadline)."""
+    import time
+
+    ctx = _native.context()
+    err = _native.C.c_int(0)
+    t0 = time.perf_counter()
+    _native.check(_native.lib().gps_px_emulate_timeout(ctx.handle, 2, 5000, 0.2, _native.C.byref(err)))
+    assert err.value == 1
+    assert time.perf_counter() - t0 < 30
