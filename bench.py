@@ -16,12 +16,16 @@ events; `e2e` times the same power iteration through the public API with
 host buffers (x in, f and the ascent direction out, A resident after a
 one-time upload from pinned host memory), and reports a full
 `solve_single_unit` from pinned host memory (16 GiB upload included) beside it.
-`--impl reference` times the CPU reference algorithm (the NumPy oracle port
-in oracle/, BLAS on all host cores) on a bounded column sample of the same
-workload and extrapolates per-iteration time linearly in n.
+`--impl reference` times the unmodified reference package (gpspca 0.1.0,
+installed into baseline/_ref) on the host cores: real iterations of its own
+loop on the FULL C2 instance (the same matrix, copied from the GPU).
 
-N > 1 (torchrun): strong scaling of the same A, column-sharded, one NCCL
-all-reduce of the p+4 exchange vector per iteration.
+N > 1 (torchrun): strong scaling of the same A, column-sharded; the one
+exchange per iteration (the p + 4 vector: g, f, nnz) is fused into the
+reduction kernel over NVLink peer memory (su_reduce_px_kernel, which also
+runs the power step in its last CTA) when every rank has its own
+peer-capable GPU, else a torch.distributed all-reduce (NCCL, or gloo for
+functional checks); `config.exchange` names the path taken.
 """
 
 import argparse
@@ -127,11 +131,13 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def make_c2(torch, p, n_local, col0, n_global, device, seed=0):
+def make_lowrank(torch, p, n_local, col0, n_global, device, n_classes, n_factors, support, seed=0):
     """Low-rank + noise A (p x n_local, column-major == torch (n_local, p)),
-    distributed like synthetic_sparse_factors(16, 256, n, 5, n//100, 4, 1, 1)."""
-    n_classes, n_factors = 16, 5
-    support = n_global // 100
+    columns [col0, col0 + n_local) of a p x n_global instance distributed like
+    synthetic_sparse_factors(n_classes, p / n_classes, n_global, n_factors,
+    support, class_scale 4, within 1, noise 1) (datasets.py:278-309): factor f
+    lives on the disjoint column block [f support, (f + 1) support) with unit
+    loadings, samples = latent W' + N(0, 1)."""
     rng = np.random.default_rng(seed)
     means = rng.standard_normal((n_classes, n_factors)) * 4.0
     labels = np.repeat(np.arange(n_classes), p // n_classes)
@@ -151,94 +157,259 @@ def make_c2(torch, p, n_local, col0, n_global, device, seed=0):
     return At
 
 
+def make_c2(torch, p, n_local, col0, n_global, device, seed=0):
+    """C2: synthetic_sparse_factors(16, 256, n, 5, n // 100, 4, 1, 1)."""
+    return make_lowrank(torch, p, n_local, col0, n_global, device, 16, 5, n_global // 100, seed)
+
+
 # ------------------------------------------------------------ reference arm
 
-def cpu_reference_sample(p, n_sample, seed=0):
-    """The bounded CPU sample: p x n_sample Gaussian columns (fp32-drawn, as
-    fp64), gamma = (0.1 max ||a_i||)^2 and the max-norm start."""
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def import_reference():
+    """The unmodified reference package (pip --target baseline/_ref, see
+    DESIGN.md 'Reference install'), or None when it is not installed."""
+    if not os.path.isdir(os.path.join(REF_DIR, "gpspca")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import gpspca
+
+    assert os.path.abspath(gpspca.__file__).startswith(REF_DIR), gpspca.__file__
+    return gpspca
+
+
+def host_c2(p, n, cols=None, seed=0):
+    """The C2 instance of our arm (make_c2, same seeds), drawn on the GPU and
+    copied to host memory as a (p, n) Fortran-ordered fp32 view: the CPU
+    runs see exactly the matrix the device solves."""
+    import torch
+
+    dev = torch.device("cuda", 0)
+    At = make_c2(torch, p, n, 0, n, dev, seed)
+    if cols is not None:
+        At = At[:cols]
+    host = At.cpu()
+    del At
+    torch.cuda.empty_cache()
+    return host.numpy().T
+
+
+def host_cores():
+    try:
+        import psutil
+
+        return psutil.cpu_count(logical=False) or os.cpu_count(), os.cpu_count()
+    except ImportError:
+        return os.cpu_count(), os.cpu_count()
+
+
+class ReferenceLoop:
+    """One power iteration of the reference loop (single_unit.py:167-180)
+    through the reference's own kernel seam (parallel.py:85-142) and
+    objective, at a fixed KernelPlan and BLAS thread count."""
+
+    def __init__(self, ref, A, gamma, workers, blas_threads):
+        from threadpoolctl import threadpool_limits
+
+        self.ref, self.A, self.gamma = ref, A, gamma
+        self.plan = ref.KernelPlan(workers=workers, chunk=256)
+        self.limits = threadpool_limits(blas_threads, user_api="blas")
+        self.workers, self.blas = workers, blas_threads
+
+    def first(self, x0):
+        from gpspca.single_unit import _objective_from_correlations
+
+        self.c = self.ref.par_matvec_t(self.A, x0, self.plan)
+        return _objective_from_correlations(self.c, self.gamma, "l0")
+
+    def step(self):
+        from gpspca.single_unit import _objective_from_correlations
+
+        g = 2.0 * self.ref.par_threshold_accumulate(self.A, self.c, self.gamma, "l0", self.plan)
+        x = g / np.linalg.norm(g)
+        self.c = self.ref.par_matvec_t(self.A, x, self.plan)
+        return _objective_from_correlations(self.c, self.gamma, "l0")
+
+    def close(self):
+        self.limits.unregister()
+
+
+def best_reference_config(ref, A_sample, cores, reps=2):
+    """the best of workers in {1, cores} x BLAS threads in
+    {1, cores}, timed on a column sample of the same instance."""
+    A = ref.DataMatrix(A_sample)
+    norms = ref.column_norms(A)
+    gamma = (0.1 * float(norms.max())) ** 2
+    x0 = A.column(int(np.argmax(norms))) / norms.max()
+    best = None
+    for workers, blas in ((cores, 1), (1, cores), (cores, cores), (1, 1)):
+        loop = ReferenceLoop(ref, A, gamma, workers, blas)
+        loop.first(x0)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            loop.step()
+        t = (time.perf_counter() - t0) / reps
+        loop.close()
+        if best is None or t < best[0]:
+            best = (t, workers, blas)
+    return best
+
+
+def reference_c2_timing(ref, p, n, steps, warmup, budget_s=150.0):
+    """Real iterations of the reference's own loop on the FULL C2 instance
+    (the matrix our arm solves, fp64 as the reference stores it), best
+    thread configuration; the number of timed steps is capped so the run
+    stays inside the driver's clock.  Returns (per-iteration seconds list,
+    info dict)."""
+    phys, logical = host_cores()
+    A32 = host_c2(p, n)
+    t_best, workers, blas = best_reference_config(ref, np.asarray(A32[:, : n // 16]), logical)
+    t0 = time.perf_counter()
+    A = ref.DataMatrix(A32)  # the reference's own fp64 copy (core.py:36)
+    del A32
+    norms = ref.column_norms(A)
+    prep_s = time.perf_counter() - t0
+    gamma = (0.1 * float(norms.max())) ** 2
+    x0 = A.column(int(np.argmax(norms))) / norms.max()
+    loop = ReferenceLoop(ref, A, gamma, workers, blas)
+    loop.first(x0)
+    times = []
+    est = t_best * 16.0
+    n_warm = max(1, warmup)
+    n_timed = int(max(3, min(steps, budget_s / max(est, 1e-3))))
+    for s in range(n_warm + n_timed):
+        t0 = time.perf_counter()
+        loop.step()
+        dt = time.perf_counter() - t0
+        if s >= n_warm:
+            times.append(dt)
+        elif s == 0:
+            n_timed = int(max(3, min(steps, budget_s / dt)))
+    loop.close()
+    info = {"workers": workers, "blas_threads": blas, "cores_physical": phys, "cores_logical": logical,
+            "prep_s": prep_s, "warmup_steps": n_warm, "steps_requested": steps, "gamma": gamma,
+            "calibration": f"best of workers in {{1,{logical}}} x BLAS threads in {{1,{logical}}} on a "
+                           f"{p}x{n // 16} column slice: {t_best * 1e3:.1f} ms/iter at workers={workers}, "
+                           f"BLAS={blas}"}
+    return times, info
+
+
+def reference_sample_timing(ref, p, n, cols, iters=3):
+    """cpu_baseline leg of our arm: the reference loop on the first `cols`
+    columns of the same instance (bounded CPU work), best thread config."""
+    phys, logical = host_cores()
+    A32 = host_c2(p, n, cols=cols)
+    t_best, workers, blas = best_reference_config(ref, np.asarray(A32[:, : cols // 4]), logical, reps=1)
+    A = ref.DataMatrix(A32)
+    norms = ref.column_norms(A)
+    gamma = (0.1 * float(norms.max())) ** 2
+    loop = ReferenceLoop(ref, A, gamma, workers, blas)
+    loop.first(A.column(int(np.argmax(norms))) / norms.max())
+    loop.step()
+    t0 = time.perf_counter()
+    for _ in range(iters):
+        loop.step()
+    t = (time.perf_counter() - t0) / iters
+    loop.close()
+    return t, workers, blas, logical
+
+
+def cpu_baseline_entry(p, n_full, cols=1 << 18, iters=3):
+    ref = import_reference()
+    if ref is not None:
+        t, workers, blas, cores = reference_sample_timing(ref, p, n_full, cols, iters)
+        per_iter_full = t * (n_full / cols)
+        return {"value": 1.0 / per_iter_full, "unit": "iters/s", "cores": cores, "kind": "reference",
+                "sample": f"{iters} power iterations of the reference's own loop (gpspca 0.1.0 from baseline/_ref: "
+                          f"par_threshold_accumulate + par_matvec_t, single_unit.py:167-180, fp64, "
+                          f"KernelPlan(workers={workers}), BLAS threads {blas}) on the first {cols} columns of "
+                          f"the same C2 instance: {t * 1e3:.0f} ms/iter, scaled by n/{cols} = {n_full / cols:g} "
+                          f"(the loop is linear in n)"}
     import oracle
 
-    rng = np.random.default_rng(seed)
-    A = np.asfortranarray(rng.standard_normal((p, n_sample)).astype(np.float32).astype(np.float64))
+    rng = np.random.default_rng(0)
+    A = np.asfortranarray(rng.standard_normal((p, cols)).astype(np.float32).astype(np.float64))
     norms = oracle.column_norms(A)
     gamma = (0.1 * float(norms.max())) ** 2
-    x = A[:, int(np.argmax(norms))] / norms.max()
-    return A, gamma, A.T @ x
-
-
-def cpu_reference_iterations(A, gamma, c, iters):
-    """Seconds per power iteration of the CPU reference algorithm (oracle port,
-    2 reads of A per iteration as in single_unit.py:167-180); returns (t, c)."""
-    import oracle
-
+    c = A.T @ (A[:, int(np.argmax(norms))] / norms.max())
     t0 = time.perf_counter()
     for _ in range(iters):
         g = oracle.su_gradient(A, c, gamma, "l0")
-        x = g / np.linalg.norm(g)
-        c = A.T @ x
-        oracle.su_objective(c, gamma, "l0")
-    return (time.perf_counter() - t0) / iters, c
-
-
-def cpu_reference_iteration_time(p, n_sample, iters, seed=0):
-    A, gamma, c = cpu_reference_sample(p, n_sample, seed)
-    return cpu_reference_iterations(A, gamma, c, iters)[0]
-
-
-def cpu_baseline_entry(p, n_full, n_sample=1 << 16, iters=8):
-    t = cpu_reference_iteration_time(p, n_sample, iters)
-    per_iter_full = t * (n_full / n_sample)
-    return {"value": 1.0 / per_iter_full, "unit": "iters/s", "cores": os.cpu_count(), "kind": "port",
-            "sample": f"{iters} power iterations of the NumPy fp64 oracle (oracle/gpower.py, BLAS threads = "
-                      f"{os.cpu_count()}) on p={p} x n={n_sample} Gaussian columns, "
-                      f"{t * 1e3:.1f} ms/iter, extrapolated linearly to n={n_full}"}
+        c = A.T @ (g / np.linalg.norm(g))
+    t = (time.perf_counter() - t0) / iters
+    return {"value": cols / (t * n_full), "unit": "iters/s", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"oracle port (baseline/_ref not installed), {iters} iterations on a {p}x{cols} Gaussian "
+                      f"sample scaled by n/{cols}"}
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    n_sample = 1 << 15
-    A, gamma, c = cpu_reference_sample(args.p, n_sample)  # generated once, outside the timed steps
-    times = []
-    for s in range(args.warmup + args.steps):
-        t, c = cpu_reference_iterations(A, gamma, c, 1)
-        if s >= args.warmup:
-            times.append(t * (args.n / n_sample))
+    ref = import_reference()
+    if ref is None:
+        print(json.dumps({"impl": "reference", "unavailable": "baseline/_ref not installed (see DESIGN.md)"}))
+        return
+    times, info = reference_c2_timing(ref, args.p, args.n, args.steps, args.warmup)
     per = statistics.mean(times)
     value = 1.0 / per
+    cores = info["cores_logical"]
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "p": args.p, "n": args.n},
-            "cpu_baseline": {"value": value, "unit": "iters/s", "cores": os.cpu_count(), "kind": "port",
-                             "sample": f"each step: 1 power iteration of the NumPy fp64 oracle on one p={args.p} x "
-                                       f"n={n_sample} Gaussian sample (BLAS on all {os.cpu_count()} host threads), "
-                                       f"extrapolated linearly to n={args.n}"},
+            "steps": len(times), "warmup": info["warmup_steps"], "ms_per_step": per * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": WORKLOAD, "p": args.p, "n": args.n, "same_instance": True},
+            "a_stream_gbs": 2 * args.p * args.n * 8 / per / 1e9,
+            "cpu_baseline": {"value": value, "unit": "iters/s", "cores": cores, "kind": "reference",
+                             "cores_physical": info["cores_physical"],
+                             "sample": f"each step: one full power iteration of the unmodified reference (gpspca "
+                                       f"0.1.0 installed in baseline/_ref; par_threshold_accumulate + par_matvec_t "
+                                       f"+ objective, single_unit.py:167-180; two reads of the fp64 A per "
+                                       f"iteration) on the full C2 instance p={args.p} n={args.n} -- the same "
+                                       f"matrix our arm solves (drawn on the GPU, copied to the host, stored by "
+                                       f"gpspca.DataMatrix as fp64); KernelPlan(workers={info['workers']}), BLAS "
+                                       f"threads {info['blas_threads']}; {len(times)} timed steps "
+                                       f"(--steps {args.steps} requested; capped to the driver clock)"},
+            "reference_config": info,
             "e2e": {"value": value, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------ our arm
 
-def block_configs(torch, gps, ctx, dev, iters=(10, 5)):
+BLOCK_CONFIGS = (
+    # name, p, n, m, penalty, mu, gamma fraction of max ||a_i||, data, timed iterations
+    ("C3", 4096, 1 << 21, 10, "l1", np.ones(10), 0.1, "lowrank", 10),
+    ("C4", 8192, 1 << 21, 64, "l0", np.linspace(1.0, 0.5, 64), 0.1, "lowrank", 5),
+    ("C4_dense", 8192, 1 << 21, 64, "l0", np.linspace(1.0, 0.5, 64), 0.03, "gauss", 3),
+)
+
+
+def block_configs(torch, gps, ctx, dev):
     """BASELINE C3 (BL1 m = 10, 4096 x 2^21) and C4 (BL0 m = 64 with mu,
-    8192 x 2^21) on this GPU: iterations/s of the device-resident block loop
-    (tensor-core filter, fp64 recomputation, T2, polar step; tol = 0 so every
-    timed iteration is a real one), CUDA events on the loop's stream, Gaussian
-    A generated on the device (A >> L2, no flush needed)."""
+    8192 x 2^21) on the SURVEY §8(d) low-rank generator, plus C4 on Gaussian
+    data at gamma = (0.03 max ||a_i||)^2 (~9 % of the columns active: the
+    dense-activity worst case of the fp64 recompute / update kernels):
+    iterations/s of the device-resident block loop (tensor-core filter, fp64
+    recomputation, T2, polar step; tol = 0 so every timed iteration is a real
+    one), CUDA events on the loop's stream, A generated on the device
+    (A >> L2, no flush needed)."""
     from paper_1312_6182_b200 import _native
     from paper_1312_6182_b200.block import BlockLoop, _top_m_columns
 
     out = {}
     stream = torch.cuda.Stream(dev)
-    for name, p, n, m, pen, mu, k in (("C3", 4096, 1 << 21, 10, "l1", np.ones(10), iters[0]),
-                                      ("C4", 8192, 1 << 21, 64, "l0", np.linspace(1.0, 0.5, 64), iters[1])):
-        g = torch.Generator(device=dev)
-        g.manual_seed(7)
-        At = torch.randn((n, p), generator=g, device=dev, dtype=torch.float32)
+    for name, p, n, m, pen, mu, frac, data, k in BLOCK_CONFIGS:
+        if data == "lowrank":
+            n_classes, n_factors, support = (16, 10, n // 200) if name == "C3" else (32, 64, n // 128)
+            At = make_lowrank(torch, p, n, 0, n, dev, n_classes, n_factors, support)
+        else:
+            g = torch.Generator(device=dev)
+            g.manual_seed(7)
+            At = torch.randn((n, p), generator=g, device=dev, dtype=torch.float32)
         A = gps.DataMatrix.from_device(At.data_ptr(), p, n, owner=At, device=dev.index)
-        top = 0.1 * float(A.norms.max())
+        top = frac * float(A.norms.max())
         gamma = np.full(m, top if pen == "l1" else top * top)
         loop = BlockLoop(A, pen, m, gamma, mu, 0.0, k + 4)
         loop.start_columns(_top_m_columns(np.asarray(A.norms), m))
@@ -257,13 +428,55 @@ def block_configs(torch, gps, ctx, dev, iters=(10, 5)):
         e1.synchronize()
         ms = e0.elapsed_time(e1) / k
         ctx.set_stream(None)
-        out[name] = {"workload": f"{'BL1' if pen == 'l1' else 'BL0'} m={m}{' with mu' if name == 'C4' else ''}, "
-                                 f"p={p} n=2^21 fp32, gamma=0.1*max||a_i||{'^2' if pen == 'l0' else ''}",
+        d, it, _ = _bk_poll(loop)
+        assert not d and it == k + 2, f"{name}: block loop stopped early (iteration {it})"
+        f_last, nnz = _native.C.c_double(), _native.C.c_double()
+        _native.check(L.gps_bk_last_sweep(loop.handle, _native.C.byref(f_last), _native.C.byref(nnz)))
+        nnz = int(nnz.value)
+        out[name] = {"workload": f"{'BL1' if pen == 'l1' else 'BL0'} m={m}{' with mu' if mu[-1] != 1 else ''}, "
+                                 f"p={p} n=2^21 fp32, {data} data, gamma={frac}*max||a_i||"
+                                 f"{'^2' if pen == 'l0' else ''}",
                      "iters_per_s": 1e3 / ms, "ms_per_iter": ms, "a_stream_gbs": p * n * 4 / (ms / 1e3) / 1e9,
-                     "iterations_timed": k}
+                     "iterations_timed": k, "active_entries_last_sweep": nnz}
         del loop, A, At
         torch.cuda.empty_cache()
     return out
+
+
+def _bk_poll(loop):
+    from paper_1312_6182_b200 import _native
+
+    d, i, c = _native.C.c_int(), _native.C.c_int(), _native.C.c_int()
+    _native.check(_native.lib().gps_bk_poll(loop.handle, _native.C.byref(d), _native.C.byref(i), _native.C.byref(c)))
+    return d.value, i.value, c.value
+
+
+def su_dense_line(torch, gps, ctx, dev, A, p, n, k=20):
+    """Single-unit l0 at gamma = 0 on the resident C2 matrix: every column is
+    active, so every column's rank-1 update runs from shared memory in the
+    fused sweep -- the worst case of K1 (SURVEY §7 'exploit w-sparsity')."""
+    from paper_1312_6182_b200 import _native
+
+    stream = torch.cuda.Stream(dev)
+    i = int(np.argmax(A.norms))
+    x0 = A.column(i) / A.norms[i]
+    loop = gps.single_unit.PowerLoop(A, "l0", 0.0, 0.0, k + 4)
+    ctx.set_stream(stream.cuda_stream)
+    loop.start(x0)
+    L = _native.lib()
+    for _ in range(2):
+        _native.check(L.gps_su_enqueue(loop.handle, 7))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(k):
+        _native.check(L.gps_su_enqueue(loop.handle, 7))
+    e1.record(stream)
+    e1.synchronize()
+    ctx.set_stream(None)
+    ms = e0.elapsed_time(e1) / k
+    gbs = p * n * 4 / (ms / 1e3) / 1e9
+    return {"workload": f"SL0 gamma=0 on the C2 matrix (p={p} n={n}, every column active)", "iters_per_s": 1e3 / ms,
+            "ms_per_iter": ms, "a_stream_gbs": gbs, "frac_of_8tbs": gbs / 8000.0, "iterations_timed": k}
 
 
 def run_ours(args):
@@ -374,6 +587,11 @@ def run_ours(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         elapsed, sweep_ms = float(t[0]), float(t[1])
     del loop
+    dense = None
+    if world == 1 and not args.no_block:
+        dense = su_dense_line(torch, gps, ctx, dev, A, p, n_local)
+        torch.cuda.set_stream(stream)
+        ctx.set_stream(stream.cuda_stream)
     read_ms = _native.C.c_double()
     _native.check(L.gps_bench_read_stream(A.handle, 5, _native.C.byref(read_ms)))
     read_peak = p * n_local * 4 / (read_ms.value / 1e3) / 1e9
@@ -442,6 +660,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        torch.cuda.empty_cache()
         cpu = cpu_baseline_entry(p, n)
 
     if rank == 0:
@@ -467,6 +686,7 @@ def run_ours(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "block_configs": block,
+            "su_gamma0": dense,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

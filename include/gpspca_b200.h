@@ -192,6 +192,9 @@ int gps_bk_result(gps_bk* s, double* X_out, double* hist_out, int* n_hist, int* 
  * violation) and the number of steps the exact Householder + Jacobi polar
  * path took. */
 int gps_bk_diagnostics(gps_bk* s, double* stiefel_out, int* status_out, int* exact_steps_out);
+/* Objective and active (column, component) count of the most recent sweep
+ * (instrumentation; the loop may still be running). */
+int gps_bk_last_sweep(gps_bk* s, double* f_out, double* nnz_out);
 /* Near-threshold log of the final block sweep: entries col * 64 + j with
  * the mu-scaled correlation s = mu_j c_ij within 1e-6 gamma_j of the
  * threshold (block.py:80-89 rules); as gps_su_band. */

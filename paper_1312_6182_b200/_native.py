@@ -74,6 +74,7 @@ SIGNATURES = {
     "gps_su_band": (C.c_int, [_vp, _i64p, C.c_int, _ip]),
     "gps_bk_diagnostics": (C.c_int, [_vp, _dp, _ip, _ip]),
     "gps_bk_band": (C.c_int, [_vp, _i64p, C.c_int, _ip]),
+    "gps_bk_last_sweep": (C.c_int, [_vp, _dp, _dp]),
     "gps_bk_create": (C.c_int, [_vp, C.c_int, C.c_int, _dp, _dp, C.c_double, C.c_int, C.POINTER(_vp)]),
     "gps_bk_destroy": (C.c_int, [_vp]),
     "gps_bk_start": (C.c_int, [_vp, _dp]),

@@ -2133,6 +2133,25 @@ int gps_bk_result(gps_bk* s, double* X_out, double* hist_out, int* n_hist, int* 
   return GPS_OK;
 }
 
+int gps_bk_last_sweep(gps_bk* s, double* f_out, double* nnz_out) {
+  if (!s) return fail(GPS_E_ARG, "NULL argument");
+  gps_ctx* ctx = s->A->ctx;
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  std::vector<double> sc(size_t(s->ngroups) * 2);
+  for (int g = 0; g < s->ngroups; ++g)
+    GPS_CUDA(cudaMemcpyAsync(sc.data() + 2 * g, s->exch + size_t(g) * s->exch_stride() + size_t(s->mg) * s->A->ld,
+                             2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  GPS_CUDA(cudaStreamSynchronize(ctx->stream));
+  double f = 0.0, nnz = 0.0;
+  for (int g = 0; g < s->ngroups; ++g) {
+    f += sc[2 * g];
+    nnz += sc[2 * g + 1];
+  }
+  if (f_out) *f_out = f;
+  if (nnz_out) *nnz_out = nnz;
+  return GPS_OK;
+}
+
 int gps_bk_diagnostics(gps_bk* s, double* stiefel_out, int* status_out, int* exact_steps_out) {
   if (!s) return fail(GPS_E_ARG, "NULL argument");
   gps_ctx* ctx = s->A->ctx;
