@@ -86,3 +86,25 @@ def test_oracle_kernel_vectors():
 def test_threshold_tie_is_inactive():
     # parallel.py:127 / reference test_parallel.py:109-114
     assert oracle.threshold(np.array([1.0, 0.0]), 1.0, "l0").tolist() == [0.0, 0.0]
+
+
+def test_chunked_oracle_matches_whole_matrix_oracle():
+    """oracle/chunked.py (the full-size checker) agrees with the pinned
+    whole-matrix restatement on the C1 golden instance, both loops."""
+    from oracle.chunked import ChunkedA, block_solve_chunked, max_norm_start, su_iterate_chunked
+
+    case = next(c for c in load_solves() if c["name"] == "c1_bl1_m10")
+    A = case_matrix(case)
+    H = ChunkedA(np.asfortranarray(A.astype(np.float32)), chunk=97, workers=4)
+    np.testing.assert_allclose(H.norms(), oracle.column_norms(A), rtol=1e-14)
+    X0, _ = max_norm_start(H, 10)
+    np.testing.assert_allclose(X0, oracle.block_initial_point(A, 10), atol=1e-12)
+    C, hist, conv, X = block_solve_chunked(H, 10, case["gamma"], 1.0, "l1", 1e-6, 1000, X0)
+    assert len(hist) - 1 == case["iterations"]
+    np.testing.assert_allclose(hist, case["history"], rtol=1e-11)
+    su = next(c for c in load_solves() if c["name"] == "c1_sl1")
+    norms = H.norms()
+    i = int(np.argmax(norms))
+    x, h, conv, c = su_iterate_chunked(H, H.column(i) / norms[i], su["gamma"], "l1", 1e-6, 1000)
+    assert len(h) - 1 == su["iterations"]
+    np.testing.assert_allclose(h, su["history"], rtol=1e-11)
