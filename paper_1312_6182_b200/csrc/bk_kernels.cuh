@@ -598,6 +598,13 @@ __device__ void bk_advance(GpsCtl* ctl, int k, int m, int rank, double err, int*
   ctl->iter = k + 1;
 }
 
+// ||M - I||_F of a reduced m x m Gram (one CTA).
+__global__ void gram_error_kernel(const double* __restrict__ M, int m, double* out) {
+  __shared__ double red[40];
+  const double e = gram_error_from(M, m, red);
+  if (threadIdx.x == 0) *out = e;
+}
+
 // One-CTA record of X_0's Stiefel error (init; block.py:202).
 __global__ void __launch_bounds__(kPolarThreads) stiefel_error_kernel(const double* X, int ld, int m,
                                                                       double* out) {

@@ -230,7 +230,10 @@ int ensure_smem_attr(const void* fn, size_t /*smem*/) {
   GPS_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lk(g_attr_mu);
   if (g_attr_done.count({dev, fn})) return GPS_OK;
-  GPS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
+  cudaFuncAttributes fa{};
+  GPS_CUDA(cudaFuncGetAttributes(&fa, fn));  // static shared memory counts against the same budget
+  GPS_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kSmemBudget - static_cast<int>(fa.sharedSizeBytes)));
   g_attr_done.insert({dev, fn});
   return GPS_OK;
 }
@@ -1396,6 +1399,7 @@ struct gps_bk {
   unsigned char* colmask = nullptr;
   unsigned char* tflag = nullptr;     // [2 * items][8] T1 tile flags (items = ceil(n / 256))
   unsigned char* item_act = nullptr;  // [items] any active column (T1x -> T2)
+  double* Wt = nullptr;               // [n][m_pad] weights of the candidates, column-major (T1x -> T2)
   double* part_s_tc = nullptr;
   CUtensorMap tmA, tmXh, tmXl;
   // multi-CTA CholeskyQR2 polar (large p*m)
@@ -1552,11 +1556,10 @@ int bk_enqueue_tc(gps_bk* s, bool with_ctl) {
   {
     const int64_t xs = int64_t(s->m_pad()) * ld, wst = int64_t(s->m_pad()) * A->n;
     const double* gam = s->mu_dev + s->m;
-#define GPS_REFINE(TA, J)                                                                                        \
-  tc_refine_kernel<TA, J><<<s->tc_ref_grid, 256, 0, ctx->stream>>>(static_cast<const TA*>(A->d), A->n, ld, s->m, \
-                                                                   s->X, xs, s->mu_dev, gam, s->penalty,       \
-                                                                   s->colmask, s->tflag, s->item_act, s->W, wst, \
-                                                                   s->part_s_tc, ctl, ctl ? s->band : nullptr)
+#define GPS_REFINE(TA, J)                                                                                      \
+  tc_refine_kernel<TA, J><<<s->tc_ref_grid, 256, tc_refine_smem(8 * J), ctx->stream>>>(                          \
+      static_cast<const TA*>(A->d), A->n, ld, s->m, s->X, xs, s->mu_dev, gam, s->penalty, s->colmask, s->tflag, \
+      s->item_act, s->W, wst, s->Wt, s->part_s_tc, ctl, ctl ? s->band : nullptr)
 #define GPS_REFINE_J(TA)            \
   switch (np / 8) {                 \
     case 2: GPS_REFINE(TA, 2); break; \
@@ -1574,17 +1577,16 @@ int bk_enqueue_tc(gps_bk* s, bool with_ctl) {
     ctx->launches++;
   }
   if (!(a.probe & 16)) {
-    const int64_t wst = int64_t(s->m_pad()) * A->n;
-#define GPS_UPDATE(TA, J)                                                                                     \
-  tc_update_kernel<TA, J><<<dim3(s->tc_gx, static_cast<unsigned>(ceil_div(A->ld, tc_upd_rows<J>()))), 256, 0, \
-                            ctx->stream>>>(static_cast<const TA*>(A->d), A->n, ld, s->m, s->colmask, s->item_act,  \
-                                           s->W, wst, np, s->part_g, ctl)
-#define GPS_UPDATE_J(TA)               \
-  switch (np / 8) {                    \
-    case 2: GPS_UPDATE(TA, 2); break;  \
-    case 4: GPS_UPDATE(TA, 4); break;  \
-    case 6: GPS_UPDATE(TA, 6); break;  \
-    default: GPS_UPDATE(TA, 8); break; \
+#define GPS_UPDATE(TA, NT)                                                                                   \
+  tc_update_kernel<TA, NT><<<dim3(s->tc_gx, static_cast<unsigned>(ceil_div(A->ld, kUpdR))), 256,              \
+                             tc_update_smem(16 * NT), ctx->stream>>>(static_cast<const TA*>(A->d), A->n, ld, s->m, \
+                                                                     s->colmask, s->item_act, s->Wt, s->part_g, ctl)
+#define GPS_UPDATE_J(TA)                \
+  switch (np / 16) {                    \
+    case 1: GPS_UPDATE(TA, 1); break;   \
+    case 2: GPS_UPDATE(TA, 2); break;   \
+    case 3: GPS_UPDATE(TA, 3); break;   \
+    default: GPS_UPDATE(TA, 4); break;  \
   }
     if (f64) {
       GPS_UPDATE_J(double)
@@ -1745,9 +1747,21 @@ int bk_qr_into_x(gps_bk* s, double* Mdev) {
 // from the initial iterate); returns it.
 int bk_record_x0(gps_bk* s, double* err_out) {
   gps_ctx* ctx = s->A->ctx;
-  stiefel_error_kernel<<<1, kPolarThreads, size_t(s->m) * s->m * sizeof(double), ctx->stream>>>(
-      s->X, static_cast<int>(s->A->ld), s->m, s->stiefel);
-  ctx->launches++;
+  const int ld = static_cast<int>(s->A->ld), p = static_cast<int>(s->A->p), m = s->m;
+  if (s->big_polar) {
+    // large p m: the polar step's multi-CTA Gram (one CTA over 8192 x 64
+    // takes ~4 ms), then the error of the reduced Gram
+    const PolarCtl on{1, 0, m, 0};
+    GPS_CUDA(cudaMemcpyAsync(s->pc, &on, sizeof(PolarCtl), cudaMemcpyHostToDevice, ctx->stream));
+    gram_partial_kernel<<<kGramBlocks, kGramThreads, 0, ctx->stream>>>(s->X, ld, p, m, s->gram_part, s->pc);
+    gram_reduce_kernel<<<(m * m + 255) / 256, 256, 0, ctx->stream>>>(s->gram_part, kGramBlocks, m * m, s->pc);
+    gram_error_kernel<<<1, 1024, 0, ctx->stream>>>(s->gram_part, m, s->stiefel);
+    ctx->launches += 3;
+  } else {
+    stiefel_error_kernel<<<1, kPolarThreads, size_t(m) * m * sizeof(double), ctx->stream>>>(s->X, ld, m,
+                                                                                          s->stiefel);
+    ctx->launches++;
+  }
   GPS_CHECK_LAUNCH("stiefel_error_kernel launch");
   double err = 0.0;
   GPS_CUDA(cudaMemcpyAsync(&err, s->stiefel, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1862,6 +1876,7 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
     alloc((void**)&s->tflag, size_t(ceil_div(n, kTcRefItem)) * 16);
     alloc((void**)&s->item_act, size_t(ceil_div(n, kTcRefItem)));
     alloc((void**)&s->part_s_tc, size_t(s->tc_ref_grid) * 4 * sizeof(double));
+    alloc((void**)&s->Wt, n * mp * sizeof(double));
   }
   alloc((void**)&s->ctl, sizeof(GpsCtl));
   alloc((void**)&s->rank_dev, sizeof(int));
@@ -1909,6 +1924,20 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
       rc = ensure_smem_attr(f64 ? reinterpret_cast<const void*>(tc_dots_kernel<double>)
                                 : reinterpret_cast<const void*>(tc_dots_kernel<float>),
                             smem);
+    if (rc == GPS_OK) {
+      // dynamic shared memory of the DMMA refine / update kernels (> 48 KB)
+      const void* fns[] = {
+          f64 ? reinterpret_cast<const void*>(tc_refine_kernel<double, 2>) : reinterpret_cast<const void*>(tc_refine_kernel<float, 2>),
+          f64 ? reinterpret_cast<const void*>(tc_refine_kernel<double, 4>) : reinterpret_cast<const void*>(tc_refine_kernel<float, 4>),
+          f64 ? reinterpret_cast<const void*>(tc_refine_kernel<double, 6>) : reinterpret_cast<const void*>(tc_refine_kernel<float, 6>),
+          f64 ? reinterpret_cast<const void*>(tc_refine_kernel<double, 8>) : reinterpret_cast<const void*>(tc_refine_kernel<float, 8>),
+          f64 ? reinterpret_cast<const void*>(tc_update_kernel<double, 1>) : reinterpret_cast<const void*>(tc_update_kernel<float, 1>),
+          f64 ? reinterpret_cast<const void*>(tc_update_kernel<double, 2>) : reinterpret_cast<const void*>(tc_update_kernel<float, 2>),
+          f64 ? reinterpret_cast<const void*>(tc_update_kernel<double, 3>) : reinterpret_cast<const void*>(tc_update_kernel<float, 3>),
+          f64 ? reinterpret_cast<const void*>(tc_update_kernel<double, 4>) : reinterpret_cast<const void*>(tc_update_kernel<float, 4>)};
+      for (const void* fn : fns)
+        if (rc == GPS_OK) rc = ensure_smem_attr(fn, 0);
+    }
     if (rc == GPS_OK && A->tc_col_delta == nullptr) {
       // candidate margins: one pass over A once per matrix (the scale
       // exponents come from the matrix's norms pass), kept with it
@@ -1964,6 +1993,7 @@ int gps_bk_destroy(gps_bk* s) {
   if (s->item_act) gps_free(s->item_act);
   if (s->colmask) gps_free(s->colmask);
   if (s->part_s_tc) gps_free(s->part_s_tc);
+  if (s->Wt) gps_free(s->Wt);
   if (s->pc) gps_free(s->pc);
   if (s->gram_part) gps_free(s->gram_part);
   if (s->R1) gps_free(s->R1);

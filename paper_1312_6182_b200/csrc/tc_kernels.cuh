@@ -678,15 +678,25 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   }
 }
 
+// fp64 tensor-core MMA (DMMA): D(8x8) += A(8x4, row-major) B(4x8, col-major).
+// Fragments: lane l holds A[l / 4][l % 4], B[l % 4][l / 4] and
+// D[l / 4][2 (l % 4) + {0, 1}].
+__device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
 // T1x: exact fp64 recomputation of the candidate columns T1 flagged.
 // Work items are 256-column ranges (two T1 tiles), assigned to CTAs
 // round-robin (item b, b + grid, ...) so contiguous runs of active columns
 // spread over the grid; an item whose two tiles carry no candidate flag is
 // skipped without reading its columns.  The candidates of a CTA's items are
 // compacted in column order into one list (across items), and every 64 of
-// them are processed as a batch: C_batch = A_batch' X, 32 rows at a time (A
-// through shared memory, X in registers); thread (lane, warp) owns columns
-// {lane, lane + 32} x components [warp JPT, warp JPT + JPT).  A final partial list of up to
+// them are processed as a batch: C_batch = A_batch' X, 32 rows at a time, on
+// the fp64 tensor cores (DMMA m8n8k4; A and X through shared memory).  The
+// weights also go to Wt (column-major by component: one contiguous row of
+// NJ doubles per column) for T2's gathers.  A final partial list of up to
 // kTcRefSmallMax candidates instead takes the CTA one column at a time,
 // threads over rows, X read straight from L2 without block barriers (staged
 // chunks would serialise p / 32 latency-bound steps for a handful of columns).
@@ -702,6 +712,10 @@ constexpr int kTcRefItem = 256;
 constexpr int kTcRefBatch = 64;
 constexpr int kTcRefRows = 32;
 constexpr int kTcRefSmallMax = 16;
+constexpr int kRefKS = kTcRefRows + 4;  // k-contiguous row stride of the DMMA tiles (= 4 mod 16 doubles)
+__host__ __device__ constexpr size_t tc_refine_smem(int nj) {
+  return (size_t(2) * kTcRefBatch * kRefKS + size_t(2) * nj * kRefKS) * sizeof(double);
+}
 template <typename TA, int JPT>
 __global__ void __launch_bounds__(256, 2) tc_refine_kernel(const TA* __restrict__ A, int64_t n, int ld, int m,
                                                            const double* __restrict__ X, int64_t x_par_stride,
@@ -711,15 +725,18 @@ __global__ void __launch_bounds__(256, 2) tc_refine_kernel(const TA* __restrict_
                                                            const unsigned char* __restrict__ tflag,
                                                            unsigned char* __restrict__ item_act,
                                                            double* __restrict__ W, int64_t w_par_stride,
-                                                           double* __restrict__ part_s, const GpsCtl* ctl,
-                                                           BandLog* band) {
+                                                           double* __restrict__ Wt, double* __restrict__ part_s,
+                                                           const GpsCtl* ctl, BandLog* band) {
   constexpr int NJ = 8 * JPT;  // padded components (X is zero beyond m)
+  constexpr int NT = NJ / 16;  // DMMA n-tiles per warp (two component halves)
   constexpr int JC = NJ < 32 ? NJ : 32;  // components per pass of the single-column mode
   if (ctl != nullptr && ctl->done) return;
   const int parity = ctl != nullptr ? (ctl->iter & 1) : 0;
   const double* Xp = X + parity * x_par_stride;
   double* Wp = W + parity * w_par_stride;
-  __shared__ TA sA[2][kTcRefRows][kTcRefBatch + 1];
+  extern __shared__ __align__(16) double ref_smem[];
+  double* sA = ref_smem;                                   // [2][64 columns][kRefKS] fp64
+  double* sX = ref_smem + 2 * kTcRefBatch * kRefKS;        // [2][NJ components][kRefKS]
   __shared__ int64_t cand[kTcRefItem + kTcRefBatch];
   __shared__ int ilist[256];
   __shared__ int wcnt[8];
@@ -758,22 +775,25 @@ __global__ void __launch_bounds__(256, 2) tc_refine_kernel(const TA* __restrict_
     if (any) item_act[c / kTcRefItem] = 1;
   };
 
-  // batch mode: candidates cand[b0 .. b0 + nb), nb <= 64.  Per 32-row chunk
-  // warp w stages batch columns 8w .. 8w + 7 (lane = row) into a double-
-  // buffered shared tile and keeps its components' X rows in registers (lane
-  // = row, broadcast by shuffles); the next chunk's loads are issued before
-  // the current chunk's FMAs, one block barrier per chunk.
+  // batch mode: candidates cand[b0 .. b0 + nb), nb <= 64, on the fp64
+  // tensor cores: C (64 columns x NJ components) = A_batch' X over 32-row
+  // chunks.  Per chunk warp w stages columns 8w .. 8w + 7 (lane = row,
+  // widened to fp64 once) and components 8w .. 8w + 7 of X (lane = row) into
+  // double-buffered shared tiles stored k-contiguous (row stride kRefKS =
+  // 36 = 4 mod 16 doubles: stores and fragment loads are conflict-free), the
+  // next chunk's loads are issued before the current chunk's DMMAs, one
+  // barrier per chunk.  Warp w owns columns 16 (w % 4) .. + 16 (2 m-tiles)
+  // and components 8 NT (w / 4) .. + 8 NT (NT n-tiles).
   auto batch = [&](int b0, int nb) {
-    const bool two = nb > 32;  // warp-uniform: second column slot in use
-    double acc[2][JPT];
+    const int g = lane >> 2, t = lane & 3, mg = warp & 3, ng = warp >> 2;
+    double acc[2][NT][2];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int u = 0; u < JPT; ++u) acc[i][u] = 0.0;
+      for (int u = 0; u < NT; ++u) acc[i][u][0] = acc[i][u][1] = 0.0;
     if (tid < kTcRefBatch) act[tid] = 0;
-    const double* xw = Xp + size_t(warp * JPT) * ld;
     TA ra[8];
-    double rx[JPT];
+    double rx[8];
     auto load = [&](int r0) {
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
@@ -781,51 +801,66 @@ __global__ void __launch_bounds__(256, 2) tc_refine_kernel(const TA* __restrict_
         ra[c] = bc < nb ? A[cand[b0 + bc] * ld + r0 + lane] : TA(0);
       }
 #pragma unroll
-      for (int u = 0; u < JPT; ++u) rx[u] = xw[size_t(u) * ld + r0 + lane];
+      for (int c = 0; c < 8; ++c) {
+        const int j = warp * 8 + c;
+        rx[c] = j < NJ ? Xp[size_t(j) * ld + r0 + lane] : 0.0;
+      }
     };
     load(0);
     int buf = 0;
     for (int r0 = 0; r0 < ld; r0 += kTcRefRows, buf ^= 1) {
+      double* a_s = sA + buf * kTcRefBatch * kRefKS;
+      double* x_s = sX + buf * NJ * kRefKS;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) sA[buf][lane][warp * 8 + c] = ra[c];
-      double xr[JPT];
+      for (int c = 0; c < 8; ++c) a_s[(warp * 8 + c) * kRefKS + lane] = static_cast<double>(ra[c]);
+      if (warp * 8 < NJ)
 #pragma unroll
-      for (int u = 0; u < JPT; ++u) xr[u] = rx[u];
+        for (int c = 0; c < 8; ++c) x_s[(warp * 8 + c) * kRefKS + lane] = rx[c];
       __syncthreads();
       if (r0 + kTcRefRows < ld) load(r0 + kTcRefRows);
-#pragma unroll 8
-      for (int r = 0; r < kTcRefRows; ++r) {
-        const double a0 = static_cast<double>(sA[buf][r][lane]);
-        const double a1 = two ? static_cast<double>(sA[buf][r][lane + 32]) : 0.0;
 #pragma unroll
-        for (int u = 0; u < JPT; ++u) {
-          const double x = __shfl_sync(0xffffffffu, xr[u], r);
-          acc[0][u] = fma(a0, x, acc[0][u]);
-          if (two) acc[1][u] = fma(a1, x, acc[1][u]);
-        }
+      for (int ks = 0; ks < kTcRefRows; ks += 4) {
+        double a[2], b[NT];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) a[mt] = a_s[(mg * 16 + mt * 8 + g) * kRefKS + ks + t];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) b[nt] = x_s[(ng * 8 * NT + nt * 8 + g) * kRefKS + ks + t];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mt][nt], a[mt], b[nt]);
       }
     }
     __syncthreads();
+    // epilogue: lane holds C[column mg 16 + mt 8 + g][component ng 8 NT + nt 8 + 2 t + {0, 1}]
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int bc = lane + 32 * i;
+    for (int mt = 0; mt < 2; ++mt) {
+      const int bc = mg * 16 + mt * 8 + g;
       if (bc < nb) {
         const int64_t c = cand[b0 + bc];
         bool any = false;
 #pragma unroll
-        for (int u = 0; u < JPT; ++u) {
-          const int j = warp * JPT + u;
-          if (j < m) {
-            const double sj = smu[j] * acc[i][u];
-            const double w = threshold_weight(sj, sgam[j], penalty);
-            band_note(band, parity, c, j, sj, sgam[j], penalty);
-            f_acc += objective_term(sj, sgam[j], penalty);
-            if (w != 0.0) {
-              nnz_acc += 1.0;
-              any = true;
+        for (int nt = 0; nt < NT; ++nt) {
+          const int j0 = ng * 8 * NT + nt * 8 + 2 * t;
+          double wv[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int j = j0 + h;
+            wv[h] = 0.0;
+            if (j < m) {
+              const double sj = smu[j] * acc[mt][nt][h];
+              const double w = threshold_weight(sj, sgam[j], penalty);
+              band_note(band, parity, c, j, sj, sgam[j], penalty);
+              f_acc += objective_term(sj, sgam[j], penalty);
+              if (w != 0.0) {
+                nnz_acc += 1.0;
+                any = true;
+              }
+              Wp[size_t(j) * n + c] = w;
+              wv[h] = w;
             }
-            Wp[size_t(j) * n + c] = w;
           }
+          *reinterpret_cast<double2*>(Wt + c * NJ + j0) = make_double2(wv[0], wv[1]);
         }
         if (any) act[bc] = 1;  // benign: every writer stores 1
       }
@@ -872,6 +907,9 @@ __global__ void __launch_bounds__(256, 2) tc_refine_kernel(const TA* __restrict_
           act[0] = 1;  // benign: every writer stores 1
         }
         Wp[size_t(jj) * n + c] = w;
+        Wt[c * NJ + jj] = w;
+      } else if (tid < JC && jh + tid < NJ) {
+        Wt[c * NJ + jh + tid] = 0.0;  // padded components (T2 reads whole rows)
       }
       __syncthreads();
     }
@@ -934,54 +972,64 @@ __global__ void __launch_bounds__(256, 2) tc_refine_kernel(const TA* __restrict_
   }
 }
 
-// T2: sparse rank-m update on the ACTIVE columns (colmask), fp64:
-// G_partial[b] = sum over active i in range b of a_i w_i' -- a DGEMM-shaped
-// product A_act W_act with A_act's columns gathered on the fly.
-// grid (GX, ceil(ld / R)); CTA (b, y) owns the 512-column blocks
+// T2: sparse rank-m update on the ACTIVE columns (colmask), fp64 on the
+// fp64 tensor cores: G_partial[b] = A_act W_act for the active columns of
+// column range b -- a DGEMM with A's columns gathered on the fly (k = the
+// gathered column, m = the row, n = the component).
+// grid (GX, ceil(ld / 128)); CTA (b, y) owns the 512-column blocks
 // [b B / GX, (b+1) B / GX) (B = ceil(n / 512), two T1x items each), rows
-// [y R, y R + R) and all components.  Warp w owns components
-// [w JPT, w JPT + JPT), lane l rows y R + l + 32 t (t < TR = 32 / JPT), so a
-// thread keeps TR x JPT accumulators and R = 32 TR.  Blocks without an active
-// item (item_act, from T1x) are skipped 256 at a time; the active columns of
-// consecutive blocks are compacted in column order into a list of up to 512,
-// which is then consumed K (8, or 4 when R = 512) columns at a time: the A
-// tile (R rows x K columns) and the W tile (K x m_pad) are staged in shared memory, the next
-// tile's loads are issued before the current tile's FMAs (one barrier per
-// tile), and every A element is read once per CTA.  Sums run in column
-// order: deterministic run to run.
+// [128 y, 128 y + 128) and all NJ = 16 NT components.  Warp w owns rows
+// 32 (w % 4) .. + 32 (4 m-tiles) and components 8 NT (w / 4) .. + 8 NT (NT
+// n-tiles): 4 NT accumulator fragments.  Blocks without an active item are
+// skipped 256 at a time; the active columns of consecutive blocks are
+// compacted in column order into a list of up to 512, consumed 16 at a time:
+// the A tile (16 columns x 128 rows, widened to fp64 once) and the W tile
+// (16 columns x NJ, from the column-major copy Wt written by T1x, one
+// contiguous 8 NJ-byte row per column) are staged in shared memory (row
+// strides = 4 mod 16 doubles: fragment loads are conflict-free), the next
+// tile's loads are issued before the current tile's 4 x 4 NT DMMAs per warp
+// and k-step.  Every A element is read and converted once per CTA; sums run
+// in column order (deterministic run to run).
 constexpr int kTcUpdBlock = 512;
-template <int JPT>
-__host__ __device__ constexpr int tc_upd_rows() { return 32 * (32 / JPT); }
-template <typename TA, int JPT>
-__global__ void __launch_bounds__(256) tc_update_kernel(const TA* __restrict__ A, int64_t n, int ld, int m,
-                                                        const unsigned char* __restrict__ colmask,
-                                                        const unsigned char* __restrict__ item_act,
-                                                        const double* __restrict__ W, int64_t w_par_stride,
-                                                        int m_pad, double* __restrict__ part_g, const GpsCtl* ctl) {
-  constexpr int TR = 32 / JPT;          // rows per lane
-  constexpr int R = 32 * TR;            // rows per CTA
-  constexpr int NJ = 8 * JPT;           // components (= m_pad)
-  constexpr int K = R > 256 ? 4 : 8;    // list columns per staged tile (shared memory <= 48 KB)
-  constexpr int AL = R * K / 256;       // A tile elements loaded per thread
-  constexpr int WL = (K * NJ + 255) / 256;
+constexpr int kUpdR = 128;          // rows per CTA
+constexpr int kUpdKT = 16;          // list columns per staged tile
+constexpr int kUpdAS = kUpdR + 4;   // sA row stride (doubles), = 4 mod 16
+__host__ __device__ constexpr int upd_ws(int nj) { return nj + 4; }  // sW row stride, = 4 mod 16
+__host__ __device__ constexpr size_t tc_update_smem(int nj) {
+  return (size_t(2) * kUpdKT * kUpdAS + size_t(2) * kUpdKT * upd_ws(nj)) * sizeof(double);
+}
+template <typename TA, int NT>
+__global__ void __launch_bounds__(256, 2) tc_update_kernel(const TA* __restrict__ A, int64_t n, int ld, int m,
+                                                           const unsigned char* __restrict__ colmask,
+                                                           const unsigned char* __restrict__ item_act,
+                                                           const double* __restrict__ Wt,
+                                                           double* __restrict__ part_g, const GpsCtl* ctl) {
+  constexpr int NJ = 16 * NT;
+  constexpr int WS = upd_ws(NJ);
+  constexpr int VN = 16 / sizeof(TA);                     // elements per 16-byte A load
+  constexpr int AV = kUpdKT * kUpdR / VN / 256;           // A vectors per thread per tile
+  constexpr int WV = (kUpdKT * NJ / 2 + 255) / 256;       // W double2 per thread per tile
+  static_assert(AV >= 1 && kUpdKT * kUpdR % (VN * 256) == 0, "A tile mapping");
+  using V = typename Vec16<TA>::T;
   if (ctl != nullptr && ctl->done) return;
-  const int parity = ctl != nullptr ? (ctl->iter & 1) : 0;
-  const double* Wp = W + parity * w_par_stride;
+  extern __shared__ __align__(16) double upd_smem[];
+  double* sA = upd_smem;                        // [2][KT][AS]
+  double* sW = upd_smem + 2 * kUpdKT * kUpdAS;  // [2][KT][WS]
   const int64_t nblk = (n + kTcUpdBlock - 1) / kTcUpdBlock;
   const int64_t b0 = nblk * blockIdx.x / gridDim.x, b1 = nblk * (blockIdx.x + 1) / gridDim.x;
-  const int r0 = blockIdx.y * R;
+  const int r0 = blockIdx.y * kUpdR;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  double g[TR][JPT];
+  const int g = lane >> 2, t = lane & 3;
+  const int rg = warp & 3, cg = warp >> 2;
+  double acc[4][NT][2];
 #pragma unroll
-  for (int t = 0; t < TR; ++t)
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int u = 0; u < JPT; ++u) g[t][u] = 0.0;
+    for (int u = 0; u < NT; ++u) acc[i][u][0] = acc[i][u][1] = 0.0;
   __shared__ int blist[256];
   __shared__ int wcnt[8];
   __shared__ int64_t alist[kTcUpdBlock];
-  __shared__ double sA[2][K][R];
-  __shared__ double sW[2][K][NJ];
-  int acc = 0;  // entries in alist (block-uniform)
+  int acc_n = 0;  // entries in alist (block-uniform)
 
   // block-wide exclusive scan of a per-thread count (fixed order)
   auto scan = [&](int v, int& total) {
@@ -1003,53 +1051,64 @@ __global__ void __launch_bounds__(256) tc_update_kernel(const TA* __restrict__ A
     }
     return off + x - v;
   };
-  // A tile element e: list column e / R, row e % R; W tile element e: column
-  // e / NJ, component e % NJ (zero past the list or past m)
-  double ra[AL], rw[WL];
+  // A tile vector e: list column e / (R / VN), rows VN (e % (R / VN)) ..;
+  // W tile double2 e: list column e / (NJ / 2), components 2 (e % (NJ / 2))
+  V ra[AV];
+  double2 rw[WV];
   auto load = [&](int k0) {
 #pragma unroll
-    for (int i = 0; i < AL; ++i) {
-      const int e = tid + 256 * i, kk = e / R, r = r0 + e % R;
-      ra[i] = (k0 + kk < acc && r < ld) ? static_cast<double>(A[alist[k0 + kk] * ld + r]) : 0.0;
+    for (int i = 0; i < AV; ++i) {
+      const int e = tid + 256 * i, kk = e / (kUpdR / VN), r = r0 + VN * (e % (kUpdR / VN));
+      V v{};
+      if (k0 + kk < acc_n && r < ld) v = *reinterpret_cast<const V*>(A + alist[k0 + kk] * ld + r);
+      ra[i] = v;
     }
 #pragma unroll
-    for (int i = 0; i < WL; ++i) {
-      const int e = tid + 256 * i, kk = e / NJ, j = e % NJ;
-      rw[i] = (e < K * NJ && k0 + kk < acc && j < m) ? Wp[size_t(j) * n + alist[k0 + kk]] : 0.0;
+    for (int i = 0; i < WV; ++i) {
+      const int e = tid + 256 * i, kk = e / (NJ / 2), j2 = e % (NJ / 2);
+      double2 w = make_double2(0.0, 0.0);
+      if (e < kUpdKT * NJ / 2 && k0 + kk < acc_n) w = *reinterpret_cast<const double2*>(Wt + alist[k0 + kk] * NJ + 2 * j2);
+      rw[i] = w;
     }
   };
   auto flush = [&]() {
-    if (acc == 0) return;
+    if (acc_n == 0) return;
     load(0);
     int buf = 0;
-    for (int k0 = 0; k0 < acc; k0 += K, buf ^= 1) {
+    for (int k0 = 0; k0 < acc_n; k0 += kUpdKT, buf ^= 1) {
+      double* a_s = sA + buf * kUpdKT * kUpdAS;
+      double* w_s = sW + buf * kUpdKT * WS;
 #pragma unroll
-      for (int i = 0; i < AL; ++i) {
-        const int e = tid + 256 * i;
-        sA[buf][e / R][e % R] = ra[i];
+      for (int i = 0; i < AV; ++i) {
+        const int e = tid + 256 * i, kk = e / (kUpdR / VN), r = VN * (e % (kUpdR / VN));
+        TA el[VN];
+        Vec16<TA>::unpack(ra[i], el);
+#pragma unroll
+        for (int u = 0; u < VN; ++u) a_s[kk * kUpdAS + r + u] = static_cast<double>(el[u]);
       }
 #pragma unroll
-      for (int i = 0; i < WL; ++i) {
-        const int e = tid + 256 * i;
-        if (e < K * NJ) sW[buf][e / NJ][e % NJ] = rw[i];
+      for (int i = 0; i < WV; ++i) {
+        const int e = tid + 256 * i, kk = e / (NJ / 2), j2 = e % (NJ / 2);
+        if (e < kUpdKT * NJ / 2) *reinterpret_cast<double2*>(w_s + kk * WS + 2 * j2) = rw[i];
       }
       __syncthreads();
-      if (k0 + K < acc) load(k0 + K);
+      if (k0 + kUpdKT < acc_n) load(k0 + kUpdKT);
 #pragma unroll
-      for (int kk = 0; kk < K; ++kk) {
-        double wv[JPT];
+      for (int ks = 0; ks < kUpdKT; ks += 4) {
+        double a[4], b[NT];
 #pragma unroll
-        for (int u = 0; u < JPT; ++u) wv[u] = sW[buf][kk][warp * JPT + u];
+        for (int mt = 0; mt < 4; ++mt) a[mt] = a_s[(ks + t) * kUpdAS + rg * 32 + mt * 8 + g];
 #pragma unroll
-        for (int t = 0; t < TR; ++t) {
-          const double v = sA[buf][kk][lane + 32 * t];
+        for (int nt = 0; nt < NT; ++nt) b[nt] = w_s[(ks + t) * WS + cg * 8 * NT + nt * 8 + g];
 #pragma unroll
-          for (int u = 0; u < JPT; ++u) g[t][u] = fma(wv[u], v, g[t][u]);
-        }
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mt][nt], a[mt], b[nt]);
       }
+      // no barrier: buffer buf is refilled two tiles later, after the next
+      // tile's barrier, which every warp reaches only once done with buf
     }
-    __syncthreads();  // tiles and alist consumed
-    acc = 0;
+    acc_n = 0;
   };
 
   for (int64_t bb = b0; bb < b1; bb += 256) {
@@ -1067,22 +1126,26 @@ __global__ void __launch_bounds__(256) tc_update_kernel(const TA* __restrict__ A
       const bool f1 = c0 + 1 < n && colmask[c0 + 1] != 0;
       int total;
       const int off = scan(int(f0) + int(f1), total);
-      if (acc + total > kTcUpdBlock) flush();  // block-uniform
-      if (f0) alist[acc + off] = c0;
-      if (f1) alist[acc + off + int(f0)] = c0 + 1;
-      acc += total;
+      if (acc_n + total > kTcUpdBlock) flush();  // block-uniform
+      if (f0) alist[acc_n + off] = c0;
+      if (f1) alist[acc_n + off + int(f0)] = c0 + 1;
+      acc_n += total;
     }
     __syncthreads();  // blist reuse
   }
   __syncthreads();
   flush();
-  double* pg = part_g + size_t(blockIdx.x) * m_pad * ld;
+  double* pg = part_g + size_t(blockIdx.x) * NJ * ld;
 #pragma unroll
-  for (int t = 0; t < TR; ++t) {
-    const int r = r0 + lane + 32 * t;
+  for (int mt = 0; mt < 4; ++mt) {
+    const int r = r0 + rg * 32 + mt * 8 + g;
     if (r < ld)
 #pragma unroll
-      for (int u = 0; u < JPT; ++u) pg[size_t(warp * JPT + u) * ld + r] = g[t][u];
+      for (int nt = 0; nt < NT; ++nt) {
+        const int j = cg * 8 * NT + nt * 8 + 2 * t;
+        pg[size_t(j) * ld + r] = acc[mt][nt][0];
+        pg[size_t(j + 1) * ld + r] = acc[mt][nt][1];
+      }
   }
 }
 
