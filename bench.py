@@ -678,7 +678,7 @@ def run_ours(args):
             "a_stream_frac_of_8tbs": stream_gbs / world / 8000.0,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(), "peak_source": peak_src,
-                         "kernel": "su_sweep_kernel<float,4,256,kFused>",
+                         "kernel": "su_sweep_kernel<float,2,512,kFused,512>",
                          "algorithmic_bytes_per_launch": a_bytes_local, "avg_launch_ms": sweep_ms,
                          "read_stream_gbs": read_peak, "frac_of_read_stream": achieved / read_peak},
             "gpu_launches": launches,

@@ -172,6 +172,9 @@ struct gps_matrix {
   // on first use and kept with the matrix (A is immutable)
   int* tc_col_exp = nullptr;
   float* tc_col_delta = nullptr;
+  // fp32 storage with p == ld: column i has only normal values (K0), so the
+  // sweeps may widen it with integer instructions (su_kernels.cuh widen_normal)
+  unsigned char* col_fast = nullptr;
 };
 
 
@@ -192,7 +195,7 @@ using SweepFn = void (*)(SweepArgs);
 struct SweepPlan {
   bool wide = false;  // p beyond the fused kernels' coverage: W1 + W2 fallback
   SweepFn fn = nullptr;
-  int gs = 0, rv = 0, ng = 0;
+  int gs = 0, rv = 0, ng = 0, workers = 256;
   int cols_per_stage = 0, stages = 0;
   size_t smem = 0;
   int64_t total_stages = 0;
@@ -200,22 +203,26 @@ struct SweepPlan {
 };
 
 template <typename TA, int MODE>
-bool pick_kernel(int ld, SweepFn& fn, int& gs, int& rv) {
+bool pick_kernel(int ld, SweepFn& fn, int& gs, int& rv, int& workers) {
   constexpr int VN = 16 / sizeof(TA);
-#define GPS_TRY(GS_, RV_)                                 \
+#define GPS_TRY(GS_, RV_, NWK_)                           \
   if (ld <= GS_ * RV_ * VN) {                             \
-    fn = su_sweep_kernel<TA, RV_, GS_, MODE>;             \
+    fn = su_sweep_kernel<TA, RV_, GS_, MODE, NWK_>;       \
     gs = GS_;                                             \
     rv = RV_;                                             \
+    workers = NWK_;                                       \
     return true;                                          \
   }
-  GPS_TRY(32, 1)
-  GPS_TRY(32, 2)
-  GPS_TRY(32, 4)
-  GPS_TRY(64, 4)
-  GPS_TRY(128, 4)
-  GPS_TRY(256, 4)
-  GPS_TRY(256, 8)
+  GPS_TRY(32, 1, 256)
+  GPS_TRY(32, 2, 256)
+  GPS_TRY(32, 4, 256)
+  GPS_TRY(64, 4, 256)
+  GPS_TRY(128, 4, 256)
+  if (sizeof(TA) == 4 && std::getenv("GPSPCA_SU_WORKERS256") == nullptr) {  // env: A/B experiments only
+    GPS_TRY(512, 2, 512)
+  }
+  GPS_TRY(256, 4, 256)
+  GPS_TRY(256, 8, 256)
 #undef GPS_TRY
   return false;
 }
@@ -242,13 +249,13 @@ int make_plan(const gps_matrix* A, int mode, SweepPlan& plan) {
   bool ok = false;
   const int ld = static_cast<int>(A->ld);
   if (A->dtype == GPS_F32) {
-    if (mode == kFused) ok = pick_kernel<float, kFused>(ld, plan.fn, plan.gs, plan.rv);
-    if (mode == kDotOnly) ok = pick_kernel<float, kDotOnly>(ld, plan.fn, plan.gs, plan.rv);
-    if (mode == kCoef) ok = pick_kernel<float, kCoef>(ld, plan.fn, plan.gs, plan.rv);
+    if (mode == kFused) ok = pick_kernel<float, kFused>(ld, plan.fn, plan.gs, plan.rv, plan.workers);
+    if (mode == kDotOnly) ok = pick_kernel<float, kDotOnly>(ld, plan.fn, plan.gs, plan.rv, plan.workers);
+    if (mode == kCoef) ok = pick_kernel<float, kCoef>(ld, plan.fn, plan.gs, plan.rv, plan.workers);
   } else {
-    if (mode == kFused) ok = pick_kernel<double, kFused>(ld, plan.fn, plan.gs, plan.rv);
-    if (mode == kDotOnly) ok = pick_kernel<double, kDotOnly>(ld, plan.fn, plan.gs, plan.rv);
-    if (mode == kCoef) ok = pick_kernel<double, kCoef>(ld, plan.fn, plan.gs, plan.rv);
+    if (mode == kFused) ok = pick_kernel<double, kFused>(ld, plan.fn, plan.gs, plan.rv, plan.workers);
+    if (mode == kDotOnly) ok = pick_kernel<double, kDotOnly>(ld, plan.fn, plan.gs, plan.rv, plan.workers);
+    if (mode == kCoef) ok = pick_kernel<double, kCoef>(ld, plan.fn, plan.gs, plan.rv, plan.workers);
   }
   if (!ok) {
     plan.wide = true;
@@ -256,7 +263,7 @@ int make_plan(const gps_matrix* A, int mode, SweepPlan& plan) {
     return GPS_OK;
   }
   const size_t esz = A->dtype == GPS_F32 ? 4 : 8;
-  plan.ng = kSweepWorkers / plan.gs;
+  plan.ng = plan.workers / plan.gs;
   plan.cols_per_stage = plan.ng * sweep_cols_per_group(plan.rv);
   const size_t stage_bytes = size_t(plan.cols_per_stage) * A->ld * esz;
   const size_t red = sweep_red_bytes(plan.ng, plan.gs, sweep_cols_per_group(plan.rv));
@@ -347,10 +354,11 @@ int launch_sweep(gps_matrix* A, const SweepPlan& plan, SweepArgs args, int mode,
   args.A = A->d;
   args.n = A->n;
   args.ld = static_cast<int>(A->ld);
+  args.col_fast = A->norms_valid ? A->col_fast : nullptr;
   args.cols_per_stage = plan.cols_per_stage;
   args.num_stages = plan.stages;
   args.total_stages = plan.total_stages;
-  plan.fn<<<plan.grid, kSweepThreads, plan.smem, A->ctx->stream>>>(args);
+  plan.fn<<<plan.grid, plan.workers + 64, plan.smem, A->ctx->stream>>>(args);
   A->ctx->launches++;
   GPS_CHECK_LAUNCH("su_sweep_kernel launch");
   return GPS_OK;
@@ -696,6 +704,7 @@ int gps_matrix_destroy(gps_matrix* A) {
   if (A->owns) gps_free(A->d);
   if (A->tc_col_exp) gps_free(A->tc_col_exp);
   if (A->tc_col_delta) gps_free(A->tc_col_delta);
+  if (A->col_fast) gps_free(A->col_fast);
   delete A;
   return GPS_OK;
 }
@@ -747,13 +756,15 @@ int matrix_norms_locked(gps_matrix* A) {
   int rc = ctx_scratch(ctx, A->ld, A->n + 1);
   if (rc) return rc;
   if (!A->tc_col_exp) GPS_CUDA(gps_malloc(&A->tc_col_exp, size_t(A->n) * sizeof(int)));
+  // rows p .. ld of a padded matrix are zeros: only unpadded fp32 matrices get the flags
+  if (!A->col_fast && A->dtype == GPS_F32 && A->p == A->ld) GPS_CUDA(gps_malloc(&A->col_fast, size_t(A->n)));
   int* flag = reinterpret_cast<int*>(ctx->dvec + A->n);
   GPS_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
   const int blocks = ctx->num_sms * 8;
   if (A->dtype == GPS_F32)
     column_norms_kernel<float, true><<<blocks, 256, 0, ctx->stream>>>(static_cast<const float*>(A->d), A->n,
                                                                       static_cast<int>(A->ld), ctx->dvec, flag,
-                                                                      A->tc_col_exp);
+                                                                      A->tc_col_exp, A->col_fast);
   else
     column_norms_kernel<double, true><<<blocks, 256, 0, ctx->stream>>>(static_cast<const double*>(A->d), A->n,
                                                                        static_cast<int>(A->ld), ctx->dvec, flag,

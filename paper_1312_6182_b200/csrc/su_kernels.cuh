@@ -11,6 +11,8 @@
 // chip -- accumulates w_i a_i into a register-resident fp64 partial of g.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace gps {
@@ -58,6 +60,7 @@ struct SweepArgs {
   int64_t w_stride;
   const GpsCtl* ctl;  // optional loop control (early exit + parity)
   BandLog* band;      // optional near-threshold log (kFused)
+  const unsigned char* col_fast;  // optional: column i is all normal fp32 (K0) -> integer widening
   int cols_per_stage; // T
   int num_stages;     // smem ring depth S
   int64_t total_stages;
@@ -70,16 +73,33 @@ constexpr int kSweepLag = 1;                          // update of stage t runs 
 
 // Columns a group handles per stage: 4 (2 when a thread owns 8 vectors of a
 // column, to keep a stage <= 64 KB).
+#ifndef GPS_DOT_WIDEN
+#define GPS_DOT_WIDEN 0  // 1: the dot pass widens flagged columns with integer ops too (experiment)
+#endif
 #ifndef GPS_SWEEP_K
 #define GPS_SWEEP_K 4
 #endif
 __host__ __device__ constexpr int sweep_cols_per_group(int rv) { return rv >= 8 ? 2 : GPS_SWEEP_K; }
 
 // Shared scratch after the ring (doubles): red[D][NG][K][NW] warp partials,
-// wsm[D][NG][K] thresholded weights, sc[NG*K][3] reducer scalars; then the
-// mbarriers full[S], empty[S], pfull[D], wready[D].
+// wsm[D][NG][K] thresholded weights, sc[NG*K][3] reducer scalars,
+// wfl[D][NG][K] integer-widening flags; then the mbarriers full[S],
+// empty[S], pfull[D], wready[D].
 __host__ __device__ inline size_t sweep_red_bytes(int ng, int gs, int k) {
-  return (size_t(kSweepD) * ng * k * (gs / 32) + size_t(kSweepD) * ng * k + size_t(ng) * k * 3) * sizeof(double);
+  return (size_t(kSweepD) * ng * k * (gs / 32) + size_t(2) * kSweepD * ng * k + size_t(ng) * k * 3) *
+         sizeof(double);
+}
+
+// fp32 -> fp64 widening with integer instructions (LOP3, LEA.HI, IMAD.SHL)
+// for NORMAL fp32 values: exponent + (1023 - 127), mantissa shifted by 29.
+// Exact for every normal float; zero and subnormals are NOT handled, so it
+// is only used on columns the norms pass (K0) flagged as all-normal.  It
+// moves half of a dense sweep's conversions off the XU pipe, where
+// F2F.F64.F32 issues at 16 per clock per SM (ncu: XU 68 % busy at gamma = 0).
+__device__ __forceinline__ double widen_normal(float f) {
+  const uint32_t u = __float_as_uint(f);
+  const uint32_t hi = (__umulhi(u & 0x7fffffffu, 1u << 29) + 0x38000000u) | (u & 0x80000000u);
+  return __hiloint2double(static_cast<int>(hi), static_cast<int>(u << 29));
 }
 // Zeroed tail after the ring covering over-reads past the last column.
 __host__ __device__ inline size_t sweep_pad_bytes(int ld, int coverage, size_t esz) {
@@ -137,9 +157,13 @@ __device__ __forceinline__ int sweep_owner_col(int lane) {
 //                   writes c / w if asked, publishes w -> arrive wready.
 // No CTA-wide barrier inside the stream; every hand-off is an mbarrier, and
 // every summation order is fixed (bitwise reproducible run to run).
-template <typename TA, int RV, int GS, int MODE>
-__global__ void __launch_bounds__(kSweepThreads, 1) su_sweep_kernel(const SweepArgs a) {
-  constexpr int NG = kSweepWorkers / GS;
+// NWK worker threads: 256 (8 warps), or 512 (16 warps, 8 rows per thread)
+// for p in (2048, 4096] fp32, where a dense sweep (every column active, two
+// conversions and two FMAs per element) needs the extra warps to hide the
+// per-stage dot -> reduce -> update latency chain.
+template <typename TA, int RV, int GS, int MODE, int NWK = kSweepWorkers>
+__global__ void __launch_bounds__(NWK + 64, 1) su_sweep_kernel(const SweepArgs a) {
+  constexpr int NG = NWK / GS;
   constexpr int NW = GS / 32;  // warps per group
   constexpr int K = sweep_cols_per_group(RV);
   constexpr int D = kSweepD;
@@ -167,6 +191,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) su_sweep_kernel(const SweepA
                                           sweep_pad_bytes(ld, GS * RV * VN, sizeof(TA)));
   double* wsm = red + D * NG * K * NW;
   double* sc = wsm + D * NG * K;
+  double* wfl = sc + NG * K * 3;
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(red) + sweep_red_bytes(NG, GS, K));
   uint64_t* empty = full + S;
   uint64_t* pfull = empty + S;
@@ -181,24 +206,24 @@ __global__ void __launch_bounds__(kSweepThreads, 1) su_sweep_kernel(const SweepA
     // zero the ring and its tail pad so over-reads (rows >= ld of the last
     // column, columns >= n of a partial stage) only ever see finite values
     const size_t nbytes = size_t(S) * stage_bytes + sweep_pad_bytes(ld, GS * RV * VN, sizeof(TA));
-    for (size_t off = size_t(tid) * 16; off < nbytes; off += size_t(kSweepThreads) * 16)
+    for (size_t off = size_t(tid) * 16; off < nbytes; off += size_t((NWK + 64)) * 16)
       *reinterpret_cast<uint4*>(ring + off) = make_uint4(0, 0, 0, 0);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (tid == 0) {
     for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], kSweepWorkers / 32);
+      mbar_init(&empty[i], NWK / 32);
     }
     for (int i = 0; i < D; ++i) {
-      mbar_init(&pfull[i], kSweepWorkers / 32);
+      mbar_init(&pfull[i], NWK / 32);
       mbar_init(&wready[i], 1);
     }
     fence_mbar_init();
   }
   __syncthreads();
 
-  if (warp == kSweepWorkers / 32 + 1) {
+  if (warp == NWK / 32 + 1) {
     // ------------------------------------------------------ producer warp
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
@@ -222,7 +247,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) su_sweep_kernel(const SweepA
     return;
   }
 
-  if (warp == kSweepWorkers / 32) {
+  if (warp == NWK / 32) {
     // ------------------------------------------------------- reducer warp
     const int i = lane;  // (group, k) handled by this lane
     const bool mine = i < NG * K;
@@ -259,6 +284,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) su_sweep_kernel(const SweepA
           w = 0.0;
         }
         wsm[(d * NG + grp) * K + k] = w;
+        wfl[(d * NG + grp) * K + k] = (a.col_fast != nullptr && col < a.n && a.col_fast[col]) ? 1.0 : 0.0;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&wready[d]);
@@ -318,14 +344,32 @@ __global__ void __launch_bounds__(kSweepThreads, 1) su_sweep_kernel(const SweepA
           double acc[CH];
 #pragma unroll
           for (int c = 0; c < CH; ++c) acc[c] = 0.0;
+#if GPS_DOT_WIDEN
+          const int64_t colk = (s_begin + t) * T + k * NG + grp;
+          const bool fast = std::is_same<TA, float>::value && a.col_fast != nullptr && colk < a.n && a.col_fast[colk];
+          if (fast) {
 #pragma unroll
-          for (int v = 0; v < RV; ++v) {
-            const V q = *reinterpret_cast<const V*>(colp + (gt + v * GS) * VN);
-            TA e[VN];
-            Vec16<TA>::unpack(q, e);
+            for (int v = 0; v < RV; ++v) {
+              const V q = *reinterpret_cast<const V*>(colp + (gt + v * GS) * VN);
+              TA e[VN];
+              Vec16<TA>::unpack(q, e);
 #pragma unroll
-            for (int u = 0; u < VN; ++u)
-              acc[(v * VN + u) % CH] = fma(static_cast<double>(e[u]), xr[v * VN + u], acc[(v * VN + u) % CH]);
+              for (int u = 0; u < VN; ++u)
+                acc[(v * VN + u) % CH] = fma(widen_normal(static_cast<float>(e[u])), xr[v * VN + u],
+                                             acc[(v * VN + u) % CH]);
+            }
+          } else
+#endif
+          {
+#pragma unroll
+            for (int v = 0; v < RV; ++v) {
+              const V q = *reinterpret_cast<const V*>(colp + (gt + v * GS) * VN);
+              TA e[VN];
+              Vec16<TA>::unpack(q, e);
+#pragma unroll
+              for (int u = 0; u < VN; ++u)
+                acc[(v * VN + u) % CH] = fma(static_cast<double>(e[u]), xr[v * VN + u], acc[(v * VN + u) % CH]);
+            }
           }
           dot[k] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
         }
@@ -342,19 +386,32 @@ __global__ void __launch_bounds__(kSweepThreads, 1) su_sweep_kernel(const SweepA
       if (MODE != kDotOnly) {
         const TA* ptile = reinterpret_cast<const TA*>(ring + uslot * stage_bytes);
         const double* wp = wsm + (d * NG + grp) * K;
+        const double* fp = wfl + (d * NG + grp) * K;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           const double w = wp[k];
           if (w != 0.0) {
             const TA* colp = ptile + size_t(k * NG + grp) * ld;
+            if (std::is_same<TA, float>::value && fp[k] != 0.0) {  // group-uniform
 #pragma unroll
-            for (int v = 0; v < RV; ++v) {
-              const V q = *reinterpret_cast<const V*>(colp + (gt + v * GS) * VN);
-              TA e[VN];
-              Vec16<TA>::unpack(q, e);
+              for (int v = 0; v < RV; ++v) {
+                const V q = *reinterpret_cast<const V*>(colp + (gt + v * GS) * VN);
+                TA e[VN];
+                Vec16<TA>::unpack(q, e);
 #pragma unroll
-              for (int uu = 0; uu < VN; ++uu)
-                gr[v * VN + uu] = fma(w, static_cast<double>(e[uu]), gr[v * VN + uu]);
+                for (int uu = 0; uu < VN; ++uu)
+                  gr[v * VN + uu] = fma(w, widen_normal(static_cast<float>(e[uu])), gr[v * VN + uu]);
+              }
+            } else {
+#pragma unroll
+              for (int v = 0; v < RV; ++v) {
+                const V q = *reinterpret_cast<const V*>(colp + (gt + v * GS) * VN);
+                TA e[VN];
+                Vec16<TA>::unpack(q, e);
+#pragma unroll
+                for (int uu = 0; uu < VN; ++uu)
+                  gr[v * VN + uu] = fma(w, static_cast<double>(e[uu]), gr[v * VN + uu]);
+              }
             }
           }
         }
@@ -377,7 +434,7 @@ __global__ void __launch_bounds__(kSweepThreads, 1) su_sweep_kernel(const SweepA
           if (r0 + e < ld) pg[r0 + e] = gr[v * VN + e];
       }
     } else {
-      named_bar_sync(1, kSweepWorkers);  // all workers done with the ring
+      named_bar_sync(1, NWK);  // all workers done with the ring
       double* scratch = reinterpret_cast<double*>(ring);
 #pragma unroll
       for (int v = 0; v < RV; ++v) {
@@ -386,8 +443,8 @@ __global__ void __launch_bounds__(kSweepThreads, 1) su_sweep_kernel(const SweepA
         for (int e = 0; e < VN; ++e)
           if (r0 + e < ld) scratch[size_t(grp) * ld + r0 + e] = gr[v * VN + e];
       }
-      named_bar_sync(1, kSweepWorkers);
-      for (int r = tid; r < ld; r += kSweepWorkers) {
+      named_bar_sync(1, NWK);
+      for (int r = tid; r < ld; r += NWK) {
         double t = 0.0;
 #pragma unroll
         for (int g = 0; g < NG; ++g) t += scratch[size_t(g) * ld + r];
@@ -567,7 +624,8 @@ __global__ void __launch_bounds__(kStepThreads) su_step_kernel(double* exch, Gps
 template <typename TA, bool WITH_EXP = false>
 __global__ void __launch_bounds__(256) column_norms_kernel(const TA* __restrict__ A, int64_t n, int ld,
                                                            double* __restrict__ norms, int* nonfinite,
-                                                           int* __restrict__ col_exp = nullptr) {
+                                                           int* __restrict__ col_exp = nullptr,
+                                                           unsigned char* __restrict__ col_fast = nullptr) {
   constexpr int VN = Vec16<TA>::N;
   using V = typename Vec16<TA>::T;
   const int lane = threadIdx.x & 31;
@@ -579,6 +637,7 @@ __global__ void __launch_bounds__(256) column_norms_kernel(const TA* __restrict_
     const V* cp = reinterpret_cast<const V*>(A + col * ld);
     double acc = 0.0;
     float mx = 0.f;
+    int subnormal_or_zero = 0;
 #pragma unroll 4
     for (int v = lane; v < nv; v += 32) {
       V q = __ldcs(cp + v);
@@ -590,10 +649,15 @@ __global__ void __launch_bounds__(256) column_norms_kernel(const TA* __restrict_
         bad |= !isfinite(d);
         acc = fma(d, d, acc);
         if (WITH_EXP) mx = fmaxf(mx, __double2float_ru(fabs(d)));
+        if (col_fast != nullptr) subnormal_or_zero |= !(fabs(d) >= 1.1754943508222875e-38);  // FLT_MIN
       }
     }
     acc = warp_sum(acc);
     if (lane == 0) norms[col] = sqrt(acc);
+    if (col_fast != nullptr) {
+      const int any = __any_sync(0xffffffffu, subnormal_or_zero);
+      if (lane == 0) col_fast[col] = any ? 0 : 1;
+    }
     if (WITH_EXP) {  // the tensor-core filter's per-column scale exponent (tc_kernels.cuh)
 #pragma unroll
       for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));

@@ -24,15 +24,18 @@ A = gps.DataMatrix.from_device(At.data_ptr(), p, n, owner=At, device=0)
 gamma = (frac * float(A.norms.max())) ** 2
 i = int(np.argmax(A.norms))
 loop = gps.single_unit.PowerLoop(A, "l0", gamma, 0.0, iters + 4)
+stream = torch.cuda.Stream()
+torch.cuda.set_stream(stream)
+_native.context().set_stream(stream.cuda_stream)
 loop.start(A.column(i) / A.norms[i])
 L = _native.lib()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 torch.cuda.synchronize()
 _native.check(L.gps_su_enqueue(loop.handle, 7))
-e0.record()
+e0.record(stream)
 for _ in range(iters):
     _native.check(L.gps_su_enqueue(loop.handle, 7))
-e1.record()
+e1.record(stream)
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / iters
 print(f"gamma_frac={frac} ms/iter={ms:.3f} GB/s={p * n * 4 / ms / 1e6:.0f}")

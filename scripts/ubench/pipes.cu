@@ -73,6 +73,42 @@ __global__ void k_bits_fma(const float* in, double* out) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// no zero handling (columns flagged all-normal by the norms pass), shift+add as IMAD.HI
+__device__ __forceinline__ double bits2_f2d(float f) {
+  const uint32_t u = __float_as_uint(f);
+  const uint32_t hi = (__umulhi(u & 0x7fffffffu, 1u << 29) + 0x38000000u) | (u & 0x80000000u);
+  return __hiloint2double((int)hi, (int)(u << 29));
+}
+
+__global__ void k_bits2_fma(const float* in, double* out) {
+  float v[8];
+  for (int i = 0; i < 8; ++i) v[i] = in[threadIdx.x * 8 + i];
+  double acc[8] = {0}, x = 0.7;
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { acc[i] = fma(bits2_f2d(v[i]), x, acc[i]); v[i] = __int_as_float(__float_as_int(v[i]) ^ 1); }
+  }
+  double s = 0; for (int i = 0; i < 8; ++i) s += acc[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+// half the elements through F2F (XU pipe), half through the integer trick
+__global__ void k_mix_fma(const float* in, double* out) {
+  float v[8];
+  for (int i = 0; i < 8; ++i) v[i] = in[threadIdx.x * 8 + i];
+  double acc[8] = {0}, x = 0.7;
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const double d = (i & 1) ? bits2_f2d(v[i]) : (double)v[i];
+      acc[i] = fma(d, x, acc[i]);
+      v[i] = __int_as_float(__float_as_int(v[i]) ^ 1);
+    }
+  }
+  double s = 0; for (int i = 0; i < 8; ++i) s += acc[i];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 template <typename T>
 void run(const char* name, void (*kern)(const T*, double*), const void* in, double* out, int threads, int sms,
          double ops_per_thread_iter) {
@@ -100,6 +136,8 @@ int main() {
     run("bits", k_bits, fin, out, threads, sms, 8);
     run("F2F+DFMA", k_f2f_fma, fin, out, threads, sms, 8);
     run("bits+DFMA", k_bits_fma, fin, out, threads, sms, 8);
+    run("bits2+DFMA", k_bits2_fma, fin, out, threads, sms, 8);
+    run("mix+DFMA", k_mix_fma, fin, out, threads, sms, 8);
   }
   cudaError_t e = cudaDeviceSynchronize();
   printf("%s\n", cudaGetErrorString(e));
