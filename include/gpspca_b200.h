@@ -281,6 +281,17 @@ int gps_knn_distances(gps_ctx* ctx, const double* test_dev, int64_t n_test, cons
                       int64_t n_train, int dim, const double* train_sqnorm_dev, double* dist_dev,
                       int64_t* argmin_dev);
 
+/* k-NN neighbour selection (datasets.py:258): the k nearest train rows of
+ * every test row of the device distance matrix (n_test x n_train), in
+ * (distance, index) order like np.argsort(kind="stable")[:, :k]; idx_dev is
+ * n_test x k int64 on the device. */
+int gps_knn_topk(gps_ctx* ctx, const double* dist_dev, int64_t n_test, int64_t n_train, int k, int64_t* idx_dev);
+/* Thin SVD of the device matrix A (p x n) by one-sided Jacobi (pca.py:37-54
+ * pca_fit's np.linalg.svd): sigma_out min(p, n) non-increasing singular
+ * values, V_out n x min(p, n) column-major right singular vectors, sweeps
+ * used in *sweeps_out. */
+int gps_matrix_svd(gps_matrix* A, double* sigma_out, double* V_out, int* sweeps_out);
+
 #ifdef __cplusplus
 }
 #endif

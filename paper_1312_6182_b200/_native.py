@@ -95,6 +95,8 @@ SIGNATURES = {
     "gps_matrix_center": (C.c_int, [_vp, _dp, C.POINTER(_vp)]),
     "gps_row_sqnorms": (C.c_int, [_vp, _vp, _i64, C.c_int, _vp]),
     "gps_knn_distances": (C.c_int, [_vp, _vp, _i64, _vp, _i64, C.c_int, _vp, _vp, _vp]),
+    "gps_knn_topk": (C.c_int, [_vp, _vp, _i64, _i64, C.c_int, _vp]),
+    "gps_matrix_svd": (C.c_int, [_vp, _dp, _dp, _ip]),
     "gps_px_create": (C.c_int, [_vp, C.c_int, C.c_int, _i64, C.POINTER(_vp)]),
     "gps_px_handle_size": (C.c_int, []),
     "gps_px_ipc_handle": (C.c_int, [_vp, _vp]),

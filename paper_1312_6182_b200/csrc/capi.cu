@@ -2840,3 +2840,120 @@ extern "C" int gpsdbg_tc_profile(unsigned long long* out, int n, int reset) {
              ? GPS_OK
              : GPS_E_CUDA;
 }
+
+// k-NN neighbour selection on the device (datasets.py:258): the k nearest
+// train rows of every test row of dist (n_test x n_train), in (distance,
+// index) order.
+extern "C" int gps_knn_topk(gps_ctx* ctx, const double* dist_dev, int64_t n_test, int64_t n_train, int k,
+                            int64_t* idx_dev) {
+  if (!ctx || !dist_dev || !idx_dev) return fail(GPS_E_ARG, "NULL argument");
+  if (n_test < 1 || n_train < 1 || k < 1 || k > n_train) return fail(GPS_E_ARG, "bad shape");
+  if (n_test > 2147483647LL) return fail(GPS_E_ARG, "too many test rows");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  row_topk_kernel<<<static_cast<unsigned>(n_test), 256, 0, ctx->stream>>>(dist_dev, n_train, k, idx_dev);
+  ctx->launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "gps_knn_topk");
+  return GPS_OK;
+}
+
+// Thin SVD of the p x n device matrix A (pca.py:37-54 computes it with
+// LAPACK): one-sided Jacobi on the columns of A (n <= p, rotations
+// accumulated in V) or of A' (n > p, whose converged columns are s_j v_j).
+// sigma_out: min(p, n) singular values, non-increasing; V_out: n x min(p, n)
+// column-major right singular vectors in the same order.
+extern "C" int gps_matrix_svd(gps_matrix* A, double* sigma_out, double* V_out, int* sweeps_out) {
+  if (!A || !sigma_out || !V_out) return fail(GPS_E_ARG, "NULL argument");
+  gps_ctx* ctx = A->ctx;
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  const int64_t p = A->p, n = A->n;
+  const bool cols = n <= p;  // orthogonalise A's columns (else A')
+  const int64_t k = cols ? n : p, rows = cols ? p : n, ldy = cols ? A->ld : ceil_div(n, 32) * 32;
+  if (k > (int64_t(1) << 20)) return fail(GPS_E_UNSUPPORTED, "min(p, n) too large for the Jacobi SVD");
+  double *Y = nullptr, *V = nullptr, *nrm = nullptr;
+  int* rot = nullptr;
+  cudaError_t e = gps_malloc(&Y, size_t(k) * ldy * sizeof(double));
+  if (e == cudaSuccess && cols) e = gps_malloc(&V, size_t(k) * k * sizeof(double));
+  if (e == cudaSuccess) e = gps_malloc(&nrm, size_t(k) * sizeof(double));
+  if (e == cudaSuccess) e = gps_malloc(&rot, sizeof(int));
+  auto cleanup = [&]() {
+    if (Y) gps_free(Y);
+    if (V) gps_free(V);
+    if (nrm) gps_free(nrm);
+    if (rot) gps_free(rot);
+  };
+  if (e != cudaSuccess) {
+    cleanup();
+    return cuda_fail(e, "gps_matrix_svd allocation");
+  }
+  const bool f32 = A->dtype == GPS_F32;
+  if (cols) {
+    const int64_t elems = k * ldy;
+    const int blocks = ctx->num_sms * 8;
+    if (f32) widen_copy_kernel<float><<<blocks, 256, 0, ctx->stream>>>(static_cast<const float*>(A->d), elems, Y);
+    else widen_copy_kernel<double><<<blocks, 256, 0, ctx->stream>>>(static_cast<const double*>(A->d), elems, Y);
+    std::vector<double> I(size_t(k) * k, 0.0);
+    for (int64_t j = 0; j < k; ++j) I[size_t(j) * k + j] = 1.0;
+    e = cudaMemcpyAsync(V, I.data(), I.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  } else {
+    e = cudaMemsetAsync(Y, 0, size_t(k) * ldy * sizeof(double), ctx->stream);
+    dim3 grid(static_cast<unsigned>(ceil_div(n, 32)), static_cast<unsigned>(ceil_div(p, 32)));
+    if (f32)
+      transpose_widen_kernel<float><<<grid, dim3(32, 8), 0, ctx->stream>>>(static_cast<const float*>(A->d), A->ld, p,
+                                                                          n, Y, ldy);
+    else
+      transpose_widen_kernel<double><<<grid, dim3(32, 8), 0, ctx->stream>>>(static_cast<const double*>(A->d), A->ld,
+                                                                           p, n, Y, ldy);
+  }
+  ctx->launches++;
+  const int mp = static_cast<int>((k + 1) & ~int64_t(1));
+  const double tol = double(rows) * 2.220446049250313e-16;
+  int sweeps = 0;
+  for (; sweeps < 60 && e == cudaSuccess; ++sweeps) {
+    e = cudaMemsetAsync(rot, 0, sizeof(int), ctx->stream);
+    for (int step = 0; step < mp - 1 && e == cudaSuccess; ++step) {
+      jacobi_step_kernel<<<mp / 2, 256, 0, ctx->stream>>>(Y, ldy, rows, V, k, static_cast<int>(k), step, tol, rot);
+      ctx->launches++;
+    }
+    int any = 0;
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&any, rot, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e == cudaSuccess && !any) {
+      ++sweeps;
+      break;
+    }
+  }
+  std::vector<double> s(k), vh(cols ? size_t(k) * k : size_t(k) * ldy);
+  if (e == cudaSuccess) {
+    col_norms_f64_kernel<<<static_cast<unsigned>(ceil_div(k * 32, 256)), 256, 0, ctx->stream>>>(Y, ldy, rows,
+                                                                                               static_cast<int>(k), nrm);
+    ctx->launches++;
+    e = cudaMemcpyAsync(s.data(), nrm, size_t(k) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+  }
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(vh.data(), cols ? V : Y, vh.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  cleanup();
+  if (e != cudaSuccess) return cuda_fail(e, "gps_matrix_svd");
+  std::vector<int64_t> order(k);
+  for (int64_t j = 0; j < k; ++j) order[j] = j;
+  std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) { return s[x] > s[y]; });
+  for (int64_t t = 0; t < k; ++t) {
+    const int64_t j = order[t];
+    sigma_out[t] = s[j];
+    double* out = V_out + size_t(t) * n;
+    if (cols) {
+      std::memcpy(out, vh.data() + size_t(j) * k, size_t(n) * sizeof(double));
+    } else {
+      const double inv = s[j] > 0.0 ? 1.0 / s[j] : 0.0;
+      for (int64_t r = 0; r < n; ++r) out[r] = vh[size_t(j) * ldy + r] * inv;
+    }
+  }
+  if (sweeps_out) *sweeps_out = sweeps;
+  return GPS_OK;
+}

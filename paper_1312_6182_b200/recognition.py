@@ -13,11 +13,12 @@ Same names, arguments and errors as the reference (`pca.py:16-103`,
   s_j = Y_j - (mean' v_j) 1 - sum_{k<j} s_k (v_k' v_j).
 * `knn_classify`: squared distances by the reference's expansion
   (|t|^2 - 2 t.s) + |s|^2 clamped at 0 and the first minimum per test row
-  (`gps_knn_distances`); k > 1 selects with a stable device sort, and the
-  vote follows datasets.py:258-270 on the k selected labels.
-* `pca_fit`: thin SVD of the centred samples on the device
-  (torch.linalg.svd, a library call like cuBLAS; pca.py:37-54 is the dense
-  baseline, not the GPower path), sign-fixed by `deterministic_signs`.
+  (`gps_knn_distances`); k > 1 selects the k nearest in (distance, index)
+  order with a device selection kernel (`gps_knn_topk`), and the vote
+  follows datasets.py:258-270 on the k selected labels.
+* `pca_fit`: centring (`gps_matrix_center`) and the thin SVD by one-sided
+  Jacobi on the device (`gps_matrix_svd`), sign-fixed by
+  `deterministic_signs`; torch only moves buffers.
 """
 
 from dataclasses import dataclass
@@ -58,21 +59,27 @@ def _torch():
 
 def pca_fit(samples, m):
     """Top-m principal components of a samples x variables matrix
-    (pca.py:37-54)."""
+    (pca.py:37-54): the leading right singular vectors of the centred data,
+    sign-fixed.  Centring (gps_matrix_center) and the thin SVD (one-sided
+    Jacobi on the device, gps_matrix_svd) run in libgpspca_b200."""
+    from .core import center_columns_with_means
+
     S = np.asarray(samples, dtype=np.float64)
     if S.ndim != 2:
         raise ValueError("samples must be a 2-d matrix")
     if not 1 <= m <= min(S.shape):
         raise ValueError(f"need 1 <= m <= min(#samples, #variables) = {min(S.shape)}")
-    torch = _torch()
-    dev = f"cuda:{_native.default_device()}"
-    St = torch.from_numpy(np.ascontiguousarray(S)).to(dev)
-    mean_t = St.mean(dim=0)
-    _, s, Vt = torch.linalg.svd(St - mean_t, full_matrices=False)
+    Ac, mean = center_columns_with_means(DataMatrix(S))
+    r = min(S.shape)
+    sigma = np.empty(r)
+    V = np.empty((S.shape[1], r), order="F")
+    sweeps = _native.C.c_int(0)
+    _native.check(_native.lib().gps_matrix_svd(Ac.handle, _native.dptr(sigma), V.ctypes.data_as(_native._dp),
+                                               _native.C.byref(sweeps)), "pca_fit SVD")
     return PcaModel(
-        components=deterministic_signs(Vt[:m].T.cpu().numpy()),
-        singular_values=s[:m].cpu().numpy().copy(),
-        mean=mean_t.cpu().numpy(),
+        components=deterministic_signs(V[:, :m]),
+        singular_values=sigma[:m].copy(),
+        mean=mean,
     )
 
 
@@ -191,7 +198,10 @@ def knn_classify(train_embedding, train_labels, test_embedding, test_labels=None
         if k == 1:
             predictions[lo:lo + T] = train_labels[amin.cpu().numpy()]
             continue
-        order = torch.sort(dist, dim=1, stable=True).indices[:, :k].cpu().numpy()
+        idx = torch.empty((T, k), dtype=torch.int64, device=dev)
+        _native.check(L.gps_knn_topk(ctx.handle, _native.C.c_void_p(dist.data_ptr()), T, R, k,
+                                     _native.C.c_void_p(idx.data_ptr())))
+        order = idx.cpu().numpy()
         for r in range(T):
             votes = train_labels[order[r]]
             labels, counts = np.unique(votes, return_counts=True)

@@ -172,3 +172,21 @@ def test_fit_projection_centres_on_device():
     Z, mean, report = fit_projection(X, "sl1", 2, 0.05)
     np.testing.assert_allclose(mean, X.mean(axis=0), rtol=1e-12)
     assert Z.shape == (30, 2) and report.iterations >= 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape", [(1500, 200), (120, 700)], ids=["tall", "wide"])
+def test_device_pca_fit_jacobi_both_orientations(shape):
+    """pca_fit's device one-sided Jacobi SVD on both orientations (columns of
+    S when n <= p, of S' otherwise) against pca.py:37-54 restated with
+    LAPACK: top components with separated singular values."""
+    g = _gps()
+    rng = np.random.default_rng(5)
+    N, F = shape
+    S = rng.standard_normal((N, F)) @ np.diag(np.linspace(3.0, 1.0, F)) + 0.5
+    model = g.pca_fit(S, 6)
+    Sc = S - S.mean(axis=0)
+    _, s, Vt = np.linalg.svd(Sc, full_matrices=False)
+    np.testing.assert_allclose(model.singular_values, s[:6], rtol=1e-11)
+    ref = g.recognition.deterministic_signs(Vt[:6].T)
+    np.testing.assert_allclose(model.components, ref, atol=1e-8)
