@@ -451,7 +451,7 @@ def _bk_poll(loop):
     return d.value, i.value, c.value
 
 
-def su_dense_line(torch, gps, ctx, dev, A, p, n, k=20):
+def su_dense_line(torch, gps, ctx, dev, A, p, n, k=60):
     """Single-unit l0 at gamma = 0 on the resident C2 matrix: every column is
     active, so every column's rank-1 update runs from shared memory in the
     fused sweep -- the worst case of K1 (SURVEY §7 'exploit w-sparsity')."""
@@ -467,16 +467,18 @@ def su_dense_line(torch, gps, ctx, dev, A, p, n, k=20):
     for _ in range(2):
         _native.check(L.gps_su_enqueue(loop.handle, 7))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(k):
-        _native.check(L.gps_su_enqueue(loop.handle, 7))
-    e1.record(stream)
-    e1.synchronize()
+    with ClockSampler(dev.index) as clocks:
+        e0.record(stream)
+        for _ in range(k):
+            _native.check(L.gps_su_enqueue(loop.handle, 7))
+        e1.record(stream)
+        e1.synchronize()
     ctx.set_stream(None)
     ms = e0.elapsed_time(e1) / k
     gbs = p * n * 4 / (ms / 1e3) / 1e9
     return {"workload": f"SL0 gamma=0 on the C2 matrix (p={p} n={n}, every column active)", "iters_per_s": 1e3 / ms,
-            "ms_per_iter": ms, "a_stream_gbs": gbs, "frac_of_8tbs": gbs / 8000.0, "iterations_timed": k}
+            "ms_per_iter": ms, "a_stream_gbs": gbs, "frac_of_8tbs": gbs / 8000.0, "iterations_timed": k,
+            "clocks": clocks.summary()}
 
 
 def run_ours(args):

@@ -626,6 +626,9 @@ __global__ void __launch_bounds__(256) column_norms_kernel(const TA* __restrict_
                                                            double* __restrict__ norms, int* nonfinite,
                                                            int* __restrict__ col_exp = nullptr,
                                                            unsigned char* __restrict__ col_fast = nullptr) {
+  // the all-normal flags ride on the once-per-matrix pass (WITH_EXP); the
+  // plain variant is gps_bench_read_stream's read-only reference stream
+  constexpr bool kFlags = WITH_EXP;
   constexpr int VN = Vec16<TA>::N;
   using V = typename Vec16<TA>::T;
   const int lane = threadIdx.x & 31;
@@ -649,12 +652,12 @@ __global__ void __launch_bounds__(256) column_norms_kernel(const TA* __restrict_
         bad |= !isfinite(d);
         acc = fma(d, d, acc);
         if (WITH_EXP) mx = fmaxf(mx, __double2float_ru(fabs(d)));
-        if (col_fast != nullptr) subnormal_or_zero |= !(fabs(d) >= 1.1754943508222875e-38);  // FLT_MIN
+        if (kFlags) subnormal_or_zero |= !(fabs(d) >= 1.1754943508222875e-38);  // FLT_MIN
       }
     }
     acc = warp_sum(acc);
     if (lane == 0) norms[col] = sqrt(acc);
-    if (col_fast != nullptr) {
+    if (kFlags && col_fast != nullptr) {
       const int any = __any_sync(0xffffffffu, subnormal_or_zero);
       if (lane == 0) col_fast[col] = any ? 0 : 1;
     }

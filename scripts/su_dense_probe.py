@@ -20,7 +20,10 @@ iters = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 p, n = 4096, 1 << 20
 dev = torch.device("cuda", 0)
 At = bench.make_c2(torch, p, n, 0, n, dev)
-A = gps.DataMatrix.from_device(At.data_ptr(), p, n, owner=At, device=0)
+if os.environ.get("PROBE_COPY"):  # engine-owned copy, as bench.py's C2 matrix
+    A = gps.DataMatrix.from_device(At.data_ptr(), p, n, ld=p, dtype=np.float32, device=0)
+else:
+    A = gps.DataMatrix.from_device(At.data_ptr(), p, n, owner=At, device=0)
 gamma = (frac * float(A.norms.max())) ** 2
 i = int(np.argmax(A.norms))
 loop = gps.single_unit.PowerLoop(A, "l0", gamma, 0.0, iters + 4)
