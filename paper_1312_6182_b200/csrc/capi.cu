@@ -2163,9 +2163,16 @@ int gps_bk_result(gps_bk* s, double* X_out, double* hist_out, int* n_hist, int* 
   if (hist_out)
     GPS_CUDA(cudaMemcpyAsync(hist_out, s->hist, size_t(k + 1) * sizeof(double), cudaMemcpyDeviceToHost,
                              ctx->stream));
-  if (W_out)
+  if (W_out) {
+    if (s->tc) {
+      tc_mask_w_kernel<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(s->W + (k & 1) * mp * n, int64_t(n), s->m,
+                                                                 s->colmask);
+      ctx->launches++;
+      GPS_CHECK_LAUNCH("tc_mask_w_kernel launch");
+    }
     GPS_CUDA(cudaMemcpyAsync(W_out, s->W + (k & 1) * mp * n, size_t(s->m) * n * sizeof(double),
                              cudaMemcpyDeviceToHost, ctx->stream));
+  }
   GPS_CUDA(cudaStreamSynchronize(ctx->stream));
   if (n_hist) *n_hist = k + 1;
   if (converged) *converged = c.converged;
@@ -2269,6 +2276,11 @@ int gps_bk_sweep(gps_matrix* A, const double* X, int m, const double* gamma, con
   std::vector<double> ex(size_t(s->ngroups) * s->exch_stride());
   if (rc == GPS_OK) {
     e = cudaMemcpyAsync(ex.data(), s->exch, ex.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess && W_out && s->tc) {
+      tc_mask_w_kernel<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(s->W, int64_t(n), m, s->colmask);
+      ctx->launches++;
+      e = cudaGetLastError();
+    }
     if (e == cudaSuccess && W_out)
       e = cudaMemcpyAsync(W_out, s->W, size_t(m) * n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);

@@ -189,7 +189,7 @@ struct TcDotsArgs {
   const double* mu;     // m
   const int* col_exp;   // n: scale exponents of the columns
   const float* col_delta;  // n: candidate margins (tc_col_delta_kernel)
-  double* w_out;        // [m_pad][n] parity slots (may be null): zeroed for non-candidate columns
+  double* w_out;        // [m_pad][n] parity slots (unused by T1: tc_mask_w_kernel zeroes filtered columns)
   int64_t w_stride;
   unsigned char* colmask;  // [2][n]: 1 if column i is a candidate (one row per epilogue group)
   unsigned char* tflag;    // [tiles][8]: any candidate in (tile, group, lane quarter)
@@ -331,7 +331,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                    const __grid_constant__ CUtensorMap tmX2, const TcDotsArgs a) {
   extern __shared__ unsigned char smem_raw[];
   if (a.ctl != nullptr && a.ctl->done) return;
-  const int parity = a.ctl != nullptr ? (a.ctl->iter & 1) : 0;
   unsigned char* smem =
       reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int NP = a.n_pad;
@@ -594,7 +593,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int q = warp & 3;
     const int g = warp >= 12 ? 1 : 0;
     const int jbase = g * 32;
-    double* wbase = a.w_out != nullptr ? a.w_out + parity * a.w_stride : nullptr;
     TcProf pf{kTcProfile && (a.probe & 64) != 0 && warp == 4, 0};
     unsigned long long w11 = 0, w12 = 0;
     const long long t_role = clock64();
@@ -654,11 +652,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           const double s = smu[j] * (fabs((static_cast<double>(ch[jj]) - static_cast<double>(cl[jj])) * unscale) + delta);
           cand |= (a.penalty == 0) ? (s >= sgam[j]) : (s * s >= sgam[j]);
         }
-        if (!cand && wbase != nullptr) {
-#pragma unroll 4
-          for (int jj = 0; jj < 32; ++jj)
-            if (jbase + jj < a.m) wbase[size_t(jbase + jj) * a.n + col] = 0.0;
-        }
+        // W is NOT zeroed here for non-candidates (1 GB of writes per C4
+        // iteration competing with the A stream): the loadings read W of the
+        // final sweep through tc_mask_w_kernel, which zeroes every column
+        // the final activity mask leaves inactive.
         a.colmask[size_t(g) * a.n + col] = cand ? 1 : 0;
       }
       // per (tile, group, lane quarter) flag: T1x skips tiles with none
@@ -1146,6 +1143,17 @@ __global__ void __launch_bounds__(256, 2) tc_update_kernel(const TA* __restrict_
         pg[size_t(j) * ld + r] = acc[mt][nt][0];
         pg[size_t(j + 1) * ld + r] = acc[mt][nt][1];
       }
+  }
+}
+
+// Loadings of the tensor-core path: W[j][col] of the final sweep is valid
+// where T1x processed the column (every candidate, with W = 0 for an
+// inactive one); the filtered-out columns still hold older values, so they
+// are zeroed here by the final activity mask (colmask[col] = 0).
+__global__ void tc_mask_w_kernel(double* __restrict__ W, int64_t n, int m, const unsigned char* __restrict__ colmask) {
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n * m; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t col = e % n;
+    if (colmask[col] == 0) W[e] = 0.0;
   }
 }
 
