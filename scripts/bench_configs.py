@@ -6,6 +6,11 @@ iterations/s and A-stream GB/s of the device-resident power loop (fixed
 iteration count, tol = 0), for the single-unit and block formulations at the
 BASELINE shapes that fit one B200.  Data: Gaussian (the timing harness's
 distribution, reference bench.py:245-246) generated on the device.
+
+--cpu adds, per (formulation, n), the reference CPU path on the box's host
+cores: real iterations of the unmodified reference (baseline/_ref) loop on
+the same matrix (copied to the host) -- the whole matrix up to n = 2^20, a
+2^20-column slice scaled linearly in n beyond (stated in the row).
 """
 
 import argparse
@@ -76,11 +81,61 @@ def full_reads(A, m):
     return (m + mg - 1) // mg
 
 
+CPU_MAX_COLS = 1 << 20
+
+
+def ref_iteration_seconds(ref, A32, config, m, iters=1):
+    """Seconds per iteration of the reference's own loop body on the host
+    matrix A32 (p x cols fp32 view): single_unit.py:167-180 or
+    block.py:211-224, best thread configuration of bench.py."""
+    import bench
+    from gpspca import block as rb
+
+    A = ref.DataMatrix(A32)
+    norms = ref.column_norms(A)
+    top = float(norms.max())
+    pen = "l1" if config[2] == "1" else "l0"
+    gamma = 0.1 * top if pen == "l1" else (0.1 * top) ** 2
+    _, workers, blas = bench.best_reference_config(ref, np.asarray(A32[:, : min(A32.shape[1], 65536)]),
+                                                   os.cpu_count(), reps=1)
+    if config.startswith("SL"):
+        loop = bench.ReferenceLoop(ref, A, gamma, workers, blas)
+        loop.first(A.column(int(np.argmax(norms))) / top)
+        t0 = time.perf_counter()
+        for _ in range(iters):
+            loop.step()
+        t = (time.perf_counter() - t0) / iters
+        loop.close()
+        return t, workers, blas
+    from threadpoolctl import threadpool_limits
+
+    plan = ref.KernelPlan(workers=workers, chunk=256)
+    g = np.full(m, gamma)
+    mu = np.ones(m)
+    with threadpool_limits(blas, user_api="blas"):
+        X = rb._init_block(A, ref.SolverConfig(penalty=pen, mode="block", m=m, gamma=gamma), plan)
+        C = rb._correlations(A, X, plan)
+        t0 = time.perf_counter()
+        for _ in range(iters):
+            G = rb._block_gradient(A, C, g, mu, pen, plan)
+            X = rb.polar_projection(G).values
+            C = rb._correlations(A, X, plan)
+            rb._block_objective_from_correlations(C, g, mu, pen)
+        t = (time.perf_counter() - t0) / iters
+    return t, workers, blas
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--tag", default="r1")
     ap.add_argument("--only", default="")
+    ap.add_argument("--cpu", action="store_true", help="also time the reference CPU path (baseline/_ref)")
     args = ap.parse_args()
+    ref = None
+    if args.cpu:
+        import bench
+
+        ref = bench.import_reference()
     import torch
 
     import paper_1312_6182_b200 as gps
@@ -91,8 +146,21 @@ def main():
         print(json.dumps(rec), flush=True)
         out.append(rec)
 
+    def cpu_rows(At, p, n):
+        """The reference CPU path beside the device rows of this matrix."""
+        cols = min(n, CPU_MAX_COLS)
+        A32 = At[:cols].cpu().numpy().T
+        for config, m in (("SL1", 1), ("SL0", 1), ("BL1 m=10", 10), ("BL0 m=10", 10)):
+            t, workers, blas = ref_iteration_seconds(ref, A32, config, m)
+            t_full = t * n / cols
+            emit({"config": config, "p": p, "n": n, "impl": "reference-cpu", "iters_per_s": 1 / t_full,
+                  "ms_per_iter": t_full * 1e3, "cores": os.cpu_count(), "workers": workers, "blas_threads": blas,
+                  "sample": "whole matrix" if cols == n else f"first {cols} columns, scaled by n/{cols}"})
+
     def su_rows(p, n, seed, iters):
         At = gauss(torch, p, n, seed)
+        if ref is not None:
+            cpu_rows(At, p, n)
         A = gps.DataMatrix.from_device(At.data_ptr(), p, n, owner=At)
         del At
         top = float(A.norms.max())
