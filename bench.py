@@ -541,9 +541,11 @@ def run_ours(args):
         # over NVLink peer memory when every rank has its own peer-capable
         # GPU, else the torch.distributed all-reduce (gloo emulation on one
         # GPU, NCCL)
-        from paper_1312_6182_b200.distributed import PeerExchange, peer_exchange_available
+        from paper_1312_6182_b200.distributed import PeerExchange, peer_exchange_available, px_self_test
 
         px = PeerExchange(ctx, comm, exch.numel()) if peer_exchange_available(comm, dev) else None
+        if px is not None and not px_self_test(px, comm, dev, exch.numel()):
+            px = None  # the peer path did not reproduce NCCL's all-reduce here: NCCL it is
         if px is not None:
             _native.check(_native.lib().gps_su_attach_px(loop.handle, px.handle))
         exchange = (lambda t: None) if px is not None else comm.all_reduce_sum

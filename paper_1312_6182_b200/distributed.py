@@ -68,9 +68,13 @@ class DeviceShardLoop:
     def start(self, x0):
         self.loop.start(x0)
 
-    def attach_px(self, comm):
-        self.px = PeerExchange(self.A_context, comm, self.buf.numel())  # ld + 4
+    def attach_px(self, comm, device):
+        px = PeerExchange(self.A_context, comm, self.buf.numel())  # ld + 4
+        if not px_self_test(px, comm, device, self.buf.numel()):
+            return False
+        self.px = px
         _native.check(_native.lib().gps_su_attach_px(self.loop.handle, self.px.handle), "gps_su_attach_px")
+        return True
 
     def enqueue_sweep(self):
         _native.check(_native.lib().gps_su_enqueue_sweep(self.loop.handle))
@@ -143,6 +147,32 @@ def peer_exchange_available(comm, device):
     return all(torch.cuda.can_device_access_peer(a, b) for a in devs for b in devs if a != b)
 
 
+def px_self_test(px, comm, device, count):
+    """Collective check of a freshly opened peer exchange: one standalone
+    peer-memory all-reduce of a seeded vector against the torch.distributed
+    all-reduce (NCCL) of the same vector.  Returns True on every rank only
+    if every rank's result agrees (1e-12; the rank-order and NCCL summation
+    orders differ in rounding) and no rank raised -- callers fall back to
+    the torch.distributed exchange otherwise, so a peer path that cannot run
+    on a given machine costs speed, never results."""
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(1234 + comm.rank)
+    v = torch.randn(count, dtype=torch.float64, device=device, generator=g)
+    ref = v.clone()
+    comm.dist.all_reduce(ref, op=comm.dist.ReduceOp.SUM, group=comm.group)
+    try:
+        px.all_reduce(v)
+        torch.cuda.synchronize(device)
+        ok = bool(torch.allclose(v, ref, rtol=1e-12, atol=1e-12))
+    except Exception:  # noqa: BLE001 -- any failure means "do not use the peer path"
+        ok = False
+    flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=device)
+    comm.dist.all_reduce(flag, op=comm.dist.ReduceOp.MIN, group=comm.group)
+    return bool(flag.item())
+
+
 def loop_all_reduce(loop, comm, device):
     """The per-iteration exchange of a device shard loop.  With peer access
     between every rank's GPU, a PeerExchange is attached to the loop and the
@@ -150,8 +180,8 @@ def loop_all_reduce(loop, comm, device):
     compute and collective in one kernel -- so the returned callable does
     nothing; otherwise the torch.distributed all-reduce."""
     if hasattr(loop, "attach_px") and peer_exchange_available(comm, device):
-        loop.attach_px(comm)
-        return lambda t: None
+        if loop.attach_px(comm, device):
+            return lambda t: None
     return comm.all_reduce_sum
 
 
@@ -311,11 +341,15 @@ class DeviceBlockShardLoop:
     def start(self, M, orthonormalize):
         (self.loop.start_qr if orthonormalize else self.loop.start_user)(M)
 
-    def attach_px(self, comm):
+    def attach_px(self, comm, device):
         stride = _native.C.c_int64()
         _native.check(_native.lib().gps_bk_exchange_stride(self.loop.handle, _native.C.byref(stride)))
-        self.px = PeerExchange(self.A_context, comm, stride.value)  # one group's exchange vector
+        px = PeerExchange(self.A_context, comm, stride.value)  # one group's exchange vector
+        if not px_self_test(px, comm, device, stride.value):
+            return False
+        self.px = px
         _native.check(_native.lib().gps_bk_attach_px(self.loop.handle, self.px.handle), "gps_bk_attach_px")
+        return True
 
     def enqueue_sweep(self):
         _native.check(_native.lib().gps_bk_enqueue_sweep(self.loop.handle))
