@@ -404,24 +404,54 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
       return;
     }
   }
-  // stage 2: R = R2 R1 (upper, row-major in W), its polar factor P by the
-  // Newton-Schulz iteration (the CholeskyQR2 path only runs for condition
-  // numbers far below the rank cutoff max(p, m) eps -- stage 1 checked --
-  // so rank = m here), then S = R2^-1 P, the right factor of X = Q1 S.
+  // stage 2: R = R2 R1 (upper, row-major in W), its polar factor P, then
+  // S = R2^-1 P, the right factor of X = Q1 S (the CholeskyQR2 path only
+  // runs for condition numbers far below the rank cutoff max(p, m) eps --
+  // stage 1 checked -- so rank = m here).  P comes from one scaled Newton
+  // step, which the triangular factors make cheap because R^-1 = R1^-1 R2^-1
+  // is at hand (R1^-1 from stage 1 in Sg, R2^-1 = Ri),
+  //   M = (zeta R + zeta^-1 R^-T) / 2,  zeta = sqrt(|R^-1|_F / |R|_F)
+  // (same singular vectors as R; the singular values move into
+  // [1, (sqrt(k) + 1 / sqrt(k)) / 2] for kappa k), followed by the
+  // Newton-Schulz iteration on M, which then starts well inside its
+  // quadratic region (~20 -> ~7 steps at kappa ~ 100).  Scratch: T1 = the
+  // m x m slot after W inside the Newton-Schulz workspace.
+  double* T1 = W + m * m;
+  for (int e = tid; e < m * m; e += nt) T1[e] = R1g[e];  // R1 (upper) into shared memory
+  __syncthreads();
   for (int e = tid; e < m * m; e += nt) {
     const int i = e / m, j = e % m;
     double t = 0.0;
-    for (int k = i; k <= j; ++k) t += R[i * m + k] * R1g[k * m + j];
-    W[e] = (i <= j) ? t : 0.0;
+    for (int k = i; k <= j; ++k) t = fma(R[i * m + k], T1[k * m + j], t);
+    W[e] = (i <= j) ? t : 0.0;  // R = R2 R1
+  }
+  __syncthreads();
+  for (int e = tid; e < m * m; e += nt) R[e] = Sg[e];  // R1^-1 (R2 is no longer needed)
+  __syncthreads();
+  for (int e = tid; e < m * m; e += nt) {
+    const int i = e / m, j = e % m;
+    double t = 0.0;
+    for (int k = i; k <= j; ++k) t = fma(R[i * m + k], Ri[k * m + j], t);
+    T1[e] = (i <= j) ? t : 0.0;  // R^-1 = R1^-1 R2^-1
   }
   __syncthreads();
   GPS_STAMP(4);
 #ifdef GPS_POLAR_DEBUG
   if (tid == 0) printf("chol stage %d R2R1 done %lld\n", stage, clock64());
 #endif
-  // M receives P (starting from R2 R1); R onwards (R2 itself is no longer
-  // needed: Ri = R2^-1 is kept) is scratch
-  for (int e = tid; e < m * m; e += nt) M[e] = W[e];
+  {
+    double a = 0.0, b = 0.0;
+    for (int e = tid; e < m * m; e += nt) {
+      a = fma(W[e], W[e], a);
+      b = fma(T1[e], T1[e], b);
+    }
+    const double fa = sqrt(block_sum_any(a, red)), fb = sqrt(block_sum_any(b, red));
+    const double zeta = sqrt(fb / fa);
+    for (int e = tid; e < m * m; e += nt) {
+      const int i = e / m, j = e % m;
+      M[e] = 0.5 * (zeta * W[e] + T1[j * m + i] / zeta);
+    }
+  }
   __syncthreads();
   if (!newton_schulz_polar(M, R, red, m, 100)) {  // not converged: exact path decides
     if (tid == 0) pc->fallback = 1;
