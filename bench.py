@@ -681,7 +681,11 @@ def run_ours(args):
             "a_stream_gbs": stream_gbs,
             "a_stream_frac_of_8tbs": stream_gbs / world / 8000.0,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic(), "peak_source": peak_src,
+                         "frac": achieved / peak, "traffic": ncu_traffic(),
+                         "traffic_source": "profiles/ncu_sweep_summary.json: dram__bytes_read.sum + "
+                                           "dram__bytes_write.sum of this kernel at this shape from one "
+                                           "committed ncu --set full capture (not measured in this run)",
+                         "peak_source": peak_src,
                          "kernel": "su_sweep_kernel<float,2,512,kFused,512>",
                          "algorithmic_bytes_per_launch": a_bytes_local, "avg_launch_ms": sweep_ms,
                          "read_stream_gbs": read_peak, "frac_of_read_stream": achieved / read_peak},
