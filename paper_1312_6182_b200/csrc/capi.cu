@@ -1366,7 +1366,8 @@ int ensure_polar_attrs() {
   const void* fns[] = {reinterpret_cast<const void*>(bk_step_kernel), reinterpret_cast<const void*>(polar_kernel),
                        reinterpret_cast<const void*>(cholqr2_kernel), reinterpret_cast<const void*>(bk_finish_kernel),
                        reinterpret_cast<const void*>(chol_stage_kernel), reinterpret_cast<const void*>(hh_init_kernel),
-                       reinterpret_cast<const void*>(stiefel_error_kernel)};
+                       reinterpret_cast<const void*>(stiefel_error_kernel),
+                       reinterpret_cast<const void*>(apply_right_kernel)};
   for (const void* fn : fns) {
     cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (err != cudaSuccess) return cuda_fail(err, "cudaFuncSetAttribute(polar)");
@@ -1641,12 +1642,12 @@ int enqueue_cholqr2_polar(gps_ctx* ctx, const CholQr2Polar& q, int ld, int p, in
   gram_reduce_kernel<<<(m * m + 255) / 256, 256, 0, ctx->stream>>>(q.gram_part, kGramBlocks, m * m, q.pc);
   chol_stage_kernel<<<1, kPolarThreads, chol_smem_bytes(m), ctx->stream>>>(q.gram_part, 1, m, p, 1, q.R1, q.Sm,
                                                                            q.pc);
-  apply_right_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(q.G, q.Sm, ld, m, q.Tm, q.pc, nullptr, 0);
+  apply_right_kernel<<<static_cast<unsigned>(ceil_div(ld, kPolarApplyRows)), 256, apply_smem_bytes(), ctx->stream>>>(q.G, q.Sm, ld, m, q.Tm, q.pc, nullptr, 0);
   gram_partial_kernel<<<kGramBlocks, kGramThreads, 0, ctx->stream>>>(q.Tm, ld, p, m, q.gram_part, q.pc);
   gram_reduce_kernel<<<(m * m + 255) / 256, 256, 0, ctx->stream>>>(q.gram_part, kGramBlocks, m * m, q.pc);
   chol_stage_kernel<<<1, kPolarThreads, chol_smem_bytes(m), ctx->stream>>>(q.gram_part, 1, m, p, 2, q.R1, q.Sm,
                                                                            q.pc);
-  apply_right_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(q.Tm, q.Sm, ld, m, q.X, q.pc, q.ctl, q.xs);
+  apply_right_kernel<<<static_cast<unsigned>(ceil_div(ld, kPolarApplyRows)), 256, apply_smem_bytes(), ctx->stream>>>(q.Tm, q.Sm, ld, m, q.X, q.pc, q.ctl, q.xs);
   // Gram of the new iterate: bk_finish checks it against the Stiefel tolerance
   gram_partial_kernel<<<kGramBlocks, kGramThreads, 0, ctx->stream>>>(q.X, ld, p, m, q.gram_part, q.pc, q.ctl, q.xs);
   gram_reduce_kernel<<<(m * m + 255) / 256, 256, 0, ctx->stream>>>(q.gram_part, kGramBlocks, m * m, q.pc);
@@ -1705,7 +1706,7 @@ int bk_qr_into_x(gps_bk* s, double* Mdev) {
       gram_reduce_kernel<<<(m * m + 255) / 256, 256, 0, ctx->stream>>>(s->gram_part, kGramBlocks, m * m, s->pc);
       chol_stage_kernel<<<1, kPolarThreads, chol_smem_bytes(m), ctx->stream>>>(s->gram_part, 1, m, p, 1, s->R1,
                                                                                s->Sm, s->pc);
-      apply_right_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(in, s->Sm, ld, m, outs[pass], s->pc, nullptr, 0);
+      apply_right_kernel<<<static_cast<unsigned>(ceil_div(ld, kPolarApplyRows)), 256, apply_smem_bytes(), ctx->stream>>>(in, s->Sm, ld, m, outs[pass], s->pc, nullptr, 0);
       in = outs[pass];
     }
     ctx->launches += 8;
@@ -2777,7 +2778,7 @@ extern "C" int gps_gram_apply_block(gps_matrix* A, const double* C, int m, doubl
   const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(n, 256), int64_t(ctx->num_sms) * 8));
   coef_mask_kernel<<<blocks, 256, 0, ctx->stream>>>(dC, n, m, mask);
   ctx->launches++;
-  dim3 grid(gx, static_cast<unsigned>(ceil_div(ld, kApplyRows)), static_cast<unsigned>(m_pad / kApplyComps));
+  dim3 grid(gx, static_cast<unsigned>(ceil_div(ld, kPolarApplyRows)), static_cast<unsigned>(m_pad / kApplyComps));
   if (A->dtype == GPS_F32)
     block_apply_kernel<float><<<grid, 256, 0, ctx->stream>>>(static_cast<const float*>(A->d), n, int(ld), m, mask, dC,
                                                               m_pad, part);

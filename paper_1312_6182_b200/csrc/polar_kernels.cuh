@@ -93,45 +93,76 @@ __global__ void bk_assemble_kernel(const double* __restrict__ exch, int mg, int 
 }
 
 // Partial Gram matrices of Y ([m][ld], rows >= p_true zero): block b covers
-// a contiguous row range; part[b][a*m + c].  Fixed summation order.
+// a contiguous row range; part[b][a*m + c].  On the fp64 tensor cores: the
+// CTA stages 32 rows of all components at a time (k-contiguous, row stride
+// 36 = 4 mod 16 doubles: conflict-free stores and fragment loads; the next
+// stage's loads are issued before the current stage's DMMAs) and warp w
+// accumulates output tile row w (components 8w .. 8w + 7) against every tile
+// column with m8n8k4 DMMA.  Fixed summation order.
 // With ctl given, Y is the parity slot the step is writing (X_{k+1}).
+constexpr int kGramKS = kGramRows + 4;
 __global__ void __launch_bounds__(kGramThreads) gram_partial_kernel(const double* __restrict__ Y, int ld, int p_true,
                                                                    int m, double* __restrict__ part,
                                                                    const PolarCtl* pc, const GpsCtl* ctl = nullptr,
                                                                    int64_t par_stride = 0) {
-  __shared__ double tile[kGramRows][kMaxGramM + 1];
+  __shared__ double tile[2][kMaxGramM * kGramKS];
   if (!pc->active || pc->fallback) return;
   if (ctl != nullptr) Y += ((ctl->iter + 1) & 1) * par_stride;
   const int rows_per = (p_true + gridDim.x - 1) / gridDim.x;
   const int r0 = blockIdx.x * rows_per;
   const int r1 = min(p_true, r0 + rows_per);
-  constexpr int EPT = (kMaxGramM * kMaxGramM + kGramThreads - 1) / kGramThreads;
-  double acc[EPT];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int nt = (m + 7) >> 3;  // 8 x 8 tiles per dimension
+  constexpr int EPT = kGramRows * kMaxGramM / kGramThreads;  // staged values per thread
+  double acc[8][2];
 #pragma unroll
-  for (int i = 0; i < EPT; ++i) acc[i] = 0.0;
-  for (int rb = r0; rb < r1; rb += kGramRows) {
-    const int nr = min(kGramRows, r1 - rb);
-    for (int e = threadIdx.x; e < kGramRows * m; e += kGramThreads) {
-      const int rr = e % kGramRows, j = e / kGramRows;
-      tile[rr][j] = rr < nr ? Y[size_t(j) * ld + rb + rr] : 0.0;
-    }
-    __syncthreads();
+  for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+  double rv[EPT];
+  auto load = [&](int rb) {
 #pragma unroll
     for (int i = 0; i < EPT; ++i) {
-      const int e = threadIdx.x + i * kGramThreads;
-      if (e < m * m) {
-        const int a = e / m, c = e % m;
-        double t = acc[i];
-        for (int rr = 0; rr < kGramRows; ++rr) t = fma(tile[rr][a], tile[rr][c], t);
-        acc[i] = t;
-      }
+      const int e = tid + kGramThreads * i, rr = e % kGramRows, j = e / kGramRows;
+      rv[i] = (rb + rr < r1 && j < m) ? Y[size_t(j) * ld + rb + rr] : 0.0;
+    }
+  };
+  if (r0 < r1) load(r0);
+  int buf = 0;
+  for (int rb = r0; rb < r1; rb += kGramRows, buf ^= 1) {
+    double* tl = tile[buf];
+#pragma unroll
+    for (int i = 0; i < EPT; ++i) {
+      const int e = tid + kGramThreads * i, rr = e % kGramRows, j = e / kGramRows;
+      tl[j * kGramKS + rr] = rv[i];
     }
     __syncthreads();
-  }
+    if (rb + kGramRows < r1) load(rb + kGramRows);
+    if (warp < nt) {
 #pragma unroll
-  for (int i = 0; i < EPT; ++i) {
-    const int e = threadIdx.x + i * kGramThreads;
-    if (e < m * m) part[size_t(blockIdx.x) * m * m + e] = acc[i];
+      for (int k0 = 0; k0 < kGramRows; k0 += 4) {
+        const double a = tl[(warp * 8 + g) * kGramKS + k0 + t];
+#pragma unroll
+        for (int tj = 0; tj < 8; ++tj)
+          if (tj < nt) {
+            const double b = tl[(tj * 8 + g) * kGramKS + k0 + t];
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                         : "+d"(acc[tj][0]), "+d"(acc[tj][1])
+                         : "d"(a), "d"(b));
+          }
+      }
+    }
+    // no trailing barrier: buffer buf is rewritten two stages later, after
+    // the next stage's barrier
+  }
+  if (warp < nt) {
+    const int a_row = warp * 8 + g;
+#pragma unroll
+    for (int tj = 0; tj < 8; ++tj) {
+      const int c = tj * 8 + 2 * t;
+      if (tj < nt && a_row < m) {
+        if (c < m) part[size_t(blockIdx.x) * m * m + a_row * m + c] = acc[tj][0];
+        if (c + 1 < m) part[size_t(blockIdx.x) * m * m + a_row * m + c + 1] = acc[tj][1];
+      }
+    }
   }
 }
 
@@ -316,6 +347,10 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
   // Right-looking Cholesky of the upper triangle, two barriers per step:
   // every thread derives the pivot itself; thread (a, g) = (tid / 16,
   // tid % 16) updates row a, columns g, g + 16, ... of the trailing block.
+  // (A blocked variant -- 8 x 8 diagonal blocks factored by one warp, block
+  // row solves, rank-8 trailing updates, 24 barriers instead of 128 --
+  // measured slower: 78K vs 63.5K clocks at m = 64, scripts/ubench/polar_ns.cu;
+  // the per-pivot chain stays, serialised in one warp.)
   const int ta = tid >> 4, tg = tid & 15;
   for (int j = 0; j < m; ++j) {
     const double d = M[j * m + j];
@@ -472,38 +507,69 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
 }
 
 // Out[j][r] = sum_b In[b][r] * S[b][j]   (In, Out: [m][ld]; S row-major m x m)
-// One thread per (row, group of 8 output components): consecutive threads
-// take consecutive rows of the same group, so In loads coalesce and the S
-// reads are shared-memory broadcasts; S is staged zero-padded to 8-column
-// groups.  (A thread per row with an m-long register array left 3/4 of the
-// SMs idle and spilled: 197 us at p = 8192, m = 64.)
+// on the fp64 tensor cores: CTA b owns rows [64 b, 64 b + 64); In's rows and
+// S are staged in shared memory k-contiguous (row stride 68 = 4 mod 16
+// doubles, zero-padded to 64 components), and warp w computes rows
+// 16 (w % 4) .. + 16 (2 m-tiles) x components 32 (w / 4) .. + 32 (4 n-tiles)
+// with m8n8k4 DMMA.  (A thread per (row, 8 components) with FMAs: 21 us at
+// p = 8192, m = 64; a thread per row with an m-long register array: 197 us.)
+constexpr int kPolarApplyRows = 64;
+constexpr int kPolarApplyStride = kMaxGramM + 4;
+__host__ __device__ constexpr size_t apply_smem_bytes() {
+  return size_t(2) * kMaxGramM * kPolarApplyStride * sizeof(double);
+}
 __global__ void __launch_bounds__(256) apply_right_kernel(const double* __restrict__ In, const double* __restrict__ S,
                                                           int ld, int m, double* Out, const PolarCtl* pc,
                                                           const GpsCtl* ctl, int64_t out_par_stride) {
-  __shared__ double s[kMaxGramM * kMaxGramM];
+  extern __shared__ __align__(16) double apply_smem[];
   if (!pc->active || pc->fallback) return;
   double* O = Out + (ctl != nullptr ? ((ctl->iter + 1) & 1) * out_par_stride : 0);
-  const int groups = (m + 7) / 8, mp = groups * 8;
-  for (int e = threadIdx.x; e < m * mp; e += blockDim.x) {
-    const int b = e / mp, j = e % mp;
-    s[e] = j < m ? S[b * m + j] : 0.0;
+  double* sI = apply_smem;                          // [b][row]  (k = b)
+  double* sS = apply_smem + kMaxGramM * kPolarApplyStride;  // [b][j]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int r0 = blockIdx.x * kPolarApplyRows;
+  const int kp = (m + 3) & ~3;  // k rounded up to the DMMA k-step (zero rows beyond m)
+  for (int e = tid; e < kMaxGramM * kMaxGramM; e += blockDim.x) {
+    const int b = e / kMaxGramM, j = e % kMaxGramM;
+    sS[b * kPolarApplyStride + j] = (b < m && j < m) ? S[b * m + j] : 0.0;
+  }
+  for (int e = tid; e < kMaxGramM * kPolarApplyRows; e += blockDim.x) {
+    const int b = e / kPolarApplyRows, rr = e % kPolarApplyRows;
+    sI[b * kPolarApplyStride + rr] = (b < m && r0 + rr < ld) ? In[size_t(b) * ld + r0 + rr] : 0.0;
   }
   __syncthreads();
-  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < int64_t(ld) * groups;
-       idx += int64_t(gridDim.x) * blockDim.x) {
-    const int r = static_cast<int>(idx % ld), j0 = static_cast<int>(idx / ld) * 8;
-    double t[8];
+  const int rg = warp & 3, cg = warp >> 2;
+  double acc[2][4][2];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) t[u] = 0.0;
-    for (int b = 0; b < m; ++b) {
-      const double v = In[size_t(b) * ld + r];
-      const double* sb = s + b * mp + j0;
+  for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int u = 0; u < 8; ++u) t[u] = fma(v, sb[u], t[u]);
-    }
+    for (int u = 0; u < 4; ++u) acc[i][u][0] = acc[i][u][1] = 0.0;
+  const int jn = (m + 7) >> 3;  // valid n-tiles
+  for (int k0 = 0; k0 < kp; k0 += 4) {
+    double a[2], bf[4];
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (j0 + u < m) O[size_t(j0 + u) * ld + r] = t[u];
+    for (int mt = 0; mt < 2; ++mt) a[mt] = sI[(k0 + t) * kPolarApplyStride + rg * 16 + mt * 8 + g];
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) bf[nt] = sS[(k0 + t) * kPolarApplyStride + cg * 32 + nt * 8 + g];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+        if (cg * 4 + nt < jn)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                       : "+d"(acc[mt][nt][0]), "+d"(acc[mt][nt][1])
+                       : "d"(a[mt]), "d"(bf[nt]));
+  }
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+    const int r = r0 + rg * 16 + mt * 8 + g;
+    if (r < ld)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const int j = cg * 32 + nt * 8 + 2 * t;
+        if (j < m) O[size_t(j) * ld + r] = acc[mt][nt][0];
+        if (j + 1 < m) O[size_t(j + 1) * ld + r] = acc[mt][nt][1];
+      }
   }
 }
 
