@@ -524,12 +524,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     unsigned long long w7 = 0, w8 = 0, w9 = 0;
     const long long t_role = clock64();
     int tt = 0, kc = 0;
+    // scale 2^e of my column (e in [-126, 126]); the next tile's exponent is
+    // loaded one chunk into the current tile, so the global-load latency is
+    // not paid on the converters' critical path at every tile start
+    auto col_scale = [&](int tile) {
+      const int64_t col = int64_t(int(blockIdx.x) + tile * int(gridDim.x)) * kTcTileM + r;
+      return col < a.n ? a.col_exp[col] : 0;
+    };
+    int e_next = my_tiles > 0 ? col_scale(0) : 0;
     float sc = 1.f;
     for (int c = 0; c < total_chunks; ++c) {
-      if (kc == 0) {
-        const int64_t col = int64_t(int(blockIdx.x) + tt * int(gridDim.x)) * kTcTileM + r;
-        sc = __int_as_float((127 + (col < a.n ? a.col_exp[col] : 0)) << 23);  // 2^e, e in [-126, 126]
-      }
+      if (kc == 0) sc = __int_as_float((127 + e_next) << 23);
+      if (kc == (kchunks > 1 ? 1 : 0) && tt + 1 < my_tiles) e_next = col_scale(tt + 1);
       pf.start();
       mbar_wait(&a_full[ra.slot], ra.ph);
       pf.stop(w7);
@@ -599,6 +605,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     int seg = 0;
     for (int tt = 0; tt < my_tiles; ++tt) {
       const int t = int(blockIdx.x) + tt * int(gridDim.x);
+      // the column's scale exponent and margin, loaded at the tile start so
+      // the candidate test at its end does not wait on global memory
+      const int64_t col_t = int64_t(t) * kTcTileM + q * 32 + lane;
+      const int e_col = col_t < a.n ? a.col_exp[col_t] : 0;
+      const float d_col = col_t < a.n ? a.col_delta[col_t] : 0.f;
       // per-tile sums with Kahan compensation in fp32 (full-rate fp32 ops
       // instead of fp64 conversions and adds)
       float ch[32], cl[32];
@@ -643,8 +654,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         // none of whose components can reach the threshold with that margin
         // is inactive (w = 0, objective term 0) for certain; every other
         // column is recomputed exactly by T1x.
-        const double unscale = ldexp(1.0, -(a.col_exp[col] + kTcXScaleExp));
-        const double delta = static_cast<double>(a.col_delta[col]);
+        const double unscale = ldexp(1.0, -(e_col + kTcXScaleExp));
+        const double delta = static_cast<double>(d_col);
 #pragma unroll
         for (int jj = 0; jj < 32; ++jj) {
           const int j = jbase + jj;
