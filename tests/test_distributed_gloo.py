@@ -309,3 +309,46 @@ def test_peer_exchange_decision_on_cpu_ranks():
     out = mgr.dict()
     mp.spawn(_px_decision_worker, args=(_free_port(), out), nprocs=WORLD, join=True)
     assert all(out[r] == (False, False) for r in range(WORLD))
+
+
+class _FakePeerExchange:
+    """Stand-in for PeerExchange: sums through gloo (correct), adds a bias
+    on one rank (a broken peer path), or raises (a peer path that cannot
+    run) -- exercising px_self_test's agreement logic without a GPU."""
+
+    def __init__(self, mode, comm):
+        self.mode, self.comm = mode, comm
+
+    def all_reduce(self, t):
+        self.comm.all_reduce_sum(t)  # the exchange itself (a device kernel in the real class)
+        if self.mode == "raise" and self.comm.rank == 1:
+            raise RuntimeError("peer exchange timed out")  # e.g. this rank's bounded wait expired
+        if self.mode == "wrong" and self.comm.rank == 0:
+            t += 1e-6
+
+
+def _self_test_worker(rank, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    try:
+        import paper_1312_6182_b200.distributed as d
+
+        comm = d.Comm()
+        # px_self_test synchronises the device; on CPU ranks make that a no-op
+        torch.cuda.synchronize = lambda *a, **k: None
+        res = {}
+        for mode in ("ok", "wrong", "raise"):
+            res[mode] = d.px_self_test(_FakePeerExchange(mode, comm), comm, torch.device("cpu"), 300)
+        out[rank] = res
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_exchange_self_test_agreement():
+    """Every rank keeps the peer path only when all ranks reproduced the
+    torch.distributed sum; one wrong or failing rank sends all to NCCL."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_self_test_worker, args=(_free_port(), out), nprocs=WORLD, join=True)
+    for r in range(WORLD):
+        assert out[r] == {"ok": True, "wrong": False, "raise": False}, out[r]

@@ -67,3 +67,15 @@ def test_column_partition(n, world):
     for (o1, k1), (o2, _) in zip(parts, parts[1:]):
         assert o1 + k1 == o2
     assert max(k for _, k in parts) - min(k for _, k in parts) <= 1
+
+
+def test_decode_band_entries():
+    """Near-threshold entries are col * 64 + component (csrc/common.cuh
+    BandLog); decode_band groups them per component, sorted and unique,
+    shifted by the shard offset."""
+    from paper_1312_6182_b200.core import decode_band
+
+    entries = np.array([5 * 64 + 1, 2 * 64 + 0, 9 * 64 + 1, 2 * 64 + 0, 7 * 64 + 3], dtype=np.int64)
+    out = decode_band(entries, 4, offset=100)
+    assert [o.tolist() for o in out] == [[102], [105, 109], [], [107]]
+    assert [o.tolist() for o in decode_band(np.zeros(0, dtype=np.int64), 2)] == [[], []]
