@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       int t = int(blockIdx.x), kc = 0;
       for (int c = 0; c < total_chunks; ++c) {
         pf.start();
-        if (c >= SA) mbar_wait_sleep(&a_empty[r.slot], r.ph ^ 1u);
+        if (c >= SA) mbar_wait_sleep(&a_empty[r.slot], r.ph ^ 1u);  // (a pure spin measured the same)
         pf.stop(w0);
         unsigned char* st = aring + r.slot * a_bytes;
         mbar_arrive_expect_tx(&a_full[r.slot], static_cast<uint32_t>(a_bytes));
