@@ -380,9 +380,9 @@ def run_reference(args):
 
 BLOCK_CONFIGS = (
     # name, p, n, m, penalty, mu, gamma fraction of max ||a_i||, data, timed iterations
-    ("C3", 4096, 1 << 21, 10, "l1", np.ones(10), 0.1, "lowrank", 10),
-    ("C4", 8192, 1 << 21, 64, "l0", np.linspace(1.0, 0.5, 64), 0.1, "lowrank", 5),
-    ("C4_dense", 8192, 1 << 21, 64, "l0", np.linspace(1.0, 0.5, 64), 0.03, "gauss", 3),
+    ("C3", 4096, 1 << 21, 10, "l1", np.ones(10), 0.1, "lowrank", 20),
+    ("C4", 8192, 1 << 21, 64, "l0", np.linspace(1.0, 0.5, 64), 0.1, "lowrank", 10),
+    ("C4_dense", 8192, 1 << 21, 64, "l0", np.linspace(1.0, 0.5, 64), 0.03, "gauss", 4),
 )
 
 
@@ -420,12 +420,13 @@ def block_configs(torch, gps, ctx, dev):
             _native.check(L.gps_bk_enqueue_sweep(loop.handle))
             _native.check(L.gps_bk_enqueue_step(loop.handle))
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(k):
-            _native.check(L.gps_bk_enqueue_sweep(loop.handle))
-            _native.check(L.gps_bk_enqueue_step(loop.handle))
-        e1.record(stream)
-        e1.synchronize()
+        with ClockSampler(dev.index) as clocks:
+            e0.record(stream)
+            for _ in range(k):
+                _native.check(L.gps_bk_enqueue_sweep(loop.handle))
+                _native.check(L.gps_bk_enqueue_step(loop.handle))
+            e1.record(stream)
+            e1.synchronize()
         ms = e0.elapsed_time(e1) / k
         ctx.set_stream(None)
         d, it, _ = _bk_poll(loop)
@@ -437,7 +438,7 @@ def block_configs(torch, gps, ctx, dev):
                                  f"p={p} n=2^21 fp32, {data} data, gamma={frac}*max||a_i||"
                                  f"{'^2' if pen == 'l0' else ''}",
                      "iters_per_s": 1e3 / ms, "ms_per_iter": ms, "a_stream_gbs": p * n * 4 / (ms / 1e3) / 1e9,
-                     "iterations_timed": k, "active_entries_last_sweep": nnz}
+                     "iterations_timed": k, "active_entries_last_sweep": nnz, "clocks": clocks.summary()}
         del loop, A, At
         torch.cuda.empty_cache()
     return out
