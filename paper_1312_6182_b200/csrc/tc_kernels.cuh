@@ -553,8 +553,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           const uint32_t row_s = smem_u32(aring + ra.slot * a_bytes + h * (a_bytes / 2) + r * 128);
 #pragma unroll
           for (int cc = 0; cc < 8; ++cc) {
-            const float4 v = (a.probe & 256) ? make_float4(1.f, 1.f, 1.f, 1.f)  // timing experiment: no smem read
-                                              : lds_f4(row_s + ((cc ^ (r & 7)) << 4));
+            const float4 v = lds_f4(row_s + ((cc ^ (r & 7)) << 4));
             p1[cc * 2] = pack_f16x2(v.x * sc, v.y * sc);  // packed column (row / 2) within the half
             p1[cc * 2 + 1] = pack_f16x2(v.z * sc, v.w * sc);
           }
