@@ -90,6 +90,11 @@ struct gps_ctx {
   std::mutex ctl_mu;
   GpsCtl* ctl_pinned = nullptr;
   std::vector<int> ctl_free;
+  // pinned staging for the one-shot sweeps' small host vectors (x in, the
+  // exchange vector out): a pageable copy is staged by the driver
+  // synchronously; these are two async DMAs plus a host memcpy each
+  double* host_stage = nullptr;
+  size_t host_stage_elems = 0;
 };
 
 namespace {
@@ -530,6 +535,7 @@ int gps_ctx_destroy(gps_ctx* ctx) {
   if (ctx->part_s) gps_free(ctx->part_s);
   if (ctx->dvec) gps_free(ctx->dvec);
   if (ctx->ctl_pinned) cudaFreeHost(ctx->ctl_pinned);
+  if (ctx->host_stage) cudaFreeHost(ctx->host_stage);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return GPS_OK;
@@ -848,9 +854,20 @@ static int one_shot(gps_matrix* A, int mode, const double* x, const double* coef
   double* dn = ctx->dvec + A->ld;
   double* exch = dn + A->n;
   double* dw = exch + A->ld + 4;
+  const size_t stage_elems = size_t(2) * (A->ld + 4);
+  if (ctx->host_stage_elems < stage_elems) {
+    if (ctx->host_stage) cudaFreeHost(ctx->host_stage);
+    ctx->host_stage = nullptr;
+    ctx->host_stage_elems = 0;
+    GPS_CUDA(cudaMallocHost(&ctx->host_stage, stage_elems * sizeof(double)));
+    ctx->host_stage_elems = stage_elems;
+  }
+  double* hx = ctx->host_stage;              // ld: x, zero padded
+  double* hex = ctx->host_stage + A->ld + 4;  // ld + 4: the exchange vector
   if (mode != kCoef) {
-    GPS_CUDA(cudaMemsetAsync(dx, 0, A->ld * sizeof(double), ctx->stream));
-    GPS_CUDA(cudaMemcpyAsync(dx, x, A->p * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    std::memcpy(hx, x, A->p * sizeof(double));
+    std::memset(hx + A->p, 0, (A->ld - A->p) * sizeof(double));
+    GPS_CUDA(cudaMemcpyAsync(dx, hx, A->ld * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   } else {
     GPS_CUDA(cudaMemcpyAsync(dn, coef, A->n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   }
@@ -868,14 +885,14 @@ static int one_shot(gps_matrix* A, int mode, const double* x, const double* coef
   if (rc) return rc;
   rc = launch_reduce(ctx, ctx->part_g, ctx->part_s, plan.grid, static_cast<int>(A->ld), exch, nullptr);
   if (rc) return rc;
-  std::vector<double> h(A->ld + 4);
-  GPS_CUDA(cudaMemcpyAsync(h.data(), exch, (A->ld + 4) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  double* h = hex;
+  GPS_CUDA(cudaMemcpyAsync(h, exch, (A->ld + 4) * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   if (c_out && mode != kCoef)
     GPS_CUDA(cudaMemcpyAsync(c_out, dn, A->n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   if (w_out && mode == kFused)
     GPS_CUDA(cudaMemcpyAsync(w_out, dw, A->n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   GPS_CUDA(cudaStreamSynchronize(ctx->stream));
-  if (g_out) std::memcpy(g_out, h.data(), A->p * sizeof(double));
+  if (g_out) std::memcpy(g_out, h, A->p * sizeof(double));
   if (f_out) *f_out = h[A->ld];
   if (nnz_out) *nnz_out = static_cast<int64_t>(h[A->ld + 1]);
   return GPS_OK;
