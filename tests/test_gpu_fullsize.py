@@ -40,8 +40,9 @@ from oracle.chunked import ChunkedA, block_solve_chunked, max_norm_start, su_ite
 
 
 def _device_and_host(At):
-    A = gps.DataMatrix.from_device(At.data_ptr(), At.shape[1], At.shape[0], owner=At, device=0)
-    host = At.cpu().numpy().T  # (p, n) Fortran-ordered fp32 view: the same numbers
+    dt = np.float64 if At.dtype == torch.float64 else np.float32
+    A = gps.DataMatrix.from_device(At.data_ptr(), At.shape[1], At.shape[0], owner=At, dtype=dt, device=0)
+    host = At.cpu().numpy().T  # (p, n) Fortran-ordered view of the same numbers
     return A, ChunkedA(host)
 
 
@@ -151,5 +152,20 @@ def test_c4_dense_k2_trajectory():
     g.manual_seed(7)
     At = torch.randn((n, p), generator=g, device="cuda", dtype=torch.float32)
     A = _block_case(At, m, "l0", 0.03, np.linspace(1.0, 0.5, m), 2)
+    del A, At
+    _free()
+
+
+def test_c3_fp64_storage_k2_trajectory():
+    """C3's shape stored in fp64 (64 GiB): the tensor-core filter's fp64
+    variant (A rounded to fp32 inside the margin before the split, 16-row fp64
+    TMA boxes) and the fp64 recomputation, against the chunked oracle."""
+    p, n, m = 4096, 1 << 21, 10
+    At32 = bench.make_lowrank(torch, p, n, 0, n, torch.device("cuda", 0), 16, 10, n // 200)
+    At = At32.double()
+    del At32
+    torch.cuda.empty_cache()
+    A = _block_case(At, m, "l1", 0.1, np.ones(m), 2)
+    assert A.dtype == np.float64
     del A, At
     _free()
