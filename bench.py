@@ -656,6 +656,46 @@ def run_ours(args):
                               "note": "DataMatrix(A pinned host) + norms pass + solve_single_unit to convergence "
                                       "(tol 1e-6) + loadings download; this synthetic C2 instance converges in "
                                       "1 iteration (planted signal below the noise at n=2^20)"}}
+    elif world > 1 and args.e2e_steps > 0:
+        # N > 1: the same per-step public-API round trip on every rank's
+        # shard, plus the all-reduce of the partial ascent direction through
+        # torch.distributed (g goes host -> device for the collective and
+        # back); the step time is the max over ranks
+        ctx.set_stream(None)
+        host = torch.empty((n_local, p), dtype=torch.float32, pin_memory=True)
+        host.copy_(At)
+        A_host = host.numpy().T
+        del A, At
+        torch.cuda.empty_cache()
+        Ad = gps.DataMatrix(A_host)
+        x = np.asarray(x0, dtype=np.float64)
+        red = torch.empty(p + 1, dtype=torch.float64, device=dev)
+        l0 = ctx.launch_count
+        t_e2e = 0.0
+        for s in range(3 + args.e2e_steps):
+            torch.distributed.barrier()
+            t0 = time.perf_counter()
+            f, g, _, _, nnz = gps.fused_sweep(Ad, x, gamma, "l0")
+            red[:p].copy_(torch.from_numpy(g))
+            red[p] = f
+            torch.distributed.all_reduce(red)
+            gr = red.cpu().numpy()
+            x = gr[:p] / np.linalg.norm(gr[:p])
+            if s >= 3:
+                t_e2e += time.perf_counter() - t0
+            else:
+                l0 = ctx.launch_count
+        e2e_launches = ctx.launch_count - l0
+        tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+        del Ad
+        e2e = {"value": args.e2e_steps / t_e2e, "unit": "iters/s", "h2d_bytes_per_step": p * 8 + (p + 1) * 8,
+               "d2h_bytes_per_step": (p + 4) * 8 + (p + 1) * 8, "steps": args.e2e_steps,
+               "gpu_launches": e2e_launches,
+               "note": "per step on every rank: fused_sweep(A_shard, x_host, gamma, 'l0') (x H2D, sweep + reduction, "
+                       "f and g D2H), then [g | f] all-reduced through torch.distributed (H2D, collective, D2H) "
+                       "and x = g/||g|| on the host; max over ranks"}
     else:
         del At
 

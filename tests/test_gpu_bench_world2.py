@@ -30,7 +30,7 @@ def test_bench_two_ranks_gloo():
     env = dict(os.environ, GPSPCA_BENCH_BACKEND="gloo")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2",
-           "--steps", "4", "--warmup", "3", "--cols", str(1 << 18), "--no-block", "--e2e-steps", "0",
+           "--steps", "4", "--warmup", "3", "--cols", str(1 << 18), "--no-block", "--e2e-steps", "3",
            "--no-cpu-baseline"]
     out = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT, env=env, timeout=600)
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
@@ -41,3 +41,4 @@ def test_bench_two_ranks_gloo():
     assert rec["config"]["exchange"] == "torch.distributed all_reduce (gloo)"
     assert rec["config"]["parallelism"] == "column-shard x2"
     assert rec["value"] > 0 and rec["gpu_launches"] > 0
+    assert rec["e2e"]["value"] > 0 and rec["e2e"]["steps"] == 3 and rec["e2e"]["h2d_bytes_per_step"] > 0
