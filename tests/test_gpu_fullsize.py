@@ -169,3 +169,31 @@ def test_c3_fp64_storage_k2_trajectory():
     assert A.dtype == np.float64
     del A, At
     _free()
+
+
+@pytest.mark.parametrize("penalty,frac", [("l1", 0.05), ("l0", 0.05)])
+def test_c2_long_trajectory(penalty, frac):
+    """C2's matrix at a lower gamma (more active columns, many iterations):
+    up to 25 iterations of both loops must agree step for step -- same
+    stopping iteration, histories to 1e-9, loadings and support."""
+    p, n = 4096, 1 << 20
+    At = bench.make_c2(torch, p, n, 0, n, torch.device("cuda", 0))
+    A, H = _device_and_host(At)
+    norms = np.asarray(A.norms)
+    top = frac * float(norms.max())
+    gamma = top if penalty == "l1" else top * top
+    i = int(np.argsort(-norms, kind="stable")[0])
+    cfg = gps.SolverConfig(penalty=penalty, gamma=gamma, max_iter=25)
+    loadings, report = gps.solve_single_unit(A, cfg)
+    t0 = time.perf_counter()
+    x, hist, conv, c = su_iterate_chunked(H, H.column(i) / norms[i], gamma, penalty, 1e-6, 25)
+    print(f"C2 {penalty} frac={frac}: {len(hist) - 1} iterations (converged={conv}), oracle "
+          f"{time.perf_counter() - t0:.1f} s; nnz {np.count_nonzero(loadings.values)}")
+    assert report.iterations == len(hist) - 1 and report.converged == conv
+    np.testing.assert_allclose(report.objective_history, hist, rtol=1e-9)
+    zr = threshold(c, gamma, penalty)
+    zr = zr / np.linalg.norm(zr)
+    _support_check(loadings.values, zr[:, None], c[:, None], np.array([gamma]), np.ones(1), penalty, report)
+    np.testing.assert_allclose(loadings.values[:, 0], zr, atol=1e-9)
+    del A, At
+    _free()
