@@ -230,6 +230,17 @@ int gps_px_handle_size(void);
 int gps_px_ipc_handle(gps_px* px, void* handle);
 int gps_px_open(gps_px* px, int peer, const void* handle);
 int gps_px_allreduce(gps_px* px, double* buf);
+/* The two halves of one exchange as separate launches (phase 1: push this
+ * rank's vector into every rank's slots and release the epoch flags; phase 2:
+ * wait for every rank's flags, rank-order sum, publish the epoch; 3: both =
+ * gps_px_allreduce).  gps_px_reduce_phase does the same for the fused
+ * reduction kernel (su_reduce_px_kernel) on given CTA partials part_g
+ * [nparts][rows], part_s [nparts_s][4] into exch [rows + 4].  Used by the
+ * cross-process test that runs several ranks on ONE GPU: with a host barrier
+ * between the phases no rank's kernel waits on another process's kernel. */
+int gps_px_allreduce_phase(gps_px* px, double* buf, int phase);
+int gps_px_reduce_phase(gps_px* px, const double* part_g, const double* part_s, int nparts, int rows, int nparts_s,
+                        double* exch, int phase);
 /* Bound (seconds) on every peer-flag wait of this exchange; default
  * GPSPCA_PX_TIMEOUT_S or 60 s.  A wait that expires raises the exchange's
  * error flag (gps_px_error) and stops the attached loop, whose run / poll

@@ -102,6 +102,8 @@ SIGNATURES = {
     "gps_px_ipc_handle": (C.c_int, [_vp, _vp]),
     "gps_px_open": (C.c_int, [_vp, C.c_int, _vp]),
     "gps_px_allreduce": (C.c_int, [_vp, _vp]),
+    "gps_px_allreduce_phase": (C.c_int, [_vp, _vp, C.c_int]),
+    "gps_px_reduce_phase": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, _vp, C.c_int]),
     "gps_px_destroy": (C.c_int, [_vp]),
     "gps_px_set_timeout": (C.c_int, [_vp, C.c_double]),
     "gps_px_error": (C.c_int, [_vp, _ip]),

@@ -1429,7 +1429,12 @@ struct gps_bk {
   unsigned char* tflag = nullptr;     // [2 * items][8] T1 tile flags (items = ceil(n / 256))
   unsigned char* item_act = nullptr;  // [items] any active column (T1x -> T2)
   double* Wt = nullptr;               // [n][m_pad] weights of the candidates, column-major (T1x -> T2)
-  double* part_s_tc = nullptr;
+  double* part_s_tc = nullptr;        // [2][tc_ref_grid][4]: T1x, then T1s (leftover lists)
+  int64_t* tc_left = nullptr;         // [tc_ref_grid][64] leftover candidates of T1x (-> T1s)
+  int* tc_left_n = nullptr;           // [tc_ref_grid]
+  int tc_split = 1, tc_split_rows = 0;  // T1s row splits (CTAs per leftover list) and rows per split
+  double* tc_lpart = nullptr;         // T1s partial dots: per group [tc_split][GS][m_pad] at its first candidate
+  unsigned int* tc_lcnt = nullptr;    // [4 tc_ref_grid] T1s arrival counters per group (zero between sweeps)
   CUtensorMap tmA, tmXh, tmXl;
   // multi-CTA CholeskyQR2 polar (large p*m)
   bool big_polar = false;
@@ -1586,9 +1591,16 @@ int bk_enqueue_tc(gps_bk* s, bool with_ctl) {
     const int64_t xs = int64_t(s->m_pad()) * ld, wst = int64_t(s->m_pad()) * A->n;
     const double* gam = s->mu_dev + s->m;
 #define GPS_REFINE(TA, J)                                                                                      \
-  tc_refine_kernel<TA, J><<<s->tc_ref_grid, 256, tc_refine_smem(8 * J), ctx->stream>>>(                          \
-      static_cast<const TA*>(A->d), A->n, ld, s->m, s->X, xs, s->mu_dev, gam, s->penalty, s->colmask, s->tflag, \
-      s->item_act, s->W, wst, s->Wt, s->part_s_tc, ctl, ctl ? s->band : nullptr)
+  do {                                                                                                         \
+    tc_refine_kernel<TA, J><<<s->tc_ref_grid, 256, tc_refine_smem(8 * J), ctx->stream>>>(                        \
+        static_cast<const TA*>(A->d), A->n, ld, s->m, s->X, xs, s->mu_dev, gam, s->penalty, s->colmask, s->tflag, \
+        s->item_act, s->W, wst, s->Wt, s->part_s_tc, ctl, ctl ? s->band : nullptr, s->tc_left, s->tc_left_n);   \
+    ctx->launches++;                                                                                           \
+    tc_refine_split_kernel<TA, J><<<ctx->num_sms, 256, tc_refine_smem(8 * J), ctx->stream>>>(                    \
+        static_cast<const TA*>(A->d), A->n, ld, s->m, s->X, xs, s->mu_dev, gam, s->penalty, s->colmask,           \
+        s->item_act, s->W, wst, s->Wt, s->part_s_tc + size_t(s->tc_ref_grid) * 4, ctl, ctl ? s->band : nullptr,  \
+        s->tc_left, s->tc_left_n, s->tc_ref_grid, s->tc_split, s->tc_split_rows, s->tc_lpart, s->tc_lcnt);      \
+  } while (0)
 #define GPS_REFINE_J(TA)            \
   switch (np / 8) {                 \
     case 2: GPS_REFINE(TA, 2); break; \
@@ -1596,14 +1608,16 @@ int bk_enqueue_tc(gps_bk* s, bool with_ctl) {
     case 6: GPS_REFINE(TA, 6); break; \
     default: GPS_REFINE(TA, 8); break; \
   }
-    if (f64) {
+    if (a.probe & 512) {
+      // timing experiments only: T1's candidate mask is left for gpsdbg_bk_colmask
+    } else if (f64) {
       GPS_REFINE_J(double)
     } else {
       GPS_REFINE_J(float)
     }
 #undef GPS_REFINE_J
 #undef GPS_REFINE
-    ctx->launches++;
+    ctx->launches++;  // T1s
   }
   if (!(a.probe & 16)) {
 #define GPS_UPDATE(TA, NT)                                                                                   \
@@ -1627,7 +1641,7 @@ int bk_enqueue_tc(gps_bk* s, bool with_ctl) {
     ctx->launches++;
   }
   GPS_CHECK_LAUNCH("tensor-core block sweep launch");
-  return launch_reduce(ctx, s->part_g, s->part_s_tc, s->tc_gx, np * ld, s->exch, ctl, s->tc_ref_grid, s->px);
+  return launch_reduce(ctx, s->part_g, s->part_s_tc, s->tc_gx, np * ld, s->exch, ctl, 5 * s->tc_ref_grid, s->px);
 }
 
 int bk_enqueue_sweeps(gps_bk* s, bool with_ctl) {
@@ -1858,6 +1872,11 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
     s->tc_grid = std::min(ctx->num_sms, s->tc_tiles);
     s->tc_gx = static_cast<int>(std::min<int64_t>(32, A->n));
     s->tc_ref_grid = static_cast<int>(std::min<int64_t>(ceil_div(A->n, kTcRefItem), int64_t(2) * ctx->num_sms));
+    // T1s: >= 1024 rows per CTA, at most kTcSplitMax CTAs per leftover list
+    s->tc_split = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kTcSplitMax, A->ld / 1024)));
+    s->tc_split_rows = static_cast<int>(ceil_div(ceil_div(A->ld, s->tc_split), kTcRefRows) * kTcRefRows);
+    static_assert(2 * 148 < kTcLeftMaxGrid, "T1s scans the T1x grid in one CTA");
+    if (s->tc_ref_grid >= kTcLeftMaxGrid) s->tc_ref_grid = kTcLeftMaxGrid - 1;
   }
   s->mg = pl.mg;
   s->ngroups = (m + pl.mg - 1) / pl.mg;
@@ -1904,7 +1923,12 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
     alloc((void**)&s->colmask, 2 * n);
     alloc((void**)&s->tflag, size_t(ceil_div(n, kTcRefItem)) * 16);
     alloc((void**)&s->item_act, size_t(ceil_div(n, kTcRefItem)));
-    alloc((void**)&s->part_s_tc, size_t(s->tc_ref_grid) * 4 * sizeof(double));
+    alloc((void**)&s->part_s_tc, size_t(5) * s->tc_ref_grid * 4 * sizeof(double));  // T1x | T1s groups (<= 4 per list)
+    alloc((void**)&s->tc_left, size_t(s->tc_ref_grid) * kTcRefBatch * sizeof(int64_t));
+    alloc((void**)&s->tc_left_n, size_t(s->tc_ref_grid) * sizeof(int));
+    alloc((void**)&s->tc_lpart, size_t(s->tc_ref_grid) * s->tc_split * kTcRefBatch * mp * sizeof(double));
+    alloc((void**)&s->tc_lcnt, size_t(4) * s->tc_ref_grid * sizeof(unsigned int));
+    if (e == cudaSuccess) e = cudaMemsetAsync(s->tc_lcnt, 0, size_t(4) * s->tc_ref_grid * sizeof(unsigned int), ctx->stream);
     alloc((void**)&s->Wt, n * mp * sizeof(double));
   }
   alloc((void**)&s->ctl, sizeof(GpsCtl));
@@ -1960,6 +1984,10 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
           f64 ? reinterpret_cast<const void*>(tc_refine_kernel<double, 4>) : reinterpret_cast<const void*>(tc_refine_kernel<float, 4>),
           f64 ? reinterpret_cast<const void*>(tc_refine_kernel<double, 6>) : reinterpret_cast<const void*>(tc_refine_kernel<float, 6>),
           f64 ? reinterpret_cast<const void*>(tc_refine_kernel<double, 8>) : reinterpret_cast<const void*>(tc_refine_kernel<float, 8>),
+          f64 ? reinterpret_cast<const void*>(tc_refine_split_kernel<double, 2>) : reinterpret_cast<const void*>(tc_refine_split_kernel<float, 2>),
+          f64 ? reinterpret_cast<const void*>(tc_refine_split_kernel<double, 4>) : reinterpret_cast<const void*>(tc_refine_split_kernel<float, 4>),
+          f64 ? reinterpret_cast<const void*>(tc_refine_split_kernel<double, 6>) : reinterpret_cast<const void*>(tc_refine_split_kernel<float, 6>),
+          f64 ? reinterpret_cast<const void*>(tc_refine_split_kernel<double, 8>) : reinterpret_cast<const void*>(tc_refine_split_kernel<float, 8>),
           f64 ? reinterpret_cast<const void*>(tc_update_kernel<double, 1>) : reinterpret_cast<const void*>(tc_update_kernel<float, 1>),
           f64 ? reinterpret_cast<const void*>(tc_update_kernel<double, 2>) : reinterpret_cast<const void*>(tc_update_kernel<float, 2>),
           f64 ? reinterpret_cast<const void*>(tc_update_kernel<double, 3>) : reinterpret_cast<const void*>(tc_update_kernel<float, 3>),
@@ -2022,6 +2050,10 @@ int gps_bk_destroy(gps_bk* s) {
   if (s->item_act) gps_free(s->item_act);
   if (s->colmask) gps_free(s->colmask);
   if (s->part_s_tc) gps_free(s->part_s_tc);
+  if (s->tc_left) gps_free(s->tc_left);
+  if (s->tc_left_n) gps_free(s->tc_left_n);
+  if (s->tc_lpart) gps_free(s->tc_lpart);
+  if (s->tc_lcnt) gps_free(s->tc_lcnt);
   if (s->Wt) gps_free(s->Wt);
   if (s->pc) gps_free(s->pc);
   if (s->gram_part) gps_free(s->gram_part);
@@ -2405,9 +2437,47 @@ int gps_px_allreduce(gps_px* px, double* buf) {
     if (!px->view.slots[q]) return fail(GPS_E_ARG, "peer %d not opened", q);
   gps_ctx* ctx = px->ctx;
   GPS_CUDA(cudaSetDevice(ctx->device));
-  px_allreduce_kernel<<<px_uniform_chunks(px->view.count), 256, 0, ctx->stream>>>(px->view, buf);
+  px_allreduce_kernel<<<px_uniform_chunks(px->view.count), 256, 0, ctx->stream>>>(px->view, buf, kPxBoth);
   ctx->launches++;
   GPS_CHECK_LAUNCH("px_allreduce_kernel launch");
+  return GPS_OK;
+}
+
+namespace {
+int px_check_phase(const gps_px* px, int phase) {
+  if (!px) return fail(GPS_E_ARG, "NULL argument");
+  if (phase < 1 || phase > 3) return fail(GPS_E_ARG, "phase %d outside {1 push, 2 gather, 3 both}", phase);
+  for (int q = 0; q < px->view.world; ++q)
+    if (!px->view.slots[q]) return fail(GPS_E_ARG, "peer %d not opened", q);
+  return GPS_OK;
+}
+}  // namespace
+
+int gps_px_allreduce_phase(gps_px* px, double* buf, int phase) {
+  if (int rc = px_check_phase(px, phase)) return rc;
+  if (!buf) return fail(GPS_E_ARG, "NULL argument");
+  gps_ctx* ctx = px->ctx;
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  px_allreduce_kernel<<<px_uniform_chunks(px->view.count), 256, 0, ctx->stream>>>(px->view, buf, phase);
+  ctx->launches++;
+  GPS_CHECK_LAUNCH("px_allreduce_kernel launch");
+  return GPS_OK;
+}
+
+int gps_px_reduce_phase(gps_px* px, const double* part_g, const double* part_s, int nparts, int rows, int nparts_s,
+                        double* exch, int phase) {
+  if (int rc = px_check_phase(px, phase)) return rc;
+  if (!part_g || !part_s || !exch || nparts < 1 || rows < 1 || nparts_s < 1) return fail(GPS_E_ARG, "bad arguments");
+  if (px->view.count != int64_t(rows) + 4)
+    return fail(GPS_E_ARG, "peer exchange sized for %lld, reduce has %d + 4",
+                static_cast<long long>(px->view.count), rows);
+  gps_ctx* ctx = px->ctx;
+  GPS_CUDA(cudaSetDevice(ctx->device));
+  su_reduce_px_kernel<<<px_uniform_chunks(rows) + 1, 256, 0, ctx->stream>>>(part_g, part_s, nparts, rows, exch,
+                                                                            nullptr, nparts_s, px->view,
+                                                                            SuStepArgs{}, phase);
+  ctx->launches++;
+  GPS_CHECK_LAUNCH("su_reduce_px_kernel launch");
   return GPS_OK;
 }
 
@@ -2869,6 +2939,33 @@ extern "C" int gpsdbg_tc_profile(unsigned long long* out, int n, int reset) {
                  cudaSuccess
              ? GPS_OK
              : GPS_E_CUDA;
+}
+
+// Tuning diagnostics: the tensor-core path's column mask (2 n bytes: T1's
+// candidate flags per epilogue group, or T1x's final activity mask) and the
+// T1x grid size (its work items are assigned round-robin over that grid).
+extern "C" int gpsdbg_bk_colmask(gps_bk* s, unsigned char* out, int* ref_grid_out) {
+  if (!s || !out || !ref_grid_out) return GPS_E_ARG;
+  if (!s->colmask) return GPS_E_UNSUPPORTED;
+  GPS_CUDA(cudaSetDevice(s->ctx->device));
+  GPS_CUDA(cudaStreamSynchronize(s->ctx->stream));
+  GPS_CUDA(cudaMemcpy(out, s->colmask, size_t(2) * s->A->n, cudaMemcpyDeviceToHost));
+  *ref_grid_out = s->tc_ref_grid;
+  return GPS_OK;
+}
+
+// Tuning diagnostics: cumulative Newton-Schulz iterations and exact-path
+// steps of a block loop's CholeskyQR2 polar step.
+extern "C" int gpsdbg_bk_polar(gps_bk* s, int* ns_iters_out, int* exact_out) {
+  if (!s || !ns_iters_out || !exact_out) return GPS_E_ARG;
+  if (!s->pc) return GPS_E_UNSUPPORTED;
+  GPS_CUDA(cudaSetDevice(s->ctx->device));
+  PolarCtl pc{};
+  GPS_CUDA(cudaMemcpyAsync(&pc, s->pc, sizeof(PolarCtl), cudaMemcpyDeviceToHost, s->ctx->stream));
+  GPS_CUDA(cudaStreamSynchronize(s->ctx->stream));
+  *ns_iters_out = pc.ns_iters;
+  *exact_out = pc.exact_steps;
+  return GPS_OK;
 }
 
 // k-NN neighbour selection on the device (datasets.py:258): the k nearest

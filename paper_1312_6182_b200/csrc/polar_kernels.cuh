@@ -38,6 +38,7 @@ struct PolarCtl {
   int fallback;     // CholeskyQR2 unusable -> Householder path
   int rank;
   int exact_steps;  // diagnostics: steps the exact path took (cumulative)
+  int ns_iters;     // diagnostics: Newton-Schulz iterations of the CholeskyQR2 path (cumulative)
 };
 
 constexpr int kMaxGramM = 64;
@@ -228,7 +229,7 @@ __device__ void mm_small(const double* A, const double* B, double* C, int m, int
 // (0, 1], so it converges; quadratically once X'X ~ I).  ws: 3 m ns_ld(m)
 // doubles of scratch (the iterate and two products at row stride ns_ld(m)).
 // Returns false if it has not converged in max_it steps.
-__device__ bool newton_schulz_polar(double* X, double* ws, double* red, int m, int max_it) {
+__device__ bool newton_schulz_polar(double* X, double* ws, double* red, int m, int max_it, int* iters = nullptr) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int ld = ns_ld(m);
   double* Xp = ws;
@@ -279,6 +280,7 @@ __device__ bool newton_schulz_polar(double* X, double* ws, double* red, int m, i
     if (tid == 0) printf("newton-schulz it %d step %.3e\n", it, dn);
 #endif
     ok = dn < 1e-15 * sqrt(double(m));
+    if (iters != nullptr && threadIdx.x == 0) *iters += 1;
   }
   if (ok)
     for (int e = tid; e < m * m; e += nt) X[e] = Xp[(e / m) * ld + e % m];
@@ -350,7 +352,11 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
   // (A blocked variant -- 8 x 8 diagonal blocks factored by one warp, block
   // row solves, rank-8 trailing updates, 24 barriers instead of 128 --
   // measured slower: 78K vs 63.5K clocks at m = 64, scripts/ubench/polar_ns.cu;
-  // the per-pivot chain stays, serialised in one warp.)
+  // the per-pivot chain stays, serialised in one warp.  So did 32 x 32
+  // blocks with the panel factored by one warp: 25K clocks per 32-step
+  // panel with the columns in registers (fully unrolled, instruction-fetch
+  // bound), 40K with them in shared memory, i.e. ~1000 clocks per pivot
+  // either way -- the pivot chain's fp64 latency, not the barriers.)
   const int ta = tid >> 4, tg = tid & 15;
   for (int j = 0; j < m; ++j) {
     const double d = M[j * m + j];
@@ -451,24 +457,17 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
   // Newton-Schulz iteration on M, which then starts well inside its
   // quadratic region (~20 -> ~7 steps at kappa ~ 100).  Scratch: T1 = the
   // m x m slot after W inside the Newton-Schulz workspace.
+  // (both triangular products on the fp64 tensor cores: mm_small over the
+  // full m x m operands, whose zero lower triangles keep the products upper;
+  // ~15-20 us less per stage at m = 64 than a thread per element)
   double* T1 = W + m * m;
   for (int e = tid; e < m * m; e += nt) T1[e] = R1g[e];  // R1 (upper) into shared memory
   __syncthreads();
-  for (int e = tid; e < m * m; e += nt) {
-    const int i = e / m, j = e % m;
-    double t = 0.0;
-    for (int k = i; k <= j; ++k) t = fma(R[i * m + k], T1[k * m + j], t);
-    W[e] = (i <= j) ? t : 0.0;  // R = R2 R1
-  }
+  mm_small(R, T1, W, m, m, false);  // R = R2 R1
   __syncthreads();
   for (int e = tid; e < m * m; e += nt) R[e] = Sg[e];  // R1^-1 (R2 is no longer needed)
   __syncthreads();
-  for (int e = tid; e < m * m; e += nt) {
-    const int i = e / m, j = e % m;
-    double t = 0.0;
-    for (int k = i; k <= j; ++k) t = fma(R[i * m + k], Ri[k * m + j], t);
-    T1[e] = (i <= j) ? t : 0.0;  // R^-1 = R1^-1 R2^-1
-  }
+  mm_small(R, Ri, T1, m, m, false);  // R^-1 = R1^-1 R2^-1
   __syncthreads();
   GPS_STAMP(4);
 #ifdef GPS_POLAR_DEBUG
@@ -488,7 +487,7 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
     }
   }
   __syncthreads();
-  if (!newton_schulz_polar(M, R, red, m, 100)) {  // not converged: exact path decides
+  if (!newton_schulz_polar(M, R, red, m, 100, &pc->ns_iters)) {  // not converged: exact path decides
     if (tid == 0) pc->fallback = 1;
     return;
   }

@@ -129,13 +129,25 @@ __device__ __forceinline__ void px_put(const PxView& v, int64_t i, double x, uns
   for (int q = 0; q < v.world; ++q) v.slots[q][(size_t(par) * v.world + v.rank) * v.count + i] = x;
 }
 
+// The two halves of every exchange launch.  Production launches run both
+// (kPxBoth); the cross-process test on ONE GPU runs them as two launches per
+// rank with a host barrier between (every rank pushes, then every rank
+// gathers flags that are already set), so no rank's kernel ever waits on a
+// kernel of another process sharing the GPU.
+constexpr int kPxPush = 1;    // put + signal
+constexpr int kPxGather = 2;  // wait + rank-order sum + epoch publication
+constexpr int kPxBoth = kPxPush | kPxGather;
+
 // CTA body: chunk c of rank v.rank at epoch e; vec is the rank's local vector.
-__device__ __forceinline__ void px_chunk(const PxView& v, double* vec, int c, unsigned long long e) {
+__device__ __forceinline__ void px_chunk(const PxView& v, double* vec, int c, unsigned long long e,
+                                         int phases = kPxBoth) {
   const int64_t lo = int64_t(c) * kPxChunk;
   const int64_t hi = lo + kPxChunk < v.count ? lo + kPxChunk : v.count;
-  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) px_put(v, i, vec[i], e);
-  px_signal(v, c, e);
-  px_gather(v, vec, c, lo, hi, e);  // a timeout is reported through v.state->error
+  if (phases & kPxPush) {
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) px_put(v, i, vec[i], e);
+    px_signal(v, c, e);
+  }
+  if (phases & kPxGather) px_gather(v, vec, c, lo, hi, e);  // a timeout is reported through v.state->error
 }
 
 // Epoch bookkeeping: every CTA reads the epoch before it finishes; the last
@@ -159,10 +171,10 @@ __device__ __forceinline__ bool px_finish(PxState* st, unsigned long long e) {
   return s_last != 0;
 }
 
-__global__ void __launch_bounds__(256) px_allreduce_kernel(const PxView v, double* vec) {
+__global__ void __launch_bounds__(256) px_allreduce_kernel(const PxView v, double* vec, int phases) {
   const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&v.state->epoch) + 1ull;
-  px_chunk(v, vec, blockIdx.x, e);
-  px_finish(v.state, e);
+  px_chunk(v, vec, blockIdx.x, e, phases);
+  if (phases & kPxGather) px_finish(v.state, e);  // a push-only launch leaves the epoch to its gather
 }
 
 // Test emulation of `world` ranks on ONE device as ONE cooperative kernel
@@ -188,9 +200,15 @@ __global__ void __launch_bounds__(256) px_emulate_kernel(const PxEmu emu) {
 // offset rows.  v.count == rows + 4.
 __device__ __forceinline__ bool px_reduce_chunk(const PxView& v, const double* __restrict__ part_g,
                                                 const double* __restrict__ part_s, int nparts, int rows,
-                                                int nparts_s, double* exch, int c, unsigned long long e) {
+                                                int nparts_s, double* exch, int c, unsigned long long e,
+                                                int phases = kPxBoth) {
   __shared__ double part[kReduceSlices][kReduceRows];
   const int nrc = (rows + kPxChunk - 1) / kPxChunk;
+  if (!(phases & kPxPush)) {  // gather half only (cross-process test)
+    const int64_t lo = c < nrc ? int64_t(c) * kPxChunk : rows;
+    const int64_t hi = c < nrc ? (lo + kPxChunk < rows ? lo + kPxChunk : rows) : int64_t(rows) + 4;
+    return px_gather(v, exch, c, lo, hi, e);
+  }
   if (c < nrc) {
     const int lo = c * kPxChunk, hi = min(rows, lo + kPxChunk);
     const int rr = threadIdx.x & (kReduceRows - 1), sl = threadIdx.x / kReduceRows;
@@ -214,7 +232,7 @@ __device__ __forceinline__ bool px_reduce_chunk(const PxView& v, const double* _
       __syncthreads();
     }
     px_signal(v, c, e);
-    return px_gather(v, exch, c, lo, hi, e);
+    return (phases & kPxGather) ? px_gather(v, exch, c, lo, hi, e) : true;
   } else {
     if (threadIdx.x < 128) {
       const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -224,7 +242,7 @@ __device__ __forceinline__ bool px_reduce_chunk(const PxView& v, const double* _
       if (lane == 0) px_put(v, rows + k, t, e);
     }
     px_signal(v, c, e);
-    return px_gather(v, exch, c, rows, int64_t(rows) + 4, e);
+    return (phases & kPxGather) ? px_gather(v, exch, c, rows, int64_t(rows) + 4, e) : true;
   }
 }
 
@@ -234,14 +252,16 @@ __device__ __forceinline__ bool px_reduce_chunk(const PxView& v, const double* _
 __global__ void __launch_bounds__(256) su_reduce_px_kernel(const double* __restrict__ part_g,
                                                            const double* __restrict__ part_s, int nparts, int rows,
                                                            double* __restrict__ exch, GpsCtl* ctl, int nparts_s,
-                                                           const PxView v, const SuStepArgs step) {
+                                                           const PxView v, const SuStepArgs step,
+                                                           int phases = kPxBoth) {
   if (ctl != nullptr && ctl->done) return;  // identical on every rank (replicated step)
   const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&v.state->epoch) + 1ull;
-  const bool ok = px_reduce_chunk(v, part_g, part_s, nparts, rows, nparts_s, exch, blockIdx.x, e);
+  const bool ok = px_reduce_chunk(v, part_g, part_s, nparts, rows, nparts_s, exch, blockIdx.x, e, phases);
   if (!ok && ctl != nullptr && threadIdx.x == 0) {
     ctl->status = kStatusExchangeTimeout;
     ctl->done = 1;
   }
+  if (!(phases & kPxGather)) return;
   const bool last = px_finish(v.state, e);
   if (last && ctl != nullptr && step.xbuf != nullptr &&
       *reinterpret_cast<volatile unsigned int*>(&v.state->error) == 0u)

@@ -695,6 +695,102 @@ __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+constexpr int kTcRefItem = 256;
+constexpr int kTcRefBatch = 64;
+constexpr int kTcRefRows = 32;
+constexpr int kRefKS = kTcRefRows + 4;  // k-contiguous row stride of the DMMA tiles (= 4 mod 16 doubles)
+constexpr int kTcSplitMax = 8;          // row splits (work units per leftover list) of T1s
+constexpr int kTcLeftMaxGrid = 1024;  // T1x grid bound of T1s's in-CTA scan (4 x 148 SMs fits)
+__host__ __device__ constexpr size_t tc_refine_smem(int nj) {
+  return (size_t(2) * kTcRefBatch * kRefKS + size_t(2) * nj * kRefKS) * sizeof(double);
+}
+
+// C (nb <= 64 candidate columns x NJ = 16 NT components) = A_cand' X over
+// rows [r_lo, r_hi) (multiples of 32) on the fp64 tensor cores (DMMA
+// m8n8k4, fp64 in, fp64 accumulate), 32 rows at a time.  Per chunk warp w
+// stages columns 8w .. 8w + 7 (lane = row, widened to fp64 once) and
+// components 8w .. 8w + 7 of X (lane = row) into double-buffered shared
+// tiles stored k-contiguous (row stride kRefKS = 36 = 4 mod 16 doubles:
+// stores and fragment loads are conflict-free), the next chunk's loads are
+// issued before the current chunk's DMMAs, one barrier per chunk.  Warp w
+// owns columns 16 (w % 4) .. + 16 (2 m-tiles) and components 8 NT (w / 4)
+// .. + 8 NT (NT n-tiles); on return lane holds
+// C[column 16 (w % 4) + 8 mt + lane / 4][component 8 NT (w / 4) + 8 nt + 2 (lane % 4) + h]
+// in acc[mt][nt][h].  256 threads; ends with a block barrier.
+template <typename TA, int NT>
+__device__ __forceinline__ void ref_batch_dots(const TA* __restrict__ A, int ld, const double* __restrict__ Xp,
+                                               const int64_t* cand, int nb, int r_lo, int r_hi, double* sA,
+                                               double* sX, double (&acc)[2][NT][2]) {
+  constexpr int NJ = 16 * NT;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3, mg = warp & 3, ng = warp >> 2;
+  // two accumulator sets (even / odd k-steps): 4 NT independent DMMA
+  // chains per warp instead of 2 NT, so the pipe's latency is covered
+  // (ncu: "wait" was 27 % of the stall samples with one set)
+  double acc2[2][NT][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int u = 0; u < NT; ++u) acc[i][u][0] = acc[i][u][1] = acc2[i][u][0] = acc2[i][u][1] = 0.0;
+  TA ra[8];
+  double rx[8];
+  auto load = [&](int r0) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int bc = warp * 8 + c;
+      ra[c] = bc < nb ? A[cand[bc] * ld + r0 + lane] : TA(0);
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int j = warp * 8 + c;
+      rx[c] = j < NJ ? Xp[size_t(j) * ld + r0 + lane] : 0.0;
+    }
+  };
+  if (r_lo < r_hi) load(r_lo);
+  int buf = 0;
+  for (int r0 = r_lo; r0 < r_hi; r0 += kTcRefRows, buf ^= 1) {
+    double* a_s = sA + buf * kTcRefBatch * kRefKS;
+    double* x_s = sX + buf * NJ * kRefKS;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) a_s[(warp * 8 + c) * kRefKS + lane] = static_cast<double>(ra[c]);
+    if (warp * 8 < NJ)
+#pragma unroll
+      for (int c = 0; c < 8; ++c) x_s[(warp * 8 + c) * kRefKS + lane] = rx[c];
+    __syncthreads();
+    if (r0 + kTcRefRows < r_hi) load(r0 + kTcRefRows);
+#pragma unroll
+    for (int ks = 0; ks < kTcRefRows; ks += 8) {
+      double a[2], b[NT], a2[2], b2[NT];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        a[mt] = a_s[(mg * 16 + mt * 8 + g) * kRefKS + ks + t];
+        a2[mt] = a_s[(mg * 16 + mt * 8 + g) * kRefKS + ks + 4 + t];
+      }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        b[nt] = x_s[(ng * 8 * NT + nt * 8 + g) * kRefKS + ks + t];
+        b2[nt] = x_s[(ng * 8 * NT + nt * 8 + g) * kRefKS + ks + 4 + t];
+      }
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+        if (mg * 16 + mt * 8 < nb)  // warp-uniform: m-tiles without a column are skipped
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            dmma_8x8x4(acc[mt][nt], a[mt], b[nt]);
+            dmma_8x8x4(acc2[mt][nt], a2[mt], b2[nt]);
+          }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int u = 0; u < NT; ++u) {
+      acc[i][u][0] += acc2[i][u][0];
+      acc[i][u][1] += acc2[i][u][1];
+    }
+}
+
 // T1x: exact fp64 recomputation of the candidate columns T1 flagged.
 // Work items are 256-column ranges (two T1 tiles), assigned to CTAs
 // round-robin (item b, b + grid, ...) so contiguous runs of active columns
@@ -702,12 +798,12 @@ __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
 // skipped without reading its columns.  The candidates of a CTA's items are
 // compacted in column order into one list (across items), and every 64 of
 // them are processed as a batch: C_batch = A_batch' X, 32 rows at a time, on
-// the fp64 tensor cores (DMMA m8n8k4; A and X through shared memory).  The
-// weights also go to Wt (column-major by component: one contiguous row of
-// NJ doubles per column) for T2's gathers.  A final partial list of up to
-// kTcRefSmallMax candidates instead takes the CTA one column at a time,
-// threads over rows, X read straight from L2 without block barriers (staged
-// chunks would serialise p / 32 latency-bound steps for a handful of columns).
+// the fp64 tensor cores (ref_batch_dots: DMMA m8n8k4; A and X through shared
+// memory).  The weights also go to Wt (column-major by component: one
+// contiguous row of NJ doubles per column) for T2's gathers.  The final
+// partial list (< 64 candidates; at C4 the whole workload: 1-2 per CTA) is
+// left in `left` for T1s, which spreads its rows over a cluster of CTAs (one
+// CTA streaming all p rows of X per leftover list took ~70 us per column).
 // fp32 a_ri is exact in fp64, so c_ij is an fp64 dot product.  Then, per
 // (column, component): s = mu_j c_ij, w_ij = threshold(s, gamma_j) (the
 // reference's parallel.py:117-128 / block.py:80-89 rules), the objective
@@ -715,15 +811,8 @@ __device__ __forceinline__ void dmma_8x8x4(double (&d)[2], double a, double b) {
 // activity mask (colmask[0][i] = any w_ij != 0, colmask[1][i] = 0) and the
 // per-item activity flag item_act for T2.  f and nnz are summed per thread in
 // a fixed order and reduced per CTA in a fixed order into part_s[blockIdx.x]
-// (deterministic run to run).
-constexpr int kTcRefItem = 256;
-constexpr int kTcRefBatch = 64;
-constexpr int kTcRefRows = 32;
-constexpr int kTcRefSmallMax = 16;
-constexpr int kRefKS = kTcRefRows + 4;  // k-contiguous row stride of the DMMA tiles (= 4 mod 16 doubles)
-__host__ __device__ constexpr size_t tc_refine_smem(int nj) {
-  return (size_t(2) * kTcRefBatch * kRefKS + size_t(2) * nj * kRefKS) * sizeof(double);
-}
+// (deterministic run to run); part_s[gridDim.x + 4 blockIdx.x + i], i < 4,
+// are T1s's group slots (zeroed here, written by T1s for existing groups).
 template <typename TA, int JPT>
 __global__ void __launch_bounds__(256, 2) tc_refine_kernel(const TA* __restrict__ A, int64_t n, int ld, int m,
                                                            const double* __restrict__ X, int64_t x_par_stride,
@@ -734,10 +823,10 @@ __global__ void __launch_bounds__(256, 2) tc_refine_kernel(const TA* __restrict_
                                                            unsigned char* __restrict__ item_act,
                                                            double* __restrict__ W, int64_t w_par_stride,
                                                            double* __restrict__ Wt, double* __restrict__ part_s,
-                                                           const GpsCtl* ctl, BandLog* band) {
+                                                           const GpsCtl* ctl, BandLog* band,
+                                                           int64_t* __restrict__ left, int* __restrict__ left_n) {
   constexpr int NJ = 8 * JPT;  // padded components (X is zero beyond m)
   constexpr int NT = NJ / 16;  // DMMA n-tiles per warp (two component halves)
-  constexpr int JC = NJ < 32 ? NJ : 32;  // components per pass of the single-column mode
   if (ctl != nullptr && ctl->done) return;
   const int parity = ctl != nullptr ? (ctl->iter & 1) : 0;
   const double* Xp = X + parity * x_par_stride;
@@ -749,7 +838,6 @@ __global__ void __launch_bounds__(256, 2) tc_refine_kernel(const TA* __restrict_
   __shared__ int ilist[256];
   __shared__ int wcnt[8];
   __shared__ unsigned char act[kTcRefBatch];
-  __shared__ double wsum[8][32];
   __shared__ double smu[NJ], sgam[NJ];
   __shared__ double red[2][8];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -784,81 +872,12 @@ __global__ void __launch_bounds__(256, 2) tc_refine_kernel(const TA* __restrict_
   };
 
   // batch mode: candidates cand[b0 .. b0 + nb), nb <= 64, on the fp64
-  // tensor cores: C (64 columns x NJ components) = A_batch' X over 32-row
-  // chunks.  Per chunk warp w stages columns 8w .. 8w + 7 (lane = row,
-  // widened to fp64 once) and components 8w .. 8w + 7 of X (lane = row) into
-  // double-buffered shared tiles stored k-contiguous (row stride kRefKS =
-  // 36 = 4 mod 16 doubles: stores and fragment loads are conflict-free), the
-  // next chunk's loads are issued before the current chunk's DMMAs, one
-  // barrier per chunk.  Warp w owns columns 16 (w % 4) .. + 16 (2 m-tiles)
-  // and components 8 NT (w / 4) .. + 8 NT (NT n-tiles).
+  // tensor cores over all rows
   auto batch = [&](int b0, int nb) {
     const int g = lane >> 2, t = lane & 3, mg = warp & 3, ng = warp >> 2;
-    // two accumulator sets (even / odd k-steps): 4 NT independent DMMA
-    // chains per warp instead of 2 NT, so the pipe's latency is covered
-    // (ncu: "wait" was 27 % of the stall samples with one set)
-    double acc[2][NT][2], acc2[2][NT][2];
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int u = 0; u < NT; ++u) acc[i][u][0] = acc[i][u][1] = acc2[i][u][0] = acc2[i][u][1] = 0.0;
+    double acc[2][NT][2];
     if (tid < kTcRefBatch) act[tid] = 0;
-    TA ra[8];
-    double rx[8];
-    auto load = [&](int r0) {
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const int bc = warp * 8 + c;
-        ra[c] = bc < nb ? A[cand[b0 + bc] * ld + r0 + lane] : TA(0);
-      }
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        const int j = warp * 8 + c;
-        rx[c] = j < NJ ? Xp[size_t(j) * ld + r0 + lane] : 0.0;
-      }
-    };
-    load(0);
-    int buf = 0;
-    for (int r0 = 0; r0 < ld; r0 += kTcRefRows, buf ^= 1) {
-      double* a_s = sA + buf * kTcRefBatch * kRefKS;
-      double* x_s = sX + buf * NJ * kRefKS;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) a_s[(warp * 8 + c) * kRefKS + lane] = static_cast<double>(ra[c]);
-      if (warp * 8 < NJ)
-#pragma unroll
-        for (int c = 0; c < 8; ++c) x_s[(warp * 8 + c) * kRefKS + lane] = rx[c];
-      __syncthreads();
-      if (r0 + kTcRefRows < ld) load(r0 + kTcRefRows);
-#pragma unroll
-      for (int ks = 0; ks < kTcRefRows; ks += 8) {
-        double a[2], b[NT], a2[2], b2[NT];
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          a[mt] = a_s[(mg * 16 + mt * 8 + g) * kRefKS + ks + t];
-          a2[mt] = a_s[(mg * 16 + mt * 8 + g) * kRefKS + ks + 4 + t];
-        }
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          b[nt] = x_s[(ng * 8 * NT + nt * 8 + g) * kRefKS + ks + t];
-          b2[nt] = x_s[(ng * 8 * NT + nt * 8 + g) * kRefKS + ks + 4 + t];
-        }
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            dmma_8x8x4(acc[mt][nt], a[mt], b[nt]);
-            dmma_8x8x4(acc2[mt][nt], a2[mt], b2[nt]);
-          }
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int u = 0; u < NT; ++u) {
-        acc[i][u][0] += acc2[i][u][0];
-        acc[i][u][1] += acc2[i][u][1];
-      }
+    ref_batch_dots<TA, NT>(A, ld, Xp, cand + b0, nb, 0, ld, sA, sX, acc);
     // epilogue: lane holds C[column mg 16 + mt 8 + g][component ng 8 NT + nt 8 + 2 t + {0, 1}]
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt) {
@@ -897,53 +916,6 @@ __global__ void __launch_bounds__(256, 2) tc_refine_kernel(const TA* __restrict_
     __syncthreads();
   };
 
-  // single-column mode: the CTA on cand[ci], threads over rows
-  auto single = [&](int ci) {
-    const int64_t c = cand[ci];
-    const TA* ac = A + c * ld;
-    if (tid == 0) act[0] = 0;
-#pragma unroll 1
-    for (int jh = 0; jh < NJ; jh += JC) {
-      double acc[JC];
-#pragma unroll
-      for (int j = 0; j < JC; ++j) acc[j] = 0.0;
-      const double* xr = Xp + size_t(jh) * ld;
-#pragma unroll 2
-      for (int r = tid; r < ld; r += 256) {
-        const double av = static_cast<double>(ac[r]);
-#pragma unroll
-        for (int j = 0; j < JC; ++j) acc[j] = fma(av, xr[size_t(j) * ld + r], acc[j]);
-      }
-#pragma unroll
-      for (int j = 0; j < JC; ++j) {
-        const double v = warp_sum(acc[j]);
-        if (lane == 0) wsum[warp][j] = v;
-      }
-      __syncthreads();
-      if (tid < JC && jh + tid < m) {
-        const int jj = jh + tid;
-        double cj = wsum[0][tid];
-#pragma unroll
-        for (int w = 1; w < 8; ++w) cj += wsum[w][tid];
-        const double sj = smu[jj] * cj;
-        const double w = threshold_weight(sj, sgam[jj], penalty);
-        band_note(band, parity, c, jj, sj, sgam[jj], penalty);
-        f_acc += objective_term(sj, sgam[jj], penalty);
-        if (w != 0.0) {
-          nnz_acc += 1.0;
-          act[0] = 1;  // benign: every writer stores 1
-        }
-        Wp[size_t(jj) * n + c] = w;
-        Wt[c * NJ + jj] = w;
-      } else if (tid < JC && jh + tid < NJ) {
-        Wt[c * NJ + jh + tid] = 0.0;  // padded components (T2 reads whole rows)
-      }
-      __syncthreads();
-    }
-    if (tid == 0) publish(c, act[0] != 0);
-    __syncthreads();
-  };
-
   int pending = 0;  // candidates in cand[0 .. pending) (block-uniform)
   for (int64_t kb = 0; int64_t(blockIdx.x) + kb * G < items; kb += 256) {
     // my items kb .. kb + 255 (item = blockIdx.x + k G): keep the flagged ones
@@ -978,11 +950,12 @@ __global__ void __launch_bounds__(256, 2) tc_refine_kernel(const TA* __restrict_
       }
     }
   }
-  if (pending > kTcRefSmallMax) {
-    batch(0, pending);
-  } else {
-    for (int ci = 0; ci < pending; ++ci) single(ci);
-  }
+  // the leftover list (< 64) goes to T1s, which groups the lists of all
+  // CTAs (in CTA order) and splits their rows over many CTAs; this CTA
+  // zeroes T1s's f / nnz slots [4 b, 4 b + 4) (T1s writes one per group)
+  if (tid < pending) left[size_t(blockIdx.x) * kTcRefBatch + tid] = cand[tid];
+  if (tid == 0) left_n[blockIdx.x] = pending;
+  if (tid < 16) part_s[(G + 4 * blockIdx.x) * 4 + tid] = 0.0;
   f_acc = warp_sum(f_acc);
   nnz_acc = warp_sum(nnz_acc);
   __syncthreads();
@@ -997,6 +970,226 @@ __global__ void __launch_bounds__(256, 2) tc_refine_kernel(const TA* __restrict_
       for (int w = 0; w < 8; ++w) t += red[tid][w];
     part_s[size_t(blockIdx.x) * 4 + tid] = t;
   }
+}
+
+// Small lists (nb <= 16 columns, two m-tiles): C = A_cand' X over rows
+// [r_lo, r_hi) with the rows split over the 8 warps (split-k), fragments
+// loaded straight from global memory (L1 / L2: one 16-byte segment per
+// column and 4-row k-step) -- no shared staging, no block barrier per step.
+// Warp w owns rows r_lo + w R8 .. + R8 (R8 = (r_hi - r_lo) / 8 rounded up to
+// 4) and every component (NJ / 8 n-tiles); the 8 warp partials are summed
+// in warp order through shared memory into part[bc NJ + j] (bc < 16).
+template <typename TA, int NJ>
+__device__ __forceinline__ void ref_small_dots(const TA* __restrict__ A, int ld, const double* __restrict__ Xp,
+                                               const int64_t* cand, int nb, int r_lo, int r_hi, double* part) {
+  constexpr int NTT = NJ / 8;  // n-tiles (all components)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int rw = (((r_hi - r_lo + 7) / 8) + 3) & ~3;
+  const int k_lo = min(r_hi, r_lo + warp * rw), k_hi = min(r_hi, k_lo + rw);
+  double acc[2][NTT][2];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NTT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+  const TA* ac0 = A + cand[min(g, nb - 1)] * ld;
+  const TA* ac1 = A + cand[min(8 + g, nb - 1)] * ld;
+  const bool two = nb > 8;  // warp-uniform
+#pragma unroll 2
+  for (int k = k_lo; k < k_hi; k += 4) {
+    const double a0 = g < nb ? static_cast<double>(ac0[k + t]) : 0.0;
+    const double a1 = 8 + g < nb ? static_cast<double>(ac1[k + t]) : 0.0;
+    double b[NTT];
+#pragma unroll
+    for (int nt = 0; nt < NTT; ++nt) b[nt] = Xp[size_t(nt * 8 + g) * ld + k + t];
+#pragma unroll
+    for (int nt = 0; nt < NTT; ++nt) dmma_8x8x4(acc[0][nt], a0, b[nt]);
+    if (two)
+#pragma unroll
+      for (int nt = 0; nt < NTT; ++nt) dmma_8x8x4(acc[1][nt], a1, b[nt]);
+  }
+  // warp partials [8][16][NJ] in shared memory, then the fixed-order sum
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NTT; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) part[(warp * 16 + mt * 8 + g) * NJ + nt * 8 + 2 * t + h] = acc[mt][nt][h];
+  __syncthreads();
+  for (int e = tid; e < 16 * NJ; e += 256) {
+    double v = part[e];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) v += part[w * 16 * NJ + e];
+    part[e] = v;
+  }
+  __syncthreads();
+}
+
+// T1s: the leftover candidate lists of T1x (< 64 columns per T1x CTA).
+// Every CTA scans the list lengths in T1x-CTA order, so the candidates get a
+// deterministic global order; groups of GS consecutive candidates (16 when
+// they total <= 256, else 64) times RS row splits form the work units of a
+// persistent grid.  Unit (group q, rs) forms the partial C over rows
+// [rs R, rs R + R) (ref_small_dots for 16 columns, else ref_batch_dots) and
+// stores it to lpart (group q's slab at its first candidate); the last of
+// the RS units to finish (counter
+// lcnt[q], reset by it) sums the RS partials in rs order (deterministic) and
+// runs T1x's per-(column, component) epilogue: threshold, band log,
+// objective, nnz, W, Wt, the final activity mask and item flag; f and nnz go
+// to part_s[q] in a fixed order.  Grouping across lists reads X once per
+// group instead of once per list.  (Per-list units measured 66-74 us at C4
+// -- ~60 lists of 1-2 columns each re-reading all of X -- and a
+// thread-block-cluster version reducing over distributed shared memory 78.)
+template <typename TA, int JPT>
+__global__ void __launch_bounds__(256) tc_refine_split_kernel(
+    const TA* __restrict__ A, int64_t n, int ld, int m, const double* __restrict__ X, int64_t x_par_stride,
+    const double* __restrict__ mu, const double* __restrict__ gamma, int penalty, unsigned char* __restrict__ colmask,
+    unsigned char* __restrict__ item_act, double* __restrict__ W, int64_t w_par_stride, double* __restrict__ Wt,
+    double* __restrict__ part_s, const GpsCtl* ctl, BandLog* band, const int64_t* __restrict__ left,
+    const int* __restrict__ left_n, int nlists, int RS, int rows_per_split, double* __restrict__ lpart,
+    unsigned int* __restrict__ lcnt) {
+  constexpr int NJ = 8 * JPT;
+  constexpr int NT = NJ / 16;
+  if (ctl != nullptr && ctl->done) return;
+  extern __shared__ __align__(16) double ref_smem[];
+  double* sA = ref_smem;
+  double* sX = ref_smem + 2 * kTcRefBatch * kRefKS;
+  __shared__ int64_t cand[kTcRefBatch];
+  __shared__ unsigned char act[kTcRefBatch];
+  __shared__ double smu[NJ], sgam[NJ];
+  __shared__ double red[2][8];
+  __shared__ int s_last;
+  __shared__ int pre[kTcLeftMaxGrid + 1];  // exclusive prefix of the list lengths
+  __shared__ int wsum[8];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int parity = ctl != nullptr ? (ctl->iter & 1) : 0;
+  const double* Xp = X + parity * x_par_stride;
+  double* Wp = W + parity * w_par_stride;
+  for (int j = tid; j < NJ; j += 256) {
+    smu[j] = j < m ? mu[j] : 1.0;
+    sgam[j] = j < m ? gamma[j] : 0.0;
+  }
+  // block-wide exclusive scan of left_n[0 .. nlists) (4 lists per thread)
+  {
+    int v[4], t = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int b = tid * 4 + u;
+      v[u] = b < nlists ? left_n[b] : 0;
+      t += v[u];
+    }
+    int incl = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    int off = 0;
+    for (int w = 0; w < warp; ++w) off += wsum[w];
+    int run = off + incl - t;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int b = tid * 4 + u;
+      if (b <= kTcLeftMaxGrid) pre[b] = run;
+      run += v[u];
+    }
+    __syncthreads();
+  }
+  const int total = pre[nlists];
+  const int GS = total <= 256 ? 16 : kTcRefBatch;
+  const int groups = (total + GS - 1) / GS;
+  for (int u = blockIdx.x; u < groups * RS; u += gridDim.x) {
+  const int q = u / RS, rs = u % RS;
+  const int g0 = q * GS, nb = min(GS, total - g0);
+  __syncthreads();  // the previous unit's readers of cand / act / part are done
+  if (tid < nb) {
+    // list of global candidate g0 + tid: the last b with pre[b] <= g0 + tid
+    const int gi = g0 + tid;
+    int lo = 0, hi = nlists - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (pre[mid] <= gi) lo = mid;
+      else hi = mid - 1;
+    }
+    cand[tid] = left[size_t(lo) * kTcRefBatch + (gi - pre[lo])];
+  }
+  if (tid < kTcRefBatch) act[tid] = 0;
+  __syncthreads();
+  const int r_lo = min(ld, rs * rows_per_split), r_hi = min(ld, r_lo + rows_per_split);
+  // this unit's partial C [nb][NJ] (shared memory), then to lpart[q][rs]
+  double* part = sA;
+  if (nb <= 16) {
+    ref_small_dots<TA, NJ>(A, ld, Xp, cand, nb, r_lo, r_hi, part);
+  } else {
+    double acc[2][NT][2];
+    ref_batch_dots<TA, NT>(A, ld, Xp, cand, nb, r_lo, r_hi, sA, sX, acc);  // the A tiles are done after it
+    const int g = lane >> 2, t = lane & 3, mg = warp & 3, ng = warp >> 2;
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          part[(mg * 16 + mt * 8 + g) * NJ + ng * 8 * NT + nt * 8 + 2 * t + h] = acc[mt][nt][h];
+    __syncthreads();
+  }
+  double* slab = lpart + size_t(g0) * RS * NJ;  // [RS][GS][NJ] per group
+  for (int e = tid; e < nb * NJ; e += 256) __stcg(slab + size_t(rs) * GS * NJ + e, part[e]);
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    s_last = atomicAdd(&lcnt[q], 1u) == unsigned(RS - 1);
+    if (s_last) lcnt[q] = 0;  // for the next sweep (stream order)
+  }
+  __syncthreads();
+  if (!s_last) continue;
+  __threadfence();
+  for (int e = tid; e < nb * NJ; e += 256) {
+    double v = __ldcg(slab + e);
+    for (int r = 1; r < RS; ++r) v += __ldcg(slab + size_t(r) * GS * NJ + e);
+    part[e] = v;
+  }
+  __syncthreads();
+  double f_acc = 0.0, nnz_acc = 0.0;
+  for (int e = tid; e < nb * NJ; e += 256) {
+    const int bc = e / NJ, j = e % NJ;
+    const int64_t c = cand[bc];
+    double w = 0.0;
+    if (j < m) {
+      const double sj = smu[j] * part[e];
+      w = threshold_weight(sj, sgam[j], penalty);
+      band_note(band, parity, c, j, sj, sgam[j], penalty);
+      f_acc += objective_term(sj, sgam[j], penalty);
+      if (w != 0.0) {
+        nnz_acc += 1.0;
+        act[bc] = 1;  // benign: every writer stores 1
+      }
+      Wp[size_t(j) * n + c] = w;
+    }
+    Wt[c * NJ + j] = w;  // padded components 0 (T2 reads whole rows)
+  }
+  __syncthreads();
+  if (tid < nb) {
+    const int64_t c = cand[tid];
+    colmask[c] = act[tid];
+    colmask[n + c] = 0;
+    if (act[tid]) item_act[c / kTcRefItem] = 1;
+  }
+  f_acc = warp_sum(f_acc);
+  nnz_acc = warp_sum(nnz_acc);
+  if (lane == 0) {
+    red[0][warp] = f_acc;
+    red[1][warp] = nnz_acc;
+  }
+  __syncthreads();
+  if (tid < 2) {
+    double t = 0.0;
+    for (int w8 = 0; w8 < 8; ++w8) t += red[tid][w8];
+    part_s[size_t(q) * 4 + tid] = t;
+  }
+  }  // units
 }
 
 // T2: sparse rank-m update on the ACTIVE columns (colmask), fp64 on the
