@@ -83,10 +83,10 @@ __host__ __device__ constexpr int sweep_cols_per_group(int rv) { return rv >= 8 
 
 // Shared scratch after the ring (doubles): red[D][NG][K][NW] warp partials,
 // wsm[D][NG][K] thresholded weights, sc[NG*K][3] reducer scalars,
-// wfl[D][NG][K] integer-widening flags; then the mbarriers full[S],
-// empty[S], pfull[D], wready[D].
+// wfl[D][NG][K] integer-widening flags, rel[D] early-release flags; then
+// the mbarriers full[S], empty[S], pfull[D], wready[D].
 __host__ __device__ inline size_t sweep_red_bytes(int ng, int gs, int k) {
-  return (size_t(kSweepD) * ng * k * (gs / 32) + size_t(2) * kSweepD * ng * k + size_t(ng) * k * 3) *
+  return (size_t(kSweepD) * ng * k * (gs / 32) + size_t(2) * kSweepD * ng * k + size_t(ng) * k * 3 + kSweepD) *
          sizeof(double);
 }
 
@@ -192,6 +192,7 @@ __global__ void __launch_bounds__(NWK + 64, 1) su_sweep_kernel(const SweepArgs a
   double* wsm = red + D * NG * K * NW;
   double* sc = wsm + D * NG * K;
   double* wfl = sc + NG * K * 3;
+  double* rel = wfl + D * NG * K;
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(red) + sweep_red_bytes(NG, GS, K));
   uint64_t* empty = full + S;
   uint64_t* pfull = empty + S;
@@ -254,9 +255,11 @@ __global__ void __launch_bounds__(NWK + 64, 1) su_sweep_kernel(const SweepArgs a
     const int grp = mine ? i / K : 0;
     const int k = mine ? i % K : 0;
     double f_acc = 0.0, nnz_acc = 0.0, s2_acc = 0.0;
+    int rslot = 0;  // ring slot of stage s
     for (int s = 0; s < ns; ++s) {
       const int d = s & (D - 1);
       mbar_wait_sleep(&pfull[d], static_cast<uint32_t>((s / D) & 1));
+      double w_pub = 0.0;
       if (mine) {
         const int64_t col = (s_begin + s) * T + k * NG + grp;
         double c, w;
@@ -285,9 +288,23 @@ __global__ void __launch_bounds__(NWK + 64, 1) su_sweep_kernel(const SweepArgs a
         }
         wsm[(d * NG + grp) * K + k] = w;
         wfl[(d * NG + grp) * K + k] = (a.col_fast != nullptr && col < a.n && a.col_fast[col]) ? 1.0 : 0.0;
+        w_pub = w;
       }
+      // Early release: a stage without an active column (or any stage of a
+      // dot-only sweep) is not read again -- its dots are done (pfull) and it
+      // has no rank-1 update -- so its ring slot goes back to the producer
+      // now, one worker iteration before the workers would release it after
+      // their (empty) update pass.  Keeps a stage more in flight on sparse
+      // sweeps.  The workers see rel[d] and skip both the pass and their
+      // own arrivals.
+      const bool release = (MODE == kDotOnly) || !__any_sync(0xffffffffu, w_pub != 0.0);
+      if (lane == 0) rel[d] = release ? 1.0 : 0.0;
       __syncwarp();
-      if (lane == 0) mbar_arrive(&wready[d]);
+      if (lane == 0) {
+        if (release) mbar_arrive_cnt(&empty[rslot], NWK / 32);
+        mbar_arrive(&wready[d]);
+      }
+      if (++rslot == S) rslot = 0;
     }
     if (mine) {
       sc[i * 3 + 0] = f_acc;
@@ -383,7 +400,8 @@ __global__ void __launch_bounds__(NWK + 64, 1) su_sweep_kernel(const SweepArgs a
       const int u = t - L;
       const int d = u & (D - 1);
       mbar_wait(&wready[d], static_cast<uint32_t>((u / D) & 1));
-      if (MODE != kDotOnly) {
+      const bool released = rel[d] != 0.0;  // the reducer returned this slot already
+      if (MODE != kDotOnly && !released) {
         const TA* ptile = reinterpret_cast<const TA*>(ring + uslot * stage_bytes);
         const double* wp = wsm + (d * NG + grp) * K;
         const double* fp = wfl + (d * NG + grp) * K;
@@ -417,7 +435,7 @@ __global__ void __launch_bounds__(NWK + 64, 1) su_sweep_kernel(const SweepArgs a
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[uslot]);
+      if (lane == 0 && !released) mbar_arrive(&empty[uslot]);
       if (++uslot == S) uslot = 0;
     }
   }
