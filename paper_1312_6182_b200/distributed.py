@@ -106,20 +106,38 @@ class PeerExchange:
 
         L = _native.lib()
         self.count = int(count)
-        h = _native._vp()
-        _native.check(L.gps_px_create(context.handle, comm.world, comm.rank, self.count, _native.C.byref(h)),
-                      "gps_px_create")
-        self.handle = h
-        size = L.gps_px_handle_size()
-        mine = (_native.C.c_char * size)()
-        _native.check(L.gps_px_ipc_handle(h, mine), "gps_px_ipc_handle")
+        self.handle = None
+        # Every rank reaches the one collective below whatever fails locally
+        # (a rank raising before it would leave its peers blocked in it);
+        # failures are recorded in self.ok, which px_self_test agrees on.
+        self.ok = True
+        mine = None
+        try:
+            h = _native._vp()
+            _native.check(L.gps_px_create(context.handle, comm.world, comm.rank, self.count, _native.C.byref(h)),
+                          "gps_px_create")
+            self.handle = h
+            size = L.gps_px_handle_size()
+            buf = (_native.C.c_char * size)()
+            _native.check(L.gps_px_ipc_handle(h, buf), "gps_px_ipc_handle")
+            mine = bytes(buf)
+        except Exception:  # noqa: BLE001 -- reported through self.ok
+            self.ok = False
         handles = [None] * comm.world
-        dist.all_gather_object(handles, bytes(mine), group=comm.group)
-        for peer, hb in enumerate(handles):
-            buf = (_native.C.c_char * size).from_buffer_copy(hb)
-            _native.check(L.gps_px_open(h, peer, buf), "gps_px_open")
+        dist.all_gather_object(handles, mine, group=comm.group)
+        if self.ok and all(hb is not None for hb in handles):
+            try:
+                size = L.gps_px_handle_size()
+                for peer, hb in enumerate(handles):
+                    _native.check(L.gps_px_open(self.handle, peer, (_native.C.c_char * size).from_buffer_copy(hb)),
+                                  "gps_px_open")
+            except Exception:  # noqa: BLE001 -- reported through self.ok
+                self.ok = False
+        else:
+            self.ok = False
 
     def all_reduce(self, t):
+        assert self.ok, "peer exchange not usable on this rank"
         assert t.numel() == self.count and t.dtype.is_floating_point and t.element_size() == 8
         _native.check(_native.lib().gps_px_allreduce(self.handle, _native._vp(t.data_ptr())), "gps_px_allreduce")
 
@@ -162,6 +180,12 @@ def px_self_test(px, comm, device, count):
     v = torch.randn(count, dtype=torch.float64, device=device, generator=g)
     ref = v.clone()
     comm.dist.all_reduce(ref, op=comm.dist.ReduceOp.SUM, group=comm.group)
+    # a rank whose construction failed must not launch: its peers' pushes
+    # would wait on it until the timeout (they agree below and fall back)
+    flag0 = torch.tensor([1 if getattr(px, "ok", True) else 0], dtype=torch.int32, device=device)
+    comm.dist.all_reduce(flag0, op=comm.dist.ReduceOp.MIN, group=comm.group)
+    if not bool(flag0.item()):
+        return False
     try:
         px.all_reduce(v)
         torch.cuda.synchronize(device)

@@ -318,8 +318,11 @@ class _FakePeerExchange:
 
     def __init__(self, mode, comm):
         self.mode, self.comm = mode, comm
+        # "broken": rank 1 could not open its peers' buffers (PeerExchange.ok)
+        self.ok = not (mode == "broken" and comm.rank == 1)
 
     def all_reduce(self, t):
+        assert self.ok, "a rank whose construction failed must not launch the exchange"
         self.comm.all_reduce_sum(t)  # the exchange itself (a device kernel in the real class)
         if self.mode == "raise" and self.comm.rank == 1:
             raise RuntimeError("peer exchange timed out")  # e.g. this rank's bounded wait expired
@@ -337,7 +340,7 @@ def _self_test_worker(rank, port, out):
         # px_self_test synchronises the device; on CPU ranks make that a no-op
         torch.cuda.synchronize = lambda *a, **k: None
         res = {}
-        for mode in ("ok", "wrong", "raise"):
+        for mode in ("ok", "wrong", "raise", "broken"):
             res[mode] = d.px_self_test(_FakePeerExchange(mode, comm), comm, torch.device("cpu"), 300)
         out[rank] = res
     finally:
@@ -346,9 +349,10 @@ def _self_test_worker(rank, port, out):
 
 def test_peer_exchange_self_test_agreement():
     """Every rank keeps the peer path only when all ranks reproduced the
-    torch.distributed sum; one wrong or failing rank sends all to NCCL."""
+    torch.distributed sum; one wrong or failing rank, or one that could not
+    open its peers' buffers, sends all to NCCL (and none of them launches)."""
     mgr = mp.Manager()
     out = mgr.dict()
     mp.spawn(_self_test_worker, args=(_free_port(), out), nprocs=WORLD, join=True)
     for r in range(WORLD):
-        assert out[r] == {"ok": True, "wrong": False, "raise": False}, out[r]
+        assert out[r] == {"ok": True, "wrong": False, "raise": False, "broken": False}, out[r]
