@@ -995,7 +995,10 @@ __device__ __forceinline__ void ref_small_dots(const TA* __restrict__ A, int ld,
   const TA* ac0 = A + cand[min(g, nb - 1)] * ld;
   const TA* ac1 = A + cand[min(8 + g, nb - 1)] * ld;
   const bool two = nb > 8;  // warp-uniform
-#pragma unroll 2
+  // k-steps in flight per warp: the loop is latency-bound (L2 / HBM loads),
+  // so unroll as far as registers allow (NTT + 2 operands per k-step)
+  constexpr int KU = NTT <= 2 ? 8 : (NTT <= 4 ? 4 : 2);
+#pragma unroll KU
   for (int k = k_lo; k < k_hi; k += 4) {
     const double a0 = g < nb ? static_cast<double>(ac0[k + t]) : 0.0;
     const double a1 = 8 + g < nb ? static_cast<double>(ac1[k + t]) : 0.0;
