@@ -1,8 +1,8 @@
 # A/B of the fused single-unit sweep: paper_1312_6182_b200/libgpspca_b200_base.so
-# vs a variant build (${VARIANT:-libgpspca_b200.so}), alternating, C2 headline
-# only, plus the gamma = 0 dense probe.
+# vs variant builds (VARIANTS="libgpspca_b200_x.so ..."), alternating, C2
+# headline only, plus the gamma = 0 dense probe.
 mkdir -p gpurun_out
-V=${VARIANT:-libgpspca_b200.so}
+V=${VARIANTS:-libgpspca_b200.so}
 for rep in 1 2 3; do
   for lib in libgpspca_b200_base.so $V; do
     GPSPCA_LIB=$PWD/paper_1312_6182_b200/$lib timeout 600 python bench.py --steps 300 --e2e-steps 0 --no-cpu-baseline --no-block 2>/dev/null \
