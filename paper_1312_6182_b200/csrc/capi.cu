@@ -371,21 +371,21 @@ int launch_sweep(gps_matrix* A, const SweepPlan& plan, SweepArgs args, int mode,
 
 int launch_reduce(gps_ctx* ctx, const double* part_g, const double* part_s, int nparts, int ld, double* exch,
                   const GpsCtl* ctl, int nparts_s = -1, const gps_px* px = nullptr,
-                  const SuStepArgs* step = nullptr) {
+                  const SuStepArgs* step = nullptr, const unsigned char* nz = nullptr) {
   if (px != nullptr) {
     // K2 fused with the peer-memory all-reduce (px_kernels.cuh)
     if (px->view.count != int64_t(ld) + 4) return fail(GPS_E_ARG, "peer exchange sized for %lld, reduce has %d + 4",
                                                       static_cast<long long>(px->view.count), ld);
     su_reduce_px_kernel<<<px_uniform_chunks(ld) + 1, 256, 0, ctx->stream>>>(
         part_g, part_s, nparts, ld, exch, const_cast<GpsCtl*>(ctl), nparts_s < 0 ? nparts : nparts_s, px->view,
-        step != nullptr ? *step : SuStepArgs{});
+        step != nullptr ? *step : SuStepArgs{}, kPxBoth, nz);
     ctx->launches++;
     GPS_CHECK_LAUNCH("su_reduce_px_kernel launch");
     return GPS_OK;
   }
-  const int blocks = (ld + kReduceRows - 1) / kReduceRows + 1;
+  const int blocks = std::min((ld + kReduceRows - 1) / kReduceRows, ctx->num_sms * 8) + 1;
   su_reduce_kernel<<<blocks, 256, 0, ctx->stream>>>(part_g, part_s, nparts, ld, exch, ctl,
-                                                    nparts_s < 0 ? nparts : nparts_s);
+                                                    nparts_s < 0 ? nparts : nparts_s, nz);
   ctx->launches++;
   GPS_CHECK_LAUNCH("su_reduce_kernel launch");
   return GPS_OK;
@@ -1434,6 +1434,8 @@ struct gps_bk {
   int* tc_left_n = nullptr;           // [tc_ref_grid]
   int tc_split = 1, tc_split_rows = 0;  // T1s row splits (CTAs per leftover list) and rows per split
   double* tc_lpart = nullptr;         // T1s partial dots: per group [tc_split][GS][m_pad] at its first candidate
+  unsigned char* tc_part_nz = nullptr;  // [tc_gx] T2 partial written (1) or empty (0), read by K2
+  unsigned int* tc_act_count = nullptr;  // active columns of the current sweep (T0 zeroes, T1x / T1s count, T2 reads)
   unsigned int* tc_lcnt = nullptr;    // [4 tc_ref_grid] T1s arrival counters per group (zero between sweeps)
   CUtensorMap tmA, tmXh, tmXl;
   // multi-CTA CholeskyQR2 polar (large p*m)
@@ -1548,7 +1550,7 @@ int bk_enqueue_tc(gps_bk* s, bool with_ctl) {
   const GpsCtl* ctl = with_ctl ? s->ctl : nullptr;
   const int ld = static_cast<int>(A->ld), np = s->mg;
   tc_split_x_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(s->X, int64_t(s->m_pad()) * ld, s->m, np, ld, s->xhi,
-                                                            s->xlo, ctl);
+                                                            s->xlo, ctl, s->tc_act_count);
   ctx->launches++;
   TcDotsArgs a{};
   a.n = A->n;
@@ -1594,12 +1596,14 @@ int bk_enqueue_tc(gps_bk* s, bool with_ctl) {
   do {                                                                                                         \
     tc_refine_kernel<TA, J><<<s->tc_ref_grid, 256, tc_refine_smem(8 * J), ctx->stream>>>(                        \
         static_cast<const TA*>(A->d), A->n, ld, s->m, s->X, xs, s->mu_dev, gam, s->penalty, s->colmask, s->tflag, \
-        s->item_act, s->W, wst, s->Wt, s->part_s_tc, ctl, ctl ? s->band : nullptr, s->tc_left, s->tc_left_n);   \
+        s->item_act, s->W, wst, s->Wt, s->part_s_tc, ctl, ctl ? s->band : nullptr, s->tc_left, s->tc_left_n,    \
+        s->tc_act_count);                                                                                      \
     ctx->launches++;                                                                                           \
     tc_refine_split_kernel<TA, J><<<ctx->num_sms, 256, tc_refine_smem(8 * J), ctx->stream>>>(                    \
         static_cast<const TA*>(A->d), A->n, ld, s->m, s->X, xs, s->mu_dev, gam, s->penalty, s->colmask,           \
         s->item_act, s->W, wst, s->Wt, s->part_s_tc + size_t(s->tc_ref_grid) * 4, ctl, ctl ? s->band : nullptr,  \
-        s->tc_left, s->tc_left_n, s->tc_ref_grid, s->tc_split, s->tc_split_rows, s->tc_lpart, s->tc_lcnt);      \
+        s->tc_left, s->tc_left_n, s->tc_ref_grid, s->tc_split, s->tc_split_rows, s->tc_lpart, s->tc_lcnt,      \
+        s->tc_act_count);                                                                                      \
   } while (0)
 #define GPS_REFINE_J(TA)            \
   switch (np / 8) {                 \
@@ -1623,7 +1627,8 @@ int bk_enqueue_tc(gps_bk* s, bool with_ctl) {
 #define GPS_UPDATE(TA, NT)                                                                                   \
   tc_update_kernel<TA, NT><<<dim3(s->tc_gx, static_cast<unsigned>(ceil_div(A->ld, kUpdR))), 256,              \
                              tc_update_smem(16 * NT), ctx->stream>>>(static_cast<const TA*>(A->d), A->n, ld, s->m, \
-                                                                     s->colmask, s->item_act, s->Wt, s->part_g, ctl)
+                                                                     s->colmask, s->item_act, s->Wt, s->part_g, ctl, \
+                                                                     s->tc_part_nz, s->tc_act_count)
 #define GPS_UPDATE_J(TA)                \
   switch (np / 16) {                    \
     case 1: GPS_UPDATE(TA, 1); break;   \
@@ -1641,7 +1646,8 @@ int bk_enqueue_tc(gps_bk* s, bool with_ctl) {
     ctx->launches++;
   }
   GPS_CHECK_LAUNCH("tensor-core block sweep launch");
-  return launch_reduce(ctx, s->part_g, s->part_s_tc, s->tc_gx, np * ld, s->exch, ctl, 5 * s->tc_ref_grid, s->px);
+  return launch_reduce(ctx, s->part_g, s->part_s_tc, s->tc_gx, np * ld, s->exch, ctl, 5 * s->tc_ref_grid, s->px,
+                       nullptr, s->tc_part_nz);
 }
 
 int bk_enqueue_sweeps(gps_bk* s, bool with_ctl) {
@@ -1927,6 +1933,9 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
     alloc((void**)&s->tc_left, size_t(s->tc_ref_grid) * kTcRefBatch * sizeof(int64_t));
     alloc((void**)&s->tc_left_n, size_t(s->tc_ref_grid) * sizeof(int));
     alloc((void**)&s->tc_lpart, size_t(s->tc_ref_grid) * s->tc_split * kTcRefBatch * mp * sizeof(double));
+    alloc((void**)&s->tc_part_nz, size_t(s->tc_gx));
+    alloc((void**)&s->tc_act_count, sizeof(unsigned int));
+    if (e == cudaSuccess) e = cudaMemsetAsync(s->tc_part_nz, 0, size_t(s->tc_gx), ctx->stream);
     alloc((void**)&s->tc_lcnt, size_t(4) * s->tc_ref_grid * sizeof(unsigned int));
     if (e == cudaSuccess) e = cudaMemsetAsync(s->tc_lcnt, 0, size_t(4) * s->tc_ref_grid * sizeof(unsigned int), ctx->stream);
     alloc((void**)&s->Wt, n * mp * sizeof(double));
@@ -2054,6 +2063,8 @@ int gps_bk_destroy(gps_bk* s) {
   if (s->tc_left_n) gps_free(s->tc_left_n);
   if (s->tc_lpart) gps_free(s->tc_lpart);
   if (s->tc_lcnt) gps_free(s->tc_lcnt);
+  if (s->tc_part_nz) gps_free(s->tc_part_nz);
+  if (s->tc_act_count) gps_free(s->tc_act_count);
   if (s->Wt) gps_free(s->Wt);
   if (s->pc) gps_free(s->pc);
   if (s->gram_part) gps_free(s->gram_part);

@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(256) px_emulate_kernel(const PxEmu emu) {
 __device__ __forceinline__ bool px_reduce_chunk(const PxView& v, const double* __restrict__ part_g,
                                                 const double* __restrict__ part_s, int nparts, int rows,
                                                 int nparts_s, double* exch, int c, unsigned long long e,
-                                                int phases = kPxBoth) {
+                                                int phases = kPxBoth, const unsigned char* nz = nullptr) {
   __shared__ double part[kReduceSlices][kReduceRows];
   const int nrc = (rows + kPxChunk - 1) / kPxChunk;
   if (!(phases & kPxPush)) {  // gather half only (cross-process test)
@@ -218,8 +218,13 @@ __device__ __forceinline__ bool px_reduce_chunk(const PxView& v, const double* _
       double t = 0.0;
       if (r < hi) {
         const double* p = part_g + r;
+        if (nz == nullptr) {
 #pragma unroll 4
-        for (int b = b0; b < b1; ++b) t += p[size_t(b) * rows];
+          for (int b = b0; b < b1; ++b) t += p[size_t(b) * rows];
+        } else {  // as su_reduce_kernel: empty partials were not written
+          for (int b = b0; b < b1; ++b)
+            if (nz[b]) t += p[size_t(b) * rows];
+        }
       }
       part[sl][rr] = t;
       __syncthreads();
@@ -253,10 +258,11 @@ __global__ void __launch_bounds__(256) su_reduce_px_kernel(const double* __restr
                                                            const double* __restrict__ part_s, int nparts, int rows,
                                                            double* __restrict__ exch, GpsCtl* ctl, int nparts_s,
                                                            const PxView v, const SuStepArgs step,
-                                                           int phases = kPxBoth) {
+                                                           int phases = kPxBoth,
+                                                           const unsigned char* __restrict__ nz = nullptr) {
   if (ctl != nullptr && ctl->done) return;  // identical on every rank (replicated step)
   const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(&v.state->epoch) + 1ull;
-  const bool ok = px_reduce_chunk(v, part_g, part_s, nparts, rows, nparts_s, exch, blockIdx.x, e, phases);
+  const bool ok = px_reduce_chunk(v, part_g, part_s, nparts, rows, nparts_s, exch, blockIdx.x, e, phases, nz);
   if (!ok && ctl != nullptr && threadIdx.x == 0) {
     ctl->status = kStatusExchangeTimeout;
     ctl->done = 1;

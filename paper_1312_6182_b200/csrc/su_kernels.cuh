@@ -479,30 +479,62 @@ __global__ void __launch_bounds__(NWK + 64, 1) su_sweep_kernel(const SweepArgs a
 // Row blocks + one scalar block.
 constexpr int kReduceRows = 32;
 constexpr int kReduceSlices = 8;
+constexpr int kReduceRowPerThread = 1 << 16;  // rows from which K2 takes a thread per row
 __global__ void __launch_bounds__(256) su_reduce_kernel(const double* __restrict__ part_g,
                                                         const double* __restrict__ part_s, int nparts,
                                                         int ld, double* __restrict__ exch,
-                                                        const GpsCtl* ctl, int nparts_s) {
+                                                        const GpsCtl* ctl, int nparts_s,
+                                                        const unsigned char* __restrict__ nz = nullptr) {
   if (ctl != nullptr && ctl->done) return;
-  const int row_blocks = (ld + kReduceRows - 1) / kReduceRows;
-  if (blockIdx.x < row_blocks) {
+  // Per row: the partials in 8 contiguous slices, each summed in order, then
+  // the slice sums in order.  The last CTA sums the scalars.
+  if (blockIdx.x + 1 < gridDim.x) {
+    if (ld >= kReduceRowPerThread) {
+      // long rows (the block path's p m-long partials): a thread per row
+      // computes the same slice-then-slices order itself, grid-stride over
+      // the rows.  (Loading every partial's entry into registers first
+      // measured slower: the predicated loads also read the unwritten
+      // partials.)
+      for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < ld; r += (gridDim.x - 1) * blockDim.x) {
+        const double* p = part_g + r;
+        double u = 0.0;
+        for (int sl = 0; sl < kReduceSlices; ++sl) {
+          const int b0 = nparts * sl / kReduceSlices, b1 = nparts * (sl + 1) / kReduceSlices;
+          double t = 0.0;
+          for (int b = b0; b < b1; ++b)
+            if (nz == nullptr || nz[b]) t += p[size_t(b) * ld];  // empty partials were not written
+          u = sl == 0 ? t : u + t;
+        }
+        exch[r] = u;
+      }
+      return;
+    }
+    const int row_blocks = (ld + kReduceRows - 1) / kReduceRows;
     __shared__ double part[kReduceSlices][kReduceRows];
     const int rr = threadIdx.x & (kReduceRows - 1), sl = threadIdx.x / kReduceRows;
-    const int r = blockIdx.x * kReduceRows + rr;
-    const int b0 = nparts * sl / kReduceSlices, b1 = nparts * (sl + 1) / kReduceSlices;
-    double t = 0.0;
-    if (r < ld) {
-      const double* p = part_g + r;
+    for (int rb = blockIdx.x; rb < row_blocks; rb += gridDim.x - 1) {
+      const int r = rb * kReduceRows + rr;
+      const int b0 = nparts * sl / kReduceSlices, b1 = nparts * (sl + 1) / kReduceSlices;
+      double t = 0.0;
+      if (r < ld) {
+        const double* p = part_g + r;
+        if (nz == nullptr) {
 #pragma unroll 4
-      for (int b = b0; b < b1; ++b) t += p[size_t(b) * ld];
-    }
-    part[sl][rr] = t;
-    __syncthreads();
-    if (sl == 0 && r < ld) {
-      double u = part[0][rr];
+          for (int b = b0; b < b1; ++b) t += p[size_t(b) * ld];
+        } else {
+          for (int b = b0; b < b1; ++b)
+            if (nz[b]) t += p[size_t(b) * ld];
+        }
+      }
+      __syncthreads();  // the previous row block's readers of part are done
+      part[sl][rr] = t;
+      __syncthreads();
+      if (sl == 0 && r < ld) {
+        double u = part[0][rr];
 #pragma unroll
-      for (int k = 1; k < kReduceSlices; ++k) u += part[k][rr];
-      exch[r] = u;
+        for (int k = 1; k < kReduceSlices; ++k) u += part[k][rr];
+        exch[r] = u;
+      }
     }
   } else if (threadIdx.x < 128) {
     // warp k sums scalar k: lane-strided partials, then the xor tree (fixed order)

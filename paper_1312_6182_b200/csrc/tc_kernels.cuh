@@ -165,8 +165,10 @@ __global__ void tc_col_delta_kernel(const TA* __restrict__ A, int64_t n, int ld,
 // T0: X (fp64 [m][ld], parity slot) -> X1 / X2 (fp16 [n_pad][ld], zero
 // padded components): x 2^14 = X1 + 2^-11 X2.
 __global__ void tc_split_x_kernel(const double* __restrict__ X, int64_t x_par_stride, int m, int n_pad, int ld,
-                                  __half* __restrict__ x1, __half* __restrict__ x2, const GpsCtl* ctl) {
+                                  __half* __restrict__ x1, __half* __restrict__ x2, const GpsCtl* ctl,
+                                  unsigned int* __restrict__ act_count) {
   if (ctl != nullptr && ctl->done) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *act_count = 0;  // this sweep's active columns (T1x / T1s count, T2 reads)
   const int parity = ctl != nullptr ? (ctl->iter & 1) : 0;
   const double* Xp = X + parity * x_par_stride;
   for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < int64_t(n_pad) * ld;
@@ -824,7 +826,8 @@ __global__ void __launch_bounds__(256, 2) tc_refine_kernel(const TA* __restrict_
                                                            double* __restrict__ W, int64_t w_par_stride,
                                                            double* __restrict__ Wt, double* __restrict__ part_s,
                                                            const GpsCtl* ctl, BandLog* band,
-                                                           int64_t* __restrict__ left, int* __restrict__ left_n) {
+                                                           int64_t* __restrict__ left, int* __restrict__ left_n,
+                                                           unsigned int* __restrict__ act_count) {
   constexpr int NJ = 8 * JPT;  // padded components (X is zero beyond m)
   constexpr int NT = NJ / 16;  // DMMA n-tiles per warp (two component halves)
   if (ctl != nullptr && ctl->done) return;
@@ -913,7 +916,8 @@ __global__ void __launch_bounds__(256, 2) tc_refine_kernel(const TA* __restrict_
     }
     __syncthreads();
     if (tid < nb) publish(cand[b0 + tid], act[tid] != 0);
-    __syncthreads();
+    const int nact = __syncthreads_count(tid < nb && act[tid] != 0);
+    if (tid == 0 && nact > 0) atomicAdd(act_count, static_cast<unsigned int>(nact));
   };
 
   int pending = 0;  // candidates in cand[0 .. pending) (block-uniform)
@@ -1050,7 +1054,7 @@ __global__ void __launch_bounds__(256) tc_refine_split_kernel(
     unsigned char* __restrict__ item_act, double* __restrict__ W, int64_t w_par_stride, double* __restrict__ Wt,
     double* __restrict__ part_s, const GpsCtl* ctl, BandLog* band, const int64_t* __restrict__ left,
     const int* __restrict__ left_n, int nlists, int RS, int rows_per_split, double* __restrict__ lpart,
-    unsigned int* __restrict__ lcnt) {
+    unsigned int* __restrict__ lcnt, unsigned int* __restrict__ act_count) {
   constexpr int NJ = 8 * JPT;
   constexpr int NT = NJ / 16;
   if (ctl != nullptr && ctl->done) return;
@@ -1173,7 +1177,8 @@ __global__ void __launch_bounds__(256) tc_refine_split_kernel(
     }
     Wt[c * NJ + j] = w;  // padded components 0 (T2 reads whole rows)
   }
-  __syncthreads();
+  const int nact = __syncthreads_count(tid < nb && act[tid] != 0);
+  if (tid == 0 && nact > 0) atomicAdd(act_count, static_cast<unsigned int>(nact));
   if (tid < nb) {
     const int64_t c = cand[tid];
     colmask[c] = act[tid];
@@ -1221,12 +1226,15 @@ __host__ __device__ constexpr int upd_ws(int nj) { return nj + 4; }  // sW row s
 __host__ __device__ constexpr size_t tc_update_smem(int nj) {
   return (size_t(2) * kUpdKT * kUpdAS + size_t(2) * kUpdKT * upd_ws(nj)) * sizeof(double);
 }
+constexpr unsigned int kUpdColsPerRange = 8;  // active columns per T2 column range (partial), at least
 template <typename TA, int NT>
 __global__ void __launch_bounds__(256, 2) tc_update_kernel(const TA* __restrict__ A, int64_t n, int ld, int m,
                                                            const unsigned char* __restrict__ colmask,
                                                            const unsigned char* __restrict__ item_act,
                                                            const double* __restrict__ Wt,
-                                                           double* __restrict__ part_g, const GpsCtl* ctl) {
+                                                           double* __restrict__ part_g, const GpsCtl* ctl,
+                                                           unsigned char* __restrict__ part_nz,
+                                                           const unsigned int* __restrict__ act_count) {
   constexpr int NJ = 16 * NT;
   constexpr int WS = upd_ws(NJ);
   constexpr int VN = 16 / sizeof(TA);                     // elements per 16-byte A load
@@ -1238,10 +1246,22 @@ __global__ void __launch_bounds__(256, 2) tc_update_kernel(const TA* __restrict_
   extern __shared__ __align__(16) double upd_smem[];
   double* sA = upd_smem;                        // [2][KT][AS]
   double* sW = upd_smem + 2 * kUpdKT * kUpdAS;  // [2][KT][WS]
-  const int64_t nblk = (n + kTcUpdBlock - 1) / kTcUpdBlock;
-  const int64_t b0 = nblk * blockIdx.x / gridDim.x, b1 = nblk * (blockIdx.x + 1) / gridDim.x;
-  const int r0 = blockIdx.y * kUpdR;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // column ranges in use: one per kUpdColsPerRange active columns (this
+  // sweep's count from T1x / T1s), at most gridDim.x -- a sparse sweep sums
+  // its few columns in a few partials instead of writing (and K2
+  // re-reading) 32 mostly-zero p x m partials.  (One range for < 2048
+  // active columns measured slower at C4: 64 CTAs each scanning all 4096
+  // block flags, 69 us against 50.)
+  const unsigned int want = (*act_count + kUpdColsPerRange - 1) / kUpdColsPerRange;
+  const int gxe = static_cast<int>(want < 1u ? 1u : (want > gridDim.x ? gridDim.x : want));
+  if (static_cast<int>(blockIdx.x) >= gxe) {
+    if (blockIdx.y == 0 && tid == 0) part_nz[blockIdx.x] = 0;
+    return;
+  }
+  const int64_t nblk = (n + kTcUpdBlock - 1) / kTcUpdBlock;
+  const int64_t b0 = nblk * blockIdx.x / gxe, b1 = nblk * (blockIdx.x + 1) / gxe;
+  const int r0 = blockIdx.y * kUpdR;
   const int g = lane >> 2, t = lane & 3;
   const int rg = warp & 3, cg = warp >> 2;
   double acc[4][NT][2];
@@ -1253,6 +1273,7 @@ __global__ void __launch_bounds__(256, 2) tc_update_kernel(const TA* __restrict_
   __shared__ int wcnt[8];
   __shared__ int64_t alist[kTcUpdBlock];
   int acc_n = 0;  // entries in alist (block-uniform)
+  int seen = 0;   // active columns of this column range (block-uniform; the same for every row block)
 
   // block-wide exclusive scan of a per-thread count (fixed order)
   auto scan = [&](int v, int& total) {
@@ -1353,10 +1374,17 @@ __global__ void __launch_bounds__(256, 2) tc_update_kernel(const TA* __restrict_
       if (f0) alist[acc_n + off] = c0;
       if (f1) alist[acc_n + off + int(f0)] = c0 + 1;
       acc_n += total;
+      seen += total;
     }
     __syncthreads();  // blist reuse
   }
   __syncthreads();
+  // A column range without an active column leaves its partial unwritten
+  // and flags it empty: K2 skips it (at C4 with 64 active columns nearly
+  // every range is empty, and writing and re-reading their zeros cost
+  // 2 x 134 MB per iteration).
+  if (blockIdx.y == 0 && tid == 0) part_nz[blockIdx.x] = seen > 0 ? 1 : 0;
+  if (seen == 0) return;
   flush();
   double* pg = part_g + size_t(blockIdx.x) * NJ * ld;
 #pragma unroll
