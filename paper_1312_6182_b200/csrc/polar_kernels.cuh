@@ -344,6 +344,70 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
 #endif
   if (tid == 0) bad = 0;
   __syncthreads();
+  if (stage == 2) {
+    // Stage 2 factors the Gram of Q1 = G R1^-1, I + E with |E| ~ kappa^2 u
+    // (<= 1e-6 inside the trust region), without the 64-step pivot chain:
+    // R2 = I + U with U upper triangular solving U + U' + U'U = E, by the
+    // fixed point U <- Phi(E - U'U) (Phi: strict upper part plus half the
+    // diagonal; each step multiplies the error by ~|E|, from |E|^2 at U0),
+    // and R2^-1 = sum_k (-U)^k (Horner).  Both are the Cholesky factor and
+    // its inverse to rounding; the step counts follow |E| (typically one
+    // and two mm_small, ~6.5K clocks each at m = 64, against 63.5K + 23.7K
+    // for the pivot loop and the back substitution).  |E| > 1e-3 means |R2 - I| far
+    // beyond the trust region below: the exact path takes the step.
+    double t = 0.0;
+    for (int e = tid; e < m * m; e += nt) {
+      if (e / m == e % m) M[e] -= 1.0;  // M := E
+      t = fma(M[e], M[e], t);
+    }
+    const double eps = sqrt(block_sum_any(t, red));
+    if (!(eps <= 1e-3)) {
+      if (tid == 0) pc->fallback = 1;
+      return;
+    }
+    // the series runs at the Newton-Schulz row stride L (conflict-free
+    // mm_small fragments; at stride m = 64 every A fragment row hits one
+    // bank): U, the product and R2^-1 in the workspace after R (3 m L
+    // doubles), E in M; then R2 = I + U goes to R via M, R2^-1 to Ri
+    const int L = ns_ld(m);
+    double* Up = R;
+    double* Wp = R + m * L;
+    double* Rp = R + 2 * m * L;
+    auto phi = [&](int i, int j, double v) { return i < j ? v : (i == j ? 0.5 * v : 0.0); };
+    for (int e = tid; e < m * m; e += nt) Up[(e / m) * L + e % m] = phi(e / m, e % m, M[e]);  // U0 = Phi(E)
+    int k_fp = 0;
+    for (double err = eps * eps; err > 1e-18 && k_fp < 4; err *= eps) ++k_fp;
+    for (int k = 0; k < k_fp; ++k) {
+      __syncthreads();
+      mm_small(Up, Up, Wp, m, L, true);  // U'U
+      __syncthreads();
+      for (int e = tid; e < m * m; e += nt) {
+        const int i = e / m, j = e % m;
+        Up[i * L + j] = phi(i, j, M[e] - Wp[i * L + j]);
+      }
+    }
+    int k_neu = 1;
+    for (double term = eps * eps; term > 1e-18 && k_neu < 6; term *= eps) ++k_neu;
+    for (int e = tid; e < m * m; e += nt) Rp[(e / m) * L + e % m] = (e / m == e % m) ? 1.0 : 0.0;
+    for (int k = 0; k < k_neu; ++k) {
+      __syncthreads();
+      mm_small(Up, Rp, Wp, m, L, false);  // U R2^-1 (partial sum)
+      __syncthreads();
+      for (int e = tid; e < m * m; e += nt) {
+        const int i = e / m, j = e % m;
+        Rp[i * L + j] = (i == j ? 1.0 : 0.0) - Wp[i * L + j];
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < m * m; e += nt) {
+      const int i = e / m, j = e % m;
+      M[e] = (i == j ? 1.0 : 0.0) + Up[i * L + j];  // R2 = I + U
+      Ri[e] = Rp[i * L + j];
+    }
+    __syncthreads();
+    for (int e = tid; e < m * m; e += nt) R[e] = M[e];
+    __syncthreads();
+  }
   double dmax = 0.0;
   for (int j = 0; j < m; ++j) dmax = fmax(dmax, M[j * m + j]);
   // Right-looking Cholesky of the upper triangle, two barriers per step:
@@ -357,60 +421,62 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
   // panel with the columns in registers (fully unrolled, instruction-fetch
   // bound), 40K with them in shared memory, i.e. ~1000 clocks per pivot
   // either way -- the pivot chain's fp64 latency, not the barriers.)
-  const int ta = tid >> 4, tg = tid & 15;
-  for (int j = 0; j < m; ++j) {
-    const double d = M[j * m + j];
-    if (!(d > 1e-28 * dmax) || !(d > 0.0)) {
-      if (tid == 0) bad = 1;
-      break;  // uniform: every thread reads the same d
-    }
-    const double rp = rsqrt(d);  // one reciprocal square root instead of sqrt + divisions
-    for (int c = j + tid; c < m; c += nt) R[j * m + c] = (c == j) ? d * rp : M[j * m + c] * rp;
-    __syncthreads();
-    if (ta > j && ta < m) {
-      const double rja = R[j * m + ta];
-      for (int c = ta + tg; c < m; c += 16) M[ta * m + c] = fma(-rja, R[j * m + c], M[ta * m + c]);
-    }
-    __syncthreads();
-  }
-  __syncthreads();
-  GPS_STAMP(2);
-#ifdef GPS_POLAR_DEBUG
-  if (tid == 0) printf("chol stage %d cholesky done %lld\n", stage, clock64());
-#endif
-  if (bad) {
-    if (tid == 0) pc->fallback = 1;
-    return;
-  }
-  // Ri = R^-1 (upper) by back substitution, one thread per column c (a
-  // column needs only its own rows below, so no barrier per row), times
-  // the diagonal reciprocals formed in parallel first.  Every lane of a
-  // warp walks the same rows i and the same k range (up to the warp's last
-  // column; entries below a column's diagonal are zero), so the R reads are
-  // broadcasts and the Ri reads are conflict-free.  Measured at m = 64
-  // (scripts/ubench/polar_ns.cu, whole stage-1 kernel): 75 us, against 95 us
-  // with a half-warp per column and shuffle sums, 100 us with one block
-  // barrier per row.
-  if (tid < m) W[tid] = 1.0 / R[tid * m + tid];
-  __syncthreads();
-  if (tid < ((m + 31) & ~31)) {
-    const int c = tid, cr = min(c, m - 1), cw = min((tid | 31), m - 1);  // cr: lanes past m read a live column
-    for (int i = cw; i >= 0; --i) {
-      double t0 = 0.0, t1 = 0.0;
-      int k = i + 1;
-      for (; k + 1 <= cw; k += 2) {
-        t0 = fma(R[i * m + k], Ri[k * m + cr], t0);
-        t1 = fma(R[i * m + k + 1], Ri[(k + 1) * m + cr], t1);
+  if (stage == 1) {  // (stage 2 factored above)
+    const int ta = tid >> 4, tg = tid & 15;
+    for (int j = 0; j < m; ++j) {
+      const double d = M[j * m + j];
+      if (!(d > 1e-28 * dmax) || !(d > 0.0)) {
+        if (tid == 0) bad = 1;
+        break;  // uniform: every thread reads the same d
       }
-      if (k <= cw) t0 = fma(R[i * m + k], Ri[k * m + cr], t0);
-      if (c < m && i <= c) Ri[i * m + c] = ((i == c ? 1.0 : 0.0) - (t0 + t1)) * W[i];
+      const double rp = rsqrt(d);  // one reciprocal square root instead of sqrt + divisions
+      for (int c = j + tid; c < m; c += nt) R[j * m + c] = (c == j) ? d * rp : M[j * m + c] * rp;
+      __syncthreads();
+      if (ta > j && ta < m) {
+        const double rja = R[j * m + ta];
+        for (int c = ta + tg; c < m; c += 16) M[ta * m + c] = fma(-rja, R[j * m + c], M[ta * m + c]);
+      }
+      __syncthreads();
     }
-  }
-  __syncthreads();
-  GPS_STAMP(3);
+    __syncthreads();
+    GPS_STAMP(2);
 #ifdef GPS_POLAR_DEBUG
-  if (tid == 0) printf("chol stage %d inverse done %lld\n", stage, clock64());
+    if (tid == 0) printf("chol stage %d cholesky done %lld\n", stage, clock64());
 #endif
+    if (bad) {
+      if (tid == 0) pc->fallback = 1;
+      return;
+    }
+    // Ri = R^-1 (upper) by back substitution, one thread per column c (a
+    // column needs only its own rows below, so no barrier per row), times
+    // the diagonal reciprocals formed in parallel first.  Every lane of a
+    // warp walks the same rows i and the same k range (up to the warp's last
+    // column; entries below a column's diagonal are zero), so the R reads are
+    // broadcasts and the Ri reads are conflict-free.  Measured at m = 64
+    // (scripts/ubench/polar_ns.cu, whole stage-1 kernel): 75 us, against 95 us
+    // with a half-warp per column and shuffle sums, 100 us with one block
+    // barrier per row.
+    if (tid < m) W[tid] = 1.0 / R[tid * m + tid];
+    __syncthreads();
+    if (tid < ((m + 31) & ~31)) {
+      const int c = tid, cr = min(c, m - 1), cw = min((tid | 31), m - 1);  // cr: lanes past m read a live column
+      for (int i = cw; i >= 0; --i) {
+        double t0 = 0.0, t1 = 0.0;
+        int k = i + 1;
+        for (; k + 1 <= cw; k += 2) {
+          t0 = fma(R[i * m + k], Ri[k * m + cr], t0);
+          t1 = fma(R[i * m + k + 1], Ri[(k + 1) * m + cr], t1);
+        }
+        if (k <= cw) t0 = fma(R[i * m + k], Ri[k * m + cr], t0);
+        if (c < m && i <= c) Ri[i * m + c] = ((i == c ? 1.0 : 0.0) - (t0 + t1)) * W[i];
+      }
+    }
+    __syncthreads();
+    GPS_STAMP(3);
+#ifdef GPS_POLAR_DEBUG
+    if (tid == 0) printf("chol stage %d inverse done %lld\n", stage, clock64());
+#endif
+  }
   if (stage == 1) {
     // kappa_F(R1) = |R1|_F |R1^-1|_F ~ kappa(G): beyond kCholQr2MaxKappa the
     // CholeskyQR2 result is not trusted and the exact path decides (rank too)

@@ -100,6 +100,19 @@ int main() {
   cudaMalloc(&dS, m * m * 8);
   cudaMalloc(&pc, sizeof(PolarCtl));
   cudaMemcpy(dG, Gm.data(), m * m * 8, cudaMemcpyHostToDevice);
+  // stage 2 factors the Gram of Q1 = G R1^-1, I + E with |E| ~ kappa^2 u
+  std::vector<double> G2(m * m, 0.0);
+  for (int a = 0; a < m; ++a)
+    for (int c = a; c < m; ++c) {
+      s = s * 1664525u + 1013904223u;
+      const double e = 1e-7 * (double(s >> 8) / double(1 << 24) - 0.5);
+      G2[a * m + c] += e;
+      if (c != a) G2[c * m + a] += e;
+    }
+  for (int a = 0; a < m; ++a) G2[a * m + a] += 1.0;
+  double* dG2;
+  cudaMalloc(&dG2, m * m * 8);
+  cudaMemcpy(dG2, G2.data(), m * m * 8, cudaMemcpyHostToDevice);
   const int ssm = int(chol_smem_bytes(m));
   cudaFuncSetAttribute(chol_stage_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ssm);
   for (int rep = 0; rep < 3; ++rep)
@@ -110,7 +123,7 @@ int main() {
       cudaEventCreate(&a);
       cudaEventCreate(&b);
       cudaEventRecord(a);
-      chol_stage_kernel<<<1, kPolarThreads, ssm>>>(dG, 1, m, 8192, stage, dR1, dS, pc);
+      chol_stage_kernel<<<1, kPolarThreads, ssm>>>(stage == 1 ? dG : dG2, 1, m, 8192, stage, dR1, dS, pc);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       float ms;
