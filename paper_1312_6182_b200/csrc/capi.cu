@@ -1386,7 +1386,7 @@ int ensure_polar_attrs() {
                        reinterpret_cast<const void*>(stiefel_error_kernel),
                        reinterpret_cast<const void*>(apply_right_kernel)};
   for (const void* fn : fns) {
-    cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     if (err != cudaSuccess) return cuda_fail(err, "cudaFuncSetAttribute(polar)");
   }
   done.insert(dev);

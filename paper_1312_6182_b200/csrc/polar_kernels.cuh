@@ -365,10 +365,10 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
       if (tid == 0) pc->fallback = 1;
       return;
     }
-    // the series runs at the Newton-Schulz row stride L (conflict-free
-    // mm_small fragments; at stride m = 64 every A fragment row hits one
-    // bank): U, the product and R2^-1 in the workspace after R (3 m L
-    // doubles), E in M; then R2 = I + U goes to R via M, R2^-1 to Ri
+    // the series and the rest of stage 2 run at the Newton-Schulz row
+    // stride L (conflict-free mm_small fragments; at stride m = 64 every A
+    // fragment row hits one bank): U, a product and R2^-1 in the padded
+    // buffers after R (chol_smem_bytes), E in M
     const int L = ns_ld(m);
     double* Up = R;
     double* Wp = R + m * L;
@@ -398,14 +398,6 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
         Rp[i * L + j] = (i == j ? 1.0 : 0.0) - Wp[i * L + j];
       }
     }
-    __syncthreads();
-    for (int e = tid; e < m * m; e += nt) {
-      const int i = e / m, j = e % m;
-      M[e] = (i == j ? 1.0 : 0.0) + Up[i * L + j];  // R2 = I + U
-      Ri[e] = Rp[i * L + j];
-    }
-    __syncthreads();
-    for (int e = tid; e < m * m; e += nt) R[e] = M[e];
     __syncthreads();
   }
   double dmax = 0.0;
@@ -456,11 +448,17 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
     // (scripts/ubench/polar_ns.cu, whole stage-1 kernel): 75 us, against 95 us
     // with a half-warp per column and shuffle sums, 100 us with one block
     // barrier per row.
+    // For m > 32 the two 32-column diagonal blocks are inverted at the same
+    // time (warp 0: rows / columns 0 .. 31, warp 1: 32 .. m-1) and the
+    // off-diagonal block follows as Ri12 = -Ri11 R12 Ri22 over all threads:
+    // the thread-per-column walk of the whole triangle made warp 1 (columns
+    // 32 .. 63, rows 63 .. 0) ~2.5x longer than warp 0 (~60K clocks).
     if (tid < m) W[tid] = 1.0 / R[tid * m + tid];
     __syncthreads();
     if (tid < ((m + 31) & ~31)) {
+      const int lo = m > 32 ? (tid & ~31) : 0;  // first row / column of this warp's diagonal block
       const int c = tid, cr = min(c, m - 1), cw = min((tid | 31), m - 1);  // cr: lanes past m read a live column
-      for (int i = cw; i >= 0; --i) {
+      for (int i = cw; i >= lo; --i) {
         double t0 = 0.0, t1 = 0.0;
         int k = i + 1;
         for (; k + 1 <= cw; k += 2) {
@@ -472,6 +470,24 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
       }
     }
     __syncthreads();
+    if (m > 32) {
+      const int n2 = m - 32;
+      double* T = W + m;  // T = R12 Ri22 (32 x n2), after the diagonal reciprocals
+      for (int e = tid; e < 32 * n2; e += nt) {
+        const int i = e / n2, c = 32 + e % n2;
+        double t = 0.0;
+        for (int k = 32; k <= c; ++k) t = fma(R[i * m + k], Ri[k * m + c], t);
+        T[e] = t;
+      }
+      __syncthreads();
+      for (int e = tid; e < 32 * n2; e += nt) {
+        const int i = e / n2, c = e % n2;
+        double t = 0.0;
+        for (int k = i; k < 32; ++k) t = fma(Ri[i * m + k], T[k * n2 + c], t);
+        Ri[i * m + 32 + c] = -t;
+      }
+      __syncthreads();
+    }
     GPS_STAMP(3);
 #ifdef GPS_POLAR_DEBUG
     if (tid == 0) printf("chol stage %d inverse done %lld\n", stage, clock64());
@@ -486,6 +502,7 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
       b = fma(Ri[e], Ri[e], b);
     }
     const double kap = sqrt(block_sum_any(a, red)) * sqrt(block_sum_any(b, red));
+    GPS_STAMP(7);
     if (!(kap <= kCholQr2MaxKappa)) {
       if (tid == 0) pc->fallback = 1;
       return;
@@ -500,10 +517,15 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
   // stage 2: Q1 = G R1^-1 is orthonormal to ~kappa^2 u when stage 1 was
   // accurate, so R2 ~ I; a larger departure means stage 1 lost accuracy and
   // the exact path takes the step.
+  const int L = ns_ld(m);
+  double* Up = R;  // padded m x L buffers (see the series above)
+  double* Wp = R + m * L;
+  double* Rp = R + 2 * m * L;
+  double* Xp = R + 3 * m * L;
   {
     double t = 0.0;
     for (int e = tid; e < m * m; e += nt) {
-      const double d = R[e] - ((e / m == e % m) ? 1.0 : 0.0);
+      const double d = Up[(e / m) * L + e % m];  // R2 - I = U
       t = fma(d, d, t);
     }
     if (!(sqrt(block_sum_any(t, red)) <= kCholQr2MaxR2Dev)) {
@@ -511,29 +533,32 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
       return;
     }
   }
-  // stage 2: R = R2 R1 (upper, row-major in W), its polar factor P, then
-  // S = R2^-1 P, the right factor of X = Q1 S (the CholeskyQR2 path only
-  // runs for condition numbers far below the rank cutoff max(p, m) eps --
-  // stage 1 checked -- so rank = m here).  P comes from one scaled Newton
-  // step, which the triangular factors make cheap because R^-1 = R1^-1 R2^-1
-  // is at hand (R1^-1 from stage 1 in Sg, R2^-1 = Ri),
+  // stage 2: R = R2 R1, its polar factor P, then S = R2^-1 P, the right
+  // factor of X = Q1 S (the CholeskyQR2 path only runs for condition numbers
+  // far below the rank cutoff max(p, m) eps -- stage 1 checked -- so rank =
+  // m here).  P comes from one scaled Newton step, which the triangular
+  // factors make cheap because R^-1 = R1^-1 R2^-1 is at hand (R1^-1 from
+  // stage 1 in Sg),
   //   M = (zeta R + zeta^-1 R^-T) / 2,  zeta = sqrt(|R^-1|_F / |R|_F)
   // (same singular vectors as R; the singular values move into
   // [1, (sqrt(k) + 1 / sqrt(k)) / 2] for kappa k), followed by the
   // Newton-Schulz iteration on M, which then starts well inside its
-  // quadratic region (~20 -> ~7 steps at kappa ~ 100).  Scratch: T1 = the
-  // m x m slot after W inside the Newton-Schulz workspace.
-  // (both triangular products on the fp64 tensor cores: mm_small over the
-  // full m x m operands, whose zero lower triangles keep the products upper;
-  // ~15-20 us less per stage at m = 64 than a thread per element)
-  double* T1 = W + m * m;
-  for (int e = tid; e < m * m; e += nt) T1[e] = R1g[e];  // R1 (upper) into shared memory
+  // quadratic region (~20 -> ~7 steps at kappa ~ 100).  Every product on
+  // the fp64 tensor cores at the padded stride (mm_small over the full
+  // m x m operands; zero lower triangles keep the triangular products
+  // upper).
+  for (int e = tid; e < m * m; e += nt) {
+    const int i = e / m, j = e % m;
+    Up[i * L + j] += (i == j) ? 1.0 : 0.0;  // R2 = I + U
+    Wp[i * L + j] = R1g[e];                 // R1
+    Ri[e] = Rp[i * L + j];                  // R2^-1 (stride m: Rp is Newton-Schulz workspace below)
+  }
   __syncthreads();
-  mm_small(R, T1, W, m, m, false);  // R = R2 R1
+  mm_small(Up, Wp, Xp, m, L, false);  // R = R2 R1
   __syncthreads();
-  for (int e = tid; e < m * m; e += nt) R[e] = Sg[e];  // R1^-1 (R2 is no longer needed)
+  for (int e = tid; e < m * m; e += nt) Wp[(e / m) * L + e % m] = Sg[e];  // R1^-1
   __syncthreads();
-  mm_small(R, Ri, T1, m, m, false);  // R^-1 = R1^-1 R2^-1
+  mm_small(Wp, Rp, Up, m, L, false);  // R^-1 = R1^-1 R2^-1
   __syncthreads();
   GPS_STAMP(4);
 #ifdef GPS_POLAR_DEBUG
@@ -542,14 +567,15 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
   {
     double a = 0.0, b = 0.0;
     for (int e = tid; e < m * m; e += nt) {
-      a = fma(W[e], W[e], a);
-      b = fma(T1[e], T1[e], b);
+      const int i = e / m, j = e % m;
+      a = fma(Xp[i * L + j], Xp[i * L + j], a);
+      b = fma(Up[i * L + j], Up[i * L + j], b);
     }
     const double fa = sqrt(block_sum_any(a, red)), fb = sqrt(block_sum_any(b, red));
     const double zeta = sqrt(fb / fa);
     for (int e = tid; e < m * m; e += nt) {
       const int i = e / m, j = e % m;
-      M[e] = 0.5 * (zeta * W[e] + T1[j * m + i] / zeta);
+      M[e] = 0.5 * (zeta * Xp[i * L + j] + Up[j * L + i] / zeta);
     }
   }
   __syncthreads();
@@ -562,12 +588,15 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
   if (tid == 0) printf("chol stage %d NS done %lld\n", stage, clock64());
 #endif
   if (tid == 0) pc->rank = m;
-  for (int e = tid; e < m * m; e += nt) {  // S = Ri (R2^-1) * P
-    const int r = e / m, c = e % m;
-    double t = 0.0;
-    for (int k = r; k < m; ++k) t += Ri[r * m + k] * M[k * m + c];
-    Sg[e] = t;
+  for (int e = tid; e < m * m; e += nt) {  // S = R2^-1 P
+    const int i = e / m, j = e % m;
+    Xp[i * L + j] = Ri[e];
+    Wp[i * L + j] = M[e];
   }
+  __syncthreads();
+  mm_small(Xp, Wp, Up, m, L, false);
+  __syncthreads();
+  for (int e = tid; e < m * m; e += nt) Sg[e] = Up[(e / m) * L + e % m];
   GPS_STAMP(6);
 }
 
@@ -674,9 +703,10 @@ __global__ void __launch_bounds__(kPolarThreads) bk_finish_kernel(double* G, dou
   }
 }
 
-// M, Ri, then max(3 m^2, the Newton-Schulz workspace) from R
+// M, Ri, then four padded m x ns_ld(m) buffers from R (the Newton-Schulz
+// workspace is the first three; stage 2's products use all four)
 __host__ __device__ inline size_t chol_smem_bytes(int m) {
-  return (size_t(2) * m * m + size_t(3) * m * ns_ld(m)) * sizeof(double) + 64;
+  return (size_t(2) * m * m + size_t(4) * m * ns_ld(m)) * sizeof(double) + 64;
 }
 
 }  // namespace gps

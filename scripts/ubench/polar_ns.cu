@@ -135,6 +135,7 @@ int main() {
              h.fallback, h.rank, ps[1] - ps[0], ps[2] - ps[1], ps[3] - ps[2]);
       if (stage == 2) printf(", R2R1 %lld, NS %lld clk", ps[4] - ps[3], ps[5] - ps[4]);
       printf(", tail %lld, total %lld clk", ps[6] - (stage == 2 ? ps[5] : ps[3]), ps[6] - ps[0]);
+      if (stage == 1) printf(" (kappa %lld)", ps[7] - ps[3]);
       printf("\n");
     }
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
