@@ -229,7 +229,8 @@ __device__ void mm_small(const double* A, const double* B, double* C, int m, int
 // (0, 1], so it converges; quadratically once X'X ~ I).  ws: 3 m ns_ld(m)
 // doubles of scratch (the iterate and two products at row stride ns_ld(m)).
 // Returns false if it has not converged in max_it steps.
-__device__ bool newton_schulz_polar(double* X, double* ws, double* red, int m, int max_it, int* iters = nullptr) {
+__device__ bool newton_schulz_polar(double* X, double* ws, double* red, int m, int max_it, int* iters = nullptr,
+                                    bool sigma_ge_one = false) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const int ld = ns_ld(m);
   double* Xp = ws;
@@ -262,8 +263,19 @@ __device__ bool newton_schulz_polar(double* X, double* ws, double* red, int m, i
   const double inv = 1.0 / sqrt(s_norm1 * s_norminf);
   for (int e = tid; e < m * m; e += nt) Xp[(e / m) * ld + e % m] = X[e] * inv;
   __syncthreads();
+  // With every singular value of X known to be >= 1 (the scaled Newton step
+  // guarantees it), X0's lie in [l, 1], l = inv: the first steps use the
+  // cubic scaled to that interval, X <- (3 a X - a^3 X X'X) / 2 with
+  // a = sqrt(3 / (1 + l + l^2)) (the image of [l, 1] is [f(a l), 1], so the
+  // bound stays valid: l <- (3 a l - a^3 l^3) / 2), until l > 0.99; plain
+  // Newton-Schulz (a = 1) finishes.  Same fixed point, fewer steps.
+  double lb = sigma_ge_one ? inv : 1.0;
   bool ok = false;
   for (int it = 0; it < max_it && !ok; ++it) {
+    const bool scaled = lb < 0.99;
+    const double al = scaled ? sqrt(3.0 / (1.0 + lb + lb * lb)) : 1.0;
+    const double c1 = 1.5 * al, c3 = 0.5 * al * al * al;
+    if (scaled) lb = 0.5 * (3.0 * al * lb - al * al * al * lb * lb * lb);
     mm_small(Xp, Xp, T, m, ld, true);  // T = X'X
     __syncthreads();
     mm_small(Xp, T, U, m, ld, false);  // U = X T
@@ -271,7 +283,7 @@ __device__ bool newton_schulz_polar(double* X, double* ws, double* red, int m, i
     double d = 0.0;
     for (int e = tid; e < m * m; e += nt) {
       const int o = (e / m) * ld + e % m;
-      const double xn = fma(-0.5, U[o], 1.5 * Xp[o]);
+      const double xn = scaled ? fma(-c3, U[o], c1 * Xp[o]) : fma(-0.5, U[o], 1.5 * Xp[o]);
       d = fma(xn - Xp[o], xn - Xp[o], d);
       Xp[o] = xn;
     }
@@ -279,7 +291,7 @@ __device__ bool newton_schulz_polar(double* X, double* ws, double* red, int m, i
 #ifdef GPS_POLAR_DEBUG
     if (tid == 0) printf("newton-schulz it %d step %.3e\n", it, dn);
 #endif
-    ok = dn < 1e-15 * sqrt(double(m));
+    ok = !scaled && dn < 1e-15 * sqrt(double(m));
     if (iters != nullptr && threadIdx.x == 0) *iters += 1;
   }
   if (ok)
@@ -579,7 +591,7 @@ __global__ void __launch_bounds__(kPolarThreads) chol_stage_kernel(const double*
     }
   }
   __syncthreads();
-  if (!newton_schulz_polar(M, R, red, m, 100, &pc->ns_iters)) {  // not converged: exact path decides
+  if (!newton_schulz_polar(M, R, red, m, 100, &pc->ns_iters, true)) {  // not converged: exact path decides
     if (tid == 0) pc->fallback = 1;
     return;
   }
