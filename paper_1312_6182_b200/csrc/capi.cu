@@ -1432,6 +1432,7 @@ struct gps_bk {
   double* part_s_tc = nullptr;        // [2][tc_ref_grid][4]: T1x, then T1s (leftover lists)
   int64_t* tc_left = nullptr;         // [tc_ref_grid][64] leftover candidates of T1x (-> T1s)
   int* tc_left_n = nullptr;           // [tc_ref_grid]
+  int tc_xterms = 1;                  // fp16 terms of X in T1's MMA (GPSPCA_TC_XTERMS=2: two, narrower margin)
   int tc_split = 1, tc_split_rows = 0;  // T1s row splits (CTAs per leftover list) and rows per split
   double* tc_lpart = nullptr;         // T1s partial dots: per group [tc_split][GS][m_pad] at its first candidate
   unsigned char* tc_part_nz = nullptr;  // [tc_gx] T2 partial written (1) or empty (0), read by K2
@@ -1550,7 +1551,8 @@ int bk_enqueue_tc(gps_bk* s, bool with_ctl) {
   const GpsCtl* ctl = with_ctl ? s->ctl : nullptr;
   const int ld = static_cast<int>(A->ld), np = s->mg;
   tc_split_x_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(s->X, int64_t(s->m_pad()) * ld, s->m, np, ld, s->xhi,
-                                                            s->xlo, ctl, s->tc_act_count);
+                                                            s->tc_xterms == 2 ? s->xlo : nullptr, ctl,
+                                                            s->tc_act_count);
   ctx->launches++;
   TcDotsArgs a{};
   a.n = A->n;
@@ -1570,6 +1572,10 @@ int bk_enqueue_tc(gps_bk* s, bool with_ctl) {
   a.x_stages = s->tc_rings[1];
   a.col_exp = s->col_exp;
   a.col_delta = s->col_delta;
+  a.x_terms = s->tc_xterms;
+  // one-term X: |x_j - 2^-14 X1_j|_2 <= 2^-11 |x_j| (fp16 rounding of normal values) + 2^-39 sqrt(ld)
+  // (subnormal spacing), |x_j| = 1 on the Stiefel manifold; times |a1_i| <= |a_i| (1 + 2^-11)
+  a.x_err = static_cast<float>((0x1p-11 + 0x1p-39 * std::sqrt(double(ld))) * (1.0 + 0x1p-10));
   {
     static const char* sg = getenv("GPSPCA_TC_SEG");  // tuning experiments only
     // two epilogue groups are busy for m > 32: drain every 256 rows there
@@ -1878,6 +1884,14 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
     s->tc_grid = std::min(ctx->num_sms, s->tc_tiles);
     s->tc_gx = static_cast<int>(std::min<int64_t>(32, A->n));
     s->tc_ref_grid = static_cast<int>(std::min<int64_t>(ceil_div(A->n, kTcRefItem), int64_t(2) * ctx->num_sms));
+    {
+      // One fp16 term of X in T1 halves its MMA work (N = m_pad): the sweep is
+      // power-bound under sustained load (C4: 12.4 -> 11.4 ms per sweep at
+      // sw_power_cap), for a margin ~2.5x wider (T1x / T1s recompute more
+      // candidates).  Two terms: GPSPCA_TC_XTERMS=2 (experiments).
+      const char* xt = std::getenv("GPSPCA_TC_XTERMS");
+      s->tc_xterms = (xt && std::atoi(xt) == 2) ? 2 : 1;
+    }
     // T1s: >= 1024 rows per CTA, at most kTcSplitMax CTAs per leftover list
     s->tc_split = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kTcSplitMax, A->ld / 1024)));
     s->tc_split_rows = static_cast<int>(ceil_div(ceil_div(A->ld, s->tc_split), kTcRefRows) * kTcRefRows);
@@ -2008,7 +2022,7 @@ int gps_bk_create(gps_matrix* A, int penalty, int m, const double* gamma, const 
       // candidate margins: one pass over A once per matrix (the scale
       // exponents come from the matrix's norms pass), kept with it
       rc = matrix_norms_locked(A);
-      cudaError_t ek = rc == GPS_OK ? gps_malloc(&A->tc_col_delta, n * sizeof(float)) : cudaSuccess;
+      cudaError_t ek = rc == GPS_OK ? gps_malloc(&A->tc_col_delta, 2 * n * sizeof(float)) : cudaSuccess;  // delta | |a|
       if (rc == GPS_OK && ek == cudaSuccess) {
         if (f64)
           tc_col_delta_kernel<double><<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(

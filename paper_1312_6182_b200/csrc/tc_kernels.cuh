@@ -158,12 +158,16 @@ __global__ void tc_col_delta_kernel(const TA* __restrict__ A, int64_t n, int ld,
     }
     ss = warp_sum(ss);
     rr = warp_sum(rr);
-    if (lane == 0) col_delta[col] = __double2float_ru((sqrt(rr) + ldexp(sqrt(ss), -kTcMarginExp)) * (1.0 + 0x1p-40));
+    if (lane == 0) {
+      col_delta[col] = __double2float_ru((sqrt(rr) + ldexp(sqrt(ss), -kTcMarginExp)) * (1.0 + 0x1p-40));
+      col_delta[n + col] = __double2float_ru(sqrt(ss) * (1.0 + 0x1p-40));  // |a_i| (one-term X margin)
+    }
   }
 }
 
 // T0: X (fp64 [m][ld], parity slot) -> X1 / X2 (fp16 [n_pad][ld], zero
-// padded components): x 2^14 = X1 + 2^-11 X2.
+// padded components): x 2^14 = X1 + 2^-11 X2 (X1 alone when x2 is null:
+// the one-term filter).
 __global__ void tc_split_x_kernel(const double* __restrict__ X, int64_t x_par_stride, int m, int n_pad, int ld,
                                   __half* __restrict__ x1, __half* __restrict__ x2, const GpsCtl* ctl,
                                   unsigned int* __restrict__ act_count) {
@@ -177,7 +181,7 @@ __global__ void tc_split_x_kernel(const double* __restrict__ X, int64_t x_par_st
     const double y = j < m ? Xp[e] * double(1 << kTcXScaleExp) : 0.0;
     const __half h = __double2half(y);
     x1[e] = h;
-    x2[e] = __double2half((y - static_cast<double>(__half2float(h))) * 2048.0);
+    if (x2 != nullptr) x2[e] = __double2half((y - static_cast<double>(__half2float(h))) * 2048.0);
   }
 }
 
@@ -199,6 +203,8 @@ struct TcDotsArgs {
   int num_tiles;
   int a_stages, x_stages;  // ring depths (<= kTcMaxStages)
   int seg_chunks;          // chunks per TMEM accumulation segment
+  int x_terms;  // fp16 terms of X in the MMA: 2 (x 2^14 = X1 + 2^-11 X2) or 1 (X1 only, wider margin)
+  float x_err;  // one-term X: bound on |x_j - 2^-14 X1_j|_2 (unit x_j), times |a_i| added to the margin
   int probe;  // timing experiments: 4 no TMEM drain, 8 no X loads, 16 no update, 128 A loads with the
               // evict_first hint,
               // 32 no TMEM stores, 64 cycle accounting
@@ -358,8 +364,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int kchunks = (a.ld + kTcKChunk - 1) / kTcKChunk;
-  // one MMA per 16 rows: A1 [X1 | X2] (N = 2 NP; the X slot holds X1 rows then X2 rows)
-  const uint32_t idesc2 = umma_idesc_f16(kTcTileM, 2 * NP);
+  // one MMA per 16 rows: A1 [X1 | X2] (N = 2 NP; the X slot holds X1 rows then X2 rows), or A1 X1 (N = NP)
+  const uint32_t idesc2 = umma_idesc_f16(kTcTileM, a.x_terms * NP);
 
   if (tid == 0) {
     for (int i = 0; i < SA; ++i) {
@@ -452,10 +458,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         pf.stop(w0);
         const bool lx = !(a.probe & 8) || c < SX;
         unsigned char* st = xring + r.slot * 2 * x_bytes;
-        mbar_arrive_expect_tx(&x_full[r.slot], static_cast<uint32_t>(lx ? 2 * x_bytes : 0));
+        mbar_arrive_expect_tx(&x_full[r.slot], static_cast<uint32_t>(lx ? a.x_terms * x_bytes : 0));
         if (lx) {
           tma_load_2d_hint(st, &tmX1, kc * kTcKChunk, 0, &x_full[r.slot], policy);
-          tma_load_2d_hint(st + x_bytes, &tmX2, kc * kTcKChunk, 0, &x_full[r.slot], policy);
+          if (a.x_terms == 2) tma_load_2d_hint(st + x_bytes, &tmX2, kc * kTcKChunk, 0, &x_full[r.slot], policy);
         }
         r.next(SX);
         if (++kc == kchunks) kc = 0;
@@ -611,7 +617,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       // the candidate test at its end does not wait on global memory
       const int64_t col_t = int64_t(t) * kTcTileM + q * 32 + lane;
       const int e_col = col_t < a.n ? a.col_exp[col_t] : 0;
-      const float d_col = col_t < a.n ? a.col_delta[col_t] : 0.f;
+      const float d_col = col_t < a.n ? (a.x_terms == 2 ? a.col_delta[col_t]
+                                                       : __fmaf_ru(a.col_delta[a.n + col_t], a.x_err, a.col_delta[col_t]))
+                                      : 0.f;
       // per-tile sums with Kahan compensation in fp32 (full-rate fp32 ops
       // instead of fp64 conversions and adds)
       float ch[32], cl[32];
@@ -631,7 +639,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             float v0[8], v1[8];
             const uint32_t ta = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(b * 2 * NP + j0);
             tmem_ld8(ta, v0);
-            tmem_ld8(ta + uint32_t(NP), v1);
+            if (a.x_terms == 2) {
+              tmem_ld8(ta + uint32_t(NP), v1);
+            } else {
+#pragma unroll
+              for (int u = 0; u < 8; ++u) v1[u] = 0.f;
+            }
             tmem_wait_ld();
 #pragma unroll
             for (int u = 0; u < 8; ++u) {

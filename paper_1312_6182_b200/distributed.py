@@ -165,6 +165,9 @@ def peer_exchange_available(comm, device):
     return all(torch.cuda.can_device_access_peer(a, b) for a in devs for b in devs if a != b)
 
 
+SELF_TEST_TIMEOUT_S = 5.0
+
+
 def px_self_test(px, comm, device, count):
     """Collective check of a freshly opened peer exchange: one standalone
     peer-memory all-reduce of a seeded vector against the torch.distributed
@@ -187,9 +190,19 @@ def px_self_test(px, comm, device, count):
     if not bool(flag0.item()):
         return False
     try:
+        # a peer path that cannot deliver (flags never visible) times out in
+        # seconds here rather than the loop's 60 s bound
+        handle = getattr(px, "handle", None)
+        if handle is not None:
+            _native.lib().gps_px_set_timeout(handle, SELF_TEST_TIMEOUT_S)
         px.all_reduce(v)
         torch.cuda.synchronize(device)
         ok = bool(torch.allclose(v, ref, rtol=1e-12, atol=1e-12))
+        if handle is not None:
+            err = _native.C.c_int(0)
+            _native.check(_native.lib().gps_px_error(handle, _native.C.byref(err)), "gps_px_error")
+            ok = ok and err.value == 0
+            _native.lib().gps_px_set_timeout(handle, float(os.environ.get("GPSPCA_PX_TIMEOUT_S", "60") or 60))
     except Exception:  # noqa: BLE001 -- any failure means "do not use the peer path"
         ok = False
     flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=device)
