@@ -383,7 +383,9 @@ int launch_reduce(gps_ctx* ctx, const double* part_g, const double* part_s, int 
     GPS_CHECK_LAUNCH("su_reduce_px_kernel launch");
     return GPS_OK;
   }
-  const int blocks = std::min((ld + kReduceRows - 1) / kReduceRows, ctx->num_sms * 8) + 1;
+  // row CTAs (grid-stride) + the scalar CTA; long rows take a thread per row
+  const int row_ctas = ld >= kReduceRowPerThread ? (ld + 255) / 256 : (ld + kReduceRows - 1) / kReduceRows;
+  const int blocks = std::min(row_ctas, ctx->num_sms * 8) + 1;
   su_reduce_kernel<<<blocks, 256, 0, ctx->stream>>>(part_g, part_s, nparts, ld, exch, ctl,
                                                     nparts_s < 0 ? nparts : nparts_s, nz);
   ctx->launches++;
