@@ -1552,7 +1552,7 @@ int bk_enqueue_tc(gps_bk* s, bool with_ctl) {
   gps_ctx* ctx = A->ctx;
   const GpsCtl* ctl = with_ctl ? s->ctl : nullptr;
   const int ld = static_cast<int>(A->ld), np = s->mg;
-  tc_split_x_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(s->X, int64_t(s->m_pad()) * ld, s->m, np, ld, s->xhi,
+  tc_split_x_kernel<<<dim3(static_cast<unsigned>(ceil_div(ld, 1024)), static_cast<unsigned>(np)), 256, 0, ctx->stream>>>(s->X, int64_t(s->m_pad()) * ld, s->m, np, ld, s->xhi,
                                                             s->tc_xterms == 2 ? s->xlo : nullptr, ctl,
                                                             s->tc_act_count);
   ctx->launches++;
@@ -1718,7 +1718,8 @@ int bk_enqueue_step(gps_bk* s) {
   // head -> assemble G -> CholeskyQR2 polar
   bk_head_kernel<<<1, 32, 0, ctx->stream>>>(s->exch, s->ngroups, s->mg, ld, s->hist, s->ctl, s->tol, s->max_iter,
                                             s->pc, m);
-  bk_assemble_kernel<<<ctx->num_sms, 256, 0, ctx->stream>>>(s->exch, s->mg, ld, m, s->mu_dev, s->G, s->pc);
+  bk_assemble_kernel<<<dim3(static_cast<unsigned>(ceil_div(ld, 1024)), static_cast<unsigned>(m)), 256, 0, ctx->stream>>>(
+      s->exch, s->mg, ld, m, s->mu_dev, s->G, s->pc);
   ctx->launches += 2;
   CholQr2Polar cq{s->G, s->Tm, s->X, xs, s->gram_part, s->R1, s->Sm, s->pc, s->ctl, s->rank_dev, s->band, s->stiefel};
   return enqueue_cholqr2_polar(ctx, cq, ld, p, m);

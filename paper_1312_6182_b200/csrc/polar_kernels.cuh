@@ -86,10 +86,17 @@ __global__ void bk_assemble_kernel(const double* __restrict__ exch, int mg, int 
                                    const double* __restrict__ mu, double* __restrict__ G, const PolarCtl* pc) {
   if (!pc->active) return;
   const size_t gstride = size_t(mg) * ld + 4;
-  for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < size_t(m) * ld;
-       e += size_t(gridDim.x) * blockDim.x) {
-    const int j = static_cast<int>(e / ld), r = static_cast<int>(e % ld);
-    G[e] = 2.0 * mu[j] * exch[(j / mg) * gstride + size_t(j % mg) * ld + r];
+  // grid (row blocks of 4 x blockDim, components): no index division per element
+  const int j = blockIdx.y;
+  if (j >= m) return;
+  const double s = 2.0 * mu[j];
+  const double* src = exch + (j / mg) * gstride + size_t(j % mg) * ld;
+  double* dst = G + size_t(j) * ld;
+  const int r0 = blockIdx.x * 4 * blockDim.x + threadIdx.x;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int r = r0 + u * blockDim.x;
+    if (r < ld) dst[r] = s * src[r];
   }
 }
 

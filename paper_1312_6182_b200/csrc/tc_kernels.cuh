@@ -172,16 +172,22 @@ __global__ void tc_split_x_kernel(const double* __restrict__ X, int64_t x_par_st
                                   __half* __restrict__ x1, __half* __restrict__ x2, const GpsCtl* ctl,
                                   unsigned int* __restrict__ act_count) {
   if (ctl != nullptr && ctl->done) return;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *act_count = 0;  // this sweep's active columns (T1x / T1s count, T2 reads)
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *act_count = 0;  // this sweep's active columns (T1x / T1s count, T2 reads)
   const int parity = ctl != nullptr ? (ctl->iter & 1) : 0;
   const double* Xp = X + parity * x_par_stride;
-  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < int64_t(n_pad) * ld;
-       e += int64_t(gridDim.x) * blockDim.x) {
-    const int j = static_cast<int>(e / ld);
-    const double y = j < m ? Xp[e] * double(1 << kTcXScaleExp) : 0.0;
+  // grid (row blocks of 4 x blockDim, padded components): no index division per element
+  const int j = blockIdx.y;
+  const double* xs = Xp + size_t(j) * ld;
+  const size_t o = size_t(j) * ld;
+  const int r0 = blockIdx.x * 4 * blockDim.x + threadIdx.x;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int r = r0 + u * blockDim.x;
+    if (r >= ld) break;
+    const double y = j < m ? xs[r] * double(1 << kTcXScaleExp) : 0.0;
     const __half h = __double2half(y);
-    x1[e] = h;
-    if (x2 != nullptr) x2[e] = __double2half((y - static_cast<double>(__half2float(h))) * 2048.0);
+    x1[o + r] = h;
+    if (x2 != nullptr) x2[o + r] = __double2half((y - static_cast<double>(__half2float(h))) * 2048.0);
   }
 }
 
