@@ -2243,8 +2243,9 @@ int gps_bk_result(gps_bk* s, double* X_out, double* hist_out, int* n_hist, int* 
                              ctx->stream));
   if (W_out) {
     if (s->tc) {
-      tc_mask_w_kernel<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(s->W + (k & 1) * mp * n, int64_t(n), s->m,
-                                                                 s->colmask);
+      tc_mask_w_kernel<<<dim3(static_cast<unsigned>(std::min<int64_t>(ceil_div(int64_t(n), 256), 1024)),
+                              static_cast<unsigned>(s->m)),
+                         256, 0, ctx->stream>>>(s->W + (k & 1) * mp * n, int64_t(n), s->m, s->colmask);
       ctx->launches++;
       GPS_CHECK_LAUNCH("tc_mask_w_kernel launch");
     }
@@ -2355,7 +2356,9 @@ int gps_bk_sweep(gps_matrix* A, const double* X, int m, const double* gamma, con
   if (rc == GPS_OK) {
     e = cudaMemcpyAsync(ex.data(), s->exch, ex.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
     if (e == cudaSuccess && W_out && s->tc) {
-      tc_mask_w_kernel<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(s->W, int64_t(n), m, s->colmask);
+      tc_mask_w_kernel<<<dim3(static_cast<unsigned>(std::min<int64_t>(ceil_div(int64_t(n), 256), 1024)),
+                              static_cast<unsigned>(m)),
+                         256, 0, ctx->stream>>>(s->W, int64_t(n), m, s->colmask);
       ctx->launches++;
       e = cudaGetLastError();
     }

@@ -1423,11 +1423,11 @@ __global__ void __launch_bounds__(256, 2) tc_update_kernel(const TA* __restrict_
 // where T1x processed the column (every candidate, with W = 0 for an
 // inactive one); the filtered-out columns still hold older values, so they
 // are zeroed here by the final activity mask (colmask[col] = 0).
+// Grid (column blocks, components), grid-stride over the columns.
 __global__ void tc_mask_w_kernel(double* __restrict__ W, int64_t n, int m, const unsigned char* __restrict__ colmask) {
-  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n * m; e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t col = e % n;
-    if (colmask[col] == 0) W[e] = 0.0;
-  }
+  double* w = W + int64_t(blockIdx.y) * n;
+  for (int64_t col = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; col < n; col += int64_t(gridDim.x) * blockDim.x)
+    if (colmask[col] == 0) w[col] = 0.0;
 }
 
 }  // namespace gps
