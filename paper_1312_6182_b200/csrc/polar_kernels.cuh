@@ -314,7 +314,15 @@ __global__ void gram_reduce_kernel(double* __restrict__ part, int nparts, int mm
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= mm) return;
   double t = 0.0;
-  for (int b = 0; b < nparts; ++b) t += part[size_t(b) * mm + e];
+  int b = 0;
+  for (; b + 8 <= nparts; b += 8) {  // 8 loads in flight, added in order
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = part[size_t(b + u) * mm + e];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t += v[u];
+  }
+  for (; b < nparts; ++b) t += part[size_t(b) * mm + e];
   part[e] = t;
 }
 
