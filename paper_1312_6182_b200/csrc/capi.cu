@@ -1580,9 +1580,11 @@ int bk_enqueue_tc(gps_bk* s, bool with_ctl) {
   a.x_err = static_cast<float>((0x1p-11 + 0x1p-39 * std::sqrt(double(ld))) * (1.0 + 0x1p-10));
   {
     static const char* sg = getenv("GPSPCA_TC_SEG");  // tuning experiments only
-    // two epilogue groups are busy for m > 32: drain every 256 rows there
-    // (~2.6e-6 relative vs ~1.4e-6 at 128 rows; the fp32 contract is 1e-4)
-    a.seg_chunks = sg && atoi(sg) > 0 ? atoi(sg) : (np > 32 ? 2 * kTcSegChunks : kTcSegChunks);
+    // two epilogue groups are busy for m > 32: drain every 512 rows there
+    // (32 MMAs per segment: accumulation error <= 2^-16 |a_i|, 8x inside the
+    // margin's 2^-13 term; C4 sustained sweep 10.03 -> 9.96 ms against
+    // 256 rows), every 128 rows otherwise (C3: no difference up to 512)
+    a.seg_chunks = sg && atoi(sg) > 0 ? atoi(sg) : (np > 32 ? 4 * kTcSegChunks : kTcSegChunks);
   }
   {
     static const char* pr = getenv("GPSPCA_TC_PROBE");  // timing experiments only

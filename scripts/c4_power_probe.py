@@ -1,4 +1,4 @@
-"""C4 block iterations under sustained load with the SM clock and throttle
+"""C4 (CFG=C3: C3) block sweeps under sustained load with the SM clock and throttle
 reasons sampled (bench.ClockSampler), for GPSPCA_TC_PROBE power experiments
 (probe 1024: T1 issues one MMA per TMEM segment instead of one per 16 rows --
 results wrong by design)."""
@@ -19,13 +19,15 @@ def main():
     from paper_1312_6182_b200 import _native
     from paper_1312_6182_b200.block import BlockLoop, _top_m_columns
 
-    name, p, n, m, pen, mu, frac, data, k = [c for c in bench.BLOCK_CONFIGS if c[0] == "C4"][0]
+    want = os.environ.get("CFG", "C4")
+    name, p, n, m, pen, mu, frac, data, k = [c for c in bench.BLOCK_CONFIGS if c[0] == want][0]
     dev = torch.device("cuda", 0)
-    At = bench.make_lowrank(torch, p, n, 0, n, dev, 32, 64, n // 128)
+    n_classes, n_factors, support = (16, 10, n // 200) if name == "C3" else (32, 64, n // 128)
+    At = bench.make_lowrank(torch, p, n, 0, n, dev, n_classes, n_factors, support)
     A = gps.DataMatrix.from_device(At.data_ptr(), p, n, owner=At, device=0)
     top = frac * float(A.norms.max())
     iters = int(os.environ.get("ITERS", 40))
-    loop = BlockLoop(A, pen, m, np.full(m, top * top), mu, 0.0, iters + 8)
+    loop = BlockLoop(A, pen, m, np.full(m, top if pen == "l1" else top * top), mu, 0.0, iters + 8)
     loop.start_columns(_top_m_columns(np.asarray(A.norms), m))
     L = _native.lib()
     s = torch.cuda.Stream(dev)
@@ -44,7 +46,7 @@ def main():
         e1.synchronize()
     A.context.set_stream(None)
     d, it, _ = bench._bk_poll(loop)
-    print(f"probe={os.environ.get('GPSPCA_TC_PROBE', '0')} C4 sweep {e0.elapsed_time(e1) / iters:.3f} ms "
+    print(f"probe={os.environ.get('GPSPCA_TC_PROBE', '0')} {name} sweep {e0.elapsed_time(e1) / iters:.3f} ms "
           f"clocks {clocks.summary()} (loop done={d} at iteration {it})", flush=True)
 
 
