@@ -1686,18 +1686,18 @@ struct CholQr2Polar {
 
 int enqueue_cholqr2_polar(gps_ctx* ctx, const CholQr2Polar& q, int ld, int p, int m) {
   gram_partial_kernel<<<kGramBlocks, kGramThreads, 0, ctx->stream>>>(q.G, ld, p, m, q.gram_part, q.pc);
-  gram_reduce_kernel<<<(m * m + 255) / 256, 256, 0, ctx->stream>>>(q.gram_part, kGramBlocks, m * m, q.pc);
+  gram_reduce_kernel<<<(m * m + 31) / 32, 256, 0, ctx->stream>>>(q.gram_part, kGramBlocks, m * m, q.pc);
   chol_stage_kernel<<<1, kPolarThreads, chol_smem_bytes(m), ctx->stream>>>(q.gram_part, 1, m, p, 1, q.R1, q.Sm,
                                                                            q.pc);
   apply_right_kernel<<<static_cast<unsigned>(ceil_div(ld, kPolarApplyRows)), 256, apply_smem_bytes(), ctx->stream>>>(q.G, q.Sm, ld, m, q.Tm, q.pc, nullptr, 0);
   gram_partial_kernel<<<kGramBlocks, kGramThreads, 0, ctx->stream>>>(q.Tm, ld, p, m, q.gram_part, q.pc);
-  gram_reduce_kernel<<<(m * m + 255) / 256, 256, 0, ctx->stream>>>(q.gram_part, kGramBlocks, m * m, q.pc);
+  gram_reduce_kernel<<<(m * m + 31) / 32, 256, 0, ctx->stream>>>(q.gram_part, kGramBlocks, m * m, q.pc);
   chol_stage_kernel<<<1, kPolarThreads, chol_smem_bytes(m), ctx->stream>>>(q.gram_part, 1, m, p, 2, q.R1, q.Sm,
                                                                            q.pc);
   apply_right_kernel<<<static_cast<unsigned>(ceil_div(ld, kPolarApplyRows)), 256, apply_smem_bytes(), ctx->stream>>>(q.Tm, q.Sm, ld, m, q.X, q.pc, q.ctl, q.xs);
   // Gram of the new iterate: bk_finish checks it against the Stiefel tolerance
   gram_partial_kernel<<<kGramBlocks, kGramThreads, 0, ctx->stream>>>(q.X, ld, p, m, q.gram_part, q.pc, q.ctl, q.xs);
-  gram_reduce_kernel<<<(m * m + 255) / 256, 256, 0, ctx->stream>>>(q.gram_part, kGramBlocks, m * m, q.pc);
+  gram_reduce_kernel<<<(m * m + 31) / 32, 256, 0, ctx->stream>>>(q.gram_part, kGramBlocks, m * m, q.pc);
   bk_finish_kernel<<<1, kPolarThreads, polar_smem_bytes(m), ctx->stream>>>(
       q.G, q.X, q.xs, ld, p, m, q.ctl, q.pc, q.rank_dev, q.gram_part, q.band, q.stiefel);
   ctx->launches += 11;
@@ -1751,7 +1751,7 @@ int bk_qr_into_x(gps_bk* s, double* Mdev) {
     double* outs[2] = {s->Tm, s->X};
     for (int pass = 0; pass < 2; ++pass) {
       gram_partial_kernel<<<kGramBlocks, kGramThreads, 0, ctx->stream>>>(in, ld, p, m, s->gram_part, s->pc);
-      gram_reduce_kernel<<<(m * m + 255) / 256, 256, 0, ctx->stream>>>(s->gram_part, kGramBlocks, m * m, s->pc);
+      gram_reduce_kernel<<<(m * m + 31) / 32, 256, 0, ctx->stream>>>(s->gram_part, kGramBlocks, m * m, s->pc);
       chol_stage_kernel<<<1, kPolarThreads, chol_smem_bytes(m), ctx->stream>>>(s->gram_part, 1, m, p, 1, s->R1,
                                                                                s->Sm, s->pc);
       apply_right_kernel<<<static_cast<unsigned>(ceil_div(ld, kPolarApplyRows)), 256, apply_smem_bytes(), ctx->stream>>>(in, s->Sm, ld, m, outs[pass], s->pc, nullptr, 0);
@@ -1814,7 +1814,7 @@ int bk_record_x0(gps_bk* s, double* err_out) {
     const PolarCtl on{1, 0, m, 0};
     GPS_CUDA(cudaMemcpyAsync(s->pc, &on, sizeof(PolarCtl), cudaMemcpyHostToDevice, ctx->stream));
     gram_partial_kernel<<<kGramBlocks, kGramThreads, 0, ctx->stream>>>(s->X, ld, p, m, s->gram_part, s->pc);
-    gram_reduce_kernel<<<(m * m + 255) / 256, 256, 0, ctx->stream>>>(s->gram_part, kGramBlocks, m * m, s->pc);
+    gram_reduce_kernel<<<(m * m + 31) / 32, 256, 0, ctx->stream>>>(s->gram_part, kGramBlocks, m * m, s->pc);
     gram_error_kernel<<<1, 1024, 0, ctx->stream>>>(s->gram_part, m, s->stiefel);
     ctx->launches += 3;
   } else {

@@ -309,21 +309,29 @@ __device__ bool newton_schulz_polar(double* X, double* ws, double* red, int m, i
 
 // part[0][e] = sum_b part[b][e] in a fixed order, many CTAs (the one-CTA
 // stage kernel then reads a single Gram).
-__global__ void gram_reduce_kernel(double* __restrict__ part, int nparts, int mm, const PolarCtl* pc) {
+// 256 threads = 8 slices of the partials x 32 elements: warp s sums slice s
+// (its eight-or-so partials' loads in flight) for 32 consecutive elements,
+// then the slices are added in order -- deterministic, one load round.
+__global__ void __launch_bounds__(256) gram_reduce_kernel(double* __restrict__ part, int nparts, int mm,
+                                                          const PolarCtl* pc) {
+  __shared__ double red[8][32];
   if (!pc->active || pc->fallback) return;
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= mm) return;
+  const int sl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int e = blockIdx.x * 32 + lane;
+  const int b0 = nparts * sl / 8, b1 = nparts * (sl + 1) / 8;
   double t = 0.0;
-  int b = 0;
-  for (; b + 8 <= nparts; b += 8) {  // 8 loads in flight, added in order
-    double v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = part[size_t(b + u) * mm + e];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) t += v[u];
+  if (e < mm) {
+#pragma unroll 8
+    for (int b = b0; b < b1; ++b) t += part[size_t(b) * mm + e];
   }
-  for (; b < nparts; ++b) t += part[size_t(b) * mm + e];
-  part[e] = t;
+  red[sl][lane] = t;
+  __syncthreads();
+  if (sl == 0 && e < mm) {
+    double u = red[0][lane];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) u += red[k][lane];
+    part[e] = u;
+  }
 }
 
 // Sum the Gram partials (fixed order), Cholesky G'G = R'R (upper R), and
