@@ -6,24 +6,28 @@
 //
 // Filter arithmetic: column i of A is scaled by s_i = 2^e_i (max |a_ji| s_i
 // in [2^14, 2^15)) and rounded to fp16, A1 = fp16(a s_i) (11 significant
-// bits); X is split into two fp16 pieces with the common scale 2^14 (its
-// columns are unit vectors), x 2^14 = X1 + 2^-11 X2.  One tensor-core MMA per
-// 16 rows forms, with fp32 accumulation (kind::f16), D = [A1 X1 | A1 X2] and
-// c~_ij = 2^-(e_i + 14) (D0 + 2^-11 D1).  The rounding of A is bounded per
-// column exactly (||a_i - a1_i||, tc_col_delta_kernel), the rest of the error
-// by 2^-17 ||a_i||; T1 flags a column when any component can
-// reach its threshold within that margin.
+// bits); X is rounded to fp16 with the common scale 2^14 (its columns are
+// unit vectors), X1 = fp16(x 2^14).  One tensor-core MMA per 16 rows forms,
+// with fp32 accumulation (kind::f16), D = A1 X1 and c~_ij = 2^-(e_i + 14) D.
+// The rounding of A is bounded per column exactly (||a_i - a1_i||,
+// tc_col_delta_kernel), that of X by |a_i| (2^-11 + 2^-39 sqrt(p)), the rest
+// by 2^-16 |a_i|; T1 flags a column when any component can reach
+// its threshold within that margin.  (GPSPCA_TC_XTERMS=2: the two-term split
+// x 2^14 = X1 + 2^-11 X2, D = [A1 X1 | A1 X2], c~ from D0 + 2^-11 D1, and
+// no X term in the margin.)
 //
-// T0 split_x:   X (fp64) -> X1, X2 (fp16, [n_pad][ld])
-// T1 tc_dots:   persistent; per tile of 128 columns accumulates D0|D1|D2 in
-//               TMEM over 64-row chunks: A arrives by TMA (128-byte swizzle),
-//               converter warps scale and split it into TMEM (tcgen05.st),
-//               both MMAs read A from TMEM and X from shared memory; epilogue
-//               warps drain TMEM segments (every kTcSegChunks chunks) and flag
-//               the columns that can reach a threshold with the margin
-//               2^-13 ||a_i||.  A is read from HBM once.
+// T0 split_x:   X (fp64) -> X1 (and X2) (fp16, [n_pad][ld])
+// T1 tc_dots:   persistent; per tile of 128 columns accumulates D in TMEM
+//               over 64-row chunks: A arrives by TMA (128-byte swizzle),
+//               converter warps scale and round it into TMEM (tcgen05.st),
+//               the MMAs read A from TMEM and X from shared memory; epilogue
+//               warps drain TMEM segments and flag the columns that can
+//               reach a threshold within the margin.  A is read from HBM once.
 // T1x tc_refine: the flagged columns again, in fp64: c, thresholds, the
-//               objective, nnz, W and the activity mask.
+//               objective, nnz, W and the activity mask; its CTAs' leftover
+//               lists (< 64 columns each) go to T1s.
+// T1s tc_refine_split: the leftover lists grouped across CTAs, rows split
+//               over a persistent grid, same epilogue.
 // T2 tc_update: G_j = sum over ACTIVE columns of w_ij a_i (fp64), row chunks
 //               x component groups; reads only the active columns again.
 // Roles of T1 (12 warps): w0 A producer (TMA), w1 MMA issuer (+TMEM owner),
@@ -46,7 +50,7 @@ constexpr int kTcAStages = 5;    // default A ring depth (32 KB stages, HBM stre
 #define GPS_TC_LO_STAGES 2
 #endif
 constexpr int kTcLoStages = GPS_TC_LO_STAGES;  // TMEM A1 slots (converter output; <= 4: columns 256..511)
-constexpr int kTcXStages = 3;    // default X1 | X2 ring depth (L2-resident)
+constexpr int kTcXStages = 3;    // default X ring depth (X1, or X1 | X2; L2-resident)
 constexpr int kTcMaxStages = 8;
 constexpr int kTcThreads = 512;  // 16 warps
 constexpr int kTcMaxN = 64;
@@ -223,7 +227,8 @@ struct TcDotsArgs {
 //   A1        2 slots x 64 TMEM columns (32 packed fp16 pairs used), written
 //             by the converters with tcgen05.st, read by the MMAs as the
 //             TMEM-resident A operand
-//   X ring    SX x (X1 | X2) chunk in shared memory (TMA, evict-last)
+//   X ring    SX x (X1 | X2) chunk slots in shared memory (TMA, evict-last;
+//             X1 only with the one-term filter)
 // TMEM: columns [0, 4 NP) = 2 accumulator buffers of [D0 | D1] (2 NP
 // each), columns [256, 384) = the two A1 slots.
 constexpr uint32_t kTcTmemCols = 512;
