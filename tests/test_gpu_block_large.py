@@ -44,6 +44,28 @@ def test_tensor_core_sweep_vs_oracle(p, n, m, pen, dtype, monkeypatch):
     assert np.abs(G - G_ref).max() <= 1e-11 * np.abs(G_ref).max()
 
 
+@pytest.mark.parametrize("p,n,m,pen", [(4096, 12000, 64, "l1"), (300, 777, 24, "l0")])
+def test_two_term_filter_vs_oracle(p, n, m, pen, monkeypatch):
+    """The two-term X filter (GPSPCA_TC_XTERMS=2: x 2^14 = X1 + 2^-11 X2,
+    narrower margin) gives the same exact results as the default one-term
+    filter."""
+    monkeypatch.setenv("GPSPCA_TC_XTERMS", "2")
+    rng = np.random.default_rng(p + m + 1)
+    A32 = rng.standard_normal((p, n)).astype(np.float32)
+    A = gps.DataMatrix(A32)
+    X = _stiefel(rng, p, m)
+    gamma = np.full(m, 2.0 if pen == "l1" else 4.0)
+    mu = np.linspace(1.0, 0.6, m)
+    A64 = A32.astype(np.float64)
+    C = A64.T @ X
+    f_ref = oracle.block_objective(C, gamma, mu, pen)
+    G_ref = oracle.block_gradient(A64, C, gamma, mu, pen)
+    f = (gps.objective_bl1 if pen == "l1" else gps.objective_bl0)(A, X, gamma, mu)
+    G = gps.ascent_direction_block(A, X, gamma, mu, pen)
+    assert f == pytest.approx(f_ref, rel=1e-11)
+    assert np.abs(G - G_ref).max() <= 1e-11 * np.abs(G_ref).max()
+
+
 @pytest.mark.parametrize("dtype", [np.float32, np.float64], ids=["fp32", "fp64"])
 def test_tensor_core_solve_vs_oracle(dtype, monkeypatch):
     monkeypatch.setenv("GPSPCA_TC_F64_MIN_BYTES", "0")
