@@ -79,6 +79,9 @@ constexpr int kSweepLag = 1;                          // update of stage t runs 
 #ifndef GPS_SWEEP_K
 #define GPS_SWEEP_K 4
 #endif
+#ifndef GPS_UPDATE_WIDEN
+#define GPS_UPDATE_WIDEN 0  // 1: the update pass widens all-normal columns with integer ops (experiment)
+#endif
 __host__ __device__ constexpr int sweep_cols_per_group(int rv) { return rv >= 8 ? 2 : GPS_SWEEP_K; }
 
 // Shared scratch after the ring (doubles): red[D][NG][K][NW] warp partials,
@@ -410,7 +413,7 @@ __global__ void __launch_bounds__(NWK + 64, 1) su_sweep_kernel(const SweepArgs a
           const double w = wp[k];
           if (w != 0.0) {
             const TA* colp = ptile + size_t(k * NG + grp) * ld;
-            if (std::is_same<TA, float>::value && fp[k] != 0.0) {  // group-uniform
+            if (GPS_UPDATE_WIDEN && std::is_same<TA, float>::value && fp[k] != 0.0) {  // group-uniform
 #pragma unroll
               for (int v = 0; v < RV; ++v) {
                 const V q = *reinterpret_cast<const V*>(colp + (gt + v * GS) * VN);
